@@ -1,0 +1,323 @@
+#!/usr/bin/env python
+"""Benchmark: sub-grid cells processed per second (FP64 ring step) on 1..N B200.
+
+Workload (default, ``--workload c4``): BASELINE.json config 4 restated on the
+pinned path: the full mini-app time step — ghost fold, 3x5
+kernel chain, per-sub-grid min + numpy-order pairwise sum, exact fsum
+checksum and min-tree dt — over 8^5 = 32768 sub-grids (16.8 M cells) PER GPU
+on a 1-D ring partitioned contiguously across ranks (weak scaling; halo
+faces by NCCL P2P, accumulator by NCCL all-reduce). ``--workload c2`` is the
+4096-sub-grid batch of config 2, ``c5`` the 8^6 ring (per GPU).
+
+One JSON line on rank 0. ``value`` = cells of all ranks per second over the
+timed steps, device-timed with CUDA events (max over ranks), inputs resident
+in HBM, L2 flushed (256 MiB write) before every timed step. ``e2e`` = the
+same metric through the host-buffer API (RingStepper.step_host: pinned H2D
+of the cells, step, D2H of the new cells and (piece, dt)). ``roofline`` is
+the fused step kernel K2 against measured HBM bandwidth. ``cpu_baseline`` is
+the C port of the reference data path (oracle/tb_oracle.c, OpenMP, all host
+threads) on a bounded sample.
+
+``--impl reference``: rank 0 times that CPU implementation on this arm's
+config and prints the same line with "impl": "reference".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "c2": (4096, "C2: 4096 sub-grids of 8^3 cells + ring ghost faces, one full step "
+                 "(ghost fold + 15 FP64 kernels + min/pairwise-sum + exact checksum)"),
+    "c4": (32768, "C4: full step at max_level 5 (8^5 = 32768 sub-grids of 8^3 cells) "
+                  "per GPU: ghost fold + 15 FP64 kernels + min/pairwise-sum + exact "
+                  "fsum checksum + min-tree dt"),
+    "c5": (262144, "C5: full step at max_level 6 (8^6 = 262144 sub-grids) per GPU"),
+}
+METRIC = "sub-grid cells processed/sec (rotating star, FP64) at 1/2/4/8 B200 vs CPU ref"
+BYTES_PER_CELL = 8 + 8 + 0.25 + 0.03125   # 16.28 B/cell-step
+GOLDEN_DEFAULTS = float.fromhex("0x1.df1096d8fa699p+20")   # run_reference(512, 15)
+FALLBACK_HBM_GBS = 6650.0
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh), "measured"
+    except (OSError, ValueError):
+        return {"hbm_gbs": FALLBACK_HBM_GBS}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons during a region."""
+
+    QUERY = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.proc = None
+        self.gpu = gpu_index
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        rows = []
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"],
+                    "samples": 0}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4)
+                          if r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def cpu_reference_sample(subgrids: int, budget_s: float, threads: int = 0):
+    """Time the C port of the reference data path (oracle/tb_oracle.c) on the
+    host: repeated full steps of ``subgrids`` sub-grids until ``budget_s``."""
+    import numpy as np
+    from oracle import c_oracle
+    threads = threads or len(os.sched_getaffinity(0))
+    old = c_oracle.init_cells(subgrids)
+    new = np.empty_like(old)
+    mins, sums = np.empty(subgrids), np.empty(subgrids)
+    steps, t0 = 0, time.perf_counter()
+    while True:
+        c_oracle.step(old, new, old[-1, -8:].copy(), old[0, :8].copy(), mins, sums,
+                      threads=threads)
+        c_oracle.fsum(sums)
+        old, new = new, old
+        steps += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s:
+            break
+    return subgrids * 512 * steps / el, threads, steps, el
+
+
+def run_reference_arm(args, workload_key, rank, world):
+    if rank != 0:
+        return 0
+    per_gpu, desc = WORKLOADS[workload_key]
+    subgrids = per_gpu * world
+    import numpy as np
+    from oracle import c_oracle
+    threads = len(os.sched_getaffinity(0))
+    old = c_oracle.init_cells(subgrids)
+    new = np.empty_like(old)
+    mins, sums = np.empty(subgrids), np.empty(subgrids)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        c_oracle.step(old, new, old[-1, -8:].copy(), old[0, :8].copy(), mins, sums,
+                      threads=threads)
+        c_oracle.fsum(sums)
+        float(mins.min())
+        el = time.perf_counter() - t0
+        old, new = new, old
+        if i >= args.warmup:
+            times.append(el)
+    sec = sum(times) / len(times)
+    value = subgrids * 512 / sec
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "cells/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (closed-form ring ICs)",
+        "config": {"workload": desc, "subgrids": subgrids, "cells": subgrids * 512,
+                   "parallelism": f"cpu-openmp-{threads}t"},
+        "cpu_baseline": {"value": value, "unit": "cells/s", "cores": threads,
+                         "kind": "port",
+                         "sample": f"{args.steps} full steps of {subgrids} sub-grids "
+                                   "(oracle/tb_oracle.c: C port of "
+                                   "pkg/src/taskbridge/reference.py:23-50)"},
+        "e2e": {"value": value, "unit": "cells/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__.splitlines()[1])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c4")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--cpu-budget", type=float, default=10.0,
+                    help="seconds of CPU work for the cpu_baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args(argv)
+    args.warmup = max(args.warmup, 3)
+
+    rank = env_int("RANK", 0)
+    world = env_int("WORLD_SIZE", 1)
+    local = env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        return run_reference_arm(args, args.workload, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_2303_08058_b200 import _native as N
+    from paper_2303_08058_b200.ring import RingStepper, run_reference_gpu
+    N.init(local)
+
+    # Parity gate in the same run: the reference's GOLDEN_DEFAULTS.
+    parity = run_reference_gpu(512, 15, device=dev)[0] == GOLDEN_DEFAULTS
+
+    per_gpu, desc = WORKLOADS[args.workload]
+    subgrids = per_gpu * world
+    total_steps = args.warmup + args.steps + args.e2e_steps + 2
+    st = RingStepper(subgrids, device=dev, rank=rank, world=world, max_steps=total_steps,
+                     group=None)
+    n_local = st.n
+    for _ in range(args.warmup):
+        st.step()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.2)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_wall = time.perf_counter()
+    for (s0, s1, k0, k1) in ev:
+        flush.fill_(1)                      # evict L2 (256 MiB > 126 MB)
+        s0.record()
+        st.step(kernel_events=(k0, k1))
+        s1.record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t_wall
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    step_ms = sum(a.elapsed_time(b) for a, b, _, _ in ev) / args.steps
+    k2_ms = sum(c.elapsed_time(d) for _, _, c, d in ev) / args.steps
+    if world > 1:
+        t = torch.tensor([step_ms, k2_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step_ms, k2_ms = t.tolist()
+    cells_total = subgrids * 512
+    value = cells_total / (step_ms * 1e-3)
+
+    # ---- e2e through the host-buffer API (pinned H2D + step + D2H) ------
+    host_in = torch.empty((n_local, 512), dtype=torch.float64, pin_memory=True)
+    host_in.copy_(st.cells)
+    host_stats = torch.empty(2, dtype=torch.float64, pin_memory=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.e2e_steps):
+        st.step_host(host_in, host_in, host_stats)
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / max(args.e2e_steps, 1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = t.item()
+    e2e_value = cells_total / (e2e_ms * 1e-3)
+
+    if rank == 0:
+        peaks, peak_kind = measured_peaks()
+        hbm = float(peaks.get("hbm_gbs", FALLBACK_HBM_GBS))
+        achieved = n_local * 512 * BYTES_PER_CELL / (k2_ms * 1e-3) / 1e9
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "k2_traffic.json")
+        if os.path.exists(tpath):
+            try:
+                with open(tpath) as fh:
+                    tj = json.load(fh)
+                if tj.get("subgrids") == n_local:
+                    traffic = tj.get("dram_bytes_per_launch")
+            except (OSError, ValueError):
+                pass
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            v, cores, nsteps, el = cpu_reference_sample(per_gpu, args.cpu_budget)
+            cpu = {"value": v, "unit": "cells/s", "cores": cores, "kind": "port",
+                   "sample": f"{nsteps} full steps of {per_gpu} sub-grids in {el:.1f}s "
+                             "(oracle/tb_oracle.c, OpenMP)"}
+        line = {
+            "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (closed-form ring ICs, src/miniapp.py:72-77)",
+            "config": {"workload": desc, "subgrids": subgrids, "subgrids_per_gpu": per_gpu,
+                       "cells": cells_total, "parallelism": f"ring-dp{world}",
+                       "l2": "flushed before every timed step (256 MiB write)"},
+            "parity": {"run_reference_512x15_equals_GOLDEN_DEFAULTS": parity},
+            "roofline": {"bound": "hbm", "kernel": "k_step<3,5> (tb_step)",
+                         "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": traffic,
+                         "peak_source": peak_kind,
+                         "bytes_per_cell": BYTES_PER_CELL, "k2_ms": k2_ms},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "cells/s",
+                    "h2d_bytes_per_step": n_local * 512 * 8,
+                    "d2h_bytes_per_step": n_local * 512 * 8 + 16,
+                    "ms_per_step": e2e_ms, "api": "RingStepper.step_host"},
+            "gpu_launches": 2 * args.steps,
+            "clocks": clocks,
+            "wall_s_timed_region": wall,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

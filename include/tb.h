@@ -1,0 +1,203 @@
+/*
+ * tb.h — C ABI of libtb, the B200-native replacement for the reference's
+ * simulated device + per-kind compute closures + poll registry.
+ *
+ * Reference: /root/reference/pkg/src/taskbridge/ (cited below as src/...).
+ * The reference is pure Python; its "device" is a discrete-event simulator
+ * (src/device.py) whose ops carry numpy closures. Each entry point below
+ * replaces one reference interface; the Python host package
+ * (paper_2303_08058_b200/) binds them with ctypes and keeps the reference's
+ * duck types (DeviceQueue / DeviceEvent / VirtualDevice / PollRegistry).
+ *
+ * Conventions
+ *  - extern "C", plain pointers and sizes; no C++ exceptions cross the ABI.
+ *  - Return codes: TB_OK (0); TB_NOT_READY (1) for queries that would block
+ *    or a busy single-entrant guard; negative values are errors:
+ *    -(int)cudaError_t for CUDA failures, TB_E_* for ABI misuse.
+ *  - Device pointers are plain `void*`/`double*` in device memory; host
+ *    staging pointers passed to the async copies should be pinned
+ *    (tb_host_alloc) for true async DMA.
+ *  - Streams are cudaStream_t values carried as uint64 (tb_stream_t); 0 is
+ *    the legacy default stream. Events are pooled cudaEvent_t
+ *    (cudaEventDisableTiming) carried as tb_event_t.
+ *  - Every kernel is hand-written for sm_100a (csrc/tb_kernels.cu).
+ */
+#ifndef TB_H_
+#define TB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TB_ABI_VERSION 1
+
+#define TB_OK 0
+#define TB_NOT_READY 1
+#define TB_E_INVALID (-10000)   /* bad argument (null pointer, n < 0, ...) */
+#define TB_E_NOMEM (-10001)     /* host-side allocation failed             */
+#define TB_E_CLOSED (-10002)    /* object already destroyed/closed         */
+
+/* Workload geometry (src/miniapp.py:30-37). */
+#define TB_CELLS 512            /* 8x8x8 cells per sub-grid                */
+#define TB_FACE 8               /* flat ring face: first/last 8 cells      */
+#define TB_KINDS 5              /* kernel kinds with fixed (C1, C2)        */
+
+/* Exact step accumulator (replaces math.fsum, src/miniapp.py:168-169, and the
+ * min-tree, src/miniapp.py:138-149). Layout in int64 words:
+ *   [0, TB_ACC_LIMBS)  signed 32-bit digits of sum(x) * 2^1074, carry-save
+ *   TB_ACC_MIN_WORD    order-preserving int64 key of min(x)
+ * Multi-GPU: all-reduce words [0, TB_ACC_LIMBS) with SUM and word
+ * TB_ACC_MIN_WORD with MIN (int64); the result is partition-independent. */
+#define TB_ACC_LIMBS 68
+#define TB_ACC_BIAS 1074
+#define TB_ACC_MIN_WORD 68
+#define TB_ACC_WORDS 72         /* padded to a 64-byte multiple            */
+
+/* Kernel descriptor ops for tb_launch / tb_agg_launch (what a registered
+ * kind's transform does; src/executors.py:171-172, src/miniapp.py:40-53). */
+#define TB_OP_NONE 0            /* launch an empty kernel (timing-only op) */
+#define TB_OP_KIND 1            /* x = x*C1[kind] + C2[kind], two roundings */
+#define TB_OP_AFFINE 2          /* x = x*c1 + c2, two roundings             */
+
+typedef uint64_t tb_stream_t;
+typedef uint64_t tb_event_t;
+typedef uint64_t tb_poll_t;     /* native poll registry handle             */
+typedef uint64_t tb_htq_t;      /* host-task queue handle                  */
+
+/* ------------------------------------------------------------ device -- */
+int tb_abi_version(void);
+const char *tb_error_string(int rc);
+/* VirtualDevice.__init__ (src/device.py:205-257): bind the calling thread to
+ * `device` (cudaSetDevice) and warm the event pool. */
+int tb_init(int device);
+int tb_device_count(int *n);
+int tb_sm_count(int device, int *n);
+int tb_device_sync(void);
+
+/* ------------------------------------------------------------ queues -- */
+/* VirtualDevice.queue() (src/device.py:259-264): one in-order queue. */
+int tb_stream_create(tb_stream_t *s);
+int tb_stream_destroy(tb_stream_t s);
+/* DeviceQueue.incomplete_count() > 0 (src/device.py:179-180): TB_OK when
+ * idle, TB_NOT_READY while work is outstanding. */
+int tb_stream_query(tb_stream_t s);
+int tb_stream_sync(tb_stream_t s);
+
+/* ------------------------------------------------------------ events -- */
+/* DeviceQueue.submit(op) -> DeviceEvent (src/device.py:176-177, 116): record a
+ * pooled event after everything queued so far. Also the DUMMY queue marker of
+ * Integration.get_future_queue (src/bridge.py:92-101). */
+int tb_event_record(tb_stream_t s, tb_event_t *ev);
+/* DeviceEvent.is_complete() (src/device.py:102-103): TB_OK when complete,
+ * TB_NOT_READY otherwise. Never blocks. */
+int tb_event_query(tb_event_t ev);
+/* VirtualDevice.event_wait (src/device.py:281-309): block until complete
+ * (the FENCE baseline). */
+int tb_event_wait(tb_event_t ev);
+int tb_event_release(tb_event_t ev);
+int tb_stream_wait_event(tb_stream_t s, tb_event_t ev);
+/* VirtualDevice(event_pool=...) (src/device.py:221,410-411): 1 = recycle
+ * events through the pool, 0 = create/destroy per record (ablation). */
+int tb_event_pool_set(int enabled);
+int tb_event_pool_stats(int64_t *created, int64_t *reused, int64_t *live);
+
+/* ------------------------------------------------------------ memory -- */
+int tb_malloc(void **p, size_t n);
+int tb_free(void *p);
+int tb_host_alloc(void **p, size_t n);       /* pinned host memory         */
+int tb_host_free(void *p);
+/* make_h2d / make_d2h compute closures (src/executors.py:278-279, 283-284). */
+int tb_memcpy_h2d(tb_stream_t s, void *dst, const void *src, size_t n);
+int tb_memcpy_d2h(tb_stream_t s, void *dst, const void *src, size_t n);
+int tb_memcpy_d2d(tb_stream_t s, void *dst, const void *src, size_t n);
+int tb_memset(tb_stream_t s, void *p, int value, size_t n);
+
+/* ----------------------------------------------------------- kernels -- */
+/* K1: kernel_transform(kind)(view) (src/miniapp.py:40-53) on n doubles in
+ * place: x = __dadd_rn(__dmul_rn(x, C1[kind]), C2[kind]). */
+int tb_transform(tb_stream_t s, int kind, double *d, int64_t n);
+/* A registered kind's transform (src/executors.py:171-172) as a descriptor:
+ * op = TB_OP_NONE | TB_OP_KIND | TB_OP_AFFINE. */
+int tb_launch(tb_stream_t s, int op, int kind, double c1, double c2, double *d,
+              int64_t n);
+/* make_barrier() (src/device.py:136-137): an empty ordering kernel. */
+int tb_barrier(tb_stream_t s);
+/* Keep a queue busy for `ns` nanoseconds (stands in for the reference tests'
+ * long make_kernel(100_000) gate ops, pkg/tests/test_executors.py:129). */
+int tb_spin(tb_stream_t s, int64_t ns);
+/* SubGrid.__init__ (src/miniapp.py:72-77) for sub-grids [lo, lo+n) of S:
+ * cells[g][i] = ((lo+g)*1000 + i) / (S*1000 + 512), correctly rounded. */
+int tb_init_cells(tb_stream_t s, double *cells, int64_t subgrids, int64_t lo,
+                  int64_t n);
+
+/* One AggregationExecutor batch (src/executors.py:257-284) as one call:
+ * H2D(dbuf <- hbuf) ; kernel(op, kind, c1, c2) over nbytes/8 doubles ;
+ * [barrier if barrier != 0] ; D2H(hbuf <- dbuf) ; record *done.
+ * hbuf holds the marshalled members on entry and the landing on completion. */
+int tb_agg_launch(tb_stream_t s, int op, int kind, double c1, double c2,
+                  double *dbuf, double *hbuf, size_t nbytes, int barrier,
+                  tb_event_t *done);
+
+/* K2: one fused time step over n consecutive sub-grids (src/miniapp.py:116-133
+ * per sub-grid == src/reference.py:31-47): ghost fold against the previous
+ * generation, chains x kernels_per_chain transforms, per-sub-grid min and
+ * numpy-order pairwise sum. old/out: [n][512] doubles (out != old).
+ * left_face: 8 doubles, right face of the sub-grid before old[0];
+ * right_face: 8 doubles, left face of the sub-grid after old[n-1] (pass
+ * old+(n-1)*512+504 and old for a full single-device ring).
+ * mins/sums: optional [n] outputs (NULL to skip).
+ * acc: optional TB_ACC_WORDS accumulator; the step's exact sum and min are
+ * added into it (NULL to skip). */
+int tb_step(tb_stream_t s, const double *old, double *out, int64_t n,
+            const double *left_face, const double *right_face, int chains,
+            int kernels_per_chain, double *mins, double *sums, int64_t *acc);
+/* Zero an accumulator (limbs = 0, min = +inf). */
+int tb_acc_reset(tb_stream_t s, int64_t *acc);
+/* Exact sum of n doubles into acc (the reduction half of tb_step). */
+int tb_acc_add(tb_stream_t s, const double *x, int64_t n, int64_t *acc);
+/* Close a step (src/miniapp.py:164-171 + :227): piece = correctly rounded
+ * sum (== math.fsum), dt = min; if checksum != NULL: *checksum += piece.
+ * Outputs are device pointers (any may be NULL). reset != 0 re-zeroes acc. */
+int tb_acc_finalize(tb_stream_t s, int64_t *acc, double *piece, double *dt,
+                    double *checksum, int reset);
+
+/* -------------------------------------------------- poll registry -- */
+/* PollRegistry (src/runtime/polling.py:17-147): a lock-free MPSC inbox of
+ * (event, token) and a poll-owned pending vector, drained by a single-entrant
+ * poll body that queries events with cudaEventQuery. */
+int tb_poll_create(tb_poll_t *reg);
+int tb_poll_destroy(tb_poll_t reg);
+/* PollRegistry.add (polling.py:53-55): any thread, lock-free. */
+int tb_poll_add(tb_poll_t reg, tb_event_t ev, uint64_t token);
+/* PollRegistry.poll (polling.py:80-120): drain inbox, re-check pending,
+ * write up to cap fired tokens. TB_NOT_READY (and *nfired = 0) when another
+ * thread holds the guard. Complete entries beyond cap stay pending. */
+int tb_poll(tb_poll_t reg, uint64_t *fired, int cap, int *nfired);
+int tb_poll_pending(tb_poll_t reg, int64_t *n);
+/* abandon_all (polling.py:122-147): remove every entry; complete[i] says
+ * whether token i's event had completed (run callback) or not (abandon). */
+int tb_poll_drain(tb_poll_t reg, uint64_t *tokens, uint8_t *complete, int cap,
+                  int *n);
+int tb_poll_entry_high_water(tb_poll_t reg, int *hw);
+
+/* ---------------------------------------------------- host tasks -- */
+/* VirtualDevice.register_host_task (src/device.py:311-321) and its
+ * dispatcher threads (src/device.py:541-567): after `ev` completes on the
+ * device, `token` becomes available to tb_htq_next. Implemented with
+ * cudaStreamWaitEvent + cudaLaunchHostFunc on side streams owned by the
+ * queue; the CUDA callback only enqueues (no CUDA calls, no Python). */
+int tb_htq_create(int side_streams, tb_htq_t *q);
+int tb_host_task(tb_htq_t q, tb_event_t ev, uint64_t token);
+/* Block up to timeout_us for the next ready token: TB_OK / TB_NOT_READY
+ * (timeout) / TB_E_CLOSED (closed and empty). */
+int tb_htq_next(tb_htq_t q, uint64_t *token, int64_t timeout_us);
+int tb_htq_close(tb_htq_t q);
+int tb_htq_destroy(tb_htq_t q);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TB_H_ */

@@ -1,0 +1,224 @@
+"""Device-resident sub-grid ring: the whole time step on the GPU.
+
+Data layout in HBM (per rank): two contiguous ``double[n_local][512]`` state
+generations (4 KiB per sub-grid, 256-B aligned — the reference keeps one
+numpy array per sub-grid, src/miniapp.py:77,87), a 72-word int64 step
+accumulator (include/tb.h TB_ACC_*), a 2x8 halo of ring-neighbour faces and
+per-step ``(piece, dt)`` records plus the running checksum.
+
+One step = K2 (``tb_step``: ghost fold + 15 transforms + per-sub-grid min and
+pairwise sum folded into the exact accumulator) + K4 (``tb_acc_finalize``:
+correctly rounded piece, dt, ``checksum += piece``). Bit-identical to
+``run_reference`` (src/reference.py:23-50) at any rank count.
+
+Multi-GPU (one process per GPU, torch.distributed/NCCL): the ring is split
+into contiguous ranges; per step each rank sends its first sub-grid's left
+face to rank-1 and its last sub-grid's right face to rank+1 (64 B each, from
+the previous generation — Jacobi, src/miniapp.py:89-93), then after K2 the
+accumulator's limbs are all-reduced with SUM and its min word with MIN
+(int64): exact, so every partition gives the single-device checksum.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import List, Optional, Tuple
+
+import torch
+
+from . import _native as N
+
+CELLS = N.TB_CELLS
+FACE = N.TB_FACE
+
+
+def ring_partition(subgrids: int, world: int, rank: int) -> Tuple[int, int]:
+    """Contiguous, balanced [lo, hi) range of sub-grid ids owned by ``rank``."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    if subgrids < world:
+        raise ValueError(f"{subgrids} sub-grids cannot be split over {world} ranks")
+    base, extra = divmod(subgrids, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def _ptr(t: torch.Tensor) -> int:
+    return t.data_ptr()
+
+
+class CudaRingOps:
+    """The product kernels (libtb) behind the stepper's five primitives."""
+
+    def __init__(self, device: torch.device):
+        if device.type != "cuda":
+            raise RuntimeError("CudaRingOps needs a CUDA device (no CPU fallback)")
+        N.init(device.index or 0)
+        self.device = device
+
+    def stream(self) -> int:
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def init_cells(self, cells: torch.Tensor, subgrids: int, lo: int) -> None:
+        N.call("tb_init_cells", self.stream(), _ptr(cells), subgrids, lo, cells.shape[0])
+
+    def step(self, old, out, left_face, right_face, chains, kpc, acc,
+             mins=None, sums=None) -> None:
+        N.call("tb_step", self.stream(), _ptr(old), _ptr(out), old.shape[0],
+               _ptr(left_face), _ptr(right_face), chains, kpc,
+               None if mins is None else _ptr(mins),
+               None if sums is None else _ptr(sums), _ptr(acc))
+
+    def acc_reset(self, acc) -> None:
+        N.call("tb_acc_reset", self.stream(), _ptr(acc))
+
+    def acc_finalize(self, acc, piece, dt, checksum) -> None:
+        N.call("tb_acc_finalize", self.stream(), _ptr(acc), _ptr(piece), _ptr(dt),
+               _ptr(checksum), 1)
+
+
+@dataclass
+class RingResult:
+    checksum: float
+    dts: List[float]
+    pieces: List[float]
+
+
+class RingStepper:
+    """Runs the sub-grid ring for ``steps`` time steps on this rank's device.
+
+    ``group`` is a torch.distributed process group (None: single device, or
+    the default group when ``world > 1``). ``ops`` defaults to the libtb
+    kernels; tests substitute a CPU double to cover the multi-rank host logic
+    under gloo.
+    """
+
+    def __init__(self, subgrids: int, device: Optional[torch.device] = None,
+                 rank: int = 0, world: int = 1, chains: int = 3,
+                 kernels_per_chain: int = 5, max_steps: int = 1 << 16,
+                 ops=None, group=None, collect_subgrid_stats: bool = False):
+        if subgrids < 1:
+            raise ValueError("subgrids must be >= 1")
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        self.device = device
+        self.ops = ops if ops is not None else CudaRingOps(device)
+        self.subgrids, self.rank, self.world = subgrids, rank, world
+        self.chains, self.kpc = chains, kernels_per_chain
+        self.group = group
+        self.lo, self.hi = ring_partition(subgrids, world, rank)
+        n = self.n = self.hi - self.lo
+        f64 = dict(dtype=torch.float64, device=device)
+        self.state = [torch.empty((n, CELLS), **f64), torch.empty((n, CELLS), **f64)]
+        self.cur = 0
+        self.acc = torch.zeros(N.TB_ACC_WORDS, dtype=torch.int64, device=device)
+        self.halo = torch.zeros((2, FACE), **f64)        # [left ghost, right ghost]
+        self.max_steps = max_steps
+        self.pieces = torch.zeros(max_steps, **f64)
+        self.dts = torch.zeros(max_steps, **f64)
+        self.checksum = torch.zeros(1, **f64)
+        self.mins = torch.empty(n, **f64) if collect_subgrid_stats else None
+        self.sums = torch.empty(n, **f64) if collect_subgrid_stats else None
+        self.steps_done = 0
+        self.ops.init_cells(self.state[0], subgrids, self.lo)
+        self.ops.acc_reset(self.acc)
+
+    # -------------------------------------------------------------- state --
+    @property
+    def cells(self) -> torch.Tensor:
+        """This rank's current generation, [n_local, 512] (device)."""
+        return self.state[self.cur]
+
+    def load_cells(self, host: torch.Tensor) -> None:
+        """Replace the current generation with ``host`` ([n_local, 512])."""
+        self.state[self.cur].copy_(host, non_blocking=True)
+
+    # --------------------------------------------------------------- step --
+    def _exchange_halo(self, old: torch.Tensor) -> Tuple[torch.Tensor, torch.Tensor]:
+        if self.world == 1:
+            # single-device ring: wrap within this rank
+            return old[self.n - 1, CELLS - FACE:], old[0, :FACE]
+        import torch.distributed as dist
+        left = (self.rank - 1) % self.world
+        right = (self.rank + 1) % self.world
+        # Issue order makes N=2 (left == right) unambiguous: the first message
+        # from a peer is its LEFT face (-> my right ghost), the second its
+        # RIGHT face (-> my left ghost).
+        ops = [dist.P2POp(dist.isend, old[0, :FACE], left, self.group),
+               dist.P2POp(dist.irecv, self.halo[1], right, self.group),
+               dist.P2POp(dist.isend, old[self.n - 1, CELLS - FACE:], right, self.group),
+               dist.P2POp(dist.irecv, self.halo[0], left, self.group)]
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+        return self.halo[0], self.halo[1]
+
+    def _reduce_acc(self) -> None:
+        if self.world == 1:
+            return
+        import torch.distributed as dist
+        dist.all_reduce(self.acc[:N.TB_ACC_LIMBS], op=dist.ReduceOp.SUM, group=self.group)
+        dist.all_reduce(self.acc[N.TB_ACC_MIN_WORD:N.TB_ACC_MIN_WORD + 1],
+                        op=dist.ReduceOp.MIN, group=self.group)
+
+    def step(self, kernel_events=None) -> None:
+        """Advance one time step (asynchronous on the current stream).
+
+        ``kernel_events``: optional (start, end) CUDA events recorded around
+        the fused K2 launch alone (bench.py uses them for the roofline).
+        """
+        if self.steps_done >= self.max_steps:
+            raise RuntimeError("max_steps exceeded; raise max_steps")
+        old, out = self.state[self.cur], self.state[1 - self.cur]
+        lf, rf = self._exchange_halo(old)
+        if kernel_events is not None:
+            kernel_events[0].record()
+        self.ops.step(old, out, lf, rf, self.chains, self.kpc, self.acc,
+                      self.mins, self.sums)
+        if kernel_events is not None:
+            kernel_events[1].record()
+        self._reduce_acc()
+        k = self.steps_done
+        self.ops.acc_finalize(self.acc, self.pieces[k:k + 1], self.dts[k:k + 1],
+                              self.checksum)
+        self.cur = 1 - self.cur
+        self.steps_done += 1
+
+    def step_host(self, host_in: torch.Tensor, host_out: torch.Tensor,
+                  host_stats: torch.Tensor) -> None:
+        """One step on host-resident cells (the drop-in, host-buffer path).
+
+        ``host_in``/``host_out``: pinned [n_local, 512] float64 (may alias);
+        ``host_stats``: pinned float64[2] receiving (piece, dt). Enqueues the
+        H2D of the input generation, the step, and the D2H of the new
+        generation and its reductions on the current stream; the caller
+        synchronises before reading host_out/host_stats.
+        """
+        self.state[self.cur].copy_(host_in, non_blocking=True)
+        k = self.steps_done
+        self.step()
+        host_out.copy_(self.state[self.cur], non_blocking=True)
+        host_stats[0:1].copy_(self.pieces[k:k + 1], non_blocking=True)
+        host_stats[1:2].copy_(self.dts[k:k + 1], non_blocking=True)
+
+    def run(self, steps: int) -> RingResult:
+        k0 = self.steps_done
+        for _ in range(steps):
+            self.step()
+        return self.result(k0)
+
+    def result(self, first_step: int = 0) -> RingResult:
+        k = self.steps_done
+        return RingResult(checksum=float(self.checksum.item()),
+                          dts=self.dts[first_step:k].tolist(),
+                          pieces=self.pieces[first_step:k].tolist())
+
+
+def run_reference_gpu(subgrids: int, steps: int, chains: int = 3,
+                      kernels_per_chain: int = 5,
+                      device: Optional[torch.device] = None) -> Tuple[float, List[float]]:
+    """Drop-in for ``run_reference(subgrids, steps)`` (src/reference.py:23)
+    computed on the GPU: returns (checksum, dts)."""
+    st = RingStepper(subgrids, device=device, chains=chains,
+                     kernels_per_chain=kernels_per_chain, max_steps=max(steps, 1))
+    res = st.run(steps)
+    return res.checksum, res.dts
