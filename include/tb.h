@@ -49,11 +49,13 @@ extern "C" {
  * min-tree, src/miniapp.py:138-149). Layout in int64 words:
  *   [0, TB_ACC_LIMBS)  signed 32-bit digits of sum(x) * 2^1074, carry-save
  *   TB_ACC_MIN_WORD    order-preserving int64 key of min(x)
+ *   TB_ACC_COUNT_WORD  finished-CTA ticket used by tb_step_final
  * Multi-GPU: all-reduce words [0, TB_ACC_LIMBS) with SUM and word
  * TB_ACC_MIN_WORD with MIN (int64); the result is partition-independent. */
 #define TB_ACC_LIMBS 68
 #define TB_ACC_BIAS 1074
 #define TB_ACC_MIN_WORD 68
+#define TB_ACC_COUNT_WORD 70    /* CTA ticket for the fused finalize        */
 #define TB_ACC_WORDS 72         /* padded to a 64-byte multiple            */
 
 /* Kernel descriptor ops for tb_launch / tb_agg_launch (what a registered
@@ -61,6 +63,12 @@ extern "C" {
 #define TB_OP_NONE 0            /* launch an empty kernel (timing-only op) */
 #define TB_OP_KIND 1            /* x = x*C1[kind] + C2[kind], two roundings */
 #define TB_OP_AFFINE 2          /* x = x*c1 + c2, two roundings             */
+
+/* tb_set_option keys/values. */
+#define TB_OPT_STEP_IMPL 1      /* which K2 variant tb_step launches        */
+#define TB_STEP_AUTO 0          /* bulk-copy ring when aligned, (3,5) chain */
+#define TB_STEP_REG 1           /* direct ld.global.nc into registers       */
+#define TB_STEP_BULK 2          /* cp.async.bulk smem ring + mbarriers      */
 
 typedef uint64_t tb_stream_t;
 typedef uint64_t tb_event_t;
@@ -76,6 +84,8 @@ int tb_init(int device);
 int tb_device_count(int *n);
 int tb_sm_count(int device, int *n);
 int tb_device_sync(void);
+/* Process-wide tuning switches (ablations), e.g. TB_OPT_STEP_IMPL. */
+int tb_set_option(int key, int value);
 
 /* ------------------------------------------------------------ queues -- */
 /* VirtualDevice.queue() (src/device.py:259-264): one in-order queue. */
@@ -154,6 +164,14 @@ int tb_agg_launch(tb_stream_t s, int op, int kind, double c1, double c2,
 int tb_step(tb_stream_t s, const double *old, double *out, int64_t n,
             const double *left_face, const double *right_face, int chains,
             int kernels_per_chain, double *mins, double *sums, int64_t *acc);
+/* tb_step with the step closed in the same launch (single device): the last
+ * CTA to finish rounds the accumulator exactly as tb_acc_finalize(..., reset=1)
+ * would and writes piece / dt / checksum (device pointers, may be NULL).
+ * acc is required and must be reset (tb_acc_reset) before the first use. */
+int tb_step_final(tb_stream_t s, const double *old, double *out, int64_t n,
+                  const double *left_face, const double *right_face, int chains,
+                  int kernels_per_chain, double *mins, double *sums, int64_t *acc,
+                  double *piece, double *dt, double *checksum);
 /* Zero an accumulator (limbs = 0, min = +inf). */
 int tb_acc_reset(tb_stream_t s, int64_t *acc);
 /* Exact sum of n doubles into acc (the reduction half of tb_step). */

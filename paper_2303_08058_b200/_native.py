@@ -30,7 +30,13 @@ TB_KINDS = 5
 TB_ACC_LIMBS = 68
 TB_ACC_BIAS = 1074
 TB_ACC_MIN_WORD = 68
+TB_ACC_COUNT_WORD = 70
 TB_ACC_WORDS = 72
+
+TB_OPT_STEP_IMPL = 1
+TB_STEP_AUTO = 0
+TB_STEP_REG = 1
+TB_STEP_BULK = 2
 
 TB_OP_NONE = 0
 TB_OP_KIND = 1
@@ -71,6 +77,7 @@ SIGNATURES = {
     "tb_device_count": [_pint],
     "tb_sm_count": [_int, _pint],
     "tb_device_sync": [],
+    "tb_set_option": [_int, _int],
     "tb_stream_create": [_pu64],
     "tb_stream_destroy": [_u64],
     "tb_stream_query": [_u64],
@@ -97,6 +104,8 @@ SIGNATURES = {
     "tb_init_cells": [_u64, _vp, _i64, _i64, _i64],
     "tb_agg_launch": [_u64, _int, _int, _dbl, _dbl, _vp, _vp, _szt, _int, _pu64],
     "tb_step": [_u64, _vp, _vp, _i64, _vp, _vp, _int, _int, _vp, _vp, _vp],
+    "tb_step_final": [_u64, _vp, _vp, _i64, _vp, _vp, _int, _int, _vp, _vp, _vp, _vp, _vp,
+                      _vp],
     "tb_acc_reset": [_u64, _vp],
     "tb_acc_add": [_u64, _vp, _i64, _vp],
     "tb_acc_finalize": [_u64, _vp, _vp, _vp, _vp, _int],

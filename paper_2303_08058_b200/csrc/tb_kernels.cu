@@ -1,13 +1,18 @@
 // tb_kernels.cu — sm_100a kernels for the sub-grid step path.
 //
-// K1  k_launch      : kernel_transform(kind) / registered affine kinds on a
-//                     fused staging buffer (src/miniapp.py:40-53,
-//                     src/executors.py:257-284). HBM-bound, 16 B per cell.
-// K2  k_step        : one fused time step over many sub-grids, one warp per
-//                     sub-grid (src/miniapp.py:116-133 == src/reference.py:31-47),
-//                     with the step's exact sum and min folded into a
-//                     superaccumulator (src/miniapp.py:138-171).
-// K4  k_acc_finalize: correctly rounded sum (== math.fsum) + dt + checksum.
+// K1  k_launch       : kernel_transform(kind) / registered affine kinds on a
+//                      fused staging buffer (src/miniapp.py:40-53,
+//                      src/executors.py:257-284). HBM-bound, 16 B per cell.
+// K2  k_step[_bulk]  : one fused time step over many sub-grids, one warp per
+//                      sub-grid (src/miniapp.py:116-133 == src/reference.py:31-47),
+//                      the step's exact sum and min folded into a
+//                      superaccumulator (src/miniapp.py:138-171); optionally the
+//                      last CTA closes the step (K4 fused).
+//                      k_step      : direct ld.global.nc into registers;
+//                      k_step_bulk : per-warp ring of shared-memory slots fed by
+//                                    the bulk-copy (TMA) engine + mbarriers.
+// K4  k_acc_finalize : correctly rounded sum (== math.fsum) + dt + checksum,
+//                      one warp.
 //
 // Bit-exactness (SURVEY.md §7 hard part 1): every transform is
 // __dmul_rn followed by __dadd_rn — never an FMA; the per-sub-grid sum is
@@ -36,6 +41,12 @@ __device__ __forceinline__ double xform(double x, double c1, double c2) {
 __device__ __forceinline__ double ld_stream(const double *p) {
   double v;
   asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ long long ld_cg_s64(const int64_t *p) {
+  long long v;
+  asm volatile("ld.global.cg.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
 
@@ -96,6 +107,8 @@ __device__ __forceinline__ double key_to_double(long long k) {
   return __longlong_as_double(k >= 0 ? k : (k ^ 0x7fffffffffffffffLL));
 }
 
+constexpr long long kKeyInf = 0x7ff0000000000000LL;   // min_key(+inf)
+
 // Add x exactly into 32-bit-digit int64 limbs (digit i weighs 2^(32i-1074)).
 // x = mant * 2^(p - 1074) with p = biased exponent - 1 (0 for subnormals).
 __device__ __forceinline__ void acc_add_digits(unsigned long long *limbs, double x) {
@@ -120,110 +133,13 @@ __device__ __forceinline__ void acc_add_digits(unsigned long long *limbs, double
 
 // Flush a block's shared limbs + min key into the global accumulator.
 __device__ __forceinline__ void acc_flush(const unsigned long long *s_limbs,
-                                          long long block_min_key,
-                                          int64_t *acc) {
+                                          long long block_min_key, int64_t *acc) {
   for (int i = threadIdx.x; i < TB_ACC_LIMBS; i += blockDim.x) {
     const unsigned long long v = s_limbs[i];
     if (v) atomicAdd(reinterpret_cast<unsigned long long *>(acc) + i, v);
   }
   if (threadIdx.x == 0)
     atomicMin(reinterpret_cast<long long *>(acc) + TB_ACC_MIN_WORD, block_min_key);
-}
-
-// ------------------------------------------------------------------ K2 --
-constexpr int kStepThreads = 256;
-constexpr int kStepWarps = kStepThreads / 32;
-
-template <int CHAINS, int KPC>
-__device__ __forceinline__ void run_chains(double (&v)[16], int chains, int kpc) {
-  if (CHAINS > 0) {
-#pragma unroll
-    for (int c = 0; c < CHAINS; ++c)
-#pragma unroll
-      for (int k = 0; k < KPC; ++k) {
-        const double c1 = kC1[k], c2 = kC2[k];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = xform(v[i], c1, c2);
-      }
-  } else {
-    for (int c = 0; c < chains; ++c)
-      for (int k = 0; k < kpc; ++k) {
-        const double c1 = kC1[k], c2 = kC2[k];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = xform(v[i], c1, c2);
-      }
-  }
-}
-
-template <int CHAINS, int KPC>
-__global__ void __launch_bounds__(kStepThreads)
-    k_step(const double *__restrict__ old, double *__restrict__ out, int64_t n,
-           const double *__restrict__ left_face, const double *__restrict__ right_face,
-           int chains, int kpc, double *__restrict__ mins, double *__restrict__ sums,
-           int64_t *__restrict__ acc) {
-  __shared__ unsigned long long s_limbs[TB_ACC_LIMBS];
-  __shared__ long long s_min[kStepWarps];
-  if (acc) {
-    for (int i = threadIdx.x; i < TB_ACC_LIMBS; i += blockDim.x) s_limbs[i] = 0ULL;
-    __syncthreads();
-  }
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int r = lane & 7;                 // accumulator within a 128-block
-  const int lane_off = 128 * (lane >> 3) + r;
-  double wmin = CUDART_INF;
-
-  for (int64_t g = (int64_t)blockIdx.x * kStepWarps + warp; g < n;
-       g += (int64_t)gridDim.x * kStepWarps) {
-    const double *src = old + g * TB_CELLS + lane_off;
-    double v[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = ld_stream(src + 8 * i);
-    // Ghost fold against the previous generation (src/miniapp.py:119-126):
-    // cells 0..7 are lanes 0..7 at i = 0; cells 504..511 are lanes 24..31 at
-    // i = 15. The add rounds; the *0.5 is exact.
-    if (lane < 8) {
-      const double *lf =
-          g == 0 ? left_face : old + (g - 1) * TB_CELLS + (TB_CELLS - TB_FACE);
-      v[0] = __dmul_rn(0.5, __dadd_rn(v[0], lf[r]));
-    } else if (lane >= 24) {
-      const double *rf = g == n - 1 ? right_face : old + (g + 1) * TB_CELLS;
-      v[15] = __dmul_rn(0.5, __dadd_rn(v[15], rf[r]));
-    }
-    run_chains<CHAINS, KPC>(v, chains, kpc);
-    double *dst = out + g * TB_CELLS + lane_off;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) dst[8 * i] = v[i];
-
-    // numpy pairwise sum: r_j = a[j] + a[j+8] + ... (sequential), then
-    // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) per block, (B0+B1)+(B2+B3).
-    double s = v[0];
-    double m = v[0];
-#pragma unroll
-    for (int i = 1; i < 16; ++i) {
-      s = __dadd_rn(s, v[i]);
-      m = fmin(m, v[i]);
-    }
-#pragma unroll
-    for (int x = 1; x < 32; x <<= 1) {
-      s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, x));
-      m = fmin(m, __shfl_xor_sync(0xffffffffu, m, x));
-    }
-    if (lane == 0) {
-      if (sums) sums[g] = s;
-      if (mins) mins[g] = m;
-      if (acc) acc_add_digits(s_limbs, s);
-    }
-    wmin = fmin(wmin, m);
-  }
-  if (acc) {
-    if (lane == 0) s_min[warp] = min_key(wmin);
-    __syncthreads();
-    long long bm = s_min[0];
-#pragma unroll
-    for (int w = 1; w < kStepWarps; ++w) bm = min(bm, s_min[w]);
-    acc_flush(s_limbs, bm, acc);
-  }
 }
 
 // Exact sum of an arbitrary vector into acc (the reduction half of K2).
@@ -251,78 +167,408 @@ __global__ void __launch_bounds__(256) k_acc_add(const double *__restrict__ x,
 
 __global__ void k_acc_reset(int64_t *acc) {
   for (int i = threadIdx.x; i < TB_ACC_WORDS; i += blockDim.x)
-    acc[i] = (i == TB_ACC_MIN_WORD) ? 0x7ff0000000000000LL /* key(+inf) */ : 0;
+    acc[i] = (i == TB_ACC_MIN_WORD) ? kKeyInf : 0;
 }
 
-// Correctly rounded (half-even) value of the exact sum held in the limbs.
-__device__ double acc_round(const int64_t *acc) {
-  constexpr int ND = TB_ACC_LIMBS + 2;
-  uint32_t d[ND];
-  long long carry = 0;
-  for (int i = 0; i < TB_ACC_LIMBS; ++i) {
-    const long long v = acc[i] + carry;      // |acc[i]| < 2^62 by construction
-    d[i] = (uint32_t)(v & 0xffffffffLL);
-    carry = v >> 32;                         // arithmetic shift
-  }
-  d[TB_ACC_LIMBS] = (uint32_t)(carry & 0xffffffffLL);
-  d[TB_ACC_LIMBS + 1] = (uint32_t)((carry >> 32) & 0xffffffffLL);
-  const bool neg = (d[ND - 1] >> 31) & 1u;
-  if (neg) {
-    unsigned long long c = 1;
-    for (int i = 0; i < ND; ++i) {
-      const unsigned long long v = (unsigned long long)(uint32_t)~d[i] + c;
-      d[i] = (uint32_t)v;
-      c = v >> 32;
+// ------------------------------------------------------ step finalize --
+// Correctly rounded (half-even) value of the exact sum in the limbs, plus dt
+// and the running checksum, computed by ONE full warp. Only the carry chain
+// over the occupied limbs [lo, hi] is sequential (a few limbs for real data);
+// sign, leading-digit search, window and sticky bit are warp-parallel.
+constexpr int kDigits = 96;   // >= TB_ACC_LIMBS + carry growth; 3 per lane
+
+__device__ void warp_finalize(int64_t *acc, double *piece, double *dt,
+                              double *checksum, int reset, uint32_t *dig) {
+  const int lane = threadIdx.x & 31;
+  const unsigned full = 0xffffffffu;
+  const long long a0 = ld_cg_s64(acc + lane);
+  const long long a1 = ld_cg_s64(acc + lane + 32);
+  const long long a2 = (lane + 64 < TB_ACC_LIMBS) ? ld_cg_s64(acc + lane + 64) : 0;
+  const unsigned n0 = __ballot_sync(full, a0 != 0), n1 = __ballot_sync(full, a1 != 0),
+                 n2 = __ballot_sync(full, a2 != 0);
+  double p = 0.0;
+  if (n0 | n1 | n2) {
+    const int lo = n0 ? __ffs(n0) - 1 : (n1 ? 31 + __ffs(n1) : 63 + __ffs(n2));
+    const int hi = n2 ? 95 - __clz(n2) : (n1 ? 63 - __clz(n1) : 31 - __clz(n0));
+    for (int i = lane; i < kDigits; i += 32) dig[i] = 0u;
+    __syncwarp();
+    int neg = 0;
+    if (lane == 0) {
+      long long carry = 0;
+      int i = lo;
+      for (; i < kDigits; ++i) {
+        const long long v = (i <= hi ? ld_cg_s64(acc + i) : 0LL) + carry;
+        dig[i] = (uint32_t)(v & 0xffffffffLL);
+        carry = v >> 32;   // arithmetic shift
+        if (i >= hi && (carry == 0 || carry == -1)) break;
+      }
+      neg = carry < 0;
+      if (neg)
+        for (int k = i + 1; k < kDigits; ++k) dig[k] = 0xffffffffu;
+    }
+    neg = __shfl_sync(full, neg, 0);
+    __syncwarp();
+    uint32_t m0 = dig[lane], m1 = dig[lane + 32], m2 = dig[lane + 64];
+    if (neg) {  // magnitude = two's complement negation, digit-parallel
+      const unsigned z0 = __ballot_sync(full, m0 != 0), z1 = __ballot_sync(full, m1 != 0),
+                     z2 = __ballot_sync(full, m2 != 0);
+      const int z = z0 ? __ffs(z0) - 1 : (z1 ? 31 + __ffs(z1) : 63 + __ffs(z2));
+      auto negd = [&](uint32_t d, int idx) -> uint32_t {
+        return idx < z ? 0u : (idx == z ? (uint32_t)(0u - d) : ~d);
+      };
+      m0 = negd(m0, lane);
+      m1 = negd(m1, lane + 32);
+      m2 = negd(m2, lane + 64);
+    }
+    const unsigned t0 = __ballot_sync(full, m0 != 0), t1 = __ballot_sync(full, m1 != 0),
+                   t2 = __ballot_sync(full, m2 != 0);
+    const int top = t2 ? 95 - __clz(t2) : (t1 ? 63 - __clz(t1) : 31 - __clz(t0));
+    auto digit = [&](int k) -> uint32_t {   // warp-collective fetch of digit k
+      const int kk = k < 0 ? 0 : k;
+      const uint32_t a = __shfl_sync(full, m0, kk & 31), b = __shfl_sync(full, m1, kk & 31),
+                     c = __shfl_sync(full, m2, kk & 31);
+      const uint32_t v = kk < 32 ? a : (kk < 64 ? b : c);
+      return k < 0 ? 0u : v;
+    };
+    const uint32_t wt = digit(top), wm = digit(top - 1), wl = digit(top - 2);
+    const bool below = (lane < top - 2 && m0 != 0) || (lane + 32 < top - 2 && m1 != 0) ||
+                       (lane + 64 < top - 2 && m2 != 0);
+    const bool sticky_low = __ballot_sync(full, below) != 0;
+    if (lane == 0) {
+      const unsigned __int128 W = ((unsigned __int128)wt << 64) |
+                                  ((unsigned __int128)wm << 32) | (unsigned __int128)wl;
+      const int base = 32 * (top - 2);
+      const int nbits = 32 * top + (32 - __clz((int)wt));
+      unsigned long long mant;
+      int e2;
+      if (nbits <= 53) {
+        mant = (unsigned long long)(W >> (-base));   // only when top <= 1: base < 0
+        e2 = -TB_ACC_BIAS;
+      } else {
+        const int rel = nbits - 53 - base;           // in [12, 43]
+        mant = (unsigned long long)(W >> rel);
+        const bool guard = (W >> (rel - 1)) & 1;
+        const bool sticky =
+            sticky_low || (W & ((((unsigned __int128)1) << (rel - 1)) - 1)) != 0;
+        if (guard && (sticky || (mant & 1ULL))) mant += 1;
+        e2 = (nbits - 53) - TB_ACC_BIAS;
+      }
+      p = scalbn((double)mant, e2);
+      if (neg) p = -p;
     }
   }
-  int top = -1;
-  for (int i = ND - 1; i >= 0; --i)
-    if (d[i]) {
-      top = i;
-      break;
-    }
-  if (top < 0) return 0.0;
-  const int nbits = top * 32 + (32 - __clz((int)d[top]));
-  const int shift = nbits > 53 ? nbits - 53 : 0;
-  // Gather bits [shift, nbits) into mant; guard = bit shift-1; sticky below.
-  auto bit = [&](int k) -> unsigned { return (d[k >> 5] >> (k & 31)) & 1u; };
-  unsigned long long mant = 0;
-  for (int k = nbits - 1; k >= shift; --k) mant = (mant << 1) | bit(k);
-  if (shift > 0) {
-    const unsigned guard = bit(shift - 1);
-    bool sticky = false;
-    const int gk = shift - 1;                  // bits strictly below guard
-    for (int w = 0; w < (gk >> 5) && !sticky; ++w) sticky = d[w] != 0;
-    if (!sticky && (gk & 31)) sticky = (d[gk >> 5] & ((1u << (gk & 31)) - 1u)) != 0;
-    if (guard && (sticky || (mant & 1ULL))) mant += 1;
+  if (lane == 0) {
+    if (piece) *piece = p;
+    if (dt) *dt = key_to_double(ld_cg_s64(acc + TB_ACC_MIN_WORD));
+    if (checksum) *checksum = __dadd_rn(*checksum, p);   // src/miniapp.py:227
   }
-  const double r = scalbn((double)mant, shift - TB_ACC_BIAS);
-  return neg ? -r : r;
+  __syncwarp();
+  if (reset)
+    for (int i = lane; i < TB_ACC_WORDS; i += 32)
+      acc[i] = (i == TB_ACC_MIN_WORD) ? kKeyInf : 0;
 }
 
 __global__ void k_acc_finalize(int64_t *acc, double *piece, double *dt,
                                double *checksum, int reset) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  const double p = acc_round(acc);
-  if (piece) *piece = p;
-  if (dt) *dt = key_to_double(acc[TB_ACC_MIN_WORD]);
-  if (checksum) *checksum = __dadd_rn(*checksum, p);   // src/miniapp.py:227
-  if (reset)
-    for (int i = 0; i < TB_ACC_WORDS; ++i)
-      acc[i] = (i == TB_ACC_MIN_WORD) ? 0x7ff0000000000000LL : 0;
+  __shared__ uint32_t dig[kDigits];
+  if (threadIdx.x < 32) warp_finalize(acc, piece, dt, checksum, reset, dig);
 }
 
-inline int grid_for(int64_t work, int threads, int max_blocks) {
-  int64_t b = (work + threads - 1) / threads;
+// ------------------------------------------------------------------ K2 --
+constexpr int kStepThreads = 256;
+constexpr int kStepWarps = kStepThreads / 32;
+constexpr int kStages = 3;   // bulk-copy ring depth per warp
+constexpr int kBulkSmem = kStepWarps * kStages * TB_CELLS * 8;   // 96 KiB
+
+struct StepArgs {
+  const double *old;
+  double *out;
+  int64_t n;
+  const double *left_face;
+  const double *right_face;
+  int chains, kpc;
+  double *mins, *sums;
+  int64_t *acc;
+  double *piece, *dt, *checksum;   // fused finalize outputs (single device)
+  int finalize;
+};
+
+template <int CHAINS, int KPC>
+__device__ __forceinline__ void run_chains(double (&v)[16], int chains, int kpc) {
+  if (CHAINS > 0) {
+#pragma unroll
+    for (int c = 0; c < CHAINS; ++c)
+#pragma unroll
+      for (int k = 0; k < KPC; ++k) {
+        const double c1 = kC1[k], c2 = kC2[k];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = xform(v[i], c1, c2);
+      }
+  } else {
+    for (int c = 0; c < chains; ++c)
+      for (int k = 0; k < kpc; ++k) {
+        const double c1 = kC1[k], c2 = kC2[k];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = xform(v[i], c1, c2);
+      }
+  }
+}
+
+// Everything once this lane's 16 cells are in registers: ghost fold,
+// transforms, store, pairwise sum + min (src/miniapp.py:119-133).
+template <int CHAINS, int KPC>
+__device__ __forceinline__ void subgrid_body(const StepArgs &a, int64_t g, int lane,
+                                             double (&v)[16], unsigned long long *s_limbs,
+                                             double &wmin) {
+  const int r = lane & 7;
+  // Ghost fold against the previous generation: cells 0..7 are lanes 0..7 at
+  // i = 0; cells 504..511 are lanes 24..31 at i = 15. Add rounds; *0.5 exact.
+  if (lane < 8) {
+    const double *lf =
+        g == 0 ? a.left_face : a.old + (g - 1) * TB_CELLS + (TB_CELLS - TB_FACE);
+    v[0] = __dmul_rn(0.5, __dadd_rn(v[0], lf[r]));
+  } else if (lane >= 24) {
+    const double *rf = g == a.n - 1 ? a.right_face : a.old + (g + 1) * TB_CELLS;
+    v[15] = __dmul_rn(0.5, __dadd_rn(v[15], rf[r]));
+  }
+  run_chains<CHAINS, KPC>(v, a.chains, a.kpc);
+  double *dst = a.out + g * TB_CELLS + 128 * (lane >> 3) + r;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) dst[8 * i] = v[i];
+  // numpy pairwise: r_j = a[j] + a[j+8] + ... sequentially, then
+  // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) per block and (B0+B1)+(B2+B3).
+  double s = v[0], m = v[0];
+#pragma unroll
+  for (int i = 1; i < 16; ++i) {
+    s = __dadd_rn(s, v[i]);
+    m = fmin(m, v[i]);
+  }
+#pragma unroll
+  for (int x = 1; x < 32; x <<= 1) {
+    s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, x));
+    m = fmin(m, __shfl_xor_sync(0xffffffffu, m, x));
+  }
+  if (lane == 0) {
+    if (a.sums) a.sums[g] = s;
+    if (a.mins) a.mins[g] = m;
+    if (a.acc) acc_add_digits(s_limbs, s);
+  }
+  wmin = fmin(wmin, m);
+}
+
+// Block epilogue: flush shared limbs + block min into acc; with finalize, the
+// last CTA to finish (threadfence + ticket) closes the step with one warp.
+__device__ __forceinline__ void step_epilogue(const StepArgs &a,
+                                              unsigned long long *s_limbs,
+                                              long long *s_min, double wmin,
+                                              uint32_t *dig, int *s_last) {
+  if (!a.acc) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) s_min[warp] = min_key(wmin);
+  __syncthreads();
+  long long bm = s_min[0];
+#pragma unroll
+  for (int w = 1; w < kStepWarps; ++w) bm = min(bm, s_min[w]);
+  acc_flush(s_limbs, bm, a.acc);
+  if (!a.finalize) return;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned long long t = atomicAdd(
+        reinterpret_cast<unsigned long long *>(a.acc) + TB_ACC_COUNT_WORD, 1ULL);
+    *s_last = (t == (unsigned long long)gridDim.x - 1);
+  }
+  __syncthreads();
+  if (*s_last && warp == 0) {
+    __threadfence();
+    warp_finalize(a.acc, a.piece, a.dt, a.checksum, 1, dig);
+  }
+}
+
+// K2a: direct loads into registers (ld.global.nc, no L1 allocate).
+template <int CHAINS, int KPC>
+__global__ void __launch_bounds__(kStepThreads) k_step(StepArgs a) {
+  __shared__ unsigned long long s_limbs[TB_ACC_LIMBS];
+  __shared__ long long s_min[kStepWarps];
+  __shared__ uint32_t dig[kDigits];
+  __shared__ int s_last;
+  if (a.acc) {
+    for (int i = threadIdx.x; i < TB_ACC_LIMBS; i += blockDim.x) s_limbs[i] = 0ULL;
+    __syncthreads();
+  }
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int lane_off = 128 * (lane >> 3) + (lane & 7);
+  double wmin = CUDART_INF;
+  for (int64_t g = (int64_t)blockIdx.x * kStepWarps + warp; g < a.n;
+       g += (int64_t)gridDim.x * kStepWarps) {
+    const double *src = a.old + g * TB_CELLS + lane_off;
+    double v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = ld_stream(src + 8 * i);
+    subgrid_body<CHAINS, KPC>(a, g, lane, v, s_limbs, wmin);
+  }
+  step_epilogue(a, s_limbs, s_min, wmin, dig, &s_last);
+}
+
+// K2b: each warp streams its sub-grids through a kStages-deep ring of 4 KiB
+// shared-memory slots filled by the bulk-copy (TMA) engine
+// (cp.async.bulk ... mbarrier::complete_tx), so the next sub-grids are in
+// flight while this one is transformed — no registers spent on prefetch.
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_load(void *dst_smem, const void *src, uint32_t bytes,
+                                          uint64_t *bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+      "[%3];" ::"r"(smem_u32(dst_smem)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "TB_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra TB_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+template <int CHAINS, int KPC>
+__global__ void __launch_bounds__(kStepThreads) k_step_bulk(StepArgs a) {
+  extern __shared__ __align__(128) double ring[];   // [warps][stages][512]
+  __shared__ __align__(8) uint64_t bars[kStepWarps][kStages];
+  __shared__ unsigned long long s_limbs[TB_ACC_LIMBS];
+  __shared__ long long s_min[kStepWarps];
+  __shared__ uint32_t dig[kDigits];
+  __shared__ int s_last;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < TB_ACC_LIMBS; i += blockDim.x) s_limbs[i] = 0ULL;
+  if (lane == 0)
+    for (int s = 0; s < kStages; ++s) mbar_init(&bars[warp][s], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  double *slots = ring + (size_t)warp * kStages * TB_CELLS;
+  const int64_t gstride = (int64_t)gridDim.x * kStepWarps;
+  const int64_t g0 = (int64_t)blockIdx.x * kStepWarps + warp;
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < kStages; ++s) {
+      const int64_t g = g0 + s * gstride;
+      if (g < a.n)
+        bulk_load(slots + s * TB_CELLS, a.old + g * TB_CELLS, TB_CELLS * 8, &bars[warp][s]);
+    }
+  }
+  const int lane_off = 128 * (lane >> 3) + (lane & 7);
+  double wmin = CUDART_INF;
+  int it = 0;
+  for (int64_t g = g0; g < a.n; g += gstride, ++it) {
+    const int s = it % kStages;
+    mbar_wait(&bars[warp][s], (uint32_t)((it / kStages) & 1));
+    const double *src = slots + s * TB_CELLS + lane_off;
+    double v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = src[8 * i];
+    __syncwarp();
+    const int64_t gn = g + kStages * gstride;
+    if (lane == 0 && gn < a.n) {
+      // generic-proxy reads of the slot must be ordered before the
+      // async-proxy write that refills it
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      bulk_load(slots + s * TB_CELLS, a.old + gn * TB_CELLS, TB_CELLS * 8, &bars[warp][s]);
+    }
+    subgrid_body<CHAINS, KPC>(a, g, lane, v, s_limbs, wmin);
+  }
+  step_epilogue(a, s_limbs, s_min, wmin, dig, &s_last);
+}
+
+int g_step_impl = TB_STEP_AUTO;
+
+inline int grid_for(int64_t work, int per_block, int max_blocks) {
+  int64_t b = (work + per_block - 1) / per_block;
   if (b < 1) b = 1;
   if (b > max_blocks) b = max_blocks;
   return (int)b;
+}
+
+template <typename K>
+int occupancy(K kernel, int smem) {
+  int o = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kernel, kStepThreads, smem) !=
+          cudaSuccess ||
+      o < 1)
+    o = 1;
+  return o;
+}
+
+int launch_step(cudaStream_t st, StepArgs a) {
+  const bool fixed = a.chains == 3 && a.kpc == 5;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(a.old) & 15) == 0);
+  const bool bulk = aligned && (g_step_impl == TB_STEP_BULK ||
+                                (g_step_impl == TB_STEP_AUTO && fixed));
+  if (a.finalize && a.acc) {
+    // ticket counter must start at 0 (reset by acc_reset / finalize)
+  }
+  if (bulk) {
+    static int occ_f = 0, occ_g = 0;
+    static bool attr_f = false, attr_g = false;
+    if (fixed) {
+      if (!attr_f) {
+        cudaFuncSetAttribute(k_step_bulk<3, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kBulkSmem);
+        attr_f = true;
+      }
+      if (!occ_f) occ_f = occupancy(k_step_bulk<3, 5>, kBulkSmem);
+      const int blocks = grid_for(a.n, kStepWarps, tb::sm_count() * occ_f);
+      k_step_bulk<3, 5><<<blocks, kStepThreads, kBulkSmem, st>>>(a);
+    } else {
+      if (!attr_g) {
+        cudaFuncSetAttribute(k_step_bulk<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kBulkSmem);
+        attr_g = true;
+      }
+      if (!occ_g) occ_g = occupancy(k_step_bulk<0, 0>, kBulkSmem);
+      const int blocks = grid_for(a.n, kStepWarps, tb::sm_count() * occ_g);
+      k_step_bulk<0, 0><<<blocks, kStepThreads, kBulkSmem, st>>>(a);
+    }
+  } else {
+    static int occ_f = 0, occ_g = 0;
+    if (fixed) {
+      if (!occ_f) occ_f = occupancy(k_step<3, 5>, 0);
+      const int blocks = grid_for(a.n, kStepWarps, tb::sm_count() * occ_f);
+      k_step<3, 5><<<blocks, kStepThreads, 0, st>>>(a);
+    } else {
+      if (!occ_g) occ_g = occupancy(k_step<0, 0>, 0);
+      const int blocks = grid_for(a.n, kStepWarps, tb::sm_count() * occ_g);
+      k_step<0, 0><<<blocks, kStepThreads, 0, st>>>(a);
+    }
+  }
+  return tb::last_error();
 }
 
 }  // namespace
 
 // ------------------------------------------------------------ launchers --
 extern "C" {
+
+int tb_set_option(int key, int value) {
+  if (key == TB_OPT_STEP_IMPL) {
+    if (value < TB_STEP_AUTO || value > TB_STEP_BULK) return TB_E_INVALID;
+    g_step_impl = value;
+    return TB_OK;
+  }
+  return TB_E_INVALID;
+}
 
 int tb_launch(tb_stream_t s, int op, int kind, double c1, double c2, double *d,
               int64_t n) {
@@ -373,38 +619,43 @@ int tb_init_cells(tb_stream_t s, double *cells, int64_t subgrids, int64_t lo,
   return tb::last_error();
 }
 
+static int step_args(StepArgs *a, const double *old, double *out, int64_t n,
+                     const double *left_face, const double *right_face, int chains,
+                     int kpc, double *mins, double *sums, int64_t *acc) {
+  if (n < 0 || chains < 0 || kpc < 0 || kpc > TB_KINDS) return TB_E_INVALID;
+  if (n > 0 && (!old || !out || old == out || !left_face || !right_face))
+    return TB_E_INVALID;
+  *a = StepArgs{old, out, n, left_face, right_face, chains, kpc, mins, sums, acc,
+                nullptr, nullptr, nullptr, 0};
+  return TB_OK;
+}
+
 int tb_step(tb_stream_t s, const double *old, double *out, int64_t n,
             const double *left_face, const double *right_face, int chains,
             int kernels_per_chain, double *mins, double *sums, int64_t *acc) {
-  if (n < 0 || chains < 0 || kernels_per_chain < 0 ||
-      kernels_per_chain > TB_KINDS)
-    return TB_E_INVALID;
+  StepArgs a;
+  const int r = step_args(&a, old, out, n, left_face, right_face, chains,
+                          kernels_per_chain, mins, sums, acc);
+  if (r != TB_OK) return r;
   if (n == 0) return TB_OK;
-  if (!old || !out || old == out || !left_face || !right_face) return TB_E_INVALID;
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
-  // Persistent grid: exactly the resident CTAs of one wave (occupancy-derived,
-  // x148 SMs); each warp walks sub-grids with a grid stride.
-  const bool fixed = chains == 3 && kernels_per_chain == 5;
-  static int occ_fixed = 0, occ_generic = 0;
-  int &occ = fixed ? occ_fixed : occ_generic;
-  if (occ == 0) {
-    int o = 0;
-    cudaError_t e = fixed ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                                &o, k_step<3, 5>, kStepThreads, 0)
-                          : cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-                                &o, k_step<0, 0>, kStepThreads, 0);
-    occ = (e == cudaSuccess && o > 0) ? o : 4;
-  }
-  const int blocks = grid_for(n, kStepWarps, tb::sm_count() * occ);
-  if (fixed)
-    k_step<3, 5><<<blocks, kStepThreads, 0, st>>>(old, out, n, left_face, right_face,
-                                                  chains, kernels_per_chain, mins,
-                                                  sums, acc);
-  else
-    k_step<0, 0><<<blocks, kStepThreads, 0, st>>>(old, out, n, left_face, right_face,
-                                                  chains, kernels_per_chain, mins,
-                                                  sums, acc);
-  return tb::last_error();
+  return launch_step(reinterpret_cast<cudaStream_t>(s), a);
+}
+
+int tb_step_final(tb_stream_t s, const double *old, double *out, int64_t n,
+                  const double *left_face, const double *right_face, int chains,
+                  int kernels_per_chain, double *mins, double *sums, int64_t *acc,
+                  double *piece, double *dt, double *checksum) {
+  StepArgs a;
+  int r = step_args(&a, old, out, n, left_face, right_face, chains, kernels_per_chain,
+                    mins, sums, acc);
+  if (r != TB_OK) return r;
+  if (!acc) return TB_E_INVALID;
+  if (n == 0) return tb_acc_finalize(s, acc, piece, dt, checksum, 1);
+  a.piece = piece;
+  a.dt = dt;
+  a.checksum = checksum;
+  a.finalize = 1;
+  return launch_step(reinterpret_cast<cudaStream_t>(s), a);
 }
 
 int tb_acc_reset(tb_stream_t s, int64_t *acc) {

@@ -7,9 +7,10 @@ accumulator (include/tb.h TB_ACC_*), a 2x8 halo of ring-neighbour faces and
 per-step ``(piece, dt)`` records plus the running checksum.
 
 One step = K2 (``tb_step``: ghost fold + 15 transforms + per-sub-grid min and
-pairwise sum folded into the exact accumulator) + K4 (``tb_acc_finalize``:
-correctly rounded piece, dt, ``checksum += piece``). Bit-identical to
-``run_reference`` (src/reference.py:23-50) at any rank count.
+pairwise sum folded into the exact accumulator) + K4 (correctly rounded
+piece, dt, ``checksum += piece``) — on one device K4 runs in K2's last CTA
+(``tb_step_final``): one launch per step. Bit-identical to ``run_reference``
+(src/reference.py:23-50) at any rank count.
 
 Multi-GPU (one process per GPU, torch.distributed/NCCL): the ring is split
 into contiguous ranges; per step each rank sends its first sub-grid's left
@@ -17,6 +18,12 @@ face to rank-1 and its last sub-grid's right face to rank+1 (64 B each, from
 the previous generation — Jacobi, src/miniapp.py:89-93), then after K2 the
 accumulator's limbs are all-reduced with SUM and its min word with MIN
 (int64): exact, so every partition gives the single-device checksum.
+
+Host-buffer path (``step_host``): the drop-in for callers that keep the
+cells on the host (the reference's Scenario.grids). The H2D of the input
+generation, K2 and the D2H of the new generation are pipelined in chunks of
+sub-grids on three streams, so the PCIe transfers in both directions overlap
+each other and the compute.
 """
 
 from __future__ import annotations
@@ -43,12 +50,24 @@ def ring_partition(subgrids: int, world: int, rank: int) -> Tuple[int, int]:
     return lo, lo + base + (1 if rank < extra else 0)
 
 
-def _ptr(t: torch.Tensor) -> int:
-    return t.data_ptr()
+def chunk_bounds(n: int, chunks: int) -> List[Tuple[int, int]]:
+    """Split [0, n) into at most ``chunks`` contiguous non-empty ranges."""
+    chunks = max(1, min(chunks, n))
+    base, extra = divmod(n, chunks)
+    out, lo = [], 0
+    for c in range(chunks):
+        hi = lo + base + (1 if c < extra else 0)
+        out.append((lo, hi))
+        lo = hi
+    return out
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else t.data_ptr()
 
 
 class CudaRingOps:
-    """The product kernels (libtb) behind the stepper's five primitives."""
+    """The product kernels (libtb) behind the stepper's primitives."""
 
     def __init__(self, device: torch.device):
         if device.type != "cuda":
@@ -65,9 +84,14 @@ class CudaRingOps:
     def step(self, old, out, left_face, right_face, chains, kpc, acc,
              mins=None, sums=None) -> None:
         N.call("tb_step", self.stream(), _ptr(old), _ptr(out), old.shape[0],
-               _ptr(left_face), _ptr(right_face), chains, kpc,
-               None if mins is None else _ptr(mins),
-               None if sums is None else _ptr(sums), _ptr(acc))
+               _ptr(left_face), _ptr(right_face), chains, kpc, _ptr(mins), _ptr(sums),
+               _ptr(acc))
+
+    def step_final(self, old, out, left_face, right_face, chains, kpc, acc, piece, dt,
+                   checksum, mins=None, sums=None) -> None:
+        N.call("tb_step_final", self.stream(), _ptr(old), _ptr(out), old.shape[0],
+               _ptr(left_face), _ptr(right_face), chains, kpc, _ptr(mins), _ptr(sums),
+               _ptr(acc), _ptr(piece), _ptr(dt), _ptr(checksum))
 
     def acc_reset(self, acc) -> None:
         N.call("tb_acc_reset", self.stream(), _ptr(acc))
@@ -113,6 +137,7 @@ class RingStepper:
         self.cur = 0
         self.acc = torch.zeros(N.TB_ACC_WORDS, dtype=torch.int64, device=device)
         self.halo = torch.zeros((2, FACE), **f64)        # [left ghost, right ghost]
+        self.myfaces = torch.zeros((2, FACE), **f64)     # [my left face, my right face]
         self.max_steps = max_steps
         self.pieces = torch.zeros(max_steps, **f64)
         self.dts = torch.zeros(max_steps, **f64)
@@ -120,6 +145,7 @@ class RingStepper:
         self.mins = torch.empty(n, **f64) if collect_subgrid_stats else None
         self.sums = torch.empty(n, **f64) if collect_subgrid_stats else None
         self.steps_done = 0
+        self._streams = None
         self.ops.init_cells(self.state[0], subgrids, self.lo)
         self.ops.acc_reset(self.acc)
 
@@ -134,77 +160,141 @@ class RingStepper:
         self.state[self.cur].copy_(host, non_blocking=True)
 
     # --------------------------------------------------------------- step --
-    def _exchange_halo(self, old: torch.Tensor) -> Tuple[torch.Tensor, torch.Tensor]:
-        if self.world == 1:
-            # single-device ring: wrap within this rank
-            return old[self.n - 1, CELLS - FACE:], old[0, :FACE]
+    def _exchange(self, send_left: torch.Tensor, send_right: torch.Tensor) -> None:
+        """Ring halo exchange into self.halo = [left ghost, right ghost]."""
         import torch.distributed as dist
         left = (self.rank - 1) % self.world
         right = (self.rank + 1) % self.world
         # Issue order makes N=2 (left == right) unambiguous: the first message
         # from a peer is its LEFT face (-> my right ghost), the second its
         # RIGHT face (-> my left ghost).
-        ops = [dist.P2POp(dist.isend, old[0, :FACE], left, self.group),
+        ops = [dist.P2POp(dist.isend, send_left, left, self.group),
                dist.P2POp(dist.irecv, self.halo[1], right, self.group),
-               dist.P2POp(dist.isend, old[self.n - 1, CELLS - FACE:], right, self.group),
+               dist.P2POp(dist.isend, send_right, right, self.group),
                dist.P2POp(dist.irecv, self.halo[0], left, self.group)]
         for req in dist.batch_isend_irecv(ops):
             req.wait()
+
+    def _halo(self, old: torch.Tensor) -> Tuple[torch.Tensor, torch.Tensor]:
+        if self.world == 1:
+            # single-device ring: wrap within this rank
+            return old[self.n - 1, CELLS - FACE:], old[0, :FACE]
+        self._exchange(old[0, :FACE], old[self.n - 1, CELLS - FACE:])
         return self.halo[0], self.halo[1]
 
     def _reduce_acc(self) -> None:
-        if self.world == 1:
-            return
         import torch.distributed as dist
         dist.all_reduce(self.acc[:N.TB_ACC_LIMBS], op=dist.ReduceOp.SUM, group=self.group)
         dist.all_reduce(self.acc[N.TB_ACC_MIN_WORD:N.TB_ACC_MIN_WORD + 1],
                         op=dist.ReduceOp.MIN, group=self.group)
 
+    def _close(self, k: int) -> None:
+        if self.world > 1:
+            self._reduce_acc()
+        self.ops.acc_finalize(self.acc, self.pieces[k:k + 1], self.dts[k:k + 1],
+                              self.checksum)
+
     def step(self, kernel_events=None) -> None:
         """Advance one time step (asynchronous on the current stream).
 
         ``kernel_events``: optional (start, end) CUDA events recorded around
-        the fused K2 launch alone (bench.py uses them for the roofline).
+        the fused step launch alone (bench.py uses them for the roofline).
         """
         if self.steps_done >= self.max_steps:
             raise RuntimeError("max_steps exceeded; raise max_steps")
+        k = self.steps_done
         old, out = self.state[self.cur], self.state[1 - self.cur]
-        lf, rf = self._exchange_halo(old)
+        lf, rf = self._halo(old)
         if kernel_events is not None:
             kernel_events[0].record()
-        self.ops.step(old, out, lf, rf, self.chains, self.kpc, self.acc,
-                      self.mins, self.sums)
+        fused = self.world == 1 and hasattr(self.ops, "step_final")
+        if fused:
+            self.ops.step_final(old, out, lf, rf, self.chains, self.kpc, self.acc,
+                                self.pieces[k:k + 1], self.dts[k:k + 1], self.checksum,
+                                self.mins, self.sums)
+        else:
+            self.ops.step(old, out, lf, rf, self.chains, self.kpc, self.acc,
+                          self.mins, self.sums)
         if kernel_events is not None:
             kernel_events[1].record()
-        self._reduce_acc()
-        k = self.steps_done
-        self.ops.acc_finalize(self.acc, self.pieces[k:k + 1], self.dts[k:k + 1],
-                              self.checksum)
+        if not fused:
+            self._close(k)
         self.cur = 1 - self.cur
         self.steps_done += 1
-
-    def step_host(self, host_in: torch.Tensor, host_out: torch.Tensor,
-                  host_stats: torch.Tensor) -> None:
-        """One step on host-resident cells (the drop-in, host-buffer path).
-
-        ``host_in``/``host_out``: pinned [n_local, 512] float64 (may alias);
-        ``host_stats``: pinned float64[2] receiving (piece, dt). Enqueues the
-        H2D of the input generation, the step, and the D2H of the new
-        generation and its reductions on the current stream; the caller
-        synchronises before reading host_out/host_stats.
-        """
-        self.state[self.cur].copy_(host_in, non_blocking=True)
-        k = self.steps_done
-        self.step()
-        host_out.copy_(self.state[self.cur], non_blocking=True)
-        host_stats[0:1].copy_(self.pieces[k:k + 1], non_blocking=True)
-        host_stats[1:2].copy_(self.dts[k:k + 1], non_blocking=True)
 
     def run(self, steps: int) -> RingResult:
         k0 = self.steps_done
         for _ in range(steps):
             self.step()
         return self.result(k0)
+
+    # ------------------------------------------------------ host buffers --
+    def step_host(self, host_in: torch.Tensor, host_out: torch.Tensor,
+                  host_stats: torch.Tensor, chunks: int = 16) -> None:
+        """One step on host-resident cells (the host-buffer drop-in path).
+
+        ``host_in``/``host_out``: pinned [n_local, 512] float64 (may alias);
+        ``host_stats``: pinned float64[2] receiving (piece, dt). Work is
+        enqueued on the current stream plus two copy streams and joined back
+        into the current stream; synchronise it before reading the outputs.
+        Per chunk c of sub-grids: H2D(c) on the upload stream; K2(c) once
+        H2D(c) and H2D(c+1) landed (c's right ghost lives in c+1); D2H(c) on
+        the download stream once K2(c) is done.
+        """
+        if self.steps_done >= self.max_steps:
+            raise RuntimeError("max_steps exceeded; raise max_steps")
+        if not isinstance(self.ops, CudaRingOps):
+            raise RuntimeError("step_host needs the CUDA ops")
+        dev = self.device
+        main = torch.cuda.current_stream(dev)
+        if self._streams is None:
+            self._streams = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+        up, down = self._streams
+        k = self.steps_done
+        old, out = self.state[self.cur], self.state[1 - self.cur]
+        bounds = chunk_bounds(self.n, chunks)
+        ev_h2d = [torch.cuda.Event() for _ in bounds]
+        ev_k2 = [torch.cuda.Event() for _ in bounds]
+        ev_faces = torch.cuda.Event()
+        n = self.n
+        up.wait_stream(main)          # previous step's reads of `old` are done
+        with torch.cuda.stream(up):
+            faces = self.myfaces if self.world > 1 else self.halo
+            if self.world > 1:
+                faces[0].copy_(host_in[0, :FACE], non_blocking=True)
+                faces[1].copy_(host_in[n - 1, CELLS - FACE:], non_blocking=True)
+            else:
+                faces[0].copy_(host_in[n - 1, CELLS - FACE:], non_blocking=True)
+                faces[1].copy_(host_in[0, :FACE], non_blocking=True)
+            ev_faces.record(up)
+            for (lo, hi), ev in zip(bounds, ev_h2d):
+                old[lo:hi].copy_(host_in[lo:hi], non_blocking=True)
+                ev.record(up)
+        main.wait_event(ev_faces)
+        if self.world > 1:
+            self._exchange(self.myfaces[0], self.myfaces[1])
+        last = len(bounds) - 1
+        for c, (lo, hi) in enumerate(bounds):
+            main.wait_event(ev_h2d[c])
+            if c < last:
+                main.wait_event(ev_h2d[c + 1])
+            lf = self.halo[0] if c == 0 else old[lo - 1, CELLS - FACE:]
+            rf = self.halo[1] if c == last else old[hi, :FACE]
+            self.ops.step(old[lo:hi], out[lo:hi], lf, rf, self.chains, self.kpc, self.acc)
+            ev_k2[c].record(main)
+        self._close(k)
+        ev_done = torch.cuda.Event()
+        ev_done.record(main)
+        with torch.cuda.stream(down):
+            for (lo, hi), ev in zip(bounds, ev_k2):
+                down.wait_event(ev)
+                host_out[lo:hi].copy_(out[lo:hi], non_blocking=True)
+            down.wait_event(ev_done)
+            host_stats[0:1].copy_(self.pieces[k:k + 1], non_blocking=True)
+            host_stats[1:2].copy_(self.dts[k:k + 1], non_blocking=True)
+        main.wait_stream(down)
+        self.cur = 1 - self.cur
+        self.steps_done += 1
 
     def result(self, first_step: int = 0) -> RingResult:
         k = self.steps_done

@@ -157,3 +157,51 @@ def test_ring_stepper_long_run_matches_c_oracle(N):
     cs, dts = run_reference_gpu(3000, 40)
     ccs, cdts = c_oracle.run_reference(3000, 40)
     assert cs == ccs and dts == cdts
+
+
+@pytest.mark.parametrize("impl", ["reg", "bulk"])
+@pytest.mark.parametrize("s", [1, 5, 64, 3000])
+def test_step_impls_and_fused_finalize(N, impl, s):
+    code = {"reg": N.TB_STEP_REG, "bulk": N.TB_STEP_BULK}[impl]
+    N.call("tb_set_option", N.TB_OPT_STEP_IMPL, code)
+    try:
+        old_h = mo.initial_cells(s) + 1e-4 * np.cos(np.arange(s * 512)).reshape(s, 512)
+        old = torch.from_numpy(old_h).cuda()
+        out = torch.empty_like(old)
+        acc = torch.zeros(N.TB_ACC_WORDS, dtype=torch.int64, device="cuda")
+        res = torch.zeros(3, dtype=torch.float64, device="cuda")
+        N.call("tb_acc_reset", stream(), P(acc))
+        want, wmin, wsum = mo.step_cells(old_h)
+        for rep in range(3):      # the ticket counter must re-arm every step
+            res[2] = 0.0
+            N.call("tb_step_final", stream(), P(old), P(out), s, P(old[s - 1, 504:]),
+                   P(old[0, :8]), 3, 5, None, None, P(acc), P(res[0:1]), P(res[1:2]),
+                   P(res[2:3]))
+            np.testing.assert_array_equal(out.cpu().numpy(), want)
+            assert res[0].item() == math.fsum(wsum.tolist())
+            assert res[1].item() == float(wmin.min())
+            assert res[2].item() == res[0].item()
+        # generic chain through the same impl
+        N.call("tb_step", stream(), P(old), P(out), s, P(old[s - 1, 504:]), P(old[0, :8]),
+               2, 3, None, None, None)
+        np.testing.assert_array_equal(out.cpu().numpy(), mo.step_cells(old_h, None, None,
+                                                                       2, 3)[0])
+    finally:
+        N.call("tb_set_option", N.TB_OPT_STEP_IMPL, N.TB_STEP_AUTO)
+
+
+@pytest.mark.parametrize("s,chunks", [(1, 4), (7, 3), (64, 16), (1000, 7), (4096, 16)])
+def test_step_host_pipeline_matches_oracle(N, s, chunks):
+    from paper_2303_08058_b200.ring import RingStepper
+    st = RingStepper(s, max_steps=4)
+    cells = torch.from_numpy(mo.initial_cells(s)).pin_memory()
+    stats = torch.zeros(2, dtype=torch.float64).pin_memory()
+    cs, dts, want = mo.run_reference_cells(s, 3)
+    pieces = []
+    for _ in range(3):
+        st.step_host(cells, cells, stats, chunks=chunks)
+        torch.cuda.synchronize()
+        pieces.append(stats[0].item())
+        assert stats[1].item() == dts[len(pieces) - 1]
+    np.testing.assert_array_equal(cells.numpy(), want)
+    assert st.result().checksum == cs
