@@ -188,6 +188,9 @@ def main(argv=None):
     ap.add_argument("--cpu-budget", type=float, default=10.0,
                     help="seconds of CPU work for the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--step-impl", choices=["auto", "reg", "bulk", "regpf"], default="auto",
+                    help="K2 variant (tb_set_option TB_OPT_STEP_IMPL)")
+    ap.add_argument("--e2e-chunks", type=int, default=16)
     args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3)
 
@@ -207,6 +210,9 @@ def main(argv=None):
     from paper_2303_08058_b200 import _native as N
     from paper_2303_08058_b200.ring import RingStepper, run_reference_gpu
     N.init(local)
+    N.call("tb_set_option", N.TB_OPT_STEP_IMPL,
+           {"auto": N.TB_STEP_AUTO, "reg": N.TB_STEP_REG, "bulk": N.TB_STEP_BULK,
+            "regpf": N.TB_STEP_REGPF}[args.step_impl])
 
     # Parity gate in the same run: the reference's GOLDEN_DEFAULTS.
     parity = run_reference_gpu(512, 15, device=dev)[0] == GOLDEN_DEFAULTS
@@ -259,7 +265,7 @@ def main(argv=None):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.e2e_steps):
-        st.step_host(host_in, host_in, host_stats)
+        st.step_host(host_in, host_in, host_stats, chunks=args.e2e_chunks)
     e1.record()
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / max(args.e2e_steps, 1)
@@ -298,7 +304,11 @@ def main(argv=None):
                        "cells": cells_total, "parallelism": f"ring-dp{world}",
                        "l2": "flushed before every timed step (256 MiB write)"},
             "parity": {"run_reference_512x15_equals_GOLDEN_DEFAULTS": parity},
-            "roofline": {"bound": "hbm", "kernel": "k_step<3,5> (tb_step)",
+            "roofline": {"bound": "hbm",
+                         "kernel": {"auto": "k_step_bulk<3,5>", "bulk": "k_step_bulk<3,5>",
+                                    "reg": "k_step<3,5>", "regpf": "k_step<3,5,pf>"}[
+                                        args.step_impl] + (" (tb_step_final: K2 + fused K4)"
+                                                           if world == 1 else " (tb_step)"),
                          "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
                          "peak_source": peak_kind,
@@ -307,8 +317,10 @@ def main(argv=None):
             "e2e": {"value": e2e_value, "unit": "cells/s",
                     "h2d_bytes_per_step": n_local * 512 * 8,
                     "d2h_bytes_per_step": n_local * 512 * 8 + 16,
-                    "ms_per_step": e2e_ms, "api": "RingStepper.step_host"},
-            "gpu_launches": 2 * args.steps,
+                    "ms_per_step": e2e_ms, "chunks": args.e2e_chunks,
+                    "api": "RingStepper.step_host (pinned H2D | K2 | D2H pipelined "
+                           "over chunks on 3 streams)"},
+            "gpu_launches": (1 if world == 1 else 2) * args.steps,
             "clocks": clocks,
             "wall_s_timed_region": wall,
         }

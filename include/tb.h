@@ -69,6 +69,7 @@ extern "C" {
 #define TB_STEP_AUTO 0          /* bulk-copy ring when aligned, (3,5) chain */
 #define TB_STEP_REG 1           /* direct ld.global.nc into registers       */
 #define TB_STEP_BULK 2          /* cp.async.bulk smem ring + mbarriers      */
+#define TB_STEP_REGPF 3         /* registers + next-sub-grid prefetch       */
 
 typedef uint64_t tb_stream_t;
 typedef uint64_t tb_event_t;

@@ -8,7 +8,8 @@
 //                      the step's exact sum and min folded into a
 //                      superaccumulator (src/miniapp.py:138-171); optionally the
 //                      last CTA closes the step (K4 fused).
-//                      k_step      : direct ld.global.nc into registers;
+//                      k_step      : direct ld.global.nc into registers
+//                                    (optionally with a register prefetch);
 //                      k_step_bulk : per-warp ring of shared-memory slots fed by
 //                                    the bulk-copy (TMA) engine + mbarriers.
 // K4  k_acc_finalize : correctly rounded sum (== math.fsum) + dt + checksum,
@@ -178,7 +179,7 @@ __global__ void k_acc_reset(int64_t *acc) {
 constexpr int kDigits = 96;   // >= TB_ACC_LIMBS + carry growth; 3 per lane
 
 __device__ void warp_finalize(int64_t *acc, double *piece, double *dt,
-                              double *checksum, int reset, uint32_t *dig) {
+                              double *checksum, int reset) {
   const int lane = threadIdx.x & 31;
   const unsigned full = 0xffffffffu;
   const long long a0 = ld_cg_s64(acc + lane);
@@ -190,25 +191,31 @@ __device__ void warp_finalize(int64_t *acc, double *piece, double *dt,
   if (n0 | n1 | n2) {
     const int lo = n0 ? __ffs(n0) - 1 : (n1 ? 31 + __ffs(n1) : 63 + __ffs(n2));
     const int hi = n2 ? 95 - __clz(n2) : (n1 ? 63 - __clz(n1) : 31 - __clz(n0));
-    for (int i = lane; i < kDigits; i += 32) dig[i] = 0u;
-    __syncwarp();
-    int neg = 0;
-    if (lane == 0) {
-      long long carry = 0;
-      int i = lo;
-      for (; i < kDigits; ++i) {
-        const long long v = (i <= hi ? ld_cg_s64(acc + i) : 0LL) + carry;
-        dig[i] = (uint32_t)(v & 0xffffffffLL);
-        carry = v >> 32;   // arithmetic shift
-        if (i >= hi && (carry == 0 || carry == -1)) break;
+    // Warp-uniform carry chain over the occupied limbs; limb i comes from its
+    // owner lane by shuffle, digit i is kept by that lane (m0/m1/m2).
+    uint32_t m0 = 0u, m1 = 0u, m2 = 0u;
+    long long carry = 0;
+    int i = lo;
+    for (; i < kDigits; ++i) {
+      const long long x0 = __shfl_sync(full, a0, i & 31);
+      const long long x1 = __shfl_sync(full, a1, i & 31);
+      const long long x2 = __shfl_sync(full, a2, i & 31);
+      const long long li = i > hi ? 0LL : (i < 32 ? x0 : (i < 64 ? x1 : x2));
+      const long long v = li + carry;
+      if (lane == (i & 31)) {
+        const uint32_t d = (uint32_t)(v & 0xffffffffLL);
+        if (i < 32) m0 = d; else if (i < 64) m1 = d; else m2 = d;
       }
-      neg = carry < 0;
-      if (neg)
-        for (int k = i + 1; k < kDigits; ++k) dig[k] = 0xffffffffu;
+      carry = v >> 32;   // arithmetic shift
+      if (i >= hi && (carry == 0 || carry == -1)) break;
     }
-    neg = __shfl_sync(full, neg, 0);
-    __syncwarp();
-    uint32_t m0 = dig[lane], m1 = dig[lane + 32], m2 = dig[lane + 64];
+    const bool neg = carry < 0;
+    if (neg) {   // sign-extend above the last written digit
+      if (lane > i) m0 = 0xffffffffu;
+      if (lane + 32 > i) m1 = 0xffffffffu;
+      if (lane + 64 > i) m2 = 0xffffffffu;
+    }
+
     if (neg) {  // magnitude = two's complement negation, digit-parallel
       const unsigned z0 = __ballot_sync(full, m0 != 0), z1 = __ballot_sync(full, m1 != 0),
                      z2 = __ballot_sync(full, m2 != 0);
@@ -270,15 +277,19 @@ __device__ void warp_finalize(int64_t *acc, double *piece, double *dt,
 
 __global__ void k_acc_finalize(int64_t *acc, double *piece, double *dt,
                                double *checksum, int reset) {
-  __shared__ uint32_t dig[kDigits];
-  if (threadIdx.x < 32) warp_finalize(acc, piece, dt, checksum, reset, dig);
+  if (threadIdx.x < 32) warp_finalize(acc, piece, dt, checksum, reset);
 }
 
 // ------------------------------------------------------------------ K2 --
 constexpr int kStepThreads = 256;
 constexpr int kStepWarps = kStepThreads / 32;
-constexpr int kStages = 3;   // bulk-copy ring depth per warp
-constexpr int kBulkSmem = kStepWarps * kStages * TB_CELLS * 8;   // 96 KiB
+constexpr int kStages = 2;   // bulk-copy ring depth per warp
+// Slot layout: the four 128-cell blocks of a sub-grid at a 1088-B pitch
+// (1 KiB + 64 B pad) so lanes (b, r) and (b+1, r) sit in opposite bank halves:
+// each 8-byte LDS of the warp is exactly 2 wavefronts (conflict-free).
+constexpr int kBlkPitch = 136;                    // doubles per padded block
+constexpr int kSlot = 4 * kBlkPitch;              // doubles per slot (4352 B)
+constexpr int kBulkSmem = kStepWarps * kStages * kSlot * 8;   // 68 KiB -> 3 CTAs/SM
 
 struct StepArgs {
   const double *old;
@@ -361,7 +372,7 @@ __device__ __forceinline__ void subgrid_body(const StepArgs &a, int64_t g, int l
 __device__ __forceinline__ void step_epilogue(const StepArgs &a,
                                               unsigned long long *s_limbs,
                                               long long *s_min, double wmin,
-                                              uint32_t *dig, int *s_last) {
+                                              int *s_last) {
   if (!a.acc) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (lane == 0) s_min[warp] = min_key(wmin);
@@ -381,16 +392,17 @@ __device__ __forceinline__ void step_epilogue(const StepArgs &a,
   __syncthreads();
   if (*s_last && warp == 0) {
     __threadfence();
-    warp_finalize(a.acc, a.piece, a.dt, a.checksum, 1, dig);
+    warp_finalize(a.acc, a.piece, a.dt, a.checksum, 1);
   }
 }
 
-// K2a: direct loads into registers (ld.global.nc, no L1 allocate).
-template <int CHAINS, int KPC>
+// K2a: direct loads into registers (ld.global.nc, no L1 allocate). With PF,
+// the next sub-grid's 16 values per lane are loaded before this one is
+// transformed (register double buffer: more MLP, fewer resident warps).
+template <int CHAINS, int KPC, bool PF>
 __global__ void __launch_bounds__(kStepThreads) k_step(StepArgs a) {
   __shared__ unsigned long long s_limbs[TB_ACC_LIMBS];
   __shared__ long long s_min[kStepWarps];
-  __shared__ uint32_t dig[kDigits];
   __shared__ int s_last;
   if (a.acc) {
     for (int i = threadIdx.x; i < TB_ACC_LIMBS; i += blockDim.x) s_limbs[i] = 0ULL;
@@ -399,16 +411,38 @@ __global__ void __launch_bounds__(kStepThreads) k_step(StepArgs a) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int lane_off = 128 * (lane >> 3) + (lane & 7);
+  const int64_t gstride = (int64_t)gridDim.x * kStepWarps;
   double wmin = CUDART_INF;
-  for (int64_t g = (int64_t)blockIdx.x * kStepWarps + warp; g < a.n;
-       g += (int64_t)gridDim.x * kStepWarps) {
-    const double *src = a.old + g * TB_CELLS + lane_off;
-    double v[16];
+  int64_t g = (int64_t)blockIdx.x * kStepWarps + warp;
+  if (PF) {
+    double nxt[16];
+    if (g < a.n) {
+      const double *src = a.old + g * TB_CELLS + lane_off;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = ld_stream(src + 8 * i);
-    subgrid_body<CHAINS, KPC>(a, g, lane, v, s_limbs, wmin);
+      for (int i = 0; i < 16; ++i) nxt[i] = ld_stream(src + 8 * i);
+    }
+    for (; g < a.n; g += gstride) {
+      double v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = nxt[i];
+      const int64_t gn = g + gstride;
+      if (gn < a.n) {
+        const double *src = a.old + gn * TB_CELLS + lane_off;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) nxt[i] = ld_stream(src + 8 * i);
+      }
+      subgrid_body<CHAINS, KPC>(a, g, lane, v, s_limbs, wmin);
+    }
+  } else {
+    for (; g < a.n; g += gstride) {
+      const double *src = a.old + g * TB_CELLS + lane_off;
+      double v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = ld_stream(src + 8 * i);
+      subgrid_body<CHAINS, KPC>(a, g, lane, v, s_limbs, wmin);
+    }
   }
-  step_epilogue(a, s_limbs, s_min, wmin, dig, &s_last);
+  step_epilogue(a, s_limbs, s_min, wmin, &s_last);
 }
 
 // K2b: each warp streams its sub-grids through a kStages-deep ring of 4 KiB
@@ -422,17 +456,21 @@ __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
                : "memory");
 }
-__device__ __forceinline__ void bulk_load(void *dst_smem, const void *src, uint32_t bytes,
-                                          uint64_t *bar) {
+// One sub-grid = four 1 KiB bulk copies into the padded slot, one barrier.
+__device__ __forceinline__ void bulk_load_subgrid(double *slot, const double *src,
+                                                  uint64_t *bar) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
+               "r"(TB_CELLS * 8)
                : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
-      "[%3];" ::"r"(smem_u32(dst_smem)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
+#pragma unroll
+  for (int b = 0; b < 4; ++b)
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+        "[%3];" ::"r"(smem_u32(slot + b * kBlkPitch)),
+        "l"(src + 128 * b), "r"(1024), "r"(smem_u32(bar))
+        : "memory");
 }
+
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
@@ -449,7 +487,6 @@ __global__ void __launch_bounds__(kStepThreads) k_step_bulk(StepArgs a) {
   __shared__ __align__(8) uint64_t bars[kStepWarps][kStages];
   __shared__ unsigned long long s_limbs[TB_ACC_LIMBS];
   __shared__ long long s_min[kStepWarps];
-  __shared__ uint32_t dig[kDigits];
   __shared__ int s_last;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -458,24 +495,22 @@ __global__ void __launch_bounds__(kStepThreads) k_step_bulk(StepArgs a) {
     for (int s = 0; s < kStages; ++s) mbar_init(&bars[warp][s], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
-  double *slots = ring + (size_t)warp * kStages * TB_CELLS;
+  double *slots = ring + (size_t)warp * kStages * kSlot;
   const int64_t gstride = (int64_t)gridDim.x * kStepWarps;
   const int64_t g0 = (int64_t)blockIdx.x * kStepWarps + warp;
   if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < kStages; ++s) {
       const int64_t g = g0 + s * gstride;
-      if (g < a.n)
-        bulk_load(slots + s * TB_CELLS, a.old + g * TB_CELLS, TB_CELLS * 8, &bars[warp][s]);
+      if (g < a.n) bulk_load_subgrid(slots + s * kSlot, a.old + g * TB_CELLS, &bars[warp][s]);
     }
   }
-  const int lane_off = 128 * (lane >> 3) + (lane & 7);
   double wmin = CUDART_INF;
   int it = 0;
   for (int64_t g = g0; g < a.n; g += gstride, ++it) {
     const int s = it % kStages;
     mbar_wait(&bars[warp][s], (uint32_t)((it / kStages) & 1));
-    const double *src = slots + s * TB_CELLS + lane_off;
+    const double *src = slots + s * kSlot + kBlkPitch * (lane >> 3) + (lane & 7);
     double v[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = src[8 * i];
@@ -485,11 +520,11 @@ __global__ void __launch_bounds__(kStepThreads) k_step_bulk(StepArgs a) {
       // generic-proxy reads of the slot must be ordered before the
       // async-proxy write that refills it
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      bulk_load(slots + s * TB_CELLS, a.old + gn * TB_CELLS, TB_CELLS * 8, &bars[warp][s]);
+      bulk_load_subgrid(slots + s * kSlot, a.old + gn * TB_CELLS, &bars[warp][s]);
     }
     subgrid_body<CHAINS, KPC>(a, g, lane, v, s_limbs, wmin);
   }
-  step_epilogue(a, s_limbs, s_min, wmin, dig, &s_last);
+  step_epilogue(a, s_limbs, s_min, wmin, &s_last);
 }
 
 int g_step_impl = TB_STEP_AUTO;
@@ -541,16 +576,27 @@ int launch_step(cudaStream_t st, StepArgs a) {
       const int blocks = grid_for(a.n, kStepWarps, tb::sm_count() * occ_g);
       k_step_bulk<0, 0><<<blocks, kStepThreads, kBulkSmem, st>>>(a);
     }
+  } else if (g_step_impl == TB_STEP_REGPF) {
+    static int occ_f = 0, occ_g = 0;
+    if (fixed) {
+      if (!occ_f) occ_f = occupancy(k_step<3, 5, true>, 0);
+      const int blocks = grid_for(a.n, kStepWarps, tb::sm_count() * occ_f);
+      k_step<3, 5, true><<<blocks, kStepThreads, 0, st>>>(a);
+    } else {
+      if (!occ_g) occ_g = occupancy(k_step<0, 0, true>, 0);
+      const int blocks = grid_for(a.n, kStepWarps, tb::sm_count() * occ_g);
+      k_step<0, 0, true><<<blocks, kStepThreads, 0, st>>>(a);
+    }
   } else {
     static int occ_f = 0, occ_g = 0;
     if (fixed) {
-      if (!occ_f) occ_f = occupancy(k_step<3, 5>, 0);
+      if (!occ_f) occ_f = occupancy(k_step<3, 5, false>, 0);
       const int blocks = grid_for(a.n, kStepWarps, tb::sm_count() * occ_f);
-      k_step<3, 5><<<blocks, kStepThreads, 0, st>>>(a);
+      k_step<3, 5, false><<<blocks, kStepThreads, 0, st>>>(a);
     } else {
-      if (!occ_g) occ_g = occupancy(k_step<0, 0>, 0);
+      if (!occ_g) occ_g = occupancy(k_step<0, 0, false>, 0);
       const int blocks = grid_for(a.n, kStepWarps, tb::sm_count() * occ_g);
-      k_step<0, 0><<<blocks, kStepThreads, 0, st>>>(a);
+      k_step<0, 0, false><<<blocks, kStepThreads, 0, st>>>(a);
     }
   }
   return tb::last_error();
@@ -563,7 +609,7 @@ extern "C" {
 
 int tb_set_option(int key, int value) {
   if (key == TB_OPT_STEP_IMPL) {
-    if (value < TB_STEP_AUTO || value > TB_STEP_BULK) return TB_E_INVALID;
+    if (value < TB_STEP_AUTO || value > TB_STEP_REGPF) return TB_E_INVALID;
     g_step_impl = value;
     return TB_OK;
   }
