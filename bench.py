@@ -47,6 +47,7 @@ METRIC = "sub-grid cells processed/sec (rotating star, FP64) at 1/2/4/8 B200 vs 
 BYTES_PER_CELL = 8 + 8 + 0.25 + 0.03125   # 16.28 B/cell-step
 GOLDEN_DEFAULTS = float.fromhex("0x1.df1096d8fa699p+20")   # run_reference(512, 15)
 FALLBACK_HBM_GBS = 6650.0
+AUTO_BULK_MIN = 65536  # TB_STEP_AUTO: bulk ring from this many sub-grids, else reg
 
 
 def env_int(name, default):
@@ -219,7 +220,7 @@ def main(argv=None):
 
     per_gpu, desc = WORKLOADS[args.workload]
     subgrids = per_gpu * world
-    total_steps = args.warmup + args.steps + args.e2e_steps + 2
+    total_steps = args.warmup + args.steps + args.e2e_steps + 4
     st = RingStepper(subgrids, device=dev, rank=rank, world=world, max_steps=total_steps,
                      group=None)
     n_local = st.n
@@ -259,6 +260,8 @@ def main(argv=None):
     host_in = torch.empty((n_local, 512), dtype=torch.float64, pin_memory=True)
     host_in.copy_(st.cells)
     host_stats = torch.empty(2, dtype=torch.float64, pin_memory=True)
+    for _ in range(2):     # warm the copy streams / events / pinned-copy paths
+        st.step_host(host_in, host_in, host_stats, chunks=args.e2e_chunks)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -285,9 +288,13 @@ def main(argv=None):
             try:
                 with open(tpath) as fh:
                     tj = json.load(fh)
-                if tj.get("subgrids") == n_local:
-                    traffic = tj.get("dram_bytes_per_launch")
-            except (OSError, ValueError):
+                impl_key = args.step_impl
+                if impl_key == "auto":
+                    impl_key = "bulk" if n_local >= AUTO_BULK_MIN else "reg"
+                ent = tj.get("by_impl", {}).get(impl_key)
+                if ent and tj.get("subgrids") == n_local:
+                    traffic = ent["dram_bytes_per_launch"]
+            except (OSError, ValueError, KeyError):
                 pass
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
@@ -305,12 +312,18 @@ def main(argv=None):
                        "l2": "flushed before every timed step (256 MiB write)"},
             "parity": {"run_reference_512x15_equals_GOLDEN_DEFAULTS": parity},
             "roofline": {"bound": "hbm",
-                         "kernel": {"auto": "k_step_bulk<3,5>", "bulk": "k_step_bulk<3,5>",
+                         "kernel": {"auto": ("k_step_bulk<3,5>" if n_local >= AUTO_BULK_MIN
+                                             else "k_step<3,5>"),
+                                    "bulk": "k_step_bulk<3,5>",
                                     "reg": "k_step<3,5>", "regpf": "k_step<3,5,pf>"}[
                                         args.step_impl] + (" (tb_step_final: K2 + fused K4)"
                                                            if world == 1 else " (tb_step)"),
                          "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": traffic,
+                         "frac": achieved / hbm,
+                         "traffic": traffic,
+                         "traffic_note": "ncu dram__bytes_read+write per K2 launch "
+                                         "(profiles/k2_traffic.json)",
+                         "algorithmic_bytes_per_launch": n_local * 512 * BYTES_PER_CELL,
                          "peak_source": peak_kind,
                          "bytes_per_cell": BYTES_PER_CELL, "k2_ms": k2_ms},
             "cpu_baseline": cpu,

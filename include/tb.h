@@ -66,7 +66,7 @@ extern "C" {
 
 /* tb_set_option keys/values. */
 #define TB_OPT_STEP_IMPL 1      /* which K2 variant tb_step launches        */
-#define TB_STEP_AUTO 0          /* bulk-copy ring when aligned, (3,5) chain */
+#define TB_STEP_AUTO 0          /* bulk ring for >= 65536 sub-grids, else reg */
 #define TB_STEP_REG 1           /* direct ld.global.nc into registers       */
 #define TB_STEP_BULK 2          /* cp.async.bulk smem ring + mbarriers      */
 #define TB_STEP_REGPF 3         /* registers + next-sub-grid prefetch       */
@@ -189,11 +189,14 @@ int tb_acc_finalize(tb_stream_t s, int64_t *acc, double *piece, double *dt,
  * poll body that queries events with cudaEventQuery. */
 int tb_poll_create(tb_poll_t *reg);
 int tb_poll_destroy(tb_poll_t reg);
-/* PollRegistry.add (polling.py:53-55): any thread, lock-free. */
-int tb_poll_add(tb_poll_t reg, tb_event_t ev, uint64_t token);
+/* PollRegistry.add (polling.py:53-55): any thread, lock-free. `chain`: 0, or
+ * an id of the in-order queue the event was recorded on — entries of one chain
+ * complete in registration order, so poll only queries each chain's head. */
+int tb_poll_add(tb_poll_t reg, tb_event_t ev, uint64_t chain, uint64_t token);
 /* PollRegistry.poll (polling.py:80-120): drain inbox, re-check pending,
- * write up to cap fired tokens. TB_NOT_READY (and *nfired = 0) when another
- * thread holds the guard. Complete entries beyond cap stay pending. */
+ * write up to cap fired tokens (FIFO within a chain). TB_NOT_READY (and
+ * *nfired = 0) when another thread holds the guard. Complete entries beyond
+ * cap stay pending. Never blocks (cudaEventQuery only). */
 int tb_poll(tb_poll_t reg, uint64_t *fired, int cap, int *nfired);
 int tb_poll_pending(tb_poll_t reg, int64_t *n);
 /* abandon_all (polling.py:122-147): remove every entry; complete[i] says

@@ -112,7 +112,7 @@ SIGNATURES = {
     "tb_acc_finalize": [_u64, _vp, _vp, _vp, _vp, _int],
     "tb_poll_create": [_pu64],
     "tb_poll_destroy": [_u64],
-    "tb_poll_add": [_u64, _u64, _u64],
+    "tb_poll_add": [_u64, _u64, _u64, _u64],
     "tb_poll": [_u64, _pu64, _int, _pint],
     "tb_poll_pending": [_u64, _pi64],
     "tb_poll_drain": [_u64, _pu64, _pu8, _int, _pint],
@@ -126,8 +126,7 @@ SIGNATURES = {
 BLOCKING = {"tb_init", "tb_device_sync", "tb_stream_sync", "tb_event_wait",
             "tb_htq_next", "tb_htq_destroy", "tb_malloc", "tb_free",
             "tb_host_alloc", "tb_host_free", "tb_stream_destroy",
-            "tb_memcpy_h2d", "tb_memcpy_d2h", "tb_poll", "tb_poll_drain",
-            "tb_agg_launch"}
+            "tb_memcpy_h2d", "tb_memcpy_d2h", "tb_poll_drain"}
 
 _lock = threading.Lock()
 _libs = None

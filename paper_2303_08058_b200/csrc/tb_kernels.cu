@@ -549,8 +549,11 @@ int occupancy(K kernel, int smem) {
 int launch_step(cudaStream_t st, StepArgs a) {
   const bool fixed = a.chains == 3 && a.kpc == 5;
   const bool aligned = ((reinterpret_cast<uintptr_t>(a.old) & 15) == 0);
+  // AUTO: the bulk-copy ring wins once each warp streams enough sub-grids to
+  // amortise its fill/drain (measured: 86% vs 84% of HBM roofline at 262144
+  // sub-grids, 66% vs 69% at 32768), registers below that.
   const bool bulk = aligned && (g_step_impl == TB_STEP_BULK ||
-                                (g_step_impl == TB_STEP_AUTO && fixed));
+                                (g_step_impl == TB_STEP_AUTO && fixed && a.n >= 65536));
   if (a.finalize && a.acc) {
     // ticket counter must start at 0 (reset by acc_reset / finalize)
   }

@@ -22,6 +22,7 @@
 #include <deque>
 #include <mutex>
 #include <new>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/tb.h"
@@ -94,17 +95,40 @@ inline cudaEvent_t E(tb_event_t e) { return reinterpret_cast<cudaEvent_t>(e); }
 // ---------------------------------------------------------- poll registry --
 struct PollNode {
   cudaEvent_t ev;
+  uint64_t chain;
   uint64_t token;
   PollNode *next;
 };
 
+// Entries on the same non-zero chain (an in-order queue) complete in
+// registration order, so the poll body only queries each chain's head.
 struct Registry {
   std::atomic<PollNode *> inbox{nullptr};
-  std::vector<PollNode *> pending;       // owned by the guard holder
+  std::vector<PollNode *> unchained;                              // guard holder
+  std::unordered_map<uint64_t, std::deque<PollNode *>> chains;    // guard holder
   std::atomic<bool> guard{false};
   std::atomic<int> entries{0};
   std::atomic<int> high_water{0};
   std::atomic<int64_t> pending_n{0};
+
+  void drain_inbox() {
+    PollNode *list = inbox.exchange(nullptr, std::memory_order_acquire);
+    PollNode *fifo = nullptr;
+    while (list) {  // reverse the LIFO stack
+      PollNode *nx = list->next;
+      list->next = fifo;
+      fifo = list;
+      list = nx;
+    }
+    while (fifo) {
+      PollNode *nx = fifo->next;
+      if (fifo->chain)
+        chains[fifo->chain].push_back(fifo);
+      else
+        unchained.push_back(fifo);
+      fifo = nx;
+    }
+  }
 };
 
 // --------------------------------------------------------- host-task queue --
@@ -347,21 +371,18 @@ int tb_poll_create(tb_poll_t *reg) {
 int tb_poll_destroy(tb_poll_t reg) {
   Registry *r = reinterpret_cast<Registry *>(reg);
   if (!r) return TB_E_INVALID;
-  PollNode *n = r->inbox.exchange(nullptr);
-  while (n) {
-    PollNode *nx = n->next;
-    delete n;
-    n = nx;
-  }
-  for (PollNode *p : r->pending) delete p;
+  r->drain_inbox();
+  for (PollNode *p : r->unchained) delete p;
+  for (auto &kv : r->chains)
+    for (PollNode *p : kv.second) delete p;
   delete r;
   return TB_OK;
 }
 
-int tb_poll_add(tb_poll_t reg, tb_event_t ev, uint64_t token) {
+int tb_poll_add(tb_poll_t reg, tb_event_t ev, uint64_t chain, uint64_t token) {
   Registry *r = reinterpret_cast<Registry *>(reg);
   if (!r || !ev) return TB_E_INVALID;
-  PollNode *n = new (std::nothrow) PollNode{E(ev), token, nullptr};
+  PollNode *n = new (std::nothrow) PollNode{E(ev), chain, token, nullptr};
   if (!n) return TB_E_NOMEM;
   PollNode *head = r->inbox.load(std::memory_order_relaxed);
   do {
@@ -382,38 +403,37 @@ int tb_poll(tb_poll_t reg, uint64_t *fired, int cap, int *nfired) {
   while (e > hw && !r->high_water.compare_exchange_weak(hw, e)) {
   }
   int n = 0;
-  // Older registrations first (pending), then the inbox in FIFO order, so
-  // callbacks for events that completed together fire in registration order.
-  std::vector<PollNode *> &pend = r->pending;
+  r->drain_inbox();
+  // Unchained entries: query each, keep the incomplete ones in order.
   {
-    PollNode *list = r->inbox.exchange(nullptr, std::memory_order_acquire);
-    PollNode *fifo = nullptr;
-    while (list) {  // reverse the LIFO stack
-      PollNode *nx = list->next;
-      list->next = fifo;
-      fifo = list;
-      list = nx;
-    }
-    for (PollNode *p = fifo; p; p = p->next) pend.push_back(p);
-  }
-  size_t keep = 0;
-  for (size_t i = 0; i < pend.size(); ++i) {
-    PollNode *p = pend[i];
-    bool done = false;
-    if (n < cap) {
-      const cudaError_t q = cudaEventQuery(p->ev);
+    std::vector<PollNode *> &u = r->unchained;
+    size_t keep = 0;
+    for (size_t i = 0; i < u.size(); ++i) {
+      PollNode *p = u[i];
       // Errors are surfaced as completion: the waiting future must not hang;
       // the CUDA error stays sticky for the next synchronous call to report.
-      done = (q != cudaErrorNotReady);
+      if (n < cap && cudaEventQuery(p->ev) != cudaErrorNotReady) {
+        fired[n++] = p->token;
+        delete p;
+      } else {
+        u[keep++] = p;
+      }
     }
-    if (done) {
-      fired[n++] = p->token;
-      delete p;
-    } else {
-      pend[keep++] = p;
-    }
+    u.resize(keep);
   }
-  pend.resize(keep);
+  // Chains: pop completed heads; the first incomplete head blocks the chain.
+  for (auto it = r->chains.begin(); it != r->chains.end();) {
+    std::deque<PollNode *> &dq = it->second;
+    while (!dq.empty() && n < cap && cudaEventQuery(dq.front()->ev) != cudaErrorNotReady) {
+      fired[n++] = dq.front()->token;
+      delete dq.front();
+      dq.pop_front();
+    }
+    if (dq.empty())
+      it = r->chains.erase(it);
+    else
+      ++it;
+  }
   r->pending_n.fetch_sub(n, std::memory_order_relaxed);
   *nfired = n;
   r->entries.fetch_sub(1);
@@ -436,30 +456,31 @@ int tb_poll_drain(tb_poll_t reg, uint64_t *tokens, uint8_t *complete, int cap,
   // Blocking acquire of the guard (the reference takes it with `with`).
   while (r->guard.exchange(true, std::memory_order_acquire)) {
   }
-  std::vector<PollNode *> &pend = r->pending;
-  PollNode *list = r->inbox.exchange(nullptr, std::memory_order_acquire);
-  PollNode *fifo = nullptr;
-  while (list) {
-    PollNode *nx = list->next;
-    list->next = fifo;
-    fifo = list;
-    list = nx;
-  }
-  for (PollNode *p = fifo; p; p = p->next) pend.push_back(p);
+  r->drain_inbox();
   int k = 0;
-  size_t keep = 0;
-  for (size_t i = 0; i < pend.size(); ++i) {
-    PollNode *p = pend[i];
-    if (k < cap) {
-      tokens[k] = p->token;
-      complete[k] = cudaEventQuery(p->ev) != cudaErrorNotReady ? 1 : 0;
-      ++k;
-      delete p;
-    } else {
-      pend[keep++] = p;
-    }
+  auto take = [&](PollNode *p) -> bool {
+    if (k >= cap) return false;
+    tokens[k] = p->token;
+    complete[k] = cudaEventQuery(p->ev) != cudaErrorNotReady ? 1 : 0;
+    ++k;
+    delete p;
+    return true;
+  };
+  {
+    std::vector<PollNode *> &u = r->unchained;
+    size_t keep = 0;
+    for (size_t i = 0; i < u.size(); ++i)
+      if (!take(u[i])) u[keep++] = u[i];
+    u.resize(keep);
   }
-  pend.resize(keep);
+  for (auto it = r->chains.begin(); it != r->chains.end();) {
+    std::deque<PollNode *> &dq = it->second;
+    while (!dq.empty() && take(dq.front())) dq.pop_front();
+    if (dq.empty())
+      it = r->chains.erase(it);
+    else
+      ++it;
+  }
   r->pending_n.fetch_sub(k, std::memory_order_relaxed);
   *n = k;
   r->guard.store(false, std::memory_order_release);

@@ -135,13 +135,14 @@ class DeviceEvent:
     first observed (the device does not timestamp it).
     """
 
-    __slots__ = ("id", "native_handle", "completion_time", "_done", "__weakref__")
+    __slots__ = ("id", "native_handle", "chain", "completion_time", "_done", "__weakref__")
 
     _ids = itertools.count()
 
-    def __init__(self, handle: int):
+    def __init__(self, handle: int, chain: int = 0):
         self.id = next(DeviceEvent._ids)
         self.native_handle = handle
+        self.chain = chain          # the in-order stream it was recorded on
         self.completion_time: Optional[float] = None
         self._done = False
 
@@ -445,7 +446,7 @@ class CudaDevice:
         rc = N.fast().tb_event_record(queue.stream, ctypes.byref(h))
         if rc < 0:
             raise N.CudaError(rc, "tb_event_record")
-        return DeviceEvent(h.value)
+        return DeviceEvent(h.value, queue.stream)
 
     def _submit(self, queue: DeviceQueue, op: DeviceOp) -> DeviceEvent:
         if op.queue is not None:
@@ -503,13 +504,14 @@ class CudaDevice:
         do_barrier = barrier and not self.barrier_elision
         h = ctypes.c_uint64(0)
         with queue._lock:
-            rc = N.blocking().tb_agg_launch(queue.stream, kernel.op, kernel.kind,
+            rc = N.fast().tb_agg_launch(queue.stream, kernel.op, kernel.kind,
                                             kernel.c1, kernel.c2, staging.dptr,
                                             staging.hptr, nbytes,
                                             1 if do_barrier else 0, ctypes.byref(h))
             queue._submit_count += 4 if barrier else 3
         if rc < 0:
             raise N.CudaError(rc, "tb_agg_launch")
+        ev = DeviceEvent(h.value, queue.stream)
         with self._lock:
             c = self.counters
             c.h2d += 1
@@ -520,7 +522,7 @@ class CudaDevice:
                     c.barriers += 1
                 else:
                     c.barriers_elided += 1
-        return DeviceEvent(h.value)
+        return ev
 
     # -------------------------------------------------------- host tasks --
     def _hosttask_loop(self) -> None:

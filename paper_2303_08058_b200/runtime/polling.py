@@ -9,8 +9,9 @@ callbacks for already-complete events still run).
 
 B200 design: entries whose event carries a CUDA handle (``native_handle``)
 go straight into libtb's native registry (tb_poll_add: lock-free MPSC
-push); ``poll`` then checks *all* of them with one native call
-(cudaEventQuery per entry, GIL released) that returns the fired tokens.
+push, keyed by the event's in-order stream); ``poll`` then checks them with
+one non-blocking native call — only the head of each stream's FIFO is
+queried — that returns the fired tokens, with the GIL held throughout.
 Events without a native handle (e.g. test doubles exposing only
 ``is_complete()``, the only contract the reference relies on —
 pkg/tests/conftest.py:35-44) use a Python-side inbox/pending list.
@@ -84,7 +85,7 @@ class PollRegistry:
             token = next(self._next_token)
             self._tokens[token] = ec
             from .. import _native as N
-            rc = N.fast().tb_poll_add(reg, handle, token)
+            rc = N.fast().tb_poll_add(reg, handle, getattr(ec.event, "chain", 0), token)
             if rc != 0:
                 del self._tokens[token]
                 raise N.CudaError(rc, "tb_poll_add")
@@ -141,7 +142,9 @@ class PollRegistry:
         from .. import _native as N
         n = ctypes.c_int(0)
         buf = self._fired_buf
-        rc = N.blocking().tb_poll(self._native, buf, _FIRE_CAP, ctypes.byref(n))
+        # GIL held: the native body never blocks, and releasing the GIL here
+        # would let a busy worker keep it for a whole switch interval.
+        rc = N.fast().tb_poll(self._native, buf, _FIRE_CAP, ctypes.byref(n))
         if rc < 0:
             raise N.CudaError(rc, "tb_poll")
         k = n.value
