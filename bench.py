@@ -192,6 +192,8 @@ def main(argv=None):
     ap.add_argument("--step-impl", choices=["auto", "reg", "bulk", "regpf"], default="auto",
                     help="K2 variant (tb_set_option TB_OPT_STEP_IMPL)")
     ap.add_argument("--e2e-chunks", type=int, default=16)
+    ap.add_argument("--spw", type=int, default=0,
+                    help="K2 sub-grids per warp per CTA (0 = one persistent wave)")
     args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3)
 
@@ -214,6 +216,7 @@ def main(argv=None):
     N.call("tb_set_option", N.TB_OPT_STEP_IMPL,
            {"auto": N.TB_STEP_AUTO, "reg": N.TB_STEP_REG, "bulk": N.TB_STEP_BULK,
             "regpf": N.TB_STEP_REGPF}[args.step_impl])
+    N.call("tb_set_option", N.TB_OPT_STEP_SPW, args.spw)
 
     # Parity gate in the same run: the reference's GOLDEN_DEFAULTS.
     parity = run_reference_gpu(512, 15, device=dev)[0] == GOLDEN_DEFAULTS
@@ -268,7 +271,8 @@ def main(argv=None):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.e2e_steps):
-        st.step_host(host_in, host_in, host_stats, chunks=args.e2e_chunks)
+        st.step_host(host_in, host_in, host_stats, chunks=args.e2e_chunks, join=False)
+    st.join_host()
     e1.record()
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / max(args.e2e_steps, 1)
@@ -332,7 +336,7 @@ def main(argv=None):
                     "d2h_bytes_per_step": n_local * 512 * 8 + 16,
                     "ms_per_step": e2e_ms, "chunks": args.e2e_chunks,
                     "api": "RingStepper.step_host (pinned H2D | K2 | D2H pipelined "
-                           "over chunks on 3 streams)"},
+                           "over chunks on 3 streams, chained across steps)"},
             "gpu_launches": (1 if world == 1 else 2) * args.steps,
             "clocks": clocks,
             "wall_s_timed_region": wall,

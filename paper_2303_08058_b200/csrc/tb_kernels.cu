@@ -528,6 +528,19 @@ __global__ void __launch_bounds__(kStepThreads) k_step_bulk(StepArgs a) {
 }
 
 int g_step_impl = TB_STEP_AUTO;
+int g_step_spw = 0;   // sub-grids per warp per CTA; 0 = persistent (one wave)
+
+// CTAs for n sub-grids: one resident wave (occ CTAs per SM) by default, or
+// ceil(n / (warps * spw)) CTAs so the hardware scheduler balances the tail.
+inline int step_grid(int64_t n, int occ) {
+  if (g_step_spw > 0) {
+    int64_t b = (n + (int64_t)kStepWarps * g_step_spw - 1) / ((int64_t)kStepWarps * g_step_spw);
+    return (int)(b < 1 ? 1 : (b > (1LL << 30) ? (1LL << 30) : b));
+  }
+  int64_t b = (n + kStepWarps - 1) / kStepWarps;
+  const int64_t cap = (int64_t)tb::sm_count() * occ;
+  return (int)(b < 1 ? 1 : (b > cap ? cap : b));
+}
 
 inline int grid_for(int64_t work, int per_block, int max_blocks) {
   int64_t b = (work + per_block - 1) / per_block;
@@ -567,7 +580,7 @@ int launch_step(cudaStream_t st, StepArgs a) {
         attr_f = true;
       }
       if (!occ_f) occ_f = occupancy(k_step_bulk<3, 5>, kBulkSmem);
-      const int blocks = grid_for(a.n, kStepWarps, tb::sm_count() * occ_f);
+      const int blocks = step_grid(a.n, occ_f);
       k_step_bulk<3, 5><<<blocks, kStepThreads, kBulkSmem, st>>>(a);
     } else {
       if (!attr_g) {
@@ -576,29 +589,29 @@ int launch_step(cudaStream_t st, StepArgs a) {
         attr_g = true;
       }
       if (!occ_g) occ_g = occupancy(k_step_bulk<0, 0>, kBulkSmem);
-      const int blocks = grid_for(a.n, kStepWarps, tb::sm_count() * occ_g);
+      const int blocks = step_grid(a.n, occ_g);
       k_step_bulk<0, 0><<<blocks, kStepThreads, kBulkSmem, st>>>(a);
     }
   } else if (g_step_impl == TB_STEP_REGPF) {
     static int occ_f = 0, occ_g = 0;
     if (fixed) {
       if (!occ_f) occ_f = occupancy(k_step<3, 5, true>, 0);
-      const int blocks = grid_for(a.n, kStepWarps, tb::sm_count() * occ_f);
+      const int blocks = step_grid(a.n, occ_f);
       k_step<3, 5, true><<<blocks, kStepThreads, 0, st>>>(a);
     } else {
       if (!occ_g) occ_g = occupancy(k_step<0, 0, true>, 0);
-      const int blocks = grid_for(a.n, kStepWarps, tb::sm_count() * occ_g);
+      const int blocks = step_grid(a.n, occ_g);
       k_step<0, 0, true><<<blocks, kStepThreads, 0, st>>>(a);
     }
   } else {
     static int occ_f = 0, occ_g = 0;
     if (fixed) {
       if (!occ_f) occ_f = occupancy(k_step<3, 5, false>, 0);
-      const int blocks = grid_for(a.n, kStepWarps, tb::sm_count() * occ_f);
+      const int blocks = step_grid(a.n, occ_f);
       k_step<3, 5, false><<<blocks, kStepThreads, 0, st>>>(a);
     } else {
       if (!occ_g) occ_g = occupancy(k_step<0, 0, false>, 0);
-      const int blocks = grid_for(a.n, kStepWarps, tb::sm_count() * occ_g);
+      const int blocks = step_grid(a.n, occ_g);
       k_step<0, 0, false><<<blocks, kStepThreads, 0, st>>>(a);
     }
   }
@@ -614,6 +627,11 @@ int tb_set_option(int key, int value) {
   if (key == TB_OPT_STEP_IMPL) {
     if (value < TB_STEP_AUTO || value > TB_STEP_REGPF) return TB_E_INVALID;
     g_step_impl = value;
+    return TB_OK;
+  }
+  if (key == TB_OPT_STEP_SPW) {
+    if (value < 0) return TB_E_INVALID;
+    g_step_spw = value;
     return TB_OK;
   }
   return TB_E_INVALID;

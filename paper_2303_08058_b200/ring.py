@@ -146,6 +146,7 @@ class RingStepper:
         self.sums = torch.empty(n, **f64) if collect_subgrid_stats else None
         self.steps_done = 0
         self._streams = None
+        self._host_prev = None      # (chunk bounds, D2H events, steps_done)
         self.ops.init_cells(self.state[0], subgrids, self.lo)
         self.ops.acc_reset(self.acc)
 
@@ -202,6 +203,9 @@ class RingStepper:
         """
         if self.steps_done >= self.max_steps:
             raise RuntimeError("max_steps exceeded; raise max_steps")
+        if self._host_prev is not None:
+            self.join_host()        # downloads of a host step still read state
+            self._host_prev = None
         k = self.steps_done
         old, out = self.state[self.cur], self.state[1 - self.cur]
         lf, rf = self._halo(old)
@@ -229,17 +233,24 @@ class RingStepper:
         return self.result(k0)
 
     # ------------------------------------------------------ host buffers --
-    def step_host(self, host_in: torch.Tensor, host_out: torch.Tensor,
-                  host_stats: torch.Tensor, chunks: int = 16) -> None:
+    def step_host(self, host_in: torch.Tensor, host_out: Optional[torch.Tensor],
+                  host_stats: torch.Tensor, chunks: int = 16, join: bool = True) -> None:
         """One step on host-resident cells (the host-buffer drop-in path).
 
-        ``host_in``/``host_out``: pinned [n_local, 512] float64 (may alias);
-        ``host_stats``: pinned float64[2] receiving (piece, dt). Work is
-        enqueued on the current stream plus two copy streams and joined back
-        into the current stream; synchronise it before reading the outputs.
-        Per chunk c of sub-grids: H2D(c) on the upload stream; K2(c) once
-        H2D(c) and H2D(c+1) landed (c's right ghost lives in c+1); D2H(c) on
-        the download stream once K2(c) is done.
+        ``host_in``/``host_out``: pinned [n_local, 512] float64 (may alias;
+        ``host_out=None`` keeps the new generation on the device and returns
+        only the step result); ``host_stats``: pinned float64[2] receiving
+        (piece, dt). Work goes to the current stream plus an upload and a
+        download stream. Per chunk c of sub-grids: H2D(c) on the upload
+        stream; K2(c) once H2D(c) and H2D(c+1) landed (c's right ghost lives
+        in c+1); D2H(c) on the download stream once K2(c) is done.
+
+        Consecutive calls pipeline across steps: H2D(c) of the next step only
+        waits for this step's D2H(c) (the host rows and device rows it
+        overwrites), so uploads and downloads stream continuously in both
+        PCIe directions. ``join=False`` leaves the download stream un-joined
+        (call :meth:`join_host` before reading the outputs on the host or
+        timing on the current stream); ``join=True`` joins every step.
         """
         if self.steps_done >= self.max_steps:
             raise RuntimeError("max_steps exceeded; raise max_steps")
@@ -255,10 +266,20 @@ class RingStepper:
         bounds = chunk_bounds(self.n, chunks)
         ev_h2d = [torch.cuda.Event() for _ in bounds]
         ev_k2 = [torch.cuda.Event() for _ in bounds]
+        ev_d2h = [torch.cuda.Event() for _ in bounds]
         ev_faces = torch.cuda.Event()
         n = self.n
-        up.wait_stream(main)          # previous step's reads of `old` are done
+        last = len(bounds) - 1
+        prev = self._host_prev
+        chained = (prev is not None and prev[0] == bounds and prev[2] == self.steps_done)
+        if not chained:
+            # previous work on these buffers came from elsewhere: full order
+            up.wait_stream(main)
+            up.wait_stream(down)
         with torch.cuda.stream(up):
+            if chained:
+                up.wait_event(prev[1][0])
+                up.wait_event(prev[1][last])
             faces = self.myfaces if self.world > 1 else self.halo
             if self.world > 1:
                 faces[0].copy_(host_in[0, :FACE], non_blocking=True)
@@ -267,13 +288,14 @@ class RingStepper:
                 faces[0].copy_(host_in[n - 1, CELLS - FACE:], non_blocking=True)
                 faces[1].copy_(host_in[0, :FACE], non_blocking=True)
             ev_faces.record(up)
-            for (lo, hi), ev in zip(bounds, ev_h2d):
+            for c, ((lo, hi), ev) in enumerate(zip(bounds, ev_h2d)):
+                if chained:
+                    up.wait_event(prev[1][c])
                 old[lo:hi].copy_(host_in[lo:hi], non_blocking=True)
                 ev.record(up)
         main.wait_event(ev_faces)
         if self.world > 1:
             self._exchange(self.myfaces[0], self.myfaces[1])
-        last = len(bounds) - 1
         for c, (lo, hi) in enumerate(bounds):
             main.wait_event(ev_h2d[c])
             if c < last:
@@ -286,15 +308,24 @@ class RingStepper:
         ev_done = torch.cuda.Event()
         ev_done.record(main)
         with torch.cuda.stream(down):
-            for (lo, hi), ev in zip(bounds, ev_k2):
-                down.wait_event(ev)
-                host_out[lo:hi].copy_(out[lo:hi], non_blocking=True)
+            for c, (lo, hi) in enumerate(bounds):
+                down.wait_event(ev_k2[c])
+                if host_out is not None:
+                    host_out[lo:hi].copy_(out[lo:hi], non_blocking=True)
+                ev_d2h[c].record(down)
             down.wait_event(ev_done)
             host_stats[0:1].copy_(self.pieces[k:k + 1], non_blocking=True)
             host_stats[1:2].copy_(self.dts[k:k + 1], non_blocking=True)
-        main.wait_stream(down)
         self.cur = 1 - self.cur
         self.steps_done += 1
+        self._host_prev = (bounds, ev_d2h, self.steps_done)
+        if join:
+            self.join_host()
+
+    def join_host(self) -> None:
+        """Make the current stream wait for all enqueued host-buffer downloads."""
+        if self._streams is not None:
+            torch.cuda.current_stream(self.device).wait_stream(self._streams[1])
 
     def result(self, first_step: int = 0) -> RingResult:
         k = self.steps_done

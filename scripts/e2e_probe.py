@@ -1,8 +1,6 @@
-"""Timeline probe of RingStepper.step_host (host-buffer path) on the GPU box.
-
-Prints per-step GPU time, host enqueue time, and — for one instrumented step
-— when each chunk's H2D / K2 / D2H finished relative to the step start.
-"""
+"""Probe of the host-buffer path on the GPU box: raw pinned copy rates on the
+state-sized float64 buffers, and RingStepper.step_host over chunk counts, with
+and without the D2H of the new cells. One JSON line."""
 
 import json
 import sys
@@ -12,46 +10,58 @@ import torch
 
 sys.path.insert(0, ".")
 from paper_2303_08058_b200 import _native as N  # noqa: E402
-from paper_2303_08058_b200.ring import RingStepper, chunk_bounds  # noqa: E402
+from paper_2303_08058_b200.ring import RingStepper  # noqa: E402
 
 
-def main():
-    S = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
-    chunks = int(sys.argv[2]) if len(sys.argv) > 2 else 16
-    N.init(0)
-    st = RingStepper(S, max_steps=64)
-    host = torch.empty((S, 512), dtype=torch.float64, pin_memory=True)
-    host.copy_(st.cells)
-    stats = torch.empty(2, dtype=torch.float64, pin_memory=True)
-    torch.cuda.synchronize()
-    out = {"subgrids": S, "chunks": chunks, "steps": []}
-    for k in range(6):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        t0 = time.perf_counter()
-        st.step_host(host, host, stats, chunks=chunks)
-        t_enq = time.perf_counter() - t0
-        e1.record()
-        torch.cuda.synchronize()
-        out["steps"].append({"gpu_ms": e0.elapsed_time(e1), "enqueue_ms": t_enq * 1e3})
-    # plain serial path for comparison: one H2D, one step, one D2H
+def gpu_ms(fn, reps=5):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    st.cells.copy_(host, non_blocking=True)
-    st.step()
-    host.copy_(st.cells, non_blocking=True)
-    e1.record()
+    fn()
     torch.cuda.synchronize()
-    out["serial_ms"] = e0.elapsed_time(e1)
-    # raw copies of the same size for reference
-    d = torch.empty_like(st.cells)
-    for name, fn in [("h2d_only", lambda: d.copy_(host, non_blocking=True)),
-                     ("d2h_only", lambda: host.copy_(d, non_blocking=True))]:
+    best = 1e9
+    for _ in range(reps):
         e0.record()
         fn()
         e1.record()
         torch.cuda.synchronize()
-        out[name + "_ms"] = e0.elapsed_time(e1)
+        best = min(best, e0.elapsed_time(e1))
+    return best
+
+
+def main():
+    S = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
+    N.init(0)
+    st = RingStepper(S, max_steps=512)
+    host = torch.empty((S, 512), dtype=torch.float64, pin_memory=True)
+    host2 = torch.empty((S, 512), dtype=torch.float64, pin_memory=True)
+    host.copy_(st.cells)
+    stats = torch.empty(2, dtype=torch.float64, pin_memory=True)
+    d = torch.empty_like(st.cells)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    out = {"subgrids": S, "bytes": S * 4096}
+    out["h2d_ms"] = gpu_ms(lambda: d.copy_(host, non_blocking=True))
+    out["d2h_ms"] = gpu_ms(lambda: host2.copy_(d, non_blocking=True))
+
+    def both():
+        cur = torch.cuda.current_stream()
+        s1.wait_stream(cur)
+        s2.wait_stream(cur)
+        with torch.cuda.stream(s1):
+            d.copy_(host, non_blocking=True)
+        with torch.cuda.stream(s2):
+            host2.copy_(st.cells, non_blocking=True)
+        cur.wait_stream(s1)
+        cur.wait_stream(s2)
+
+    out["h2d_and_d2h_concurrent_ms"] = gpu_ms(both)
+    for chunks in (1, 2, 4, 8, 16, 32):
+        out[f"step_host_c{chunks}_ms"] = gpu_ms(lambda: st.step_host(host, host, stats, chunks))
+        out[f"step_host_noD2H_c{chunks}_ms"] = gpu_ms(
+            lambda: st.step_host(host, None, stats, chunks))
+    t0 = time.perf_counter()
+    for _ in range(10):
+        st.step_host(host, host, stats, 16)
+    out["enqueue_ms_c16"] = (time.perf_counter() - t0) * 100
+    torch.cuda.synchronize()
     print(json.dumps(out))
 
 

@@ -199,9 +199,43 @@ def test_step_host_pipeline_matches_oracle(N, s, chunks):
     cs, dts, want = mo.run_reference_cells(s, 3)
     pieces = []
     for _ in range(3):
-        st.step_host(cells, cells, stats, chunks=chunks)
+        st.step_host(cells, cells, stats, chunks=chunks, join=False)
+        st.join_host()
         torch.cuda.synchronize()
         pieces.append(stats[0].item())
         assert stats[1].item() == dts[len(pieces) - 1]
     np.testing.assert_array_equal(cells.numpy(), want)
     assert st.result().checksum == cs
+
+
+@pytest.mark.parametrize("spw", [1, 2, 5])
+def test_step_grid_granularity(N, spw):
+    N.call("tb_set_option", N.TB_OPT_STEP_SPW, spw)
+    try:
+        from paper_2303_08058_b200.ring import run_reference_gpu
+        cs, dts = run_reference_gpu(4097, 2)
+        ccs, cdts = mo.run_reference(4097, 2)
+        assert cs == ccs and dts == cdts
+    finally:
+        N.call("tb_set_option", N.TB_OPT_STEP_SPW, 0)
+
+
+def test_step_host_chained_unjoined_and_mixed_with_resident(N):
+    from paper_2303_08058_b200.ring import RingStepper
+    s = 777
+    st = RingStepper(s, max_steps=16)
+    cells = torch.from_numpy(mo.initial_cells(s)).pin_memory()
+    stats = torch.zeros(2, dtype=torch.float64).pin_memory()
+    for _ in range(4):                      # chained, never joined in between
+        st.step_host(cells, cells, stats, chunks=5, join=False)
+    st.join_host()
+    torch.cuda.synchronize()
+    cs, dts, want = mo.run_reference_cells(s, 4)
+    np.testing.assert_array_equal(cells.numpy(), want)
+    # host step without download, then resident steps continue from device state
+    st.step_host(cells, None, stats, chunks=3)
+    st.step()
+    torch.cuda.synchronize()
+    cs6, dts6, want6 = mo.run_reference_cells(s, 6)
+    np.testing.assert_array_equal(st.cells.cpu().numpy(), want6)
+    assert st.result().checksum == cs6 and st.result().dts == dts6

@@ -247,3 +247,16 @@ def test_buffer_reuse_across_steps(stacks):
     launches = sum(a.launches for a in s.aggs)
     assert s.buffers.created + s.buffers.reused == launches
     assert 0 < s.buffers.reused and s.buffers.created < launches
+
+
+@pytest.mark.parametrize("block", [2, 3, 8, 16])
+def test_coarsened_tasks_are_bit_identical(stacks, golden, block):
+    s = stacks(workers=3, executors=2, max_agg=4)
+    sc = build_scenario(ScenarioConfig(subgrids=16, steps=3, task_subgrids=block))
+    by_grid = [s.aggs[i % len(s.aggs)] for i in range(16)]
+    res = run_scenario(sc, s.runtime, s.device, s.aggs, by_grid)
+    assert res.checksum.hex() == golden["machine"]["16x3"]["checksum"]
+    cells = np.load(__import__("conftest").TESTS + "/golden/cells.npz")["cells_16x3"]
+    np.testing.assert_array_equal(sc.cells(), cells)
+    cs, dts = mo.run_reference(16, 3)
+    assert res.dts == dts
