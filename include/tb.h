@@ -70,6 +70,8 @@ extern "C" {
 #define TB_STEP_REG 1           /* direct ld.global.nc into registers       */
 #define TB_STEP_BULK 2          /* cp.async.bulk smem ring + mbarriers      */
 #define TB_STEP_REGPF 3         /* registers + next-sub-grid prefetch       */
+#define TB_STEP_LEAN 4          /* registers capped at 48 (more warps/SM)   */
+#define TB_STEP_PAIR 5          /* a warp pair per sub-grid, 8 cells/lane   */
 #define TB_OPT_STEP_SPW 2       /* K2 sub-grids per warp per CTA; 0 = one
                                    persistent wave (default)                 */
 

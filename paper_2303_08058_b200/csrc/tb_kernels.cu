@@ -399,8 +399,8 @@ __device__ __forceinline__ void step_epilogue(const StepArgs &a,
 // K2a: direct loads into registers (ld.global.nc, no L1 allocate). With PF,
 // the next sub-grid's 16 values per lane are loaded before this one is
 // transformed (register double buffer: more MLP, fewer resident warps).
-template <int CHAINS, int KPC, bool PF>
-__global__ void __launch_bounds__(kStepThreads) k_step(StepArgs a) {
+template <int CHAINS, int KPC, bool PF, int MINB = 1>
+__global__ void __launch_bounds__(kStepThreads, MINB) k_step(StepArgs a) {
   __shared__ unsigned long long s_limbs[TB_ACC_LIMBS];
   __shared__ long long s_min[kStepWarps];
   __shared__ int s_last;
@@ -441,6 +441,105 @@ __global__ void __launch_bounds__(kStepThreads) k_step(StepArgs a) {
       for (int i = 0; i < 16; ++i) v[i] = ld_stream(src + 8 * i);
       subgrid_body<CHAINS, KPC>(a, g, lane, v, s_limbs, wmin);
     }
+  }
+  step_epilogue(a, s_limbs, s_min, wmin, &s_last);
+}
+
+// K2c: a warp PAIR per sub-grid, 8 cells per lane (half the registers of
+// K2a, so twice the resident warps). Warp q of the pair holds blocks 2q and
+// 2q+1; lane (h, bb, r) holds a[128(2q+bb) + r + 8(8h + i')], i' = 0..7. The
+// pairwise order is kept exactly: the h=0 lane's sequential partial of r_j is
+// handed to its h=1 partner (shuffle) which continues the same sequence;
+// butterflies give B_{2q}+B_{2q+1} per warp; (B0+B1)+(B2+B3) is formed across
+// the pair through shared memory behind a 64-thread named barrier.
+template <int CHAINS, int KPC>
+__device__ __forceinline__ void run_chains8(double (&v)[8], int chains, int kpc) {
+  if (CHAINS > 0) {
+#pragma unroll
+    for (int c = 0; c < CHAINS; ++c)
+#pragma unroll
+      for (int k = 0; k < KPC; ++k) {
+        const double c1 = kC1[k], c2 = kC2[k];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = xform(v[i], c1, c2);
+      }
+  } else {
+    for (int c = 0; c < chains; ++c)
+      for (int k = 0; k < kpc; ++k) {
+        const double c1 = kC1[k], c2 = kC2[k];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = xform(v[i], c1, c2);
+      }
+  }
+}
+
+template <int CHAINS, int KPC>
+__global__ void __launch_bounds__(kStepThreads, 6) k_step_pair(StepArgs a) {
+  __shared__ unsigned long long s_limbs[TB_ACC_LIMBS];
+  __shared__ long long s_min[kStepWarps];
+  __shared__ double s_pair[2][kStepWarps / 2][2][2];   // [parity][pair][q][sum,min]
+  __shared__ int s_last;
+  if (a.acc) {
+    for (int i = threadIdx.x; i < TB_ACC_LIMBS; i += blockDim.x) s_limbs[i] = 0ULL;
+    __syncthreads();
+  }
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int pair = warp >> 1, q = warp & 1;
+  const int h = lane >> 4, bb = (lane >> 3) & 1, r = lane & 7;
+  const int blk = 2 * q + bb;
+  const int lane_off = 128 * blk + r + 64 * h;
+  constexpr int kPairs = kStepWarps / 2;
+  double wmin = CUDART_INF;
+  int it = 0;
+  for (int64_t g = (int64_t)blockIdx.x * kPairs + pair; g < a.n;
+       g += (int64_t)gridDim.x * kPairs, ++it) {
+    const double *src = a.old + g * TB_CELLS + lane_off;
+    double v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = ld_stream(src + 8 * i);
+    if (q == 0 && lane < 8) {            // cells 0..7: block 0, i = 0
+      const double *lf =
+          g == 0 ? a.left_face : a.old + (g - 1) * TB_CELLS + (TB_CELLS - TB_FACE);
+      v[0] = __dmul_rn(0.5, __dadd_rn(v[0], lf[r]));
+    } else if (q == 1 && lane >= 24) {   // cells 504..511: block 3, i = 15
+      const double *rf = g == a.n - 1 ? a.right_face : a.old + (g + 1) * TB_CELLS;
+      v[7] = __dmul_rn(0.5, __dadd_rn(v[7], rf[r]));
+    }
+    run_chains8<CHAINS, KPC>(v, a.chains, a.kpc);
+    double *dst = a.out + g * TB_CELLS + lane_off;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dst[8 * i] = v[i];
+    double part = v[0], m = v[0];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) m = fmin(m, v[i]);
+    if (h == 0) {
+#pragma unroll
+      for (int i = 1; i < 8; ++i) part = __dadd_rn(part, v[i]);
+    }
+    const double from_h0 = __shfl_xor_sync(0xffffffffu, part, 16);
+    double sacc = from_h0;   // h=1: continue the sequence a[j+64], a[j+72], ...
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sacc = __dadd_rn(sacc, v[i]);
+    // r-butterfly (xor 1, 2, 4) then the bb pair (xor 8); meaningful in h=1
+#pragma unroll
+    for (int x = 1; x < 16; x <<= 1) sacc = __dadd_rn(sacc, __shfl_xor_sync(0xffffffffu, sacc, x));
+#pragma unroll
+    for (int x = 1; x < 32; x <<= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, x));
+    double(*slot)[2] = s_pair[it & 1][pair];
+    if (lane == 16) {
+      slot[q][0] = sacc;
+      slot[q][1] = m;
+    }
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + pair), "r"(64) : "memory");
+    if (q == 0 && lane == 0) {
+      const double s = __dadd_rn(slot[0][0], slot[1][0]);
+      const double mm = fmin(slot[0][1], slot[1][1]);
+      if (a.sums) a.sums[g] = s;
+      if (a.mins) a.mins[g] = mm;
+      if (a.acc) acc_add_digits(s_limbs, s);
+    }
+    wmin = fmin(wmin, m);
   }
   step_epilogue(a, s_limbs, s_min, wmin, &s_last);
 }
@@ -603,6 +702,21 @@ int launch_step(cudaStream_t st, StepArgs a) {
       const int blocks = step_grid(a.n, occ_g);
       k_step<0, 0, true><<<blocks, kStepThreads, 0, st>>>(a);
     }
+  } else if (g_step_impl == TB_STEP_LEAN && fixed) {
+    // registers capped at 48 (5 CTAs = 40 warps per SM; a few spill slots)
+    static int occ = 0;
+    if (!occ) occ = occupancy(k_step<3, 5, false, 5>, 0);
+    k_step<3, 5, false, 5><<<step_grid(a.n, occ), kStepThreads, 0, st>>>(a);
+  } else if (g_step_impl == TB_STEP_PAIR) {
+    // a warp pair per sub-grid: the grid helper counts pairs as "warps"
+    static int occ_f = 0, occ_g = 0;
+    int &occ = fixed ? occ_f : occ_g;
+    if (!occ) occ = fixed ? occupancy(k_step_pair<3, 5>, 0) : occupancy(k_step_pair<0, 0>, 0);
+    const int blocks = step_grid(2 * a.n, occ);
+    if (fixed)
+      k_step_pair<3, 5><<<blocks, kStepThreads, 0, st>>>(a);
+    else
+      k_step_pair<0, 0><<<blocks, kStepThreads, 0, st>>>(a);
   } else {
     static int occ_f = 0, occ_g = 0;
     if (fixed) {
@@ -625,7 +739,7 @@ extern "C" {
 
 int tb_set_option(int key, int value) {
   if (key == TB_OPT_STEP_IMPL) {
-    if (value < TB_STEP_AUTO || value > TB_STEP_REGPF) return TB_E_INVALID;
+    if (value < TB_STEP_AUTO || value > TB_STEP_PAIR) return TB_E_INVALID;
     g_step_impl = value;
     return TB_OK;
   }

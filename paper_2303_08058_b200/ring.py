@@ -13,11 +13,13 @@ piece, dt, ``checksum += piece``) — on one device K4 runs in K2's last CTA
 (src/reference.py:23-50) at any rank count.
 
 Multi-GPU (one process per GPU, torch.distributed/NCCL): the ring is split
-into contiguous ranges; per step each rank sends its first sub-grid's left
-face to rank-1 and its last sub-grid's right face to rank+1 (64 B each, from
-the previous generation — Jacobi, src/miniapp.py:89-93), then after K2 the
-accumulator's limbs are all-reduced with SUM and its min word with MIN
-(int64): exact, so every partition gives the single-device checksum.
+into contiguous ranges; per step each rank posts the send of its first
+sub-grid's left face to rank-1 and its last sub-grid's right face to rank+1
+(64 B each, from the previous generation — Jacobi, src/miniapp.py:89-93),
+runs K2 on its interior sub-grids while the faces are in flight, then the two
+boundary sub-grids; the accumulator's limbs are then all-reduced with SUM and
+its min word with MIN (int64): exact, so every partition gives the
+single-device checksum.
 
 Host-buffer path (``step_host``): the drop-in for callers that keep the
 cells on the host (the reference's Scenario.grids). The H2D of the input
@@ -161,8 +163,9 @@ class RingStepper:
         self.state[self.cur].copy_(host, non_blocking=True)
 
     # --------------------------------------------------------------- step --
-    def _exchange(self, send_left: torch.Tensor, send_right: torch.Tensor) -> None:
-        """Ring halo exchange into self.halo = [left ghost, right ghost]."""
+    def _exchange_start(self, send_left: torch.Tensor, send_right: torch.Tensor):
+        """Post the ring halo exchange into self.halo = [left ghost, right
+        ghost]; returns the requests (wait them before reading the halo)."""
         import torch.distributed as dist
         left = (self.rank - 1) % self.world
         right = (self.rank + 1) % self.world
@@ -173,15 +176,11 @@ class RingStepper:
                dist.P2POp(dist.irecv, self.halo[1], right, self.group),
                dist.P2POp(dist.isend, send_right, right, self.group),
                dist.P2POp(dist.irecv, self.halo[0], left, self.group)]
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
+        return dist.batch_isend_irecv(ops)
 
-    def _halo(self, old: torch.Tensor) -> Tuple[torch.Tensor, torch.Tensor]:
-        if self.world == 1:
-            # single-device ring: wrap within this rank
-            return old[self.n - 1, CELLS - FACE:], old[0, :FACE]
-        self._exchange(old[0, :FACE], old[self.n - 1, CELLS - FACE:])
-        return self.halo[0], self.halo[1]
+    def _exchange(self, send_left: torch.Tensor, send_right: torch.Tensor) -> None:
+        for req in self._exchange_start(send_left, send_right):
+            req.wait()
 
     def _reduce_acc(self) -> None:
         import torch.distributed as dist
@@ -208,23 +207,52 @@ class RingStepper:
             self._host_prev = None
         k = self.steps_done
         old, out = self.state[self.cur], self.state[1 - self.cur]
-        lf, rf = self._halo(old)
-        if kernel_events is not None:
-            kernel_events[0].record()
-        fused = self.world == 1 and hasattr(self.ops, "step_final")
-        if fused:
-            self.ops.step_final(old, out, lf, rf, self.chains, self.kpc, self.acc,
-                                self.pieces[k:k + 1], self.dts[k:k + 1], self.checksum,
-                                self.mins, self.sums)
-        else:
-            self.ops.step(old, out, lf, rf, self.chains, self.kpc, self.acc,
-                          self.mins, self.sums)
-        if kernel_events is not None:
-            kernel_events[1].record()
-        if not fused:
+        n = self.n
+        if self.world > 1:
+            self._step_partitioned(old, out, kernel_events)
             self._close(k)
+        else:
+            lf, rf = old[n - 1, CELLS - FACE:], old[0, :FACE]   # ring wraps locally
+            if kernel_events is not None:
+                kernel_events[0].record()
+            if hasattr(self.ops, "step_final"):
+                self.ops.step_final(old, out, lf, rf, self.chains, self.kpc, self.acc,
+                                    self.pieces[k:k + 1], self.dts[k:k + 1],
+                                    self.checksum, self.mins, self.sums)
+            else:
+                self.ops.step(old, out, lf, rf, self.chains, self.kpc, self.acc,
+                              self.mins, self.sums)
+                self._close(k)
+            if kernel_events is not None:
+                kernel_events[1].record()
         self.cur = 1 - self.cur
         self.steps_done += 1
+
+    def _step_partitioned(self, old, out, kernel_events) -> None:
+        """N>1: post the halo exchange, run K2 on the interior sub-grids while
+        the 2 x 64 B faces are in flight, then the two boundary sub-grids."""
+        n = self.n
+        reqs = self._exchange_start(old[0, :FACE], old[n - 1, CELLS - FACE:])
+        if kernel_events is not None:
+            kernel_events[0].record()
+        mins, sums = self.mins, self.sums
+
+        def part(lo, hi, lf, rf):
+            self.ops.step(old[lo:hi], out[lo:hi], lf, rf, self.chains, self.kpc, self.acc,
+                          None if mins is None else mins[lo:hi],
+                          None if sums is None else sums[lo:hi])
+
+        if n > 2:       # interior: every ghost face is local
+            part(1, n - 1, old[0, CELLS - FACE:], old[n - 1, :FACE])
+        for req in reqs:
+            req.wait()
+        if n == 1:
+            part(0, 1, self.halo[0], self.halo[1])
+        else:
+            part(0, 1, self.halo[0], old[1, :FACE])
+            part(n - 1, n, old[n - 2, CELLS - FACE:], self.halo[1])
+        if kernel_events is not None:
+            kernel_events[1].record()
 
     def run(self, steps: int) -> RingResult:
         k0 = self.steps_done

@@ -81,7 +81,7 @@ def _worker(rank, world, port, subgrids, steps, q):
 
 
 @pytest.mark.parametrize("world,subgrids,steps", [(2, 8, 2), (2, 3, 3), (3, 16, 3),
-                                                  (3, 7, 2)])
+                                                  (3, 7, 2), (4, 4, 2), (4, 13, 2)])
 def test_partitioned_ring_matches_single_device(world, subgrids, steps):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
