@@ -149,6 +149,8 @@ class DeviceEvent:
     def is_complete(self) -> bool:
         if self._done:
             return True
+        if not self.native_handle:
+            return False            # parked by a lazy device, not issued yet
         rc = N.fast().tb_event_query(self.native_handle)
         if rc == N.TB_NOT_READY:
             return False
@@ -293,8 +295,6 @@ class CudaDevice:
                  hosttask_side_streams: int = 4):
         if clock_mode is not ClockMode.REAL:
             raise ModeError("a CUDA device runs on the real clock only")
-        if lazy_submit:
-            raise ModeError("lazy_submit is not supported on the CUDA device")
         if compute_slots < 1:
             raise ValueError("compute_slots must be >= 1")
         N.init(device_index)
@@ -304,7 +304,11 @@ class CudaDevice:
         self.clock_mode = clock_mode
         self.latency = latency
         self.barrier_elision = barrier_elision
-        self.lazy_submit = False
+        # Lazy submit (src/device.py:441-453, the hipSYCL flush workaround,
+        # PAPER.md:587-600): ops park on the host until flush() — which the
+        # Integration installs as a poll-registry flush hook — issues them.
+        self.lazy_submit = lazy_submit
+        self._held: list = []            # (queue, op, placeholder event, issue fn)
         self.event_pool = event_pool
         self.record_timeline = record_timeline
         self.timeline: list = []
@@ -352,6 +356,8 @@ class CudaDevice:
         self.barrier_elision = enabled
 
     def event_status(self, event: DeviceEvent) -> EventStatus:
+        if self.lazy_submit and not event.native_handle:
+            self.flush()            # first status query kicks the lazy scheduler
         return event.status
 
     def event_wait(self, event: DeviceEvent) -> None:
@@ -360,6 +366,8 @@ class CudaDevice:
             self.counters.event_waits += 1
             if not self._alive:
                 raise DeviceGoneError("device destroyed while waiting")
+        if self.lazy_submit and not event.native_handle:
+            self.flush()
         if event.is_complete():
             return
         worker = _context.current_worker()
@@ -379,6 +387,8 @@ class CudaDevice:
 
     def register_host_task(self, event: DeviceEvent, cb: Callable[[], None],
                            on_abandon: Optional[Callable] = None) -> None:
+        if self.lazy_submit and not event.native_handle:
+            self.flush()
         with self._ht_lock:
             if not self._alive:
                 raise DeviceGoneError("device destroyed")
@@ -393,10 +403,27 @@ class CudaDevice:
             raise N.CudaError(rc, "tb_host_task")
 
     def flush(self) -> None:
-        """Nothing is parked on a CUDA device (no lazy submit)."""
+        """Issue every op parked by lazy submit, in submission order."""
+        if not self.lazy_submit:
+            return
+        with self._lock:
+            held, self._held = self._held, []
+        for queue, op, ev, issue in held:
+            real = issue()
+            # hand the recorded CUDA event to the placeholder callers hold
+            ev.native_handle, real.native_handle = real.native_handle, 0
+            ev.chain = real.chain
+            if op is not None:
+                op.event = ev
 
     def has_pending(self) -> bool:
+        """Ops issued to the GPU and not yet complete (parked ops excluded,
+        as in the reference's lazy mode, src/device.py:355-357)."""
         return any(q.incomplete_count() for q in self._queues)
+
+    def held_count(self) -> int:
+        with self._lock:
+            return len(self._held)
 
     def hosttask_backlog(self) -> int:
         with self._ht_lock:
@@ -448,11 +475,25 @@ class CudaDevice:
             raise N.CudaError(rc, "tb_event_record")
         return DeviceEvent(h.value, queue.stream)
 
+    def _park(self, queue: DeviceQueue, op, issue) -> DeviceEvent:
+        ev = DeviceEvent(0)
+        if op is not None:
+            op.event = ev
+        with self._lock:
+            self._held.append((queue, op, ev, issue))
+        return ev
+
     def _submit(self, queue: DeviceQueue, op: DeviceOp) -> DeviceEvent:
         if op.queue is not None:
             raise ValueError("op already submitted")
         if not self._alive:
             raise DeviceGoneError("device destroyed")
+        if self.lazy_submit:
+            op.queue = queue
+            return self._park(queue, op, lambda: self._issue(queue, op))
+        return self._issue(queue, op)
+
+    def _issue(self, queue: DeviceQueue, op: DeviceOp) -> DeviceEvent:
         c = self.counters
         s = queue.stream
         with queue._lock:
@@ -501,6 +542,13 @@ class CudaDevice:
         H2D(staging) ; kernel ; [barrier] ; D2H(staging) ; record."""
         if not self._alive:
             raise DeviceGoneError("device destroyed")
+        if self.lazy_submit:
+            return self._park(queue, None, lambda: self._issue_batch(
+                queue, kernel, staging, nbytes, barrier))
+        return self._issue_batch(queue, kernel, staging, nbytes, barrier)
+
+    def _issue_batch(self, queue: DeviceQueue, kernel: DeviceKernel,
+                     staging: DeviceBuffer, nbytes: int, barrier: bool) -> DeviceEvent:
         do_barrier = barrier and not self.barrier_elision
         h = ctypes.c_uint64(0)
         with queue._lock:

@@ -382,3 +382,42 @@ def test_native_poll_registry_single_entrant_under_hammer(stacks):
         t.join()
     assert fired[0] == 2000
     assert reg.entry_high_water == 1
+
+
+def test_lazy_device_flushes_from_the_poll_hook():
+    # pkg/tests/test_bridge.py:234-251 on CUDA: parked until a poll flushes
+    rt = Runtime(2)
+    d = CudaDevice(lazy_submit=True)
+    try:
+        integ = Integration(rt, d, IntegrationMode.POLLING)
+        q = d.queue()
+        ev = q.submit(make_kernel(16))
+        assert d.held_count() == 1 and d.snapshot_counters()["kernels"] == 0
+        assert not ev.is_complete()
+        fut = integ.get_future(ev)
+        fut.result(timeout=10)               # idle workers poll -> flush hook
+        assert ev.is_complete() and d.held_count() == 0
+        assert d.snapshot_counters()["kernels"] == 1
+    finally:
+        rt.shutdown()
+        d.destroy()
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_lazy_device_machine_golden(golden, mode):
+    rt = Runtime(2, seed=3)
+    d = CudaDevice(lazy_submit=True)
+    try:
+        integ = Integration(rt, d, mode)
+        pool = ExecutorPool(integ, 2)
+        bufs = BufferPool(d)
+        aggs = [AggregationExecutor(ex, 4, bufs) for ex in pool.executors]
+        for a in aggs:
+            for k in range(5):
+                a.register_kind(k, kernel_transform(k))
+        sc = build_scenario(ScenarioConfig(subgrids=8, steps=2))
+        res = run_scenario(sc, rt, d, aggs, [aggs[i % 2] for i in range(8)])
+        assert res.checksum == fx(golden["reference_test_literals"]["GOLDEN_8X2"])
+    finally:
+        rt.shutdown()
+        d.destroy()
