@@ -189,7 +189,7 @@ def main(argv=None):
     ap.add_argument("--cpu-budget", type=float, default=10.0,
                     help="seconds of CPU work for the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--step-impl", choices=["auto", "reg", "bulk", "regpf", "lean", "pair"], default="auto",
+    ap.add_argument("--step-impl", choices=["auto", "reg", "bulk", "regpf", "lean", "pair", "bulk1"], default="auto",
                     help="K2 variant (tb_set_option TB_OPT_STEP_IMPL)")
     ap.add_argument("--e2e-chunks", type=int, default=16)
     ap.add_argument("--spw", type=int, default=0,
@@ -216,7 +216,7 @@ def main(argv=None):
     N.call("tb_set_option", N.TB_OPT_STEP_IMPL,
            {"auto": N.TB_STEP_AUTO, "reg": N.TB_STEP_REG, "bulk": N.TB_STEP_BULK,
             "regpf": N.TB_STEP_REGPF, "lean": N.TB_STEP_LEAN,
-            "pair": N.TB_STEP_PAIR}[args.step_impl])
+            "pair": N.TB_STEP_PAIR, "bulk1": N.TB_STEP_BULK1}[args.step_impl])
     N.call("tb_set_option", N.TB_OPT_STEP_SPW, args.spw)
 
     # Parity gate in the same run: the reference's GOLDEN_DEFAULTS.
@@ -322,7 +322,8 @@ def main(argv=None):
                                     "bulk": "k_step_bulk<3,5>",
                                     "reg": "k_step<3,5>", "regpf": "k_step<3,5,pf>",
                                     "lean": "k_step<3,5,lean48>",
-                                    "pair": "k_step_pair<3,5>"}[
+                                    "pair": "k_step_pair<3,5>",
+                                    "bulk1": "k_step_bulk<3,5,1 stage>"}[
                                         args.step_impl] + (" (tb_step_final: K2 + fused K4)"
                                                            if world == 1 else " (tb_step)"),
                          "achieved": achieved, "peak": hbm, "unit": "GB/s",

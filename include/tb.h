@@ -72,6 +72,7 @@ extern "C" {
 #define TB_STEP_REGPF 3         /* registers + next-sub-grid prefetch       */
 #define TB_STEP_LEAN 4          /* registers capped at 48 (more warps/SM)   */
 #define TB_STEP_PAIR 5          /* a warp pair per sub-grid, 8 cells/lane   */
+#define TB_STEP_BULK1 6         /* bulk-copy ring, 1 slot per warp          */
 #define TB_OPT_STEP_SPW 2       /* K2 sub-grids per warp per CTA; 0 = one
                                    persistent wave (default)                 */
 

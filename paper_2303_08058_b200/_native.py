@@ -40,6 +40,7 @@ TB_STEP_BULK = 2
 TB_STEP_REGPF = 3
 TB_STEP_LEAN = 4
 TB_STEP_PAIR = 5
+TB_STEP_BULK1 = 6
 TB_OPT_STEP_SPW = 2
 
 TB_OP_NONE = 0

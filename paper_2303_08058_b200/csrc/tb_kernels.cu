@@ -283,13 +283,15 @@ __global__ void k_acc_finalize(int64_t *acc, double *piece, double *dt,
 // ------------------------------------------------------------------ K2 --
 constexpr int kStepThreads = 256;
 constexpr int kStepWarps = kStepThreads / 32;
-constexpr int kStages = 2;   // bulk-copy ring depth per warp
+constexpr int kStages = 2;   // default bulk-copy ring depth per warp
 // Slot layout: the four 128-cell blocks of a sub-grid at a 1088-B pitch
 // (1 KiB + 64 B pad) so lanes (b, r) and (b+1, r) sit in opposite bank halves:
 // each 8-byte LDS of the warp is exactly 2 wavefronts (conflict-free).
 constexpr int kBlkPitch = 136;                    // doubles per padded block
 constexpr int kSlot = 4 * kBlkPitch;              // doubles per slot (4352 B)
-constexpr int kBulkSmem = kStepWarps * kStages * kSlot * 8;   // 68 KiB -> 3 CTAs/SM
+constexpr int bulk_smem(int stages) { return kStepWarps * stages * kSlot * 8; }
+// 2 stages: 68 KiB/CTA -> 3 CTAs (24 warps)/SM; 1 stage: 34 KiB -> 4 CTAs
+// (32 warps, register-limited) with one sub-grid in flight per warp.
 
 struct StepArgs {
   const double *old;
@@ -580,9 +582,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       : "memory");
 }
 
-template <int CHAINS, int KPC>
+template <int CHAINS, int KPC, int STAGES>
 __global__ void __launch_bounds__(kStepThreads) k_step_bulk(StepArgs a) {
-  extern __shared__ __align__(128) double ring[];   // [warps][stages][512]
+  constexpr int kStages = STAGES;
+  extern __shared__ __align__(128) double ring[];   // [warps][stages][padded 512]
   __shared__ __align__(8) uint64_t bars[kStepWarps][kStages];
   __shared__ unsigned long long s_limbs[TB_ACC_LIMBS];
   __shared__ long long s_min[kStepWarps];
@@ -658,6 +661,18 @@ int occupancy(K kernel, int smem) {
   return o;
 }
 
+template <int CHAINS, int KPC, int STAGES>
+void launch_bulk(cudaStream_t st, const StepArgs &a) {
+  static int occ = 0;
+  if (!occ) {
+    cudaFuncSetAttribute(k_step_bulk<CHAINS, KPC, STAGES>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, bulk_smem(STAGES));
+    occ = occupancy(k_step_bulk<CHAINS, KPC, STAGES>, bulk_smem(STAGES));
+  }
+  k_step_bulk<CHAINS, KPC, STAGES>
+      <<<step_grid(a.n, occ), kStepThreads, bulk_smem(STAGES), st>>>(a);
+}
+
 int launch_step(cudaStream_t st, StepArgs a) {
   const bool fixed = a.chains == 3 && a.kpc == 5;
   const bool aligned = ((reinterpret_cast<uintptr_t>(a.old) & 15) == 0);
@@ -670,27 +685,15 @@ int launch_step(cudaStream_t st, StepArgs a) {
     // ticket counter must start at 0 (reset by acc_reset / finalize)
   }
   if (bulk) {
-    static int occ_f = 0, occ_g = 0;
-    static bool attr_f = false, attr_g = false;
-    if (fixed) {
-      if (!attr_f) {
-        cudaFuncSetAttribute(k_step_bulk<3, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kBulkSmem);
-        attr_f = true;
-      }
-      if (!occ_f) occ_f = occupancy(k_step_bulk<3, 5>, kBulkSmem);
-      const int blocks = step_grid(a.n, occ_f);
-      k_step_bulk<3, 5><<<blocks, kStepThreads, kBulkSmem, st>>>(a);
-    } else {
-      if (!attr_g) {
-        cudaFuncSetAttribute(k_step_bulk<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kBulkSmem);
-        attr_g = true;
-      }
-      if (!occ_g) occ_g = occupancy(k_step_bulk<0, 0>, kBulkSmem);
-      const int blocks = step_grid(a.n, occ_g);
-      k_step_bulk<0, 0><<<blocks, kStepThreads, kBulkSmem, st>>>(a);
-    }
+    if (fixed)
+      launch_bulk<3, 5, kStages>(st, a);
+    else
+      launch_bulk<0, 0, kStages>(st, a);
+  } else if (g_step_impl == TB_STEP_BULK1 && aligned) {
+    if (fixed)
+      launch_bulk<3, 5, 1>(st, a);
+    else
+      launch_bulk<0, 0, 1>(st, a);
   } else if (g_step_impl == TB_STEP_REGPF) {
     static int occ_f = 0, occ_g = 0;
     if (fixed) {
@@ -739,7 +742,7 @@ extern "C" {
 
 int tb_set_option(int key, int value) {
   if (key == TB_OPT_STEP_IMPL) {
-    if (value < TB_STEP_AUTO || value > TB_STEP_PAIR) return TB_E_INVALID;
+    if (value < TB_STEP_AUTO || value > TB_STEP_BULK1) return TB_E_INVALID;
     g_step_impl = value;
     return TB_OK;
   }

@@ -159,11 +159,11 @@ def test_ring_stepper_long_run_matches_c_oracle(N):
     assert cs == ccs and dts == cdts
 
 
-@pytest.mark.parametrize("impl", ["reg", "bulk", "regpf", "lean", "pair"])
+@pytest.mark.parametrize("impl", ["reg", "bulk", "regpf", "lean", "pair", "bulk1"])
 @pytest.mark.parametrize("s", [1, 5, 64, 3000])
 def test_step_impls_and_fused_finalize(N, impl, s):
     code = {"reg": N.TB_STEP_REG, "bulk": N.TB_STEP_BULK, "regpf": N.TB_STEP_REGPF,
-            "lean": N.TB_STEP_LEAN, "pair": N.TB_STEP_PAIR}[impl]
+            "lean": N.TB_STEP_LEAN, "pair": N.TB_STEP_PAIR, "bulk1": N.TB_STEP_BULK1}[impl]
     N.call("tb_set_option", N.TB_OPT_STEP_IMPL, code)
     try:
         old_h = mo.initial_cells(s) + 1e-4 * np.cos(np.arange(s * 512)).reshape(s, 512)
