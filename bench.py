@@ -47,7 +47,7 @@ METRIC = "sub-grid cells processed/sec (rotating star, FP64) at 1/2/4/8 B200 vs 
 BYTES_PER_CELL = 8 + 8 + 0.25 + 0.03125   # 16.28 B/cell-step
 GOLDEN_DEFAULTS = float.fromhex("0x1.df1096d8fa699p+20")   # run_reference(512, 15)
 FALLBACK_HBM_GBS = 6650.0
-AUTO_BULK_MIN = 65536  # TB_STEP_AUTO: bulk ring from this many sub-grids, else reg
+AUTO_IMPL = "bulk1"    # what TB_STEP_AUTO launches for the aligned (3, 5) chain
 
 
 def env_int(name, default):
@@ -293,9 +293,7 @@ def main(argv=None):
             try:
                 with open(tpath) as fh:
                     tj = json.load(fh)
-                impl_key = args.step_impl
-                if impl_key == "auto":
-                    impl_key = "bulk" if n_local >= AUTO_BULK_MIN else "reg"
+                impl_key = AUTO_IMPL if args.step_impl == "auto" else args.step_impl
                 ent = tj.get("by_impl", {}).get(impl_key)
                 if ent and tj.get("subgrids") == n_local:
                     traffic = ent["dram_bytes_per_launch"]
@@ -317,8 +315,7 @@ def main(argv=None):
                        "l2": "flushed before every timed step (256 MiB write)"},
             "parity": {"run_reference_512x15_equals_GOLDEN_DEFAULTS": parity},
             "roofline": {"bound": "hbm",
-                         "kernel": {"auto": ("k_step_bulk<3,5>" if n_local >= AUTO_BULK_MIN
-                                             else "k_step<3,5>"),
+                         "kernel": {"auto": "k_step_bulk<3,5,1 stage>",
                                     "bulk": "k_step_bulk<3,5>",
                                     "reg": "k_step<3,5>", "regpf": "k_step<3,5,pf>",
                                     "lean": "k_step<3,5,lean48>",

@@ -66,7 +66,7 @@ extern "C" {
 
 /* tb_set_option keys/values. */
 #define TB_OPT_STEP_IMPL 1      /* which K2 variant tb_step launches        */
-#define TB_STEP_AUTO 0          /* bulk ring for >= 65536 sub-grids, else reg */
+#define TB_STEP_AUTO 0          /* 1-slot bulk ring (aligned, 3x5 chain)    */
 #define TB_STEP_REG 1           /* direct ld.global.nc into registers       */
 #define TB_STEP_BULK 2          /* cp.async.bulk smem ring + mbarriers      */
 #define TB_STEP_REGPF 3         /* registers + next-sub-grid prefetch       */

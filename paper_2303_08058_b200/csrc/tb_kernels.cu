@@ -676,11 +676,14 @@ void launch_bulk(cudaStream_t st, const StepArgs &a) {
 int launch_step(cudaStream_t st, StepArgs a) {
   const bool fixed = a.chains == 3 && a.kpc == 5;
   const bool aligned = ((reinterpret_cast<uintptr_t>(a.old) & 15) == 0);
-  // AUTO: the bulk-copy ring wins once each warp streams enough sub-grids to
-  // amortise its fill/drain (measured: 86% vs 84% of HBM roofline at 262144
-  // sub-grids, 66% vs 69% at 32768), registers below that.
-  const bool bulk = aligned && (g_step_impl == TB_STEP_BULK ||
-                                (g_step_impl == TB_STEP_AUTO && fixed && a.n >= 65536));
+  // AUTO = the single-slot bulk-copy ring (measured, % of HBM roofline at
+  // 32768 / 262144 sub-grids: bulk1 70.4 / 87.5, reg 70.2 / 84.5,
+  // bulk (2 slots) 65.2 / 86.2); registers when the state is not 16-B aligned.
+  const bool bulk = aligned && g_step_impl == TB_STEP_BULK;
+  if (g_step_impl == TB_STEP_AUTO && aligned && fixed) {
+    launch_bulk<3, 5, 1>(st, a);
+    return tb::last_error();
+  }
   if (a.finalize && a.acc) {
     // ticket counter must start at 0 (reset by acc_reset / finalize)
   }
