@@ -240,3 +240,53 @@ def test_step_host_chained_unjoined_and_mixed_with_resident(N):
     cs6, dts6, want6 = mo.run_reference_cells(s, 6)
     np.testing.assert_array_equal(st.cells.cpu().numpy(), want6)
     assert st.result().checksum == cs6 and st.result().dts == dts6
+
+
+@pytest.mark.parametrize("world,subgrids", [(2, 64), (3, 100), (4, 4), (2, 3), (8, 1000)])
+def test_partitioned_step_on_gpu_matches_single_device(N, world, subgrids):
+    """The N>1 device path (interior K2 while the halo is in flight, then the
+    two boundary sub-grids; limbs summed and min keys min-reduced across
+    ranks) run for all ranks inside one process on one GPU, with the NCCL
+    exchange and all-reduce replaced by in-process copies."""
+    from paper_2303_08058_b200.ring import CELLS, FACE, RingStepper
+    ranks = [RingStepper(subgrids, rank=r, world=world, max_steps=4) for r in range(world)]
+    for st in ranks:
+        st._exchange_start = lambda *a, **k: []      # halo filled below
+
+    for _ in range(3):
+        olds = [st.state[st.cur] for st in ranks]
+        for r, st in enumerate(ranks):
+            left, right = ranks[(r - 1) % world], ranks[(r + 1) % world]
+            st.halo[0].copy_(olds[(r - 1) % world][left.n - 1, CELLS - FACE:])
+            st.halo[1].copy_(olds[(r + 1) % world][0, :FACE])
+        for st in ranks:
+            st._step_partitioned(st.state[st.cur], st.state[1 - st.cur], None)
+        limbs = sum(st.acc[:N.TB_ACC_LIMBS] for st in ranks)
+        mkey = torch.stack([st.acc[N.TB_ACC_MIN_WORD] for st in ranks]).min()
+        for st in ranks:
+            st.acc[:N.TB_ACC_LIMBS].copy_(limbs)
+            st.acc[N.TB_ACC_MIN_WORD] = mkey
+            k = st.steps_done
+            st.ops.acc_finalize(st.acc, st.pieces[k:k + 1], st.dts[k:k + 1], st.checksum)
+            st.cur = 1 - st.cur
+            st.steps_done += 1
+    cs, dts, cells = mo.run_reference_cells(subgrids, 3)
+    for st in ranks:
+        res = st.result()
+        assert res.checksum == cs and res.dts == dts
+        np.testing.assert_array_equal(st.cells.cpu().numpy(), cells[st.lo:st.hi])
+
+
+def test_step_host_inplace_chain_faces_from_device(N):
+    from paper_2303_08058_b200.ring import RingStepper
+    for s, chunks in [(1, 1), (2, 2), (500, 7)]:
+        st = RingStepper(s, max_steps=8)
+        cells = torch.from_numpy(mo.initial_cells(s)).pin_memory()
+        stats = torch.zeros(2, dtype=torch.float64).pin_memory()
+        for _ in range(5):
+            st.step_host(cells, cells, stats, chunks=chunks, join=False)
+        st.join_host()
+        torch.cuda.synchronize()
+        cs, dts, want = mo.run_reference_cells(s, 5)
+        np.testing.assert_array_equal(cells.numpy(), want)
+        assert st.result().checksum == cs and st.result().dts == dts
