@@ -191,7 +191,7 @@ def main(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--step-impl", choices=["auto", "reg", "bulk", "regpf", "lean", "pair", "bulk1"], default="auto",
                     help="K2 variant (tb_set_option TB_OPT_STEP_IMPL)")
-    ap.add_argument("--e2e-chunks", type=int, default=16)
+    ap.add_argument("--e2e-chunks", type=int, default=8)
     ap.add_argument("--spw", type=int, default=0,
                     help="K2 sub-grids per warp per CTA (0 = one persistent wave)")
     args = ap.parse_args(argv)

@@ -224,6 +224,41 @@ int tb_htq_next(tb_htq_t q, uint64_t *token, int64_t timeout_us);
 int tb_htq_close(tb_htq_t q);
 int tb_htq_destroy(tb_htq_t q);
 
+/* ------------------------------------------------- native machine -- */
+/* The reference machine (src/cli.py:199-232 run_single: Runtime + device +
+ * Integration + executors + run_scenario) as one native call: a C++
+ * work-stealing pool whose workers run the mini-app's per-sub-grid tasks, an
+ * aggregation executor per CUDA stream, and completion surfaced by event
+ * POLLING in the workers' idle loop, by HOSTTASK threads, or by FENCE. */
+#define TB_MODE_POLLING 0
+#define TB_MODE_HOSTTASK 1
+#define TB_MODE_FENCE 2
+
+typedef struct {
+  int64_t subgrids;          /* ScenarioConfig.subgrids                     */
+  int64_t steps;
+  int64_t chains;            /* 3 */
+  int64_t kernels_per_chain; /* 5 */
+  int64_t workers;           /* RunConfig.workers                            */
+  int64_t executors;         /* RunConfig.executors (CUDA streams)           */
+  int64_t max_agg;           /* RunConfig.max_agg                            */
+  int64_t mode;              /* TB_MODE_*                                    */
+  int64_t inject_barriers;   /* barrier op between kernel and D2H            */
+  int64_t barrier_elision;   /* drop those barriers                          */
+  int64_t task_subgrids;     /* sub-grids per task (1 = reference structure) */
+  int64_t hosttask_threads;  /* 2 */
+} tb_machine_config;
+
+typedef struct {             /* StepMetrics (src/miniapp.py:103-113)         */
+  double wall_ms, dt, piece;
+  int64_t launches, transfers, event_waits, full, idle, members;
+} tb_machine_step;
+
+/* Runs cfg->steps steps; *checksum = sum of pieces (src/miniapp.py:227);
+ * steps_out[cfg->steps] (optional); cells_out[subgrids*512] (optional). */
+int tb_machine_run(const tb_machine_config *cfg, double *checksum,
+                   tb_machine_step *steps_out, double *cells_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -43,6 +43,10 @@ TB_STEP_PAIR = 5
 TB_STEP_BULK1 = 6
 TB_OPT_STEP_SPW = 2
 
+TB_MODE_POLLING = 0
+TB_MODE_HOSTTASK = 1
+TB_MODE_FENCE = 2
+
 TB_OP_NONE = 0
 TB_OP_KIND = 1
 TB_OP_AFFINE = 2
@@ -126,11 +130,12 @@ SIGNATURES = {
     "tb_htq_next": [_u64, _pu64, _i64],
     "tb_htq_close": [_u64],
     "tb_htq_destroy": [_u64],
+    "tb_machine_run": [_vp, _vp, _vp, _vp],
 }
 BLOCKING = {"tb_init", "tb_device_sync", "tb_stream_sync", "tb_event_wait",
             "tb_htq_next", "tb_htq_destroy", "tb_malloc", "tb_free",
             "tb_host_alloc", "tb_host_free", "tb_stream_destroy",
-            "tb_memcpy_h2d", "tb_memcpy_d2h", "tb_poll_drain"}
+            "tb_memcpy_h2d", "tb_memcpy_d2h", "tb_poll_drain", "tb_machine_run"}
 
 _lock = threading.Lock()
 _libs = None

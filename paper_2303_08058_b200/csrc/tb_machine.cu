@@ -1,0 +1,710 @@
+// tb_machine.cu — the paper's machine rebuilt natively: a work-stealing C++
+// task runtime whose workers poll CUDA events between tasks (or, for the
+// ablation, complete them from host-task threads or by fencing), per-executor
+// dynamic kernel aggregation on CUDA streams, and the mini-app step driver.
+//
+// Same structure and semantics as the reference machine, without the GIL:
+//   runtime/pool.py      -> Pool (per-worker deques, injector, random-victim
+//                           steal, idle hook after every task + 5..100 us
+//                           backoff while idle)
+//   runtime/polling.py   -> Poller (MPSC inbox, single-entrant try-lock body,
+//                           only each in-order stream's head queried)
+//   bridge.py            -> bridge(): POLLING | HOSTTASK | FENCE
+//   executors.py:147-304 -> Aggregator (launch on Full or on Idle via one
+//                           queue-marker probe per batch; one tb_agg_launch)
+//   miniapp.py:116-171   -> SubTask state machine + step driver (host ghost
+//                           fold / post-process, exact fsum, min-tree dt)
+// Results are bit-identical to the reference (the kernels are K1; the host
+// reductions follow numpy's pairwise order and math.fsum exactly).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <deque>
+#include <map>
+#include <mutex>
+#include <random>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/tb.h"
+#include "tb_internal.h"
+
+namespace tbm {
+
+using Clock = std::chrono::steady_clock;
+
+struct Task {
+  void (*fn)(void *);
+  void *arg;
+};
+
+// ------------------------------------------------------------------ pool --
+class Pool;
+thread_local Pool *t_pool = nullptr;
+thread_local int t_worker = -1;
+
+class Pool {
+ public:
+  Pool(int workers, int device, uint64_t seed) : device_(device) {
+    qs_.resize(workers);
+    for (int i = 0; i < workers; ++i) qs_[i].reset(new Queue());
+    for (int i = 0; i < workers; ++i)
+      threads_.emplace_back([this, i, seed] { run(i, seed + i); });
+  }
+  ~Pool() { stop(); }
+
+  void set_idle_hook(int (*hook)(void *), void *arg) {
+    hook_ = hook;
+    hook_arg_ = arg;
+  }
+
+  void push(Task t) {
+    active_.fetch_add(1, std::memory_order_relaxed);
+    if (t_pool == this && t_worker >= 0) {
+      std::lock_guard<std::mutex> g(qs_[t_worker]->mu);
+      qs_[t_worker]->dq.push_back(t);
+    } else {
+      std::lock_guard<std::mutex> g(inj_mu_);
+      inj_.push_back(t);
+    }
+  }
+
+  void stop() {
+    if (!alive_.exchange(false)) return;
+    for (auto &t : threads_) t.join();
+  }
+
+  int64_t busy_ns() const { return busy_ns_.load(); }
+
+ private:
+  struct Queue {
+    std::mutex mu;
+    std::deque<Task> dq;
+  };
+
+  bool take(int w, std::mt19937_64 &rng, Task *out) {
+    {
+      Queue &q = *qs_[w];
+      std::lock_guard<std::mutex> g(q.mu);
+      if (!q.dq.empty()) {
+        *out = q.dq.front();
+        q.dq.pop_front();
+        return true;
+      }
+    }
+    {
+      std::lock_guard<std::mutex> g(inj_mu_);
+      if (!inj_.empty()) {
+        *out = inj_.front();
+        inj_.pop_front();
+        return true;
+      }
+    }
+    const int n = (int)qs_.size();
+    if (n > 1) {
+      const int v = (int)(rng() % n);
+      if (v != w) {
+        Queue &q = *qs_[v];
+        std::lock_guard<std::mutex> g(q.mu);
+        if (!q.dq.empty()) {
+          *out = q.dq.back();
+          q.dq.pop_back();
+          return true;
+        }
+      }
+    }
+    return false;
+  }
+
+  void run(int w, uint64_t seed) {
+    cudaSetDevice(device_);
+    t_pool = this;
+    t_worker = w;
+    std::mt19937_64 rng(seed);
+    int nap_us = 5;
+    while (alive_.load(std::memory_order_relaxed)) {
+      Task t;
+      if (take(w, rng, &t)) {
+        const auto t0 = Clock::now();
+        t.fn(t.arg);
+        busy_ns_.fetch_add(
+            std::chrono::duration_cast<std::chrono::nanoseconds>(Clock::now() - t0).count(),
+            std::memory_order_relaxed);
+        active_.fetch_sub(1, std::memory_order_relaxed);
+        nap_us = 5;
+        if (hook_) hook_(hook_arg_);
+        continue;
+      }
+      if (hook_ && hook_(hook_arg_)) {
+        nap_us = 5;
+        continue;
+      }
+      std::this_thread::sleep_for(std::chrono::microseconds(nap_us));
+      nap_us = std::min(nap_us * 2, 100);
+    }
+    t_pool = nullptr;
+    t_worker = -1;
+  }
+
+  int device_;
+  std::vector<std::unique_ptr<Queue>> qs_;
+  std::mutex inj_mu_;
+  std::deque<Task> inj_;
+  std::vector<std::thread> threads_;
+  std::atomic<bool> alive_{true};
+  std::atomic<int64_t> active_{0};
+  std::atomic<int64_t> busy_ns_{0};
+  int (*hook_)(void *) = nullptr;
+  void *hook_arg_ = nullptr;
+};
+
+// ---------------------------------------------------------------- poller --
+// Completion callbacks keyed to CUDA events; the body runs on whichever worker
+// wins the try-lock, queries only each stream's head, and pushes the fired
+// continuations as pool tasks.
+class Poller {
+ public:
+  explicit Poller(Pool *pool) : pool_(pool) {}
+
+  void add(cudaEvent_t ev, uint64_t chain, Task cont) {
+    std::lock_guard<std::mutex> g(inbox_mu_);
+    inbox_.push_back(Entry{ev, chain, cont});
+    waiting_.fetch_add(1, std::memory_order_relaxed);
+  }
+
+  static int hook(void *self) { return static_cast<Poller *>(self)->poll(); }
+
+  int poll() {
+    if (waiting_.load(std::memory_order_relaxed) == 0) return 0;
+    std::unique_lock<std::mutex> guard(body_, std::try_to_lock);
+    if (!guard.owns_lock()) return 0;
+    {
+      std::lock_guard<std::mutex> g(inbox_mu_);
+      for (const Entry &e : inbox_) chains_[e.chain].push_back(e);
+      inbox_.clear();
+    }
+    int fired = 0;
+    for (auto it = chains_.begin(); it != chains_.end();) {
+      auto &dq = it->second;
+      while (!dq.empty() && cudaEventQuery(dq.front().ev) != cudaErrorNotReady) {
+        Entry e = dq.front();
+        dq.pop_front();
+        tb_event_release(reinterpret_cast<tb_event_t>(e.ev));
+        pool_->push(e.cont);
+        ++fired;
+      }
+      it = dq.empty() ? chains_.erase(it) : std::next(it);
+    }
+    waiting_.fetch_sub(fired, std::memory_order_relaxed);
+    return fired;
+  }
+
+ private:
+  struct Entry {
+    cudaEvent_t ev;
+    uint64_t chain;
+    Task cont;
+  };
+  Pool *pool_;
+  std::mutex inbox_mu_;
+  std::vector<Entry> inbox_;
+  std::mutex body_;
+  std::unordered_map<uint64_t, std::deque<Entry>> chains_;
+  std::atomic<int64_t> waiting_{0};
+};
+
+// ------------------------------------------------------ host-task threads --
+class HostTasks {
+ public:
+  HostTasks(Pool *pool, int threads, int device, int side_streams) : pool_(pool) {
+    cudaSetDevice(device);
+    for (int i = 0; i < side_streams; ++i) {
+      cudaStream_t s;
+      cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+      side_.push_back(s);
+    }
+    for (int i = 0; i < threads; ++i) threads_.emplace_back([this] { run(); });
+  }
+  ~HostTasks() {
+    for (auto s : side_) cudaStreamSynchronize(s);
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      closed_ = true;
+    }
+    cv_.notify_all();
+    for (auto &t : threads_) t.join();
+    for (auto s : side_) cudaStreamDestroy(s);
+  }
+  void add(cudaEvent_t ev, Task cont) {
+    auto *item = new Item{this, ev, cont};
+    cudaStream_t side = side_[rr_.fetch_add(1) % side_.size()];
+    cudaStreamWaitEvent(side, ev, 0);
+    cudaLaunchHostFunc(side, &HostTasks::trampoline, item);
+  }
+  int64_t dispatched() const { return dispatched_.load(); }
+
+ private:
+  struct Item {
+    HostTasks *self;
+    cudaEvent_t ev;
+    Task cont;
+  };
+  static void CUDART_CB trampoline(void *p) {   // CUDA driver thread: enqueue only
+    Item *it = static_cast<Item *>(p);
+    {
+      std::lock_guard<std::mutex> g(it->self->mu_);
+      it->self->ready_.push_back(it);
+    }
+    it->self->cv_.notify_one();
+  }
+  void run() {
+    for (;;) {
+      Item *it = nullptr;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return closed_ || !ready_.empty(); });
+        if (ready_.empty()) return;
+        it = ready_.front();
+        ready_.pop_front();
+      }
+      tb_event_release(reinterpret_cast<tb_event_t>(it->ev));
+      pool_->push(it->cont);   // foreign thread -> pool injector
+      dispatched_.fetch_add(1);
+      delete it;
+    }
+  }
+  Pool *pool_;
+  std::vector<cudaStream_t> side_;
+  std::atomic<unsigned> rr_{0};
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::deque<Item *> ready_;
+  bool closed_ = false;
+  std::vector<std::thread> threads_;
+  std::atomic<int64_t> dispatched_{0};
+};
+
+// ---------------------------------------------------------------- machine --
+constexpr int kCells = TB_CELLS;
+constexpr int kFace = TB_FACE;
+
+struct Machine;
+struct SubTask;
+
+struct Staging {
+  size_t bytes;
+  double *host;   // pinned
+  double *dev;
+};
+
+struct Req {
+  const double *src;
+  double *dst;
+  int64_t n;
+  SubTask *task;
+};
+
+struct Executor;
+
+struct Batch {
+  Executor *ex;
+  int kind;
+  std::vector<Req> members;
+  bool launched = false;
+  bool idle = false;
+  Staging *staging = nullptr;
+};
+
+struct Executor {
+  Machine *m;
+  int id;
+  cudaStream_t stream;
+  std::mutex mu;
+  Batch *open[TB_KINDS] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+};
+
+struct SubTask {
+  Machine *m;
+  Executor *ex;
+  int64_t lo, n;          // sub-grids [lo, lo+n)
+  int round;
+  std::vector<double> a, b;
+  double *work, *out;
+};
+
+struct Machine {
+  tb_machine_config cfg;
+  std::vector<double> cells;       // [S][512]
+  std::vector<double> faces;       // [S][2][8] previous generation
+  std::vector<double> mins, sums;  // per sub-grid, this step
+  std::unique_ptr<Pool> pool;
+  std::unique_ptr<Poller> poller;
+  std::unique_ptr<HostTasks> hosttasks;
+  std::vector<std::unique_ptr<Executor>> execs;
+  std::vector<std::unique_ptr<SubTask>> tasks;
+  std::mutex staging_mu;
+  std::map<size_t, std::vector<Staging *>> staging_free;
+  std::vector<Staging *> staging_all;
+  // step completion
+  std::mutex done_mu;
+  std::condition_variable done_cv;
+  std::atomic<int64_t> remaining{0};
+  // metrics
+  std::atomic<int64_t> launches{0}, transfers{0}, event_waits{0}, full{0}, idle{0},
+      members{0}, kernels{0};
+  int error = TB_OK;
+};
+
+Staging *staging_alloc(Machine *m, size_t bytes) {
+  {
+    std::lock_guard<std::mutex> g(m->staging_mu);
+    auto &v = m->staging_free[bytes];
+    if (!v.empty()) {
+      Staging *s = v.back();
+      v.pop_back();
+      return s;
+    }
+  }
+  Staging *s = new Staging{bytes, nullptr, nullptr};
+  cudaHostAlloc(reinterpret_cast<void **>(&s->host), bytes, cudaHostAllocPortable);
+  cudaMalloc(reinterpret_cast<void **>(&s->dev), bytes);
+  std::lock_guard<std::mutex> g(m->staging_mu);
+  m->staging_all.push_back(s);
+  return s;
+}
+
+void staging_release(Machine *m, Staging *s) {
+  std::lock_guard<std::mutex> g(m->staging_mu);
+  m->staging_free[s->bytes].push_back(s);
+}
+
+// Bridge a recorded event into the runtime: the continuation `cont` becomes
+// a pool task once the event completes (src/bridge.py:54-101).
+void bridge(Machine *m, Executor *ex, cudaEvent_t ev, Task cont) {
+  switch (m->cfg.mode) {
+    case TB_MODE_POLLING:
+      m->poller->add(ev, reinterpret_cast<uint64_t>(ex->stream), cont);
+      break;
+    case TB_MODE_HOSTTASK:
+      m->hosttasks->add(ev, cont);
+      break;
+    default:  // FENCE: block this worker, then the future is ready
+      m->event_waits.fetch_add(1, std::memory_order_relaxed);
+      cudaEventSynchronize(ev);
+      tb_event_release(reinterpret_cast<tb_event_t>(ev));
+      m->pool->push(cont);
+      break;
+  }
+}
+
+void resume_task(void *p);
+
+void batch_done(void *p) {   // AggregationExecutor finish (src/executors.py:286-301)
+  Batch *b = static_cast<Batch *>(p);
+  Machine *m = b->ex->m;
+  int64_t off = 0;
+  for (const Req &r : b->members) {
+    std::memcpy(r.dst, b->staging->host + off, sizeof(double) * r.n);
+    off += r.n;
+  }
+  staging_release(m, b->staging);
+  m->launches.fetch_add(1, std::memory_order_relaxed);
+  m->members.fetch_add((int64_t)b->members.size(), std::memory_order_relaxed);
+  (b->idle ? m->idle : m->full).fetch_add(1, std::memory_order_relaxed);
+  for (const Req &r : b->members) m->pool->push(Task{resume_task, r.task});
+  delete b;
+}
+
+void launch(Batch *b, bool idle) {   // src/executors.py:257-284 as one launch
+  Executor *ex = b->ex;
+  Machine *m = ex->m;
+  b->idle = idle;
+  int64_t total = 0;
+  for (const Req &r : b->members) total += r.n;
+  const size_t bytes = sizeof(double) * total;
+  b->staging = staging_alloc(m, bytes);
+  int64_t off = 0;
+  for (const Req &r : b->members) {
+    std::memcpy(b->staging->host + off, r.src, sizeof(double) * r.n);
+    off += r.n;
+  }
+  tb_event_t ev = 0;
+  const int do_barrier = m->cfg.inject_barriers && !m->cfg.barrier_elision;
+  const int rc = tb_agg_launch(reinterpret_cast<tb_stream_t>(ex->stream), TB_OP_KIND, b->kind,
+                               0.0, 0.0, b->staging->dev, b->staging->host, bytes, do_barrier,
+                               &ev);
+  if (rc != TB_OK) m->error = rc;
+  m->transfers.fetch_add(2, std::memory_order_relaxed);
+  m->kernels.fetch_add(1, std::memory_order_relaxed);
+  bridge(m, ex, reinterpret_cast<cudaEvent_t>(ev), Task{batch_done, b});
+}
+
+void idle_fire(void *p) {   // the idleness probe completed (src/executors.py:209-218)
+  Batch *b = static_cast<Batch *>(p);
+  Executor *ex = b->ex;
+  {
+    std::lock_guard<std::mutex> g(ex->mu);
+    if (b->launched) return;            // the full trigger won
+    if (ex->open[b->kind] == b) ex->open[b->kind] = nullptr;
+    b->launched = true;
+  }
+  launch(b, true);
+}
+
+void schedule(Executor *ex, int kind, const double *src, double *dst, int64_t n,
+              SubTask *t) {   // src/executors.py:174-221
+  Machine *m = ex->m;
+  Batch *opened = nullptr, *full = nullptr;
+  {
+    std::lock_guard<std::mutex> g(ex->mu);
+    Batch *b = ex->open[kind];
+    if (!b) {
+      b = new Batch();
+      b->ex = ex;
+      b->kind = kind;
+      if (m->cfg.max_agg > 1) ex->open[kind] = b;
+      opened = b;
+    }
+    b->members.push_back(Req{src, dst, n, t});
+    if ((int64_t)b->members.size() >= m->cfg.max_agg) {
+      if (ex->open[kind] == b) ex->open[kind] = nullptr;
+      b->launched = true;
+      full = b;
+    }
+  }
+  if (opened && opened != full) {
+    // One idleness probe per batch: a queue marker event (src/bridge.py:92-101).
+    tb_event_t ev = 0;
+    tb_event_record(reinterpret_cast<tb_stream_t>(ex->stream), &ev);
+    bridge(m, ex, reinterpret_cast<cudaEvent_t>(ev), Task{idle_fire, opened});
+  }
+  if (full) launch(full, false);
+}
+
+// numpy's pairwise sum of 512 contiguous doubles (see oracle/tb_oracle.c)
+double pairwise512(const double *a) {
+  double bsum[4];
+  for (int blk = 0; blk < 4; ++blk) {
+    const double *p = a + 128 * blk;
+    double r[8];
+    for (int j = 0; j < 8; ++j) r[j] = p[j];
+    for (int i = 8; i < 128; i += 8)
+      for (int j = 0; j < 8; ++j) r[j] += p[i + j];
+    bsum[blk] = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  }
+  return (bsum[0] + bsum[1]) + (bsum[2] + bsum[3]);
+}
+
+void start_task(void *p) {   // ghost fold + first round (src/miniapp.py:116-130)
+  SubTask *t = static_cast<SubTask *>(p);
+  Machine *m = t->m;
+  const int64_t S = m->cfg.subgrids;
+  t->work = t->a.data();
+  t->out = t->b.data();
+  for (int64_t k = 0; k < t->n; ++k) {
+    const int64_t g = t->lo + k;
+    double *w = t->work + k * kCells;
+    std::memcpy(w, m->cells.data() + g * kCells, sizeof(double) * kCells);
+    const double *left = m->faces.data() + ((g - 1 + S) % S) * 2 * kFace + kFace;
+    const double *right = m->faces.data() + ((g + 1) % S) * 2 * kFace;
+    for (int i = 0; i < kFace; ++i) w[i] = 0.5 * (w[i] + left[i]);
+    for (int i = 0; i < kFace; ++i)
+      w[kCells - kFace + i] = 0.5 * (w[kCells - kFace + i] + right[i]);
+  }
+  t->round = 0;
+  schedule(t->ex, 0, t->work, t->out, t->n * kCells, t);
+}
+
+void resume_task(void *p) {   // next round, or write-back + post-process
+  SubTask *t = static_cast<SubTask *>(p);
+  Machine *m = t->m;
+  std::swap(t->work, t->out);
+  const int kpc = (int)m->cfg.kernels_per_chain;
+  const int rounds = (int)(m->cfg.chains * kpc);
+  if (++t->round < rounds) {
+    schedule(t->ex, t->round % kpc, t->work, t->out, t->n * kCells, t);
+    return;
+  }
+  for (int64_t k = 0; k < t->n; ++k) {
+    const int64_t g = t->lo + k;
+    const double *w = t->work + k * kCells;
+    std::memcpy(m->cells.data() + g * kCells, w, sizeof(double) * kCells);
+    double mn = w[0];
+    for (int i = 1; i < kCells; ++i) mn = w[i] < mn ? w[i] : mn;
+    m->mins[g] = mn;
+    m->sums[g] = pairwise512(w);
+  }
+  if (m->remaining.fetch_sub(1) == 1) {
+    std::lock_guard<std::mutex> g(m->done_mu);
+    m->done_cv.notify_all();
+  }
+}
+
+// exact sum (== math.fsum): 32-bit digits in int64 limbs, half-even rounding
+double exact_sum(const double *x, int64_t n) {
+  long long acc[TB_ACC_LIMBS + 2] = {0};
+  for (int64_t i = 0; i < n; ++i) {
+    const double v = x[i];
+    if (v == 0.0) continue;
+    unsigned long long bits;
+    std::memcpy(&bits, &v, 8);
+    const int ex = (int)((bits >> 52) & 0x7ff);
+    unsigned long long mant = bits & ((1ULL << 52) - 1);
+    int p = 0;
+    if (ex) {
+      mant |= 1ULL << 52;
+      p = ex - 1;
+    }
+    const int limb = p >> 5, off = p & 31;
+    const unsigned __int128 w = (unsigned __int128)mant << off;
+    const long long s = (long long)(bits >> 63) ? -1 : 1;
+    acc[limb] += s * (long long)(uint64_t)(w & 0xffffffffu);
+    acc[limb + 1] += s * (long long)(uint64_t)((w >> 32) & 0xffffffffu);
+    acc[limb + 2] += s * (long long)(uint64_t)(w >> 64);
+  }
+  constexpr int ND = TB_ACC_LIMBS + 4;
+  uint32_t d[ND];
+  long long carry = 0;
+  for (int i = 0; i < ND; ++i) {
+    const long long v = (i < TB_ACC_LIMBS + 2 ? acc[i] : 0) + carry;
+    d[i] = (uint32_t)(v & 0xffffffffLL);
+    carry = v >> 32;
+  }
+  const bool neg = (d[ND - 1] >> 31) & 1u;
+  if (neg) {
+    unsigned long long c = 1;
+    for (int i = 0; i < ND; ++i) {
+      const unsigned long long v = (unsigned long long)(uint32_t)~d[i] + c;
+      d[i] = (uint32_t)v;
+      c = v >> 32;
+    }
+  }
+  int top = -1;
+  for (int i = ND - 1; i >= 0; --i)
+    if (d[i]) {
+      top = i;
+      break;
+    }
+  if (top < 0) return 0.0;
+  const int nbits = top * 32 + (32 - __builtin_clz(d[top]));
+  auto bit = [&](int k) -> unsigned { return (d[k >> 5] >> (k & 31)) & 1u; };
+  const int shift = nbits > 53 ? nbits - 53 : 0;
+  unsigned long long mant = 0;
+  for (int k = nbits - 1; k >= shift; --k) mant = (mant << 1) | bit(k);
+  if (shift > 0) {
+    const unsigned guard = bit(shift - 1);
+    bool sticky = false;
+    for (int k = shift - 2; k >= 0 && !sticky; --k) sticky = bit(k);
+    if (guard && (sticky || (mant & 1ULL))) mant += 1;
+  }
+  const double r = std::ldexp((double)mant, shift - TB_ACC_BIAS);
+  return neg ? -r : r;
+}
+
+}  // namespace tbm
+
+using namespace tbm;
+
+extern "C" int tb_machine_run(const tb_machine_config *cfg_in, double *checksum,
+                              tb_machine_step *steps_out, double *cells_out) {
+  if (!cfg_in || !checksum) return TB_E_INVALID;
+  const tb_machine_config &c = *cfg_in;
+  if (c.subgrids < 1 || c.steps < 0 || c.workers < 1 || c.executors < 1 || c.max_agg < 1 ||
+      c.chains < 0 || c.kernels_per_chain < 1 || c.kernels_per_chain > TB_KINDS ||
+      c.task_subgrids < 1 || c.mode < TB_MODE_POLLING || c.mode > TB_MODE_FENCE)
+    return TB_E_INVALID;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  Machine m;
+  m.cfg = c;
+  const int64_t S = c.subgrids;
+  m.cells.resize(S * kCells);
+  const double scale = (double)(S * 1000 + kCells);
+  for (int64_t g = 0; g < S; ++g)   // src/miniapp.py:72-77
+    for (int i = 0; i < kCells; ++i)
+      m.cells[g * kCells + i] = ((double)g * 1000.0 + (double)i) / scale;
+  m.faces.resize(S * 2 * kFace);
+  m.mins.resize(S);
+  m.sums.resize(S);
+  m.pool.reset(new Pool((int)c.workers, dev, 1234));
+  m.poller.reset(new Poller(m.pool.get()));
+  if (c.mode == TB_MODE_POLLING) m.pool->set_idle_hook(&Poller::hook, m.poller.get());
+  m.hosttasks.reset(new HostTasks(m.pool.get(), (int)std::max<int64_t>(1, c.hosttask_threads),
+                                  dev, 4));
+  for (int64_t e = 0; e < c.executors; ++e) {
+    auto ex = std::make_unique<Executor>();
+    ex->m = &m;
+    ex->id = (int)e;
+    cudaStreamCreateWithFlags(&ex->stream, cudaStreamNonBlocking);
+    m.execs.push_back(std::move(ex));
+  }
+  // tasks: contiguous blocks of task_subgrids, round-robin over executors
+  // (src/cli.py:224 aggs_by_grid)
+  int64_t k = 0;
+  for (int64_t lo = 0; lo < S; lo += c.task_subgrids, ++k) {
+    auto t = std::make_unique<SubTask>();
+    t->m = &m;
+    t->lo = lo;
+    t->n = std::min<int64_t>(c.task_subgrids, S - lo);
+    t->ex = m.execs[(size_t)(lo % c.executors)].get();
+    t->a.resize(t->n * kCells);
+    t->b.resize(t->n * kCells);
+    m.tasks.push_back(std::move(t));
+  }
+  double cs = 0.0;
+  for (int64_t step = 0; step < c.steps; ++step) {
+    const int64_t k0 = m.kernels, t0n = m.transfers, w0 = m.event_waits, f0 = m.full,
+                  i0 = m.idle, mb0 = m.members;
+    const auto t0 = Clock::now();
+    for (int64_t g = 0; g < S; ++g) {   // face snapshot (src/miniapp.py:89-93)
+      std::memcpy(&m.faces[g * 2 * kFace], &m.cells[g * kCells], sizeof(double) * kFace);
+      std::memcpy(&m.faces[g * 2 * kFace + kFace], &m.cells[g * kCells + kCells - kFace],
+                  sizeof(double) * kFace);
+    }
+    m.remaining.store((int64_t)m.tasks.size());
+    for (auto &t : m.tasks) m.pool->push(Task{start_task, t.get()});
+    {
+      std::unique_lock<std::mutex> lk(m.done_mu);
+      m.done_cv.wait(lk, [&] { return m.remaining.load() == 0; });
+    }
+    double dt = m.mins[0];
+    for (int64_t g = 1; g < S; ++g) dt = m.mins[g] < dt ? m.mins[g] : dt;
+    const double piece = exact_sum(m.sums.data(), S);
+    const auto t1 = Clock::now();
+    cs += piece;
+    if (steps_out) {
+      tb_machine_step &o = steps_out[step];
+      o.wall_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+      o.dt = dt;
+      o.piece = piece;
+      o.launches = m.kernels - k0;
+      o.transfers = m.transfers - t0n;
+      o.event_waits = m.event_waits - w0;
+      o.full = m.full - f0;
+      o.idle = m.idle - i0;
+      o.members = m.members - mb0;
+    }
+  }
+  *checksum = cs;
+  if (cells_out) std::memcpy(cells_out, m.cells.data(), sizeof(double) * S * kCells);
+  m.pool->stop();
+  m.hosttasks.reset();
+  for (auto &ex : m.execs) {
+    cudaStreamSynchronize(ex->stream);
+    cudaStreamDestroy(ex->stream);
+  }
+  for (Staging *s : m.staging_all) {
+    cudaFreeHost(s->host);
+    cudaFree(s->dev);
+    delete s;
+  }
+  const int err = tb::rc(cudaGetLastError());
+  return m.error != TB_OK ? m.error : err;
+}

@@ -1,0 +1,71 @@
+"""The native machine (tb_machine_run: C++ work-stealing runtime + CUDA
+aggregation executors + polling/host-task/fence bridging): goldens in every
+mode, unfused counts, coarsened tasks, and the polling-vs-fence ablation."""
+
+import numpy as np
+import pytest
+
+from conftest import fx
+from oracle import miniapp_oracle as mo
+
+pytestmark = pytest.mark.gpu
+pytest.importorskip("torch")
+
+from paper_2303_08058_b200.bridge import IntegrationMode  # noqa: E402
+from paper_2303_08058_b200.native_machine import run_native  # noqa: E402
+
+MODES = [IntegrationMode.POLLING, IntegrationMode.HOSTTASK, IntegrationMode.FENCE]
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_native_machine_goldens(golden, mode):
+    lit = golden["reference_test_literals"]
+    res, _ = run_native(4, 2, workers=2, executors=2, max_agg=8, mode=mode)
+    assert res.checksum == fx(lit["GOLDEN_4X2"])
+    assert res.dts == [fx(h) for h in lit["GOLDEN_4X2_DTS"]]
+    res, cells = run_native(16, 3, workers=4, executors=3, max_agg=4, mode=mode,
+                            return_cells=True)
+    assert res.checksum.hex() == golden["machine"]["16x3"]["checksum"]
+    want = np.load(__import__("conftest").TESTS + "/golden/cells.npz")["cells_16x3"]
+    np.testing.assert_array_equal(cells, want)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_native_machine_unfused_counts(golden, mode):
+    res, _ = run_native(8, 2, workers=2, executors=1, max_agg=1, mode=mode)
+    for m in res.per_step:
+        assert m.launches == 8 * 15 and m.transfers == 8 * 30
+        assert m.reasons_full == 120 and m.reasons_idle == 0
+        assert (m.event_waits > 0) == (mode is IntegrationMode.FENCE)
+    assert res.checksum == fx(golden["reference_test_literals"]["GOLDEN_8X2"])
+
+
+@pytest.mark.parametrize("e,m,w,block,elide", [(1, 1, 1, 1, False), (8, 8, 4, 1, True),
+                                               (32, 32, 8, 1, False), (4, 8, 8, 3, True),
+                                               (2, 4, 3, 7, False)])
+def test_native_machine_checksum_invariant(golden, e, m, w, block, elide):
+    want = fx(golden["reference_test_literals"]["GOLDEN_8X2"])
+    for mode in MODES:
+        res, _ = run_native(8, 2, workers=w, executors=e, max_agg=m, mode=mode,
+                            task_subgrids=block, barrier_elision=elide)
+        assert res.checksum == want
+
+
+def test_native_machine_c1_and_coarsened_large(golden):
+    res, _ = run_native(512, 1, workers=8, executors=32, max_agg=1)
+    assert res.per_step[0].launches == 7680 and res.per_step[0].transfers == 15360
+    assert res.checksum.hex() == golden["run_reference"]["512x1"]["checksum"]
+    res, _ = run_native(4096, 1, workers=8, executors=16, max_agg=8, task_subgrids=8)
+    assert res.checksum.hex() == golden["run_reference"]["4096x1"]["checksum"]
+    assert [d.hex() for d in res.dts] == golden["run_reference"]["4096x1"]["dts"]
+
+
+def test_native_polling_beats_fence():
+    kw = dict(workers=8, executors=32, max_agg=8)
+    poll = [run_native(512, 4, mode=IntegrationMode.POLLING, **kw)[0] for _ in range(3)]
+    fence = [run_native(512, 4, mode=IntegrationMode.FENCE, **kw)[0] for _ in range(3)]
+    pm = sorted(np.mean(r.step_ms[1:]) for r in poll)[1]
+    fm = sorted(np.mean(r.step_ms[1:]) for r in fence)[1]
+    print(f"native: polling {pm:.3f} ms/step vs fence {fm:.3f} -> {fm / pm:.3f}x")
+    assert poll[0].checksum == fence[0].checksum
+    assert fm / pm >= 1.05

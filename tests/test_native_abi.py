@@ -40,7 +40,8 @@ def test_abi_version_and_constants(lib):
     for name in ("TB_CELLS", "TB_FACE", "TB_KINDS", "TB_ACC_LIMBS", "TB_ACC_BIAS",
                  "TB_ACC_MIN_WORD", "TB_ACC_COUNT_WORD", "TB_ACC_WORDS", "TB_OPT_STEP_IMPL",
                  "TB_STEP_AUTO", "TB_STEP_REG", "TB_STEP_BULK", "TB_STEP_REGPF", "TB_STEP_LEAN", "TB_STEP_PAIR", "TB_STEP_BULK1", "TB_OPT_STEP_SPW", "TB_OP_NONE", "TB_OP_KIND",
-                 "TB_OP_AFFINE", "TB_OK", "TB_NOT_READY"):
+                 "TB_OP_AFFINE", "TB_OK", "TB_NOT_READY", "TB_MODE_POLLING", "TB_MODE_HOSTTASK",
+                 "TB_MODE_FENCE"):
         m = re.search(rf"#define {name} \(?(-?\d+)\)?", text)
         assert m and int(m.group(1)) == getattr(N, name), name
 
@@ -80,3 +81,20 @@ def test_device_calls_fail_loudly_without_gpu():
     from paper_2303_08058_b200 import CudaDevice
     with pytest.raises(N.CudaError):
         CudaDevice()
+
+
+def test_machine_struct_layout_matches_header():
+    from paper_2303_08058_b200.native_machine import MachineConfig, MachineStep
+    text = open(HEADER).read()
+    cfg = re.search(r"typedef struct \{(.*?)\} tb_machine_config;", text, re.S).group(1)
+    fields = re.findall(r"int64_t (\w+);", cfg)
+    assert fields == [f for f, _ in MachineConfig._fields_]
+    assert ctypes.sizeof(MachineStep) == 3 * 8 + 6 * 8
+
+
+def test_machine_rejects_bad_config_without_gpu():
+    from paper_2303_08058_b200.native_machine import MachineConfig
+    cfg = MachineConfig(0, 1, 3, 5, 1, 1, 1, 0, 1, 0, 1, 2)     # subgrids = 0
+    cs = ctypes.c_double()
+    assert N.fast().tb_machine_run(ctypes.addressof(cfg), ctypes.addressof(cs), None,
+                                   None) == N.TB_E_INVALID
