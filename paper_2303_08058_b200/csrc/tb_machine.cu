@@ -313,6 +313,9 @@ struct Req {
 
 struct Executor;
 
+// A batch is referenced by its launch (released in batch_done) and, when it
+// opened with an idleness probe, by that probe (released in idle_fire) — the
+// probe may complete long after a full launch finished.
 struct Batch {
   Executor *ex;
   int kind;
@@ -320,7 +323,12 @@ struct Batch {
   bool launched = false;
   bool idle = false;
   Staging *staging = nullptr;
+  std::atomic<int> refs{1};
 };
+
+inline void batch_release(Batch *b) {
+  if (b->refs.fetch_sub(1, std::memory_order_acq_rel) == 1) delete b;
+}
 
 struct Executor {
   Machine *m;
@@ -419,7 +427,7 @@ void batch_done(void *p) {   // AggregationExecutor finish (src/executors.py:286
   m->members.fetch_add((int64_t)b->members.size(), std::memory_order_relaxed);
   (b->idle ? m->idle : m->full).fetch_add(1, std::memory_order_relaxed);
   for (const Req &r : b->members) m->pool->push(Task{resume_task, r.task});
-  delete b;
+  batch_release(b);
 }
 
 void launch(Batch *b, bool idle) {   // src/executors.py:257-284 as one launch
@@ -449,13 +457,17 @@ void launch(Batch *b, bool idle) {   // src/executors.py:257-284 as one launch
 void idle_fire(void *p) {   // the idleness probe completed (src/executors.py:209-218)
   Batch *b = static_cast<Batch *>(p);
   Executor *ex = b->ex;
+  bool mine = false;
   {
     std::lock_guard<std::mutex> g(ex->mu);
-    if (b->launched) return;            // the full trigger won
-    if (ex->open[b->kind] == b) ex->open[b->kind] = nullptr;
-    b->launched = true;
+    if (!b->launched) {                 // else the full trigger won
+      if (ex->open[b->kind] == b) ex->open[b->kind] = nullptr;
+      b->launched = true;
+      mine = true;
+    }
   }
-  launch(b, true);
+  if (mine) launch(b, true);
+  batch_release(b);                     // the probe's reference
 }
 
 void schedule(Executor *ex, int kind, const double *src, double *dst, int64_t n,
@@ -469,7 +481,10 @@ void schedule(Executor *ex, int kind, const double *src, double *dst, int64_t n,
       b = new Batch();
       b->ex = ex;
       b->kind = kind;
-      if (m->cfg.max_agg > 1) ex->open[kind] = b;
+      if (m->cfg.max_agg > 1) {
+        ex->open[kind] = b;
+        b->refs.store(2, std::memory_order_relaxed);   // launch + idleness probe
+      }
       opened = b;
     }
     b->members.push_back(Req{src, dst, n, t});
