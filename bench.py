@@ -135,6 +135,32 @@ def cpu_reference_sample(subgrids: int, budget_s: float, threads: int = 0):
     return subgrids * 512 * steps / el, threads, steps, el
 
 
+def machine_ablation(subgrids=512, steps=5, repeats=3):
+    """The paper's ablation in the same run: the mini-app machine (native C++
+    runtime, tb_machine_run) at the paper's scenario size (512 sub-grids,
+    PAPER.md:775-782) with 32 executors x max 8 aggregated, 8 workers
+    (PAPER.md:931-933), completion by POLLING vs HOSTTASK vs FENCE. Median of
+    `repeats` runs of the mean step time over steps 2..N."""
+    from paper_2303_08058_b200.bridge import IntegrationMode
+    from paper_2303_08058_b200.native_machine import run_native
+    out = {"config": f"native machine, {subgrids} sub-grids x {steps} steps, "
+                     "8 workers, 32 executors, max 8 aggregated, median of "
+                     f"{repeats}"}
+    checks = set()
+    for mode in (IntegrationMode.POLLING, IntegrationMode.HOSTTASK, IntegrationMode.FENCE):
+        ms = []
+        for _ in range(repeats):
+            res, _ = run_native(subgrids, steps, workers=8, executors=32, max_agg=8,
+                                mode=mode)
+            ms.append(statistics.fmean(res.step_ms[1:]))
+            checks.add(res.checksum.hex())
+        out[f"{mode.value}_ms_per_step"] = statistics.median(ms)
+    out["speedup_polling_vs_fence"] = out["fence_ms_per_step"] / out["polling_ms_per_step"]
+    out["speedup_hosttask_vs_fence"] = out["fence_ms_per_step"] / out["hosttask_ms_per_step"]
+    out["checksums_identical"] = len(checks) == 1
+    return out
+
+
 def run_reference_arm(args, workload_key, rank, world):
     if rank != 0:
         return 0
@@ -192,6 +218,8 @@ def main(argv=None):
     ap.add_argument("--step-impl", choices=["auto", "reg", "bulk", "regpf", "lean", "pair", "bulk1"], default="auto",
                     help="K2 variant (tb_set_option TB_OPT_STEP_IMPL)")
     ap.add_argument("--e2e-chunks", type=int, default=8)
+    ap.add_argument("--no-ablation", action="store_true",
+                    help="skip the polling/host-task/fence machine ablation")
     ap.add_argument("--spw", type=int, default=0,
                     help="K2 sub-grids per warp per CTA (0 = one persistent wave)")
     args = ap.parse_args(argv)
@@ -299,6 +327,9 @@ def main(argv=None):
                     traffic = ent["dram_bytes_per_launch"]
             except (OSError, ValueError, KeyError):
                 pass
+        ablation = None
+        if not args.no_ablation:
+            ablation = machine_ablation()
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             v, cores, nsteps, el = cpu_reference_sample(per_gpu, args.cpu_budget)
@@ -338,6 +369,7 @@ def main(argv=None):
                     "ms_per_step": e2e_ms, "chunks": args.e2e_chunks,
                     "api": "RingStepper.step_host (pinned H2D | K2 | D2H pipelined "
                            "over chunks on 3 streams, chained across steps)"},
+            "ablation": ablation,
             "gpu_launches": (1 if world == 1 else 2) * args.steps,
             "clocks": clocks,
             "wall_s_timed_region": wall,

@@ -258,11 +258,12 @@ class HostTasks {
   };
   static void CUDART_CB trampoline(void *p) {   // CUDA driver thread: enqueue only
     Item *it = static_cast<Item *>(p);
+    HostTasks *self = it->self;   // `it` may be consumed as soon as it is queued
     {
-      std::lock_guard<std::mutex> g(it->self->mu_);
-      it->self->ready_.push_back(it);
+      std::lock_guard<std::mutex> g(self->mu_);
+      self->ready_.push_back(it);
     }
-    it->self->cv_.notify_one();
+    self->cv_.notify_one();
   }
   void run() {
     for (;;) {

@@ -69,3 +69,11 @@ def test_native_polling_beats_fence():
     print(f"native: polling {pm:.3f} ms/step vs fence {fm:.3f} -> {fm / pm:.3f}x")
     assert poll[0].checksum == fence[0].checksum
     assert fm / pm >= 1.05
+
+
+def test_native_machine_repeated_runs_every_mode():
+    # several full machine lifetimes in one process (the cli's repeats)
+    for mode in MODES:
+        for _ in range(3):
+            res, _ = run_native(64, 3, workers=8, executors=8, max_agg=4, mode=mode)
+            assert res.checksum == mo.run_reference(64, 3)[0]
