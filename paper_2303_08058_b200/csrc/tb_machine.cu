@@ -47,6 +47,7 @@ struct Task {
 
 // ------------------------------------------------------------------ pool --
 class Pool;
+constexpr int kIdleSpins = 256;
 thread_local Pool *t_pool = nullptr;
 thread_local int t_worker = -1;
 
@@ -107,17 +108,20 @@ class Pool {
         return true;
       }
     }
+    // steal: scan every other worker once, from a random start (a single
+    // random victim, as in src/runtime/pool.py:212-217, leaves fired
+    // continuations stranded on the polling worker's deque)
     const int n = (int)qs_.size();
-    if (n > 1) {
-      const int v = (int)(rng() % n);
-      if (v != w) {
-        Queue &q = *qs_[v];
-        std::lock_guard<std::mutex> g(q.mu);
-        if (!q.dq.empty()) {
-          *out = q.dq.back();
-          q.dq.pop_back();
-          return true;
-        }
+    const int start = n > 1 ? (int)(rng() % n) : 0;
+    for (int k = 0; k < n; ++k) {
+      const int v = (start + k) % n;
+      if (v == w) continue;
+      Queue &q = *qs_[v];
+      std::lock_guard<std::mutex> g(q.mu);
+      if (!q.dq.empty()) {
+        *out = q.dq.back();
+        q.dq.pop_back();
+        return true;
       }
     }
     return false;
@@ -129,9 +133,11 @@ class Pool {
     t_worker = w;
     std::mt19937_64 rng(seed);
     int nap_us = 5;
+    int spins = 0;
     while (alive_.load(std::memory_order_relaxed)) {
       Task t;
       if (take(w, rng, &t)) {
+        spins = 0;
         const auto t0 = Clock::now();
         t.fn(t.arg);
         busy_ns_.fetch_add(
@@ -144,6 +150,13 @@ class Pool {
       }
       if (hook_ && hook_(hook_arg_)) {
         nap_us = 5;
+        spins = 0;
+        continue;
+      }
+      // Idle: yield-spin first (a Linux sleep is >= ~50 us of timer slack,
+      // far longer than a B200 batch), then the reference's 5..100 us backoff.
+      if (++spins < kIdleSpins) {
+        std::this_thread::yield();
         continue;
       }
       std::this_thread::sleep_for(std::chrono::microseconds(nap_us));
