@@ -67,50 +67,91 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi sampling of SM clocks and throttle reasons during a region."""
+    """SM clock + throttle reasons sampled DURING the timed region: NVML in a
+    background thread every 5 ms (falls back to ``nvidia-smi -lms 50``)."""
 
-    QUERY = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+               "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+               "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+               "sw_power_cap": "nvmlClocksEventReasonSwPowerCap"}
 
     def __init__(self, gpu_index: int):
-        self.proc = None
         self.gpu = gpu_index
+        self.samples = []          # (sm_mhz, max_mhz, reasons bitmask)
+        self._stop = None
+        self._thread = None
+        self._nvml = None
+        self._proc = None
 
     def start(self):
+        import threading
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.QUERY}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except OSError:
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self._nvml = (pynvml, h)
+        except Exception:  # noqa: BLE001 - no NVML: use nvidia-smi
+            self._nvml = None
+        if self._nvml is None:
+            try:
+                q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                     "clocks_event_reasons.hw_thermal_slowdown,"
+                     "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+                self._proc = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                     "--format=csv,noheader,nounits", "-lms", "50"],
+                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            except OSError:
+                self._proc = None
+            return
+        self._stop = threading.Event()
+
+        def loop():
+            pynvml, h = self._nvml
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            while not self._stop.is_set():
+                try:
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append((sm, mx, rs))
+                except Exception:  # noqa: BLE001
+                    pass
+                self._stop.wait(0.005)
+
+        self._thread = threading.Thread(target=loop, daemon=True)
+        self._thread.start()
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            out, _ = self.proc.communicate(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-            out, _ = self.proc.communicate()
-        rows = []
-        for line in out.strip().splitlines():
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 8:
-                rows.append(parts)
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"],
+        if self._nvml is not None:
+            self._stop.set()
+            self._thread.join(timeout=2)
+            pynvml = self._nvml[0]
+            names = sorted({name for _, _, rs in self.samples
+                            for name, attr in self.REASONS.items()
+                            if rs & getattr(pynvml, attr, 0)})
+            sm = [s for s, _, _ in self.samples]
+            return {"sm_mhz": statistics.median(sm) if sm else None,
+                    "sm_max_mhz": max((m for _, m, _ in self.samples), default=None),
+                    "reasons": names, "samples": len(sm), "source": "nvml/5ms"}
+        if self._proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no clock source"],
                     "samples": 0}
-        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        self._proc.terminate()
+        try:
+            out, _ = self._proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self._proc.kill()
+            out, _ = self._proc.communicate()
+        rows = [[p.strip() for p in ln.split(",")] for ln in out.strip().splitlines()]
+        rows = [r for r in rows if len(r) >= 6]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4)
-                          if r[4 + i].lower() == "active"})
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
         return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(rows)}
+                "sm_max_mhz": max((float(r[1]) for r in rows
+                                   if r[1].replace(".", "").isdigit()), default=None),
+                "reasons": sorted({names[i] for r in rows for i in range(4)
+                                   if r[2 + i].lower() == "active"}),
+                "samples": len(rows), "source": "nvidia-smi/50ms"}
 
 
 def cpu_reference_sample(subgrids: int, budget_s: float, threads: int = 0):
@@ -207,7 +248,7 @@ def run_reference_arm(args, workload_key, rank, world):
 def main(argv=None):
     ap = argparse.ArgumentParser(description=__doc__.splitlines()[1])
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c4")
@@ -263,11 +304,10 @@ def main(argv=None):
            torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     sampler = ClockSampler(local)
-    sampler.start()
-    time.sleep(0.2)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    sampler.start()
     t_wall = time.perf_counter()
     for (s0, s1, k0, k1) in ev:
         flush.fill_(1)                      # evict L2 (256 MiB > 126 MB)
