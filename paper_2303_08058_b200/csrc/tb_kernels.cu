@@ -329,21 +329,34 @@ __device__ __forceinline__ void run_chains(double (&v)[16], int chains, int kpc)
 
 // Everything once this lane's 16 cells are in registers: ghost fold,
 // transforms, store, pairwise sum + min (src/miniapp.py:119-133).
-template <int CHAINS, int KPC>
-__device__ __forceinline__ void subgrid_body(const StepArgs &a, int64_t g, int lane,
-                                             double (&v)[16], unsigned long long *s_limbs,
-                                             double &wmin) {
+// The ghost-face value this lane folds in (lanes 0..7: the left neighbour's
+// right face; lanes 24..31: the right neighbour's left face; others 0). Issued
+// together with the sub-grid's own loads so its latency overlaps theirs.
+__device__ __forceinline__ double load_face(const StepArgs &a, int64_t g, int lane) {
   const int r = lane & 7;
-  // Ghost fold against the previous generation: cells 0..7 are lanes 0..7 at
-  // i = 0; cells 504..511 are lanes 24..31 at i = 15. Add rounds; *0.5 exact.
   if (lane < 8) {
     const double *lf =
         g == 0 ? a.left_face : a.old + (g - 1) * TB_CELLS + (TB_CELLS - TB_FACE);
-    v[0] = __dmul_rn(0.5, __dadd_rn(v[0], lf[r]));
-  } else if (lane >= 24) {
-    const double *rf = g == a.n - 1 ? a.right_face : a.old + (g + 1) * TB_CELLS;
-    v[15] = __dmul_rn(0.5, __dadd_rn(v[15], rf[r]));
+    return ld_stream(lf + r);
   }
+  if (lane >= 24) {
+    const double *rf = g == a.n - 1 ? a.right_face : a.old + (g + 1) * TB_CELLS;
+    return ld_stream(rf + r);
+  }
+  return 0.0;
+}
+
+template <int CHAINS, int KPC>
+__device__ __forceinline__ void subgrid_body(const StepArgs &a, int64_t g, int lane,
+                                             double (&v)[16], double face,
+                                             unsigned long long *s_limbs, double &wmin) {
+  const int r = lane & 7;
+  // Ghost fold against the previous generation: cells 0..7 are lanes 0..7 at
+  // i = 0; cells 504..511 are lanes 24..31 at i = 15. Add rounds; *0.5 exact.
+  if (lane < 8)
+    v[0] = __dmul_rn(0.5, __dadd_rn(v[0], face));
+  else if (lane >= 24)
+    v[15] = __dmul_rn(0.5, __dadd_rn(v[15], face));
   run_chains<CHAINS, KPC>(v, a.chains, a.kpc);
   double *dst = a.out + g * TB_CELLS + 128 * (lane >> 3) + r;
 #pragma unroll
@@ -373,26 +386,31 @@ __device__ __forceinline__ void subgrid_body(const StepArgs &a, int64_t g, int l
 // last CTA to finish (threadfence + ticket) closes the step with one warp.
 __device__ __forceinline__ void step_epilogue(const StepArgs &a,
                                               unsigned long long *s_limbs,
-                                              long long *s_min, double wmin,
-                                              int *s_last) {
+                                              long long *s_min, double wmin) {
   if (!a.acc) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (lane == 0) s_min[warp] = min_key(wmin);
-  __syncthreads();
+  __syncthreads();                    // the CTA's limbs and warp minima are in smem
+  if (warp != 0) return;              // warp 0 publishes; the rest retire now
   long long bm = s_min[0];
 #pragma unroll
   for (int w = 1; w < kStepWarps; ++w) bm = min(bm, s_min[w]);
-  acc_flush(s_limbs, bm, a.acc);
-  if (!a.finalize) return;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned long long t = atomicAdd(
-        reinterpret_cast<unsigned long long *>(a.acc) + TB_ACC_COUNT_WORD, 1ULL);
-    *s_last = (t == (unsigned long long)gridDim.x - 1);
+  for (int i = lane; i < TB_ACC_LIMBS; i += 32) {
+    const unsigned long long v = s_limbs[i];
+    if (v) atomicAdd(reinterpret_cast<unsigned long long *>(a.acc) + i, v);
   }
-  __syncthreads();
-  if (*s_last && warp == 0) {
+  if (lane == 0)
+    atomicMin(reinterpret_cast<long long *>(a.acc) + TB_ACC_MIN_WORD, bm);
+  if (!a.finalize) return;
+  // Last-CTA ticket: each publishing lane fences its own atomics, then lane 0
+  // takes a ticket; the CTA that draws gridDim.x-1 closes the step.
+  __threadfence();
+  __syncwarp();
+  unsigned long long t = 0;
+  if (lane == 0)
+    t = atomicAdd(reinterpret_cast<unsigned long long *>(a.acc) + TB_ACC_COUNT_WORD, 1ULL);
+  t = __shfl_sync(0xffffffffu, t, 0);
+  if (t == (unsigned long long)gridDim.x - 1) {
     __threadfence();
     warp_finalize(a.acc, a.piece, a.dt, a.checksum, 1);
   }
@@ -405,7 +423,6 @@ template <int CHAINS, int KPC, bool PF, int MINB = 1>
 __global__ void __launch_bounds__(kStepThreads, MINB) k_step(StepArgs a) {
   __shared__ unsigned long long s_limbs[TB_ACC_LIMBS];
   __shared__ long long s_min[kStepWarps];
-  __shared__ int s_last;
   if (a.acc) {
     for (int i = threadIdx.x; i < TB_ACC_LIMBS; i += blockDim.x) s_limbs[i] = 0ULL;
     __syncthreads();
@@ -417,23 +434,26 @@ __global__ void __launch_bounds__(kStepThreads, MINB) k_step(StepArgs a) {
   double wmin = CUDART_INF;
   int64_t g = (int64_t)blockIdx.x * kStepWarps + warp;
   if (PF) {
-    double nxt[16];
+    double nxt[16], nface = 0.0;
     if (g < a.n) {
       const double *src = a.old + g * TB_CELLS + lane_off;
 #pragma unroll
       for (int i = 0; i < 16; ++i) nxt[i] = ld_stream(src + 8 * i);
+      nface = load_face(a, g, lane);
     }
     for (; g < a.n; g += gstride) {
       double v[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] = nxt[i];
+      const double face = nface;
       const int64_t gn = g + gstride;
       if (gn < a.n) {
         const double *src = a.old + gn * TB_CELLS + lane_off;
 #pragma unroll
         for (int i = 0; i < 16; ++i) nxt[i] = ld_stream(src + 8 * i);
+        nface = load_face(a, gn, lane);
       }
-      subgrid_body<CHAINS, KPC>(a, g, lane, v, s_limbs, wmin);
+      subgrid_body<CHAINS, KPC>(a, g, lane, v, face, s_limbs, wmin);
     }
   } else {
     for (; g < a.n; g += gstride) {
@@ -441,10 +461,11 @@ __global__ void __launch_bounds__(kStepThreads, MINB) k_step(StepArgs a) {
       double v[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] = ld_stream(src + 8 * i);
-      subgrid_body<CHAINS, KPC>(a, g, lane, v, s_limbs, wmin);
+      const double face = load_face(a, g, lane);
+      subgrid_body<CHAINS, KPC>(a, g, lane, v, face, s_limbs, wmin);
     }
   }
-  step_epilogue(a, s_limbs, s_min, wmin, &s_last);
+  step_epilogue(a, s_limbs, s_min, wmin);
 }
 
 // K2c: a warp PAIR per sub-grid, 8 cells per lane (half the registers of
@@ -480,7 +501,6 @@ __global__ void __launch_bounds__(kStepThreads, 6) k_step_pair(StepArgs a) {
   __shared__ unsigned long long s_limbs[TB_ACC_LIMBS];
   __shared__ long long s_min[kStepWarps];
   __shared__ double s_pair[2][kStepWarps / 2][2][2];   // [parity][pair][q][sum,min]
-  __shared__ int s_last;
   if (a.acc) {
     for (int i = threadIdx.x; i < TB_ACC_LIMBS; i += blockDim.x) s_limbs[i] = 0ULL;
     __syncthreads();
@@ -543,7 +563,7 @@ __global__ void __launch_bounds__(kStepThreads, 6) k_step_pair(StepArgs a) {
     }
     wmin = fmin(wmin, m);
   }
-  step_epilogue(a, s_limbs, s_min, wmin, &s_last);
+  step_epilogue(a, s_limbs, s_min, wmin);
 }
 
 // K2b: each warp streams its sub-grids through a kStages-deep ring of 4 KiB
@@ -589,7 +609,6 @@ __global__ void __launch_bounds__(kStepThreads) k_step_bulk(StepArgs a) {
   __shared__ __align__(8) uint64_t bars[kStepWarps][kStages];
   __shared__ unsigned long long s_limbs[TB_ACC_LIMBS];
   __shared__ long long s_min[kStepWarps];
-  __shared__ int s_last;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < TB_ACC_LIMBS; i += blockDim.x) s_limbs[i] = 0ULL;
@@ -609,6 +628,7 @@ __global__ void __launch_bounds__(kStepThreads) k_step_bulk(StepArgs a) {
   }
   double wmin = CUDART_INF;
   int it = 0;
+  double face = g0 < a.n ? load_face(a, g0, lane) : 0.0;
   for (int64_t g = g0; g < a.n; g += gstride, ++it) {
     const int s = it % kStages;
     mbar_wait(&bars[warp][s], (uint32_t)((it / kStages) & 1));
@@ -624,9 +644,11 @@ __global__ void __launch_bounds__(kStepThreads) k_step_bulk(StepArgs a) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       bulk_load_subgrid(slots + s * kSlot, a.old + gn * TB_CELLS, &bars[warp][s]);
     }
-    subgrid_body<CHAINS, KPC>(a, g, lane, v, s_limbs, wmin);
+    const double cur_face = face;
+    if (g + gstride < a.n) face = load_face(a, g + gstride, lane);   // next one's face
+    subgrid_body<CHAINS, KPC>(a, g, lane, v, cur_face, s_limbs, wmin);
   }
-  step_epilogue(a, s_limbs, s_min, wmin, &s_last);
+  step_epilogue(a, s_limbs, s_min, wmin);
 }
 
 int g_step_impl = TB_STEP_AUTO;
