@@ -628,9 +628,11 @@ __global__ void __launch_bounds__(kStepThreads) k_step_bulk(StepArgs a) {
   }
   double wmin = CUDART_INF;
   int it = 0;
-  double face = g0 < a.n ? load_face(a, g0, lane) : 0.0;
   for (int64_t g = g0; g < a.n; g += gstride, ++it) {
     const int s = it % kStages;
+    // this sub-grid's ghost faces: issued before waiting for its bulk copy so
+    // the two latencies overlap (neighbour warps are loading those lines now)
+    const double face = load_face(a, g, lane);
     mbar_wait(&bars[warp][s], (uint32_t)((it / kStages) & 1));
     const double *src = slots + s * kSlot + kBlkPitch * (lane >> 3) + (lane & 7);
     double v[16];
@@ -644,9 +646,7 @@ __global__ void __launch_bounds__(kStepThreads) k_step_bulk(StepArgs a) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       bulk_load_subgrid(slots + s * kSlot, a.old + gn * TB_CELLS, &bars[warp][s]);
     }
-    const double cur_face = face;
-    if (g + gstride < a.n) face = load_face(a, g + gstride, lane);   // next one's face
-    subgrid_body<CHAINS, KPC>(a, g, lane, v, cur_face, s_limbs, wmin);
+    subgrid_body<CHAINS, KPC>(a, g, lane, v, face, s_limbs, wmin);
   }
   step_epilogue(a, s_limbs, s_min, wmin);
 }
