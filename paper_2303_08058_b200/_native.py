@@ -169,11 +169,13 @@ def _load():
 
 
 def fast():
-    return _load()[0]
+    libs = _libs
+    return libs[0] if libs is not None else _load()[0]
 
 
 def blocking():
-    return _load()[1]
+    libs = _libs
+    return libs[1] if libs is not None else _load()[1]
 
 
 def call(name: str, *args) -> int:

@@ -25,6 +25,8 @@ import threading
 from collections import deque
 from typing import Callable, Dict, Optional
 
+from .. import _native as N
+
 
 class EventCallback:
     """An event paired with what to run once it completes (or on abandon)."""
@@ -71,7 +73,6 @@ class PollRegistry:
         if self._native is None:
             with self._native_lock:
                 if self._native is None:
-                    from .. import _native as N
                     h = ctypes.c_uint64(0)
                     N.call("tb_poll_create", ctypes.byref(h))
                     self._fired_buf = (ctypes.c_uint64 * _FIRE_CAP)()
@@ -84,7 +85,6 @@ class PollRegistry:
             reg = self._native_reg()
             token = next(self._next_token)
             self._tokens[token] = ec
-            from .. import _native as N
             rc = N.fast().tb_poll_add(reg, handle, getattr(ec.event, "chain", 0), token)
             if rc != 0:
                 del self._tokens[token]
@@ -139,7 +139,6 @@ class PollRegistry:
         return fired
 
     def _poll_native(self) -> int:
-        from .. import _native as N
         n = ctypes.c_int(0)
         buf = self._fired_buf
         # GIL held: the native body never blocks, and releasing the GIL here
@@ -185,7 +184,6 @@ class PollRegistry:
                 ec = self._inbox.popleft()
                 entries.append((ec, ec.event.is_complete()))
             if self._native is not None:
-                from .. import _native as N
                 cap = max(1, len(self._tokens))
                 toks = (ctypes.c_uint64 * cap)()
                 done = (ctypes.c_uint8 * cap)()
@@ -207,7 +205,6 @@ class PollRegistry:
 
     def close(self) -> None:
         if self._native is not None:
-            from .. import _native as N
             N.call("tb_poll_destroy", self._native)
             self._native = None
 
