@@ -383,6 +383,7 @@ def main(argv=None):
             "dtype": "f64", "data": "synthetic (closed-form ring ICs, src/miniapp.py:72-77)",
             "config": {"workload": desc, "subgrids": subgrids, "subgrids_per_gpu": per_gpu,
                        "cells": cells_total, "parallelism": f"ring-dp{world}",
+                       "halo": st.halo_mode,
                        "l2": "flushed before every timed step (256 MiB write)"},
             "parity": {"run_reference_512x15_equals_GOLDEN_DEFAULTS": parity},
             "roofline": {"bound": "hbm",

@@ -188,6 +188,17 @@ int tb_acc_add(tb_stream_t s, const double *x, int64_t n, int64_t *acc);
 int tb_acc_finalize(tb_stream_t s, int64_t *acc, double *piece, double *dt,
                     double *checksum, int reset);
 
+/* ---------------------------------------------------- peer memory -- */
+/* CUDA IPC for the multi-GPU ring: export a device allocation (handle =
+ * TB_IPC_HANDLE_BYTES bytes), map a peer's export, unmap. With the
+ * neighbours' state buffers mapped, tb_step's left_face/right_face may point
+ * into peer HBM: the ring halo exchange (src/miniapp.py:119-121 across a
+ * partition boundary) is then two 64-byte NVLink loads inside K2. */
+#define TB_IPC_HANDLE_BYTES 64
+int tb_ipc_get_handle(void *dptr, uint8_t *handle);
+int tb_ipc_open_handle(const uint8_t *handle, void **dptr);
+int tb_ipc_close(void *dptr);
+
 /* -------------------------------------------------- poll registry -- */
 /* PollRegistry (src/runtime/polling.py:17-147): a lock-free MPSC inbox of
  * (event, token) and a poll-owned pending vector, drained by a single-entrant

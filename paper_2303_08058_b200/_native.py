@@ -32,6 +32,7 @@ TB_ACC_BIAS = 1074
 TB_ACC_MIN_WORD = 68
 TB_ACC_COUNT_WORD = 70
 TB_ACC_WORDS = 72
+TB_IPC_HANDLE_BYTES = 64
 
 TB_OPT_STEP_IMPL = 1
 TB_STEP_AUTO = 0
@@ -131,6 +132,9 @@ SIGNATURES = {
     "tb_htq_close": [_u64],
     "tb_htq_destroy": [_u64],
     "tb_machine_run": [_vp, _vp, _vp, _vp],
+    "tb_ipc_get_handle": [_vp, _vp],
+    "tb_ipc_open_handle": [_vp, _pvp],
+    "tb_ipc_close": [_vp],
 }
 BLOCKING = {"tb_init", "tb_device_sync", "tb_stream_sync", "tb_event_wait",
             "tb_htq_next", "tb_htq_destroy", "tb_malloc", "tb_free",

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstring>
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
@@ -343,6 +344,33 @@ int tb_memset(tb_stream_t s, void *p, int value, size_t n) {
   if (n && !p) return TB_E_INVALID;
   ensure_device();
   return n ? rc(cudaMemsetAsync(p, value, n, S(s))) : TB_OK;
+}
+
+// ------------------------------------------------------------ peer memory
+// CUDA IPC: a rank exports its state buffers, ring neighbours map them and
+// K2 reads the two ghost faces straight out of the neighbour's HBM (NVLink
+// P2P on a multi-GPU node) — the halo exchange becomes two 64-byte loads.
+int tb_ipc_get_handle(void *dptr, uint8_t *handle) {
+  if (!dptr || !handle) return TB_E_INVALID;
+  ensure_device();
+  cudaIpcMemHandle_t h;
+  const int r = rc(cudaIpcGetMemHandle(&h, dptr));
+  if (r == TB_OK) memcpy(handle, &h, sizeof h);
+  return r;
+}
+
+int tb_ipc_open_handle(const uint8_t *handle, void **dptr) {
+  if (!handle || !dptr) return TB_E_INVALID;
+  ensure_device();
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof h);
+  return rc(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+}
+
+int tb_ipc_close(void *dptr) {
+  if (!dptr) return TB_E_INVALID;
+  ensure_device();
+  return rc(cudaIpcCloseMemHandle(dptr));
 }
 
 // ------------------------------------------------------- aggregation batch

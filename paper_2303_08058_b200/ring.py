@@ -64,8 +64,11 @@ def chunk_bounds(n: int, chunks: int) -> List[Tuple[int, int]]:
     return out
 
 
-def _ptr(t: Optional[torch.Tensor]):
-    return None if t is None else t.data_ptr()
+def _ptr(t):
+    """Device address of a tensor (or a raw address already, e.g. peer HBM)."""
+    if t is None or isinstance(t, int):
+        return t
+    return t.data_ptr()
 
 
 class CudaRingOps:
@@ -122,7 +125,8 @@ class RingStepper:
     def __init__(self, subgrids: int, device: Optional[torch.device] = None,
                  rank: int = 0, world: int = 1, chains: int = 3,
                  kernels_per_chain: int = 5, max_steps: int = 1 << 16,
-                 ops=None, group=None, collect_subgrid_stats: bool = False):
+                 ops=None, group=None, collect_subgrid_stats: bool = False,
+                 halo: str = "auto"):
         if subgrids < 1:
             raise ValueError("subgrids must be >= 1")
         if device is None:
@@ -152,6 +156,56 @@ class RingStepper:
         self._host_prev = None
         self.ops.init_cells(self.state[0], subgrids, self.lo)
         self.ops.acc_reset(self.acc)
+        # Multi-GPU halo: "p2p" maps the ring neighbours' state buffers (CUDA
+        # IPC) so K2 reads the ghost faces straight from their HBM; "nccl"
+        # sends them with NCCL P2P; "auto" tries p2p, else nccl.
+        self.halo_mode = "local" if world == 1 else "nccl"
+        self._peers = None
+        if world > 1 and halo not in ("auto", "p2p", "nccl"):
+            raise ValueError(f"unknown halo mode {halo!r}")
+        if world > 1 and halo != "nccl" and isinstance(self.ops, CudaRingOps):
+            try:
+                self._peers = self._map_peers()
+                self.halo_mode = "p2p"
+            except Exception:
+                if halo == "p2p":
+                    raise
+                self._peers = None
+
+    def _map_peers(self):
+        """Exchange IPC handles of both state generations with every rank and
+        map the left and right ring neighbours' buffers into this process."""
+        import ctypes
+
+        import torch.distributed as dist
+        mine = []
+        for t in self.state:
+            share = t.untyped_storage()._share_cuda_()
+            # (device, ipc handle bytes, storage bytes, offset of the storage
+            #  within its cudaMalloc allocation, ...)
+            mine.append((bytes(share[1]), int(share[3]) + t.storage_offset() * 8))
+        table = [None] * self.world
+        dist.all_gather_object(table, (mine, self.n), group=self.group)
+        left, right = (self.rank - 1) % self.world, (self.rank + 1) % self.world
+        opened = {}
+        for peer in sorted({left, right}):
+            ptrs = []
+            for handle, offset in table[peer][0]:
+                base = ctypes.c_void_p()
+                buf = (ctypes.c_uint8 * N.TB_IPC_HANDLE_BYTES).from_buffer_copy(
+                    handle[:N.TB_IPC_HANDLE_BYTES])
+                N.call("tb_ipc_open_handle", buf, ctypes.byref(base))
+                ptrs.append((base.value, base.value + offset))
+            opened[peer] = (ptrs, table[peer][1])
+        return {"left": opened[left], "right": opened[right], "opened": opened}
+
+    def close(self) -> None:
+        """Unmap neighbours' buffers (p2p halo)."""
+        if self._peers is not None:
+            for ptrs, _ in self._peers["opened"].values():
+                for base, _ in ptrs:
+                    N.call("tb_ipc_close", base)
+            self._peers = None
 
     # -------------------------------------------------------------- state --
     @property
@@ -230,9 +284,24 @@ class RingStepper:
         self.steps_done += 1
 
     def _step_partitioned(self, old, out, kernel_events) -> None:
-        """N>1: post the halo exchange, run K2 on the interior sub-grids while
-        the 2 x 64 B faces are in flight, then the two boundary sub-grids."""
+        """N>1. p2p halo: one K2 launch whose two ghost-face pointers point
+        into the neighbours' HBM (the previous step's all-reduce orders every
+        rank's K2(t-1) before any K2(t), and K2(t) before any K2(t+1), so no
+        extra synchronisation is needed). nccl halo: post the exchange, run K2
+        on the interior sub-grids while the 2 x 64 B faces are in flight, then
+        the two boundary sub-grids."""
         n = self.n
+        if self._peers is not None:
+            (lptrs, ln), (rptrs, _) = self._peers["left"], self._peers["right"]
+            lf = lptrs[self.cur][1] + ((ln - 1) * CELLS + CELLS - FACE) * 8
+            rf = rptrs[self.cur][1]
+            if kernel_events is not None:
+                kernel_events[0].record()
+            self.ops.step(old, out, lf, rf, self.chains, self.kpc, self.acc,
+                          self.mins, self.sums)
+            if kernel_events is not None:
+                kernel_events[1].record()
+            return
         reqs = self._exchange_start(old[0, :FACE], old[n - 1, CELLS - FACE:])
         if kernel_events is not None:
             kernel_events[0].record()
