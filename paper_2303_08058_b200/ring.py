@@ -180,10 +180,14 @@ class RingStepper:
         import torch.distributed as dist
         mine = []
         for t in self.state:
-            share = t.untyped_storage()._share_cuda_()
-            # (device, ipc handle bytes, storage bytes, offset of the storage
-            #  within its cudaMalloc allocation, ...)
-            mine.append((bytes(share[1]), int(share[3]) + t.storage_offset() * 8))
+            # The caching allocator sub-allocates: IPC exports whole cudaMalloc
+            # blocks, so export the block base and ship the tensor's offset.
+            storage = t.untyped_storage()
+            block_offset = int(storage._share_cuda_()[3])
+            base = storage.data_ptr() - block_offset
+            handle = (ctypes.c_uint8 * N.TB_IPC_HANDLE_BYTES)()
+            N.call("tb_ipc_get_handle", base, handle)
+            mine.append((bytes(handle), block_offset + t.storage_offset() * 8))
         table = [None] * self.world
         dist.all_gather_object(table, (mine, self.n), group=self.group)
         left, right = (self.rank - 1) % self.world, (self.rank + 1) % self.world
@@ -192,8 +196,7 @@ class RingStepper:
             ptrs = []
             for handle, offset in table[peer][0]:
                 base = ctypes.c_void_p()
-                buf = (ctypes.c_uint8 * N.TB_IPC_HANDLE_BYTES).from_buffer_copy(
-                    handle[:N.TB_IPC_HANDLE_BYTES])
+                buf = (ctypes.c_uint8 * N.TB_IPC_HANDLE_BYTES).from_buffer_copy(handle)
                 N.call("tb_ipc_open_handle", buf, ctypes.byref(base))
                 ptrs.append((base.value, base.value + offset))
             opened[peer] = (ptrs, table[peer][1])

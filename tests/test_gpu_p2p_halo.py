@@ -50,10 +50,14 @@ def test_p2p_halo_ring_matches_reference(world, subgrids, steps):
              for r in range(world)]
     for p in procs:
         p.start()
-    outs = [q.get(timeout=300) for _ in range(world)]
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
+    try:
+        outs = [q.get(timeout=120) for _ in range(world)]
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    assert all(p.exitcode == 0 for p in procs)
     cs, dts, cells = mo.run_reference_cells(subgrids, steps)
     for rank, mode, got_cs, got_dts, lo, got in outs:
         assert mode == "p2p"
