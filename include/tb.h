@@ -199,6 +199,18 @@ int tb_ipc_get_handle(void *dptr, uint8_t *handle);
 int tb_ipc_open_handle(const uint8_t *handle, void **dptr);
 int tb_ipc_close(void *dptr);
 
+/* The step's cross-rank reduction over peer memory (replaces the two
+ * all-reduces of the multi-GPU step, and is its step barrier): adds
+ * local_acc into every rank's accumulator for this step's parity
+ * (peer_accs: DEVICE array of nranks pointers, IPC-mapped, own entry local)
+ * with system-scope atomics, bumps each rank's TB_ACC_COUNT_WORD, resets
+ * local_acc, waits until my_acc has nranks arrivals, then finalises my_acc
+ * exactly as tb_acc_finalize(..., reset=1). Accumulators must alternate
+ * between two parities step to step. */
+int tb_acc_allreduce_p2p(tb_stream_t s, int64_t *local_acc, int64_t *const *peer_accs,
+                         int nranks, int64_t *my_acc, double *piece, double *dt,
+                         double *checksum);
+
 /* -------------------------------------------------- poll registry -- */
 /* PollRegistry (src/runtime/polling.py:17-147): a lock-free MPSC inbox of
  * (event, token) and a poll-owned pending vector, drained by a single-entrant

@@ -135,6 +135,7 @@ SIGNATURES = {
     "tb_ipc_get_handle": [_vp, _vp],
     "tb_ipc_open_handle": [_vp, _pvp],
     "tb_ipc_close": [_vp],
+    "tb_acc_allreduce_p2p": [_u64, _vp, _vp, _int, _vp, _vp, _vp, _vp],
 }
 BLOCKING = {"tb_init", "tb_device_sync", "tb_stream_sync", "tb_event_wait",
             "tb_htq_next", "tb_htq_destroy", "tb_malloc", "tb_free",

@@ -760,6 +760,59 @@ int launch_step(cudaStream_t st, StepArgs a) {
   return tb::last_error();
 }
 
+
+// ------------------------------------------- peer-memory accumulator reduce --
+// The step's cross-rank reduction without a collective library: every rank
+// adds its local limbs into EVERY rank's accumulator with system-scope
+// atomics over NVLink (a handful of non-zero limbs), bumps each rank's
+// arrival counter, then spins until its own counter reaches nranks and
+// finalises locally — all ranks round the identical exact sum. The arrival
+// wait is also the cross-rank step barrier the peer-memory halo relies on.
+// peer_accs[p] points at rank p's accumulator for this step's parity (mapped
+// with CUDA IPC; the own entry is local). Accumulators alternate parity each
+// step, so a fast rank's next contributions never meet a slow rank's reset.
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void k_acc_allreduce_p2p(int64_t *local_acc, int64_t *const *peer_accs,
+                                    int nranks, int64_t *my_acc, double *piece, double *dt,
+                                    double *checksum) {
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x >= 32) return;
+  // 1. publish this rank's contribution to every rank (including itself)
+  for (int p = 0; p < nranks; ++p) {
+    unsigned long long *dst = reinterpret_cast<unsigned long long *>(peer_accs[p]);
+    for (int i = lane; i < TB_ACC_LIMBS; i += 32) {
+      const long long v = ld_cg_s64(local_acc + i);
+      if (v) atomicAdd_system(dst + i, (unsigned long long)v);
+    }
+    if (lane == 0)
+      atomicMin_system(reinterpret_cast<long long *>(dst) + TB_ACC_MIN_WORD,
+                       ld_cg_s64(local_acc + TB_ACC_MIN_WORD));
+  }
+  __threadfence_system();
+  __syncwarp();
+  if (lane == 0)
+    for (int p = 0; p < nranks; ++p)
+      atomicAdd_system(reinterpret_cast<unsigned long long *>(peer_accs[p]) + TB_ACC_COUNT_WORD,
+                       1ULL);
+  // 2. local accumulator is free again
+  for (int i = lane; i < TB_ACC_WORDS; i += 32)
+    local_acc[i] = (i == TB_ACC_MIN_WORD) ? kKeyInf : 0;
+  // 3. wait for every rank's contribution, then round it (and reset)
+  if (lane == 0) {
+    const unsigned long long *cnt =
+        reinterpret_cast<const unsigned long long *>(my_acc) + TB_ACC_COUNT_WORD;
+    while (ld_acquire_sys_u64(cnt) < (unsigned long long)nranks) __nanosleep(200);
+  }
+  __syncwarp();
+  __threadfence_system();
+  warp_finalize(my_acc, piece, dt, checksum, 1);
+}
+
 }  // namespace
 
 // ------------------------------------------------------------ launchers --
@@ -886,6 +939,15 @@ int tb_acc_finalize(tb_stream_t s, int64_t *acc, double *piece, double *dt,
   if (!acc) return TB_E_INVALID;
   k_acc_finalize<<<1, 32, 0, reinterpret_cast<cudaStream_t>(s)>>>(acc, piece, dt,
                                                                    checksum, reset);
+  return tb::last_error();
+}
+
+int tb_acc_allreduce_p2p(tb_stream_t s, int64_t *local_acc, int64_t *const *peer_accs,
+                         int nranks, int64_t *my_acc, double *piece, double *dt,
+                         double *checksum) {
+  if (!local_acc || !peer_accs || !my_acc || nranks < 1) return TB_E_INVALID;
+  k_acc_allreduce_p2p<<<1, 32, 0, reinterpret_cast<cudaStream_t>(s)>>>(
+      local_acc, peer_accs, nranks, my_acc, piece, dt, checksum);
   return tb::last_error();
 }
 

@@ -172,42 +172,61 @@ class RingStepper:
                     raise
                 self._peers = None
 
+    @staticmethod
+    def _export(t: torch.Tensor):
+        """(IPC handle of t's cudaMalloc block, byte offset of t in it). The
+        caching allocator sub-allocates; IPC exports whole blocks."""
+        import ctypes
+        storage = t.untyped_storage()
+        block_offset = int(storage._share_cuda_()[3])
+        handle = (ctypes.c_uint8 * N.TB_IPC_HANDLE_BYTES)()
+        N.call("tb_ipc_get_handle", storage.data_ptr() - block_offset, handle)
+        return bytes(handle), block_offset + t.storage_offset() * t.element_size()
+
     def _map_peers(self):
-        """Exchange IPC handles of both state generations with every rank and
-        map the left and right ring neighbours' buffers into this process."""
+        """Exchange IPC handles with every rank; map the ring neighbours' two
+        state generations (peer-memory halo) and every rank's reduction
+        accumulators (peer-memory all-reduce)."""
         import ctypes
 
         import torch.distributed as dist
-        mine = []
-        for t in self.state:
-            # The caching allocator sub-allocates: IPC exports whole cudaMalloc
-            # blocks, so export the block base and ship the tensor's offset.
-            storage = t.untyped_storage()
-            block_offset = int(storage._share_cuda_()[3])
-            base = storage.data_ptr() - block_offset
-            handle = (ctypes.c_uint8 * N.TB_IPC_HANDLE_BYTES)()
-            N.call("tb_ipc_get_handle", base, handle)
-            mine.append((bytes(handle), block_offset + t.storage_offset() * 8))
+        # two parities of the cross-rank accumulator (see tb_acc_allreduce_p2p)
+        self.gacc = torch.zeros((2, N.TB_ACC_WORDS), dtype=torch.int64, device=self.device)
+        self.gacc[:, N.TB_ACC_MIN_WORD] = 0x7FF0000000000000      # key(+inf)
+        mine = ([self._export(t) for t in self.state], self.n, self._export(self.gacc))
         table = [None] * self.world
-        dist.all_gather_object(table, (mine, self.n), group=self.group)
-        left, right = (self.rank - 1) % self.world, (self.rank + 1) % self.world
+        dist.all_gather_object(table, mine, group=self.group)
         opened = {}
+
+        def open_handle(handle, offset):
+            base = ctypes.c_void_p()
+            buf = (ctypes.c_uint8 * N.TB_IPC_HANDLE_BYTES).from_buffer_copy(handle)
+            N.call("tb_ipc_open_handle", buf, ctypes.byref(base))
+            opened.setdefault(base.value, 0)
+            return base.value, base.value + offset
+
+        left, right = (self.rank - 1) % self.world, (self.rank + 1) % self.world
+        state = {}
         for peer in sorted({left, right}):
-            ptrs = []
-            for handle, offset in table[peer][0]:
-                base = ctypes.c_void_p()
-                buf = (ctypes.c_uint8 * N.TB_IPC_HANDLE_BYTES).from_buffer_copy(handle)
-                N.call("tb_ipc_open_handle", buf, ctypes.byref(base))
-                ptrs.append((base.value, base.value + offset))
-            opened[peer] = (ptrs, table[peer][1])
-        return {"left": opened[left], "right": opened[right], "opened": opened}
+            state[peer] = ([open_handle(h, off) for h, off in table[peer][0]], table[peer][1])
+        row = self.gacc.stride(0) * self.gacc.element_size()
+        tab = [[0] * self.world for _ in range(2)]
+        for p in range(self.world):
+            if p == self.rank:
+                base_ptr = self.gacc.data_ptr()
+            else:
+                base_ptr = open_handle(*table[p][2])[1]
+            for parity in range(2):
+                tab[parity][p] = base_ptr + parity * row
+        self.peer_tab = torch.tensor(tab, dtype=torch.int64, device=self.device)
+        return {"left": state[left], "right": state[right], "bases": list(opened)}
 
     def close(self) -> None:
         """Unmap neighbours' buffers (p2p halo)."""
         if self._peers is not None:
-            for ptrs, _ in self._peers["opened"].values():
-                for base, _ in ptrs:
-                    N.call("tb_ipc_close", base)
+            torch.cuda.synchronize(self.device)
+            for base in self._peers["bases"]:
+                N.call("tb_ipc_close", base)
             self._peers = None
 
     # -------------------------------------------------------------- state --
@@ -268,7 +287,14 @@ class RingStepper:
         n = self.n
         if self.world > 1:
             self._step_partitioned(old, out, kernel_events)
-            self._close(k)
+            if self._peers is not None:
+                # exact cross-rank reduction + step barrier over peer memory
+                N.call("tb_acc_allreduce_p2p", self.ops.stream(), _ptr(self.acc),
+                       self.peer_tab[k & 1].data_ptr(), self.world,
+                       self.gacc[k & 1].data_ptr(), _ptr(self.pieces[k:k + 1]),
+                       _ptr(self.dts[k:k + 1]), _ptr(self.checksum))
+            else:
+                self._close(k)
         else:
             lf, rf = old[n - 1, CELLS - FACE:], old[0, :FACE]   # ring wraps locally
             if kernel_events is not None:
