@@ -384,6 +384,9 @@ def main(argv=None):
             "config": {"workload": desc, "subgrids": subgrids, "subgrids_per_gpu": per_gpu,
                        "cells": cells_total, "parallelism": f"ring-dp{world}",
                        "halo": st.halo_mode,
+                       "reduction": ("peer-memory atomics (tb_acc_allreduce_p2p)"
+                                     if st.halo_mode == "p2p" else
+                                     ("nccl all_reduce" if world > 1 else "in-kernel")),
                        "l2": "flushed before every timed step (256 MiB write)"},
             "parity": {"run_reference_512x15_equals_GOLDEN_DEFAULTS": parity},
             "roofline": {"bound": "hbm",
