@@ -259,6 +259,11 @@ def main(argv=None):
     ap.add_argument("--step-impl", choices=["auto", "reg", "bulk", "regpf", "lean", "pair", "bulk1"], default="auto",
                     help="K2 variant (tb_set_option TB_OPT_STEP_IMPL)")
     ap.add_argument("--e2e-chunks", type=int, default=8)
+    ap.add_argument("--dist-backend", default="nccl",
+                    help="torch.distributed backend for N>1 (gloo only to exercise the "
+                         "multi-rank code path with several ranks on one GPU)")
+    ap.add_argument("--same-gpu", action="store_true",
+                    help="all ranks on cuda:0 (with --dist-backend gloo: code-path test)")
     ap.add_argument("--no-ablation", action="store_true",
                     help="skip the polling/host-task/fence machine ablation")
     ap.add_argument("--spw", type=int, default=0,
@@ -269,6 +274,8 @@ def main(argv=None):
     rank = env_int("RANK", 0)
     world = env_int("WORLD_SIZE", 1)
     local = env_int("LOCAL_RANK", 0)
+    if args.same_gpu:
+        local = 0
     if args.impl == "reference":
         return run_reference_arm(args, args.workload, rank, world)
 
@@ -277,7 +284,10 @@ def main(argv=None):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:   # code-path testing only (several ranks sharing one GPU)
+            dist.init_process_group(args.dist_backend)
 
     from paper_2303_08058_b200 import _native as N
     from paper_2303_08058_b200.ring import RingStepper, run_reference_gpu
@@ -329,27 +339,34 @@ def main(argv=None):
     value = cells_total / (step_ms * 1e-3)
 
     # ---- e2e through the host-buffer API (pinned H2D + step + D2H) ------
-    host_in = torch.empty((n_local, 512), dtype=torch.float64, pin_memory=True)
-    host_in.copy_(st.cells)
-    host_stats = torch.empty(2, dtype=torch.float64, pin_memory=True)
-    for _ in range(2):     # warm the copy streams / events / pinned-copy paths
-        st.step_host(host_in, host_in, host_stats, chunks=args.e2e_chunks)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(args.e2e_steps):
-        st.step_host(host_in, host_in, host_stats, chunks=args.e2e_chunks, join=False)
-    st.join_host()
-    e1.record()
-    torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1) / max(args.e2e_steps, 1)
-    if world > 1:
-        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = t.item()
-    e2e_value = cells_total / (e2e_ms * 1e-3)
+    e2e = None
+    if args.e2e_steps > 0:
+        host_in = torch.empty((n_local, 512), dtype=torch.float64, pin_memory=True)
+        host_in.copy_(st.cells)
+        host_stats = torch.empty(2, dtype=torch.float64, pin_memory=True)
+        for _ in range(2):     # warm the copy streams / events / pinned-copy paths
+            st.step_host(host_in, host_in, host_stats, chunks=args.e2e_chunks)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.e2e_steps):
+            st.step_host(host_in, host_in, host_stats, chunks=args.e2e_chunks, join=False)
+        st.join_host()
+        e1.record()
+        torch.cuda.synchronize()
+        e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
+        if world > 1:
+            t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = t.item()
+        e2e = {"value": cells_total / (e2e_ms * 1e-3), "unit": "cells/s",
+               "h2d_bytes_per_step": n_local * 512 * 8,
+               "d2h_bytes_per_step": n_local * 512 * 8 + 16,
+               "ms_per_step": e2e_ms, "chunks": args.e2e_chunks,
+               "api": "RingStepper.step_host (pinned H2D | K2 | D2H pipelined "
+                      "over chunks on 3 streams, chained across steps)"}
 
     if rank == 0:
         peaks, peak_kind = measured_peaks()
@@ -407,12 +424,7 @@ def main(argv=None):
                          "peak_source": peak_kind,
                          "bytes_per_cell": BYTES_PER_CELL, "k2_ms": k2_ms},
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_value, "unit": "cells/s",
-                    "h2d_bytes_per_step": n_local * 512 * 8,
-                    "d2h_bytes_per_step": n_local * 512 * 8 + 16,
-                    "ms_per_step": e2e_ms, "chunks": args.e2e_chunks,
-                    "api": "RingStepper.step_host (pinned H2D | K2 | D2H pipelined "
-                           "over chunks on 3 streams, chained across steps)"},
+            "e2e": e2e,
             "ablation": ablation,
             "gpu_launches": (1 if world == 1 else 2) * args.steps,
             "clocks": clocks,

@@ -189,13 +189,14 @@ int tb_acc_finalize(tb_stream_t s, int64_t *acc, double *piece, double *dt,
                     double *checksum, int reset);
 
 /* ---------------------------------------------------- peer memory -- */
-/* CUDA IPC for the multi-GPU ring: export a device allocation (handle =
- * TB_IPC_HANDLE_BYTES bytes), map a peer's export, unmap. With the
+/* CUDA IPC for the multi-GPU ring: export the allocation containing dptr
+ * (handle = TB_IPC_HANDLE_BYTES bytes; *offset = dptr - allocation base, so
+ * sub-allocated buffers work), map a peer's export (returns the base), unmap. With the
  * neighbours' state buffers mapped, tb_step's left_face/right_face may point
  * into peer HBM: the ring halo exchange (src/miniapp.py:119-121 across a
  * partition boundary) is then two 64-byte NVLink loads inside K2. */
 #define TB_IPC_HANDLE_BYTES 64
-int tb_ipc_get_handle(void *dptr, uint8_t *handle);
+int tb_ipc_get_handle(void *dptr, uint8_t *handle, uint64_t *offset);
 int tb_ipc_open_handle(const uint8_t *handle, void **dptr);
 int tb_ipc_close(void *dptr);
 

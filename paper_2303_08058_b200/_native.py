@@ -132,7 +132,7 @@ SIGNATURES = {
     "tb_htq_close": [_u64],
     "tb_htq_destroy": [_u64],
     "tb_machine_run": [_vp, _vp, _vp, _vp],
-    "tb_ipc_get_handle": [_vp, _vp],
+    "tb_ipc_get_handle": [_vp, _vp, _pu64],
     "tb_ipc_open_handle": [_vp, _pvp],
     "tb_ipc_close": [_vp],
     "tb_acc_allreduce_p2p": [_u64, _vp, _vp, _int, _vp, _vp, _vp, _vp],

@@ -350,12 +350,31 @@ int tb_memset(tb_stream_t s, void *p, int value, size_t n) {
 // CUDA IPC: a rank exports its state buffers, ring neighbours map them and
 // K2 reads the two ghost faces straight out of the neighbour's HBM (NVLink
 // P2P on a multi-GPU node) — the halo exchange becomes two 64-byte loads.
-int tb_ipc_get_handle(void *dptr, uint8_t *handle) {
-  if (!dptr || !handle) return TB_E_INVALID;
+int tb_ipc_get_handle(void *dptr, uint8_t *handle, uint64_t *offset) {
+  if (!dptr || !handle || !offset) return TB_E_INVALID;
   ensure_device();
+  // IPC exports whole allocations; sub-allocators (e.g. a caching allocator)
+  // hand out interior pointers, so find the allocation base first.
+  using GetRange = int (*)(unsigned long long *, size_t *, unsigned long long);
+  static GetRange get_range = nullptr;
+  if (!get_range) {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    int r = rc(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+    if (r != TB_OK) return r;
+    if (!fn || q != cudaDriverEntryPointSuccess) return TB_E_INVALID;
+    get_range = reinterpret_cast<GetRange>(fn);
+  }
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, reinterpret_cast<unsigned long long>(dptr)) != 0)
+    return TB_E_INVALID;
   cudaIpcMemHandle_t h;
-  const int r = rc(cudaIpcGetMemHandle(&h, dptr));
-  if (r == TB_OK) memcpy(handle, &h, sizeof h);
+  const int r = rc(cudaIpcGetMemHandle(&h, reinterpret_cast<void *>(base)));
+  if (r == TB_OK) {
+    memcpy(handle, &h, sizeof h);
+    *offset = reinterpret_cast<unsigned long long>(dptr) - base;
+  }
   return r;
 }
 

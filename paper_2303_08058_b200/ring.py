@@ -174,14 +174,12 @@ class RingStepper:
 
     @staticmethod
     def _export(t: torch.Tensor):
-        """(IPC handle of t's cudaMalloc block, byte offset of t in it). The
-        caching allocator sub-allocates; IPC exports whole blocks."""
+        """(IPC handle of the allocation holding t, byte offset of t in it)."""
         import ctypes
-        storage = t.untyped_storage()
-        block_offset = int(storage._share_cuda_()[3])
         handle = (ctypes.c_uint8 * N.TB_IPC_HANDLE_BYTES)()
-        N.call("tb_ipc_get_handle", storage.data_ptr() - block_offset, handle)
-        return bytes(handle), block_offset + t.storage_offset() * t.element_size()
+        offset = ctypes.c_uint64(0)
+        N.call("tb_ipc_get_handle", t.data_ptr(), handle, ctypes.byref(offset))
+        return bytes(handle), offset.value
 
     def _map_peers(self):
         """Exchange IPC handles with every rank; map the ring neighbours' two
