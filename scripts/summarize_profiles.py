@@ -58,7 +58,7 @@ def launches(tag):
             pass
     tot = sum(sum(v) for v in agg.values())
     lines = [f"# ncu launch list (gpu__time_duration.sum, --clock-control none; cold, "
-             f"serialised) of: python bench.py --steps 5 --warmup 3 --e2e-steps 2",
+             f"serialised) of: python bench.py --steps 20 --warmup 3 --e2e-steps 2 --no-cpu-baseline --no-ablation (k_step_bulk mixes the 15 parity-check launches at 512 sub-grids, warm-up and timed C4 steps, and e2e chunk launches)",
              f"# {'launches':>8} {'total_us':>10} {'share':>6} {'avg_us':>8}  kernel"]
     for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
         lines.append(f"  {len(v):8d} {sum(v)/1e3:10.1f} {100*sum(v)/tot:5.1f}% "
