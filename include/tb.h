@@ -212,6 +212,16 @@ int tb_acc_allreduce_p2p(tb_stream_t s, int64_t *local_acc, int64_t *const *peer
                          int nranks, int64_t *my_acc, double *piece, double *dt,
                          double *checksum);
 
+/* K6 (north_star "hydro reconstruct+flux only", BASELINE config 2; PARITY
+ * UNPINNED — no hydro exists in the reference, SPEC.md:17,490 — the spec is
+ * oracle/hydro_oracle.py): dU/dt of a batch of nsub sub-grids.
+ * U: [nsub][5][12][12][12] float64 (rho, sx, sy, sz, E; 8^3 interior cells
+ * with 2-cell ghost layers, i fastest, 16-B aligned); dudt: [nsub][5][8][8][8];
+ * amax: [nsub] max signal speed (CFL). Minmod PLM on primitives + Kurganov-
+ * Tadmor/LLF flux, ideal gas with adiabatic index gamma, cell size dx. */
+int tb_hydro_flux(tb_stream_t s, const double *U, double *dudt, double *amax,
+                  int64_t nsub, double dx, double gamma);
+
 /* -------------------------------------------------- poll registry -- */
 /* PollRegistry (src/runtime/polling.py:17-147): a lock-free MPSC inbox of
  * (event, token) and a poll-owned pending vector, drained by a single-entrant

@@ -136,6 +136,7 @@ SIGNATURES = {
     "tb_ipc_open_handle": [_vp, _pvp],
     "tb_ipc_close": [_vp],
     "tb_acc_allreduce_p2p": [_u64, _vp, _vp, _int, _vp, _vp, _vp, _vp],
+    "tb_hydro_flux": [_u64, _vp, _vp, _vp, _i64, _dbl, _dbl],
 }
 BLOCKING = {"tb_init", "tb_device_sync", "tb_stream_sync", "tb_event_wait",
             "tb_htq_next", "tb_htq_destroy", "tb_malloc", "tb_free",

@@ -1,0 +1,247 @@
+// tb_hydro.cu — K6: hydro reconstruct-and-flux over a batch of octree leaf
+// sub-grids (8^3 interior cells + 2-cell ghost layers, 5 conserved FP64
+// fields in SoA), the north_star's "hydro reconstruct+flux only" kernel.
+//
+// PARITY UNPINNED (no hydro in the reference): the
+// arithmetic is the self-authored spec in oracle/hydro_oracle.py, restated
+// operation by operation (no FMA) so the GPU is bit-identical to it.
+//
+// Per CTA and sub-grid: one bulk copy (TMA engine, mbarrier completion)
+// stages the 69,120-byte ghosted sub-grid in shared memory; conserved ->
+// primitive in place; for each direction the 576 face fluxes (minmod PLM +
+// Kurganov-Tadmor/LLF) go to a shared flux buffer and every thread folds the
+// flux differences of its interior cells into registers; dU/dt is written
+// coalesced and the sub-grid's max signal speed is block-reduced.
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+#include "../../include/tb.h"
+#include "tb_internal.h"
+
+namespace {
+
+constexpr int NG = 2, NI = 8, NT = 12, NF = 5;
+constexpr int NCELL = NT * NT * NT;            // 1728
+constexpr int NFACE = (NI + 1) * NI * NI;      // 576 faces per direction
+constexpr int kThreads = 256;
+constexpr int kCellsPerThread = NI * NI * NI / kThreads;   // 2
+constexpr int kSmem = (NF * NCELL + NF * NFACE) * 8;       // 92,160 B
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+struct State {
+  double u[NF], f[NF], a;
+};
+
+// Left/right state -> conserved vector, flux along d, signal speed |vn|+cs.
+__device__ __forceinline__ void face_state(double rho, double vx, double vy, double vz,
+                                           double p, double gamma, double gm1, int d,
+                                           State &s) {
+  const double cs = __dsqrt_rn(__ddiv_rn(__dmul_rn(gamma, p), rho));
+  const double vv = __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)),
+                              __dmul_rn(vz, vz));
+  const double e = __dadd_rn(__ddiv_rn(p, gm1), __dmul_rn(__dmul_rn(0.5, rho), vv));
+  const double vn = d == 0 ? vx : (d == 1 ? vy : vz);
+  const double mx = __dmul_rn(rho, vx), my = __dmul_rn(rho, vy), mz = __dmul_rn(rho, vz);
+  s.u[0] = rho;
+  s.u[1] = mx;
+  s.u[2] = my;
+  s.u[3] = mz;
+  s.u[4] = e;
+  double fmx = __dmul_rn(mx, vn), fmy = __dmul_rn(my, vn), fmz = __dmul_rn(mz, vn);
+  if (d == 0)
+    fmx = __dadd_rn(fmx, p);
+  else if (d == 1)
+    fmy = __dadd_rn(fmy, p);
+  else
+    fmz = __dadd_rn(fmz, p);
+  s.f[0] = __dmul_rn(rho, vn);
+  s.f[1] = fmx;
+  s.f[2] = fmy;
+  s.f[3] = fmz;
+  s.f[4] = __dmul_rn(__dadd_rn(e, p), vn);
+  s.a = __dadd_rn(fabs(vn), cs);
+}
+
+__device__ __forceinline__ double minmod(double dl, double dr) {
+  const double pick = fabs(dl) < fabs(dr) ? dl : dr;
+  return __dmul_rn(dl, dr) <= 0.0 ? 0.0 : pick;
+}
+
+__global__ void __launch_bounds__(kThreads, 2)
+    k_hydro_flux(const double *__restrict__ U, double *__restrict__ dudt,
+                 double *__restrict__ amax_out, int64_t nsub, double dx, double gamma) {
+  extern __shared__ __align__(128) double sm[];
+  double *W = sm;                        // [5][1728] primitives (staged U)
+  double *Fb = sm + NF * NCELL;          // [5][576] one direction's face fluxes
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ double s_amax[kThreads / 32];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const double gm1 = __dadd_rn(gamma, -1.0);
+  if (t == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t phase = 0;
+  for (int64_t s = blockIdx.x; s < nsub; s += gridDim.x, phase ^= 1) {
+    // ---- stage the ghosted sub-grid (one bulk copy of 69,120 B) ----------
+    if (t == 0) {
+      const uint32_t bytes = NF * NCELL * 8;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                       smem_u32(&bar)),
+                   "r"(bytes)
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], "
+          "%2, [%3];" ::"r"(smem_u32(W)),
+          "l"(U + s * (int64_t)(NF * NCELL)), "r"(bytes), "r"(smem_u32(&bar))
+          : "memory");
+    }
+    asm volatile(
+        "{\n\t.reg .pred p;\nHW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra HW_%=;\n}" ::"r"(smem_u32(&bar)),
+        "r"(phase)
+        : "memory");
+    // ---- conserved -> primitive, in place --------------------------------
+    for (int c = t; c < NCELL; c += kThreads) {
+      const double rho = W[c], sx = W[NCELL + c], sy = W[2 * NCELL + c],
+                   sz = W[3 * NCELL + c], E = W[4 * NCELL + c];
+      const double vx = __ddiv_rn(sx, rho), vy = __ddiv_rn(sy, rho), vz = __ddiv_rn(sz, rho);
+      const double ke = __dmul_rn(
+          0.5, __dadd_rn(__dadd_rn(__dmul_rn(sx, vx), __dmul_rn(sy, vy)), __dmul_rn(sz, vz)));
+      W[NCELL + c] = vx;
+      W[2 * NCELL + c] = vy;
+      W[3 * NCELL + c] = vz;
+      W[4 * NCELL + c] = __dmul_rn(gm1, __dadd_rn(E, -ke));
+    }
+    __syncthreads();
+    double du[NF][kCellsPerThread];
+    double amax = -CUDART_INF;
+#pragma unroll 1
+    for (int d = 0; d < 3; ++d) {
+      const int stride = d == 0 ? 1 : (d == 1 ? NT : NT * NT);
+      // ---- face fluxes along d ------------------------------------------
+      for (int f = t; f < NFACE; f += kThreads) {
+        // enumerate with the x-index fastest (stride-1 shared-memory reads)
+        int c, ti, tj;   // c: face index along d (0..8); ti, tj: transverse
+        int i, j, k;     // 12-grid coordinates of the face's left cell
+        if (d == 0) {
+          c = f % 9;
+          ti = (f / 9) % NI;
+          tj = f / (9 * NI);
+          i = 1 + c, j = NG + ti, k = NG + tj;
+        } else if (d == 1) {
+          ti = f % NI;
+          c = (f / NI) % 9;
+          tj = f / (NI * 9);
+          i = NG + ti, j = 1 + c, k = NG + tj;
+        } else {
+          ti = f % NI;
+          tj = (f / NI) % NI;
+          c = f / (NI * NI);
+          i = NG + ti, j = NG + tj, k = 1 + c;
+        }
+        const int base = (k * NT + j) * NT + i;
+        double qL[NF], qR[NF];
+#pragma unroll
+        for (int v = 0; v < NF; ++v) {
+          const double *w = W + v * NCELL + base;
+          const double qm = w[-stride], q0 = w[0], qp = w[stride], qpp = w[2 * stride];
+          const double s0 = minmod(__dadd_rn(q0, -qm), __dadd_rn(qp, -q0));
+          const double s1 = minmod(__dadd_rn(qp, -q0), __dadd_rn(qpp, -qp));
+          qL[v] = __dadd_rn(q0, __dmul_rn(0.5, s0));
+          qR[v] = __dadd_rn(qp, -__dmul_rn(0.5, s1));
+        }
+        State L, R;
+        face_state(qL[0], qL[1], qL[2], qL[3], qL[4], gamma, gm1, d, L);
+        face_state(qR[0], qR[1], qR[2], qR[3], qR[4], gamma, gm1, d, R);
+        const double a = fmax(L.a, R.a);
+        amax = fmax(amax, a);
+        const double ha = __dmul_rn(0.5, a);
+        // flux buffer index: (slow transverse, fast transverse, c) so the
+        // accumulation below reads lo/hi faces at a fixed layout per d
+        int idx;
+        if (d == 0)
+          idx = (tj * NI + ti) * 9 + c;          // (k, j, face i)
+        else if (d == 1)
+          idx = (tj * 9 + c) * NI + ti;          // (k, face j, i)
+        else
+          idx = (c * NI + tj) * NI + ti;         // (face k, j, i)
+#pragma unroll
+        for (int v = 0; v < NF; ++v)
+          Fb[v * NFACE + idx] = __dadd_rn(__dmul_rn(0.5, __dadd_rn(L.f[v], R.f[v])),
+                                          -__dmul_rn(ha, __dadd_rn(R.u[v], -L.u[v])));
+      }
+      __syncthreads();
+      // ---- fold this direction's flux differences into the cells ----------
+#pragma unroll
+      for (int m = 0; m < kCellsPerThread; ++m) {
+        const int cell = t + kThreads * m;          // interior index (k, j, i)
+        const int ci = cell % NI, cj = (cell / NI) % NI, ck = cell / (NI * NI);
+        int lo, hi;
+        if (d == 0) {
+          lo = (ck * NI + cj) * 9 + ci;
+          hi = lo + 1;
+        } else if (d == 1) {
+          lo = (ck * 9 + cj) * NI + ci;
+          hi = lo + NI;
+        } else {
+          lo = (ck * NI + cj) * NI + ci;
+          hi = lo + NI * NI;
+        }
+#pragma unroll
+        for (int v = 0; v < NF; ++v) {
+          const double diff = __dadd_rn(Fb[v * NFACE + hi], -Fb[v * NFACE + lo]);
+          du[v][m] = d == 0 ? diff : __dadd_rn(du[v][m], diff);
+        }
+      }
+      __syncthreads();
+    }
+    // ---- dU/dt = -(du / dx), coalesced ------------------------------------
+    double *out = dudt + s * (int64_t)(NF * NI * NI * NI);
+#pragma unroll
+    for (int m = 0; m < kCellsPerThread; ++m)
+#pragma unroll
+      for (int v = 0; v < NF; ++v)
+        out[v * (NI * NI * NI) + t + kThreads * m] = -__ddiv_rn(du[v][m], dx);
+    // ---- max signal speed of the sub-grid ---------------------------------
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    if (lane == 0) s_amax[warp] = amax;
+    __syncthreads();
+    if (t == 0) {
+      double m = s_amax[0];
+      for (int w = 1; w < kThreads / 32; ++w) m = fmax(m, s_amax[w]);
+      amax_out[s] = m;
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" int tb_hydro_flux(tb_stream_t s, const double *U, double *dudt, double *amax,
+                             int64_t nsub, double dx, double gamma) {
+  if (nsub < 0 || (nsub > 0 && (!U || !dudt || !amax)) || !(dx > 0.0) || !(gamma > 1.0))
+    return TB_E_INVALID;
+  if (nsub == 0) return TB_OK;
+  if (reinterpret_cast<uintptr_t>(U) & 15) return TB_E_INVALID;
+  static int occ = 0;
+  if (!occ) {
+    cudaFuncSetAttribute(k_hydro_flux, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hydro_flux, kThreads, kSmem) !=
+            cudaSuccess ||
+        occ < 1)
+      occ = 1;
+  }
+  int64_t blocks = (int64_t)tb::sm_count() * occ;
+  if (blocks > nsub) blocks = nsub;
+  k_hydro_flux<<<(int)blocks, kThreads, kSmem, reinterpret_cast<cudaStream_t>(s)>>>(
+      U, dudt, amax, nsub, dx, gamma);
+  return tb::last_error();
+}
