@@ -222,6 +222,16 @@ int tb_acc_allreduce_p2p(tb_stream_t s, int64_t *local_acc, int64_t *const *peer
 int tb_hydro_flux(tb_stream_t s, const double *U, double *dudt, double *amax,
                   int64_t nsub, double dx, double gamma);
 
+/* FP64 issue-rate probe (roofline denominator; no reference counterpart):
+ * runs one FP64 instruction type on 8 independent chains per thread over a
+ * full grid on the current device and returns thread-instructions/s and the
+ * nominal SM clock (MHz). op = TB_PROBE_*. Blocking. */
+#define TB_PROBE_DADD 0
+#define TB_PROBE_DMUL 1
+#define TB_PROBE_DFMA 2
+#define TB_PROBE_DMUL_DADD 3
+int tb_fp64_probe(int op, int64_t iters, double *instr_per_s, double *sm_mhz);
+
 /* -------------------------------------------------- poll registry -- */
 /* PollRegistry (src/runtime/polling.py:17-147): a lock-free MPSC inbox of
  * (event, token) and a poll-owned pending vector, drained by a single-entrant

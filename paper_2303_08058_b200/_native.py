@@ -48,6 +48,11 @@ TB_MODE_POLLING = 0
 TB_MODE_HOSTTASK = 1
 TB_MODE_FENCE = 2
 
+TB_PROBE_DADD = 0
+TB_PROBE_DMUL = 1
+TB_PROBE_DFMA = 2
+TB_PROBE_DMUL_DADD = 3
+
 TB_OP_NONE = 0
 TB_OP_KIND = 1
 TB_OP_AFFINE = 2
@@ -137,11 +142,13 @@ SIGNATURES = {
     "tb_ipc_close": [_vp],
     "tb_acc_allreduce_p2p": [_u64, _vp, _vp, _int, _vp, _vp, _vp, _vp],
     "tb_hydro_flux": [_u64, _vp, _vp, _vp, _i64, _dbl, _dbl],
+    "tb_fp64_probe": [_int, _i64, _vp, _vp],
 }
 BLOCKING = {"tb_init", "tb_device_sync", "tb_stream_sync", "tb_event_wait",
             "tb_htq_next", "tb_htq_destroy", "tb_malloc", "tb_free",
             "tb_host_alloc", "tb_host_free", "tb_stream_destroy",
-            "tb_memcpy_h2d", "tb_memcpy_d2h", "tb_poll_drain", "tb_machine_run"}
+            "tb_memcpy_h2d", "tb_memcpy_d2h", "tb_poll_drain", "tb_machine_run",
+            "tb_fp64_probe"}
 
 _lock = threading.Lock()
 _libs = None
