@@ -222,6 +222,24 @@ int tb_acc_allreduce_p2p(tb_stream_t s, int64_t *local_acc, int64_t *const *peer
 int tb_hydro_flux(tb_stream_t s, const double *U, double *dudt, double *amax,
                   int64_t nsub, double dx, double gamma);
 
+/* K7 (north_star "FMM monopole/multipole stencil-interaction kernels",
+ * BASELINE config 3; PARITY UNPINNED — no gravity exists in the reference,
+ * the spec is oracle/fmm_oracle.py, matched to 1e-10
+ * relative): gravity of a uniform octree of depth max_level (1..7) whose
+ * leaves are the N^3 cells of rho (N = 8 * 2^max_level, lattice z,y,x with
+ * x fastest, unit cube, isolated boundary). work: device workspace of
+ * tb_fmm_workspace_bytes (per-level moments and local expansions);
+ * out: [4][N^3] = phi, gx, gy, gz (g = -grad phi, G = 1).
+ * tb_fmm_solve = upward (P2M + M2M) ; m2l (all multipole levels, one launch) ;
+ * downward (L2L) ; leaf (monopole stencil + L2P), all on stream s. */
+int tb_fmm_workspace_bytes(int max_level, uint64_t *bytes);
+int tb_fmm_upward(tb_stream_t s, int max_level, const double *rho, double *work);
+int tb_fmm_m2l(tb_stream_t s, int max_level, double *work);
+int tb_fmm_downward(tb_stream_t s, int max_level, double *work);
+int tb_fmm_leaf(tb_stream_t s, int max_level, const double *rho, const double *work,
+                double *out);
+int tb_fmm_solve(tb_stream_t s, int max_level, const double *rho, double *work, double *out);
+
 /* FP64 issue-rate probe (roofline denominator; no reference counterpart):
  * runs one FP64 instruction type on 8 independent chains per thread over a
  * full grid on the current device and returns thread-instructions/s and the

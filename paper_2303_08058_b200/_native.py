@@ -143,6 +143,12 @@ SIGNATURES = {
     "tb_acc_allreduce_p2p": [_u64, _vp, _vp, _int, _vp, _vp, _vp, _vp],
     "tb_hydro_flux": [_u64, _vp, _vp, _vp, _i64, _dbl, _dbl],
     "tb_fp64_probe": [_int, _i64, _vp, _vp],
+    "tb_fmm_workspace_bytes": [_int, _pu64],
+    "tb_fmm_upward": [_u64, _int, _vp, _vp],
+    "tb_fmm_m2l": [_u64, _int, _vp],
+    "tb_fmm_downward": [_u64, _int, _vp],
+    "tb_fmm_leaf": [_u64, _int, _vp, _vp, _vp],
+    "tb_fmm_solve": [_u64, _int, _vp, _vp, _vp],
 }
 BLOCKING = {"tb_init", "tb_device_sync", "tb_stream_sync", "tb_event_wait",
             "tb_htq_next", "tb_htq_destroy", "tb_malloc", "tb_free",

@@ -1,0 +1,747 @@
+// tb_fmm.cu — K7: FMM gravity over a uniform octree of 8^3-cell sub-grids
+// (the north_star's "FMM monopole/multipole stencil-interaction kernels",
+// BASELINE.json config 3).
+//
+// PARITY UNPINNED (the reference has no gravity solver): the
+// spec is the self-authored oracle/fmm_oracle.py; results agree with it per
+// cell within the north_star's FP64 tolerance (1e-10 relative), not bit for
+// bit — FMAs and rsqrt are used freely here.
+//
+// Layout (one device workspace, tb_fmm_workspace_bytes):
+//   for level l in [0, L): Mhat_l [20][N_l^3], Loc_l [20][N_l^3]   (N_l = 8*2^l,
+//   lattices z,y,x with x fastest); L0part [8][20][512].
+//   Mhat holds the raw Cartesian moments pre-multiplied by the M2L source
+//   coefficient -(-1)^m mult(B)/m!, so the interaction is a pure FMA chain.
+//
+// Kernels
+//   k_fmm_up    P2M+M2M, one level per launch: 8 lanes = the 8 children of a
+//               parent; shifted moments are summed with xor-shuffles (the
+//               warp-level multipole sums).
+//   k_fmm_m2l   multipole interactions of ALL levels in ONE launch (a CTA per
+//               level-l sub-grid, heaviest level first; level 0 split over 8
+//               CTAs). The interaction stencil is walked as 33 parent-near
+//               offsets P: for each, the 8^3 x 20 source block at 2P is staged
+//               by one 4-D TMA load (OOB = zero mass: the isolated boundary),
+//               double-buffered on mbarriers; each thread (one target cell)
+//               takes the 8 children of its parent's neighbour P, builds the
+//               1/r derivative tensor D(R) to order 3 and contracts it with the
+//               source moments (84 FMAs).
+//   k_fmm_down  L2L, one level per launch (level 0: sums the 8 partials).
+//   k_fmm_leaf  monopole interactions at the leaves: a 264-point stencil whose
+//               weights 1/|q|, q/|q|^3 depend only on the integer offset q; a
+//               warp owns one child octant so q is warp-uniform and the
+//               weights come from constant memory; the leaf densities are
+//               staged parity-split in shared memory (conflict-free). Then the
+//               parent's local expansion is evaluated at the leaf (L2P).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+#include <utility>
+
+#include "../../include/tb.h"
+#include "tb_internal.h"
+
+namespace {
+
+constexpr int NC = 20;
+constexpr int kMaxLevel = 7;
+
+// ------------------------------------------------------- compile-time tables
+struct Comp {
+  int n, a[3];
+};
+constexpr Comp kComps[NC] = {
+    {0, {0, 0, 0}}, {1, {0, 0, 0}}, {1, {1, 0, 0}}, {1, {2, 0, 0}}, {2, {0, 0, 0}},
+    {2, {0, 1, 0}}, {2, {0, 2, 0}}, {2, {1, 1, 0}}, {2, {1, 2, 0}}, {2, {2, 2, 0}},
+    {3, {0, 0, 0}}, {3, {0, 0, 1}}, {3, {0, 0, 2}}, {3, {0, 1, 1}}, {3, {0, 1, 2}},
+    {3, {0, 2, 2}}, {3, {1, 1, 1}}, {3, {1, 1, 2}}, {3, {1, 2, 2}}, {3, {2, 2, 2}}};
+
+constexpr int find_comp(int n, const int *a) {
+  for (int k = 0; k < NC; ++k) {
+    if (kComps[k].n != n) continue;
+    bool eq = true;
+    for (int q = 0; q < n; ++q)
+      if (kComps[k].a[q] != a[q]) eq = false;
+    if (eq) return k;
+  }
+  return -1;
+}
+
+// Index of the sorted concatenation of two components (or -1 beyond order 3).
+constexpr int merge(int t, int s) {
+  int a[6] = {0, 0, 0, 0, 0, 0};
+  int n = 0;
+  for (int q = 0; q < kComps[t].n; ++q) a[n++] = kComps[t].a[q];
+  for (int q = 0; q < kComps[s].n; ++q) a[n++] = kComps[s].a[q];
+  if (n > 3) return -1;
+  for (int i = 0; i < n; ++i)
+    for (int j = i + 1; j < n; ++j)
+      if (a[j] < a[i]) {
+        const int x = a[i];
+        a[i] = a[j];
+        a[j] = x;
+      }
+  return find_comp(n, a);
+}
+
+constexpr int fact(int n) { return n <= 1 ? 1 : n * fact(n - 1); }
+
+constexpr int mult(int s) {
+  int c[3] = {0, 0, 0};
+  for (int q = 0; q < kComps[s].n; ++q) c[kComps[s].a[q]]++;
+  return fact(kComps[s].n) / (fact(c[0]) * fact(c[1]) * fact(c[2]));
+}
+
+// M2L source coefficient: L^(n)_A = sum_s [-(-1)^m mult(s)/m!] M_s D_{A+s}.
+constexpr double m2l_scale(int s) {
+  return (kComps[s].n % 2 ? 1.0 : -1.0) * mult(s) / fact(kComps[s].n);
+}
+// L2L monomial coefficient mult(B)/k!.
+constexpr double l2l_scale(int b) { return double(mult(b)) / fact(kComps[b].n); }
+
+struct Term {
+  int t, s, b, c;
+};
+template <int CAP>
+struct Table {
+  Term v[CAP];
+  int n;
+};
+
+// M2L: L[t] += Mhat[s] * D[merge(t,s)]   (t, s, b = D index)
+constexpr Table<84> make_m2l() {
+  Table<84> T{};
+  int k = 0;
+  for (int t = 0; t < NC; ++t)
+    for (int s = 0; s < NC; ++s)
+      if (kComps[t].n + kComps[s].n <= 3) T.v[k++] = Term{t, s, merge(t, s), 1};
+  T.n = k;
+  return T;
+}
+// L2L / L2P: Lchild[t] += Lparent[merge(t,b)] * mono_hat[b]   (t, s = parent, b)
+constexpr Table<84> make_l2l() {
+  Table<84> T{};
+  int k = 0;
+  for (int t = 0; t < NC; ++t)
+    for (int b = 0; b < NC; ++b)
+      if (kComps[t].n + kComps[b].n <= 3) T.v[k++] = Term{t, merge(t, b), b, 1};
+  T.n = k;
+  return T;
+}
+// M2M: Mparent[t] += c * Mchild[s] * d^b, from prod_a (s_a + d_a) over the
+// subsets of t's index positions.
+constexpr Table<84> make_m2m() {
+  Table<84> T{};
+  int k = 0;
+  for (int t = 0; t < NC; ++t) {
+    const int n = kComps[t].n;
+    for (int mask = 0; mask < (1 << n); ++mask) {
+      int sa[3] = {0, 0, 0}, ra[3] = {0, 0, 0};
+      int ns = 0, nr = 0;
+      for (int q = 0; q < n; ++q) {
+        if (mask >> q & 1)
+          sa[ns++] = kComps[t].a[q];
+        else
+          ra[nr++] = kComps[t].a[q];
+      }
+      const int b = find_comp(ns, sa), s = find_comp(nr, ra);   // already sorted
+      bool found = false;
+      for (int e = 0; e < k; ++e)
+        if (T.v[e].t == t && T.v[e].s == s && T.v[e].b == b) {
+          T.v[e].c += 1;
+          found = true;
+        }
+      if (!found) T.v[k++] = Term{t, s, b, 1};
+    }
+  }
+  T.n = k;
+  return T;
+}
+
+constexpr auto kM2L = make_m2l();
+constexpr auto kL2L = make_l2l();
+constexpr auto kM2M = make_m2m();
+static_assert(kM2L.n == 84 && kL2L.n == 84 && kM2M.n == 84, "term tables");
+
+template <typename F, int... K>
+__device__ __forceinline__ void unroll_impl(F &&f, std::integer_sequence<int, K...>) {
+  (f(std::integral_constant<int, K>{}), ...);
+}
+template <int N, typename F>
+__device__ __forceinline__ void unroll(F &&f) {
+  unroll_impl(f, std::make_integer_sequence<int, N>{});
+}
+
+// d^b for every component b (times a per-component constant from SCALE).
+template <bool L2L_SCALED>
+__device__ __forceinline__ void monomials(double dx, double dy, double dz, double (&m)[NC]) {
+  const double d[3] = {dx, dy, dz};
+  unroll<NC>([&](auto K) {
+    constexpr Comp C = kComps[K];
+    double v = 1.0;
+    if (C.n > 0) v = d[C.a[0]];
+    if (C.n > 1) v = v * d[C.a[1]];
+    if (C.n > 2) v = v * d[C.a[2]];
+    constexpr double sc = l2l_scale(K);
+    if (L2L_SCALED) v = v * sc;
+    m[K] = v;
+  });
+}
+
+// Derivative tensor of 1/r at R up to order 3 (symmetric storage).
+__device__ __forceinline__ void d_tensor(double x, double y, double z, double (&D)[NC]) {
+  const double r2 = fma(z, z, fma(y, y, x * x));
+  const double r1 = rsqrt(r2);
+  const double i2 = r1 * r1;
+  const double r3 = r1 * i2;
+  const double f5 = 3.0 * r3 * i2;          // 3 / r^5
+  const double f7 = 5.0 * f5 * i2;          // 15 / r^7
+  const double R[3] = {x, y, z};
+  D[0] = r1;
+  D[1] = -x * r3;
+  D[2] = -y * r3;
+  D[3] = -z * r3;
+  unroll<NC>([&](auto K) {
+    constexpr Comp C = kComps[K];
+    if constexpr (C.n == 2) {
+      const double v = R[C.a[0]] * R[C.a[1]] * f5;
+      D[K] = C.a[0] == C.a[1] ? v - r3 : v;
+    } else if constexpr (C.n == 3) {
+      constexpr int a = C.a[0], b = C.a[1], c = C.a[2];
+      const double p = R[a] * R[b] * R[c];
+      double t = 0.0;
+      if (b == c) t += R[a];
+      if (a == c) t += R[b];
+      if (a == b) t += R[c];
+      D[K] = (a == b || b == c || a == c) ? fma(f5, t, -p * f7) : -p * f7;
+    }
+  });
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\nFW_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra FW_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+// One 4-D TMA box {8,8,8,20} (x, y, z, component) of a level's moments.
+__device__ __forceinline__ void tma_load_block(const CUtensorMap *map, double *dst,
+                                               uint64_t *bar, int x, int y, int z) {
+  constexpr uint32_t bytes = 8 * 8 * 8 * NC * 8;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(0),
+      "r"(smem_u32(bar))
+      : "memory");
+}
+
+// The 33 parent-near offsets (|P|^2 <= 4), x fastest — same order as
+// oracle/fmm_oracle.py PNEAR.
+struct PTab {
+  int8_t p[33][3];
+};
+constexpr PTab make_ptab() {
+  PTab T{};
+  int k = 0;
+  for (int z = -2; z <= 2; ++z)
+    for (int y = -2; y <= 2; ++y)
+      for (int x = -2; x <= 2; ++x)
+        if (x * x + y * y + z * z <= 4) {
+          T.p[k][0] = (int8_t)x;
+          T.p[k][1] = (int8_t)y;
+          T.p[k][2] = (int8_t)z;
+          ++k;
+        }
+  return T;
+}
+__constant__ PTab c_pnear = make_ptab();
+
+// Leaf stencil weights by integer offset q = i - j in [-5,5]^3:
+// (1/|q|, qx/|q|^3, qy/|q|^3, qz/|q|^3); q = 0 -> 0 (the self term).
+__constant__ double c_w[11 * 11 * 11][4];
+
+struct Params {
+  CUtensorMap maps[kMaxLevel];     // level l moments, 4-D {N,N,N,20}
+  double *M[kMaxLevel];
+  double *Loc[kMaxLevel];
+  double *L0part;
+  int L;                           // max_level (leaves); multipole levels 0..L-1
+};
+
+// ---------------------------------------------------------------- upward
+// Parents at lattice Np from children (rho leaves when rho != nullptr).
+__global__ void __launch_bounds__(256) k_fmm_up(const double *__restrict__ rho,
+                                                const double *__restrict__ child,
+                                                double *__restrict__ parent, int Np,
+                                                double hc) {
+  const int lane = threadIdx.x & 31, c = lane & 7, g = lane >> 3;
+  const int64_t npar = (int64_t)Np * Np * Np;
+  const int64_t pidx = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 4 + g;
+  const bool valid = pidx < npar;
+  const int64_t pp = valid ? pidx : 0;
+  const int px = (int)(pp % Np), py = (int)((pp / Np) % Np), pz = (int)(pp / ((int64_t)Np * Np));
+  const int cx = c & 1, cy = (c >> 1) & 1, cz = c >> 2;
+  const int Nc = 2 * Np;
+  const int64_t nch = (int64_t)Nc * Nc * Nc;
+  const int64_t cf = ((int64_t)(2 * pz + cz) * Nc + (2 * py + cy)) * Nc + (2 * px + cx);
+  double mono[NC];
+  monomials<false>((cx - 0.5) * hc, (cy - 0.5) * hc, (cz - 0.5) * hc, mono);
+  double out[NC];
+  if (rho) {
+    const double m = valid ? rho[cf] * (hc * hc * hc) : 0.0;
+    unroll<NC>([&](auto K) { out[K] = m * mono[K]; });
+  } else {
+    double Mc[NC];
+    unroll<NC>([&](auto K) {
+      constexpr double inv = 1.0 / m2l_scale(K);
+      Mc[K] = valid ? child[K * nch + cf] * inv : 0.0;
+      out[K] = 0.0;
+    });
+    unroll<kM2M.n>([&](auto E) {
+      constexpr Term T = kM2M.v[E];
+      out[T.t] = fma(T.c * Mc[T.s], mono[T.b], out[T.t]);
+    });
+  }
+  // the 8 children's shifted moments -> the parent's (xor butterfly)
+  unroll<NC>([&](auto K) {
+    double v = out[K];
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    v += __shfl_xor_sync(0xffffffffu, v, 2);
+    v += __shfl_xor_sync(0xffffffffu, v, 4);
+    constexpr double sc = m2l_scale(K);
+    if (valid && (K & 7) == c) parent[K * npar + pidx] = v * sc;
+  });
+}
+
+// ------------------------------------------------------------------- M2L
+constexpr int kM2LThreads = 512;
+constexpr int kBlock = 8 * 8 * 8;                 // doubles per component per stage
+constexpr int kStage = kBlock * NC;               // 10240 doubles = 80 KB
+constexpr int kM2LSmem = 2 * kStage * 8;          // 160 KB
+
+__device__ __forceinline__ void contract(double (&L)[NC], const double *Ms, int off,
+                                         const double (&D)[NC]) {
+  double M[NC];
+  unroll<NC>([&](auto K) { M[K] = Ms[K * kBlock + off]; });
+  unroll<kM2L.n>([&](auto E) {
+    constexpr Term T = kM2L.v[E];
+    L[T.t] = fma(M[T.s], D[T.b], L[T.t]);
+  });
+}
+
+__global__ void __launch_bounds__(kM2LThreads, 1) k_fmm_m2l(const __grid_constant__ Params P) {
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t bar[2];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int ox = lane & 1, oy = (lane >> 1) & 1, oz = (lane >> 2) & 1;
+  const int px = lane >> 3, py = w & 3, pz = w >> 2;
+  const int lx = 2 * px + ox, ly = 2 * py + oy, lz = 2 * pz + oz;   // target in sub-grid
+  // decode the job: levels L-1 .. 1 (8^l sub-grids each), then 8 level-0 slabs
+  int job = blockIdx.x, lev = 0, sub = 0;
+  for (int l = P.L - 1; l >= 1; --l) {
+    const int cnt = 1 << (3 * l);
+    if (job < cnt) {
+      lev = l;
+      sub = job;
+      break;
+    }
+    job -= cnt;
+  }
+  if (t == 0) {
+    mbar_init(&bar[0]);
+    mbar_init(&bar[1]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  double L[NC];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) L[k] = 0.0;
+  const double h = 1.0 / double(8 << lev);
+  const CUtensorMap *map = &P.maps[lev];
+
+  if (lev == 0) {
+    // level-0 slab `job`: all 512 targets against the sources with z == job
+    if (t == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tma_load_block(map, sm, &bar[0], 0, 0, 0);
+    }
+    mbar_wait(&bar[0], 0);
+    const int jz = job;
+#pragma unroll 1
+    for (int jy = 0; jy < 8; ++jy)
+#pragma unroll 2
+      for (int jx = 0; jx < 8; ++jx) {
+        const int qx = lx - jx, qy = ly - jy, qz = lz - jz;
+        if (qx * qx + qy * qy + qz * qz > 4) {
+          double D[NC];
+          d_tensor(qx * h, qy * h, qz * h, D);
+          contract(L, sm, (jz * 8 + jy) * 8 + jx, D);
+        }
+      }
+    double *dst = P.L0part + (size_t)job * NC * 512 + (lz * 8 + ly) * 8 + lx;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) dst[k * 512] = L[k];
+    return;
+  }
+
+  const int nb = 1 << lev;
+  const int bx = sub % nb, by = (sub / nb) % nb, bz = sub / (nb * nb);
+  const int X0 = 8 * bx, Y0 = 8 * by, Z0 = 8 * bz;
+  if (t == 0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    for (int s = 0; s < 2; ++s)
+      tma_load_block(map, sm + s * kStage, &bar[s], X0 + 2 * c_pnear.p[s][0],
+                     Y0 + 2 * c_pnear.p[s][1], Z0 + 2 * c_pnear.p[s][2]);
+  }
+#pragma unroll 1
+  for (int k = 0; k < 33; ++k) {
+    const int buf = k & 1;
+    mbar_wait(&bar[buf], (k >> 1) & 1);
+    const double *Ms = sm + buf * kStage;
+    const int Px = c_pnear.p[k][0], Py = c_pnear.p[k][1], Pz = c_pnear.p[k][2];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int cx = c & 1, cy = (c >> 1) & 1, cz = c >> 2;
+      const int qx = ox - 2 * Px - cx, qy = oy - 2 * Py - cy, qz = oz - 2 * Pz - cz;
+      if (qx * qx + qy * qy + qz * qz > 4) {
+        double D[NC];
+        d_tensor(qx * h, qy * h, qz * h, D);
+        contract(L, Ms, ((2 * pz + cz) * 8 + (2 * py + cy)) * 8 + (2 * px + cx), D);
+      }
+    }
+    __syncthreads();            // every thread is done with this buffer
+    if (t == 0 && k + 2 < 33) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tma_load_block(map, sm + buf * kStage, &bar[buf], X0 + 2 * c_pnear.p[k + 2][0],
+                     Y0 + 2 * c_pnear.p[k + 2][1], Z0 + 2 * c_pnear.p[k + 2][2]);
+    }
+  }
+  const int N = 8 << lev;
+  const size_t ncell = (size_t)N * N * N;
+  double *dst = P.Loc[lev] + ((size_t)(Z0 + lz) * N + (Y0 + ly)) * N + (X0 + lx);
+#pragma unroll
+  for (int k = 0; k < NC; ++k) dst[k * ncell] = L[k];
+}
+
+// ------------------------------------------------------------------ L2L
+__global__ void __launch_bounds__(256) k_fmm_down(const double *__restrict__ Lp,
+                                                  double *__restrict__ Lc,
+                                                  const double *__restrict__ L0part, int N,
+                                                  double h) {
+  const int64_t n = (int64_t)N * N * N;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (L0part) {   // level 0: sum the 8 slab partials in a fixed order
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      double v = 0.0;
+      for (int s = 0; s < 8; ++s) v += L0part[((size_t)s * NC + k) * 512 + i];
+      Lc[k * n + i] = v;
+    }
+    return;
+  }
+  const int x = (int)(i % N), y = (int)((i / N) % N), z = (int)(i / ((int64_t)N * N));
+  const int Nq = N / 2;
+  const int64_t np = (int64_t)Nq * Nq * Nq;
+  const int64_t pi = ((int64_t)(z >> 1) * Nq + (y >> 1)) * Nq + (x >> 1);
+  double mono[NC], Lpar[NC], out[NC];
+  monomials<true>(((x & 1) - 0.5) * h, ((y & 1) - 0.5) * h, ((z & 1) - 0.5) * h, mono);
+  unroll<NC>([&](auto K) {
+    Lpar[K] = Lp[K * np + pi];
+    out[K] = Lc[K * n + i];
+  });
+  unroll<kL2L.n>([&](auto E) {
+    constexpr Term T = kL2L.v[E];
+    out[T.t] = fma(Lpar[T.s], mono[T.b], out[T.t]);
+  });
+  unroll<NC>([&](auto K) { Lc[K * n + i] = out[K]; });
+}
+
+// ------------------------------------------------------------ leaf (P2P)
+constexpr int kLeafThreads = 256;
+constexpr int kTX = 8, kTY = 8, kTZ = 16;                // targets per CTA tile
+constexpr int kSX = 12, kSY = 8, kSZ = (kTZ + 8) / 2;   // per-parity staged extents
+constexpr int kPar = kSX * kSY * kSZ;                    // x' padded 8 -> 12 (banks)
+constexpr int kLeafSmem = 8 * kPar * 8;                  // 73,728 B
+
+__global__ void __launch_bounds__(kLeafThreads, 2)
+    k_fmm_leaf(const double *__restrict__ rho, const double *__restrict__ Lpar,
+               double *__restrict__ out, int N, double h) {
+  extern __shared__ __align__(128) double S[];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int ntx = N / kTX, nty = N / kTY;
+  const int tile = blockIdx.x;
+  const int X0 = (tile % ntx) * kTX, Y0 = ((tile / ntx) % nty) * kTY,
+            Z0 = (tile / (ntx * nty)) * kTZ;
+  // ---- stage rho over [X0-4, X0+12) x [Y0-4, Y0+12) x [Z0-4, Z0+20), split by
+  //      parity: S[c][z'][y'][x'] with coordinate = 2*primed + c
+  for (int r = w; r < 16 * 24; r += kLeafThreads / 32) {
+    const int ry = r % 16, rz = r / 16;
+    if (lane < 16) {
+      const int gx = X0 - 4 + lane, gy = Y0 - 4 + ry, gz = Z0 - 4 + rz;
+      double v = 0.0;
+      if (gx >= 0 && gx < N && gy >= 0 && gy < N && gz >= 0 && gz < N)
+        v = __ldg(rho + ((size_t)gz * N + gy) * N + gx);
+      const int c = (lane & 1) | ((ry & 1) << 1) | ((rz & 1) << 2);
+      S[c * kPar + ((rz >> 1) * kSY + (ry >> 1)) * kSX + (lane >> 1)] = v;
+    }
+  }
+  __syncthreads();
+  // ---- warp = child octant o; lane = (px, py, pz low bit); 4 targets over pz
+  const int ox = w & 1, oy = (w >> 1) & 1, oz = w >> 2;
+  const int px = lane & 3, py = (lane >> 2) & 3, pzl = lane >> 4;
+  double acc[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc[r][k] = 0.0;
+#pragma unroll 1
+  for (int k = 0; k < 33; ++k) {
+    const int Px = c_pnear.p[k][0], Py = c_pnear.p[k][1], Pz = c_pnear.p[k][2];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int cx = c & 1, cy = (c >> 1) & 1, cz = c >> 2;
+      const int qx = ox - 2 * Px - cx, qy = oy - 2 * Py - cy, qz = oz - 2 * Pz - cz;
+      const int wi = ((qz + 5) * 11 + (qy + 5)) * 11 + (qx + 5);
+      const double w0 = c_w[wi][0], w1 = c_w[wi][1], w2 = c_w[wi][2], w3 = c_w[wi][3];
+      const double *base = S + c * kPar + ((py + Py + 2) * kSX) + (px + Px + 2);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const double m = base[(pzl + 2 * r + Pz + 2) * (kSX * kSY)];
+        acc[r][0] = fma(m, w0, acc[r][0]);
+        acc[r][1] = fma(m, w1, acc[r][1]);
+        acc[r][2] = fma(m, w2, acc[r][2]);
+        acc[r][3] = fma(m, w3, acc[r][3]);
+      }
+    }
+  }
+  // ---- L2P from the parent's expansion (level L-1) and the output --------
+  double mono[NC];
+  monomials<true>((ox - 0.5) * h, (oy - 0.5) * h, (oz - 0.5) * h, mono);
+  const int Nq = N / 2;
+  const size_t np = (size_t)Nq * Nq * Nq, n = (size_t)N * N * N;
+  const double h2 = h * h;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int x = X0 + 2 * px + ox, y = Y0 + 2 * py + oy, z = Z0 + 2 * (pzl + 2 * r) + oz;
+    double phi = -h2 * acc[r][0];
+    double gr[3] = {h * acc[r][1], h * acc[r][2], h * acc[r][3]};
+    if (Lpar) {
+      const size_t pi = ((size_t)(z >> 1) * Nq + (y >> 1)) * Nq + (x >> 1);
+      double Lp[NC];
+      unroll<NC>([&](auto K) { Lp[K] = __ldg(Lpar + K * np + pi); });
+      unroll<kL2L.n>([&](auto E) {
+        constexpr Term T = kL2L.v[E];
+        if constexpr (T.t == 0) phi = fma(Lp[T.s], mono[T.b], phi);
+        if constexpr (T.t >= 1 && T.t <= 3) gr[T.t - 1] = fma(Lp[T.s], mono[T.b], gr[T.t - 1]);
+      });
+    }
+    const size_t i = ((size_t)z * N + y) * N + x;
+    out[i] = phi;
+    out[n + i] = -gr[0];
+    out[2 * n + i] = -gr[1];
+    out[3 * n + i] = -gr[2];
+  }
+}
+
+// ------------------------------------------------------------------ host
+struct Layout {
+  size_t M[kMaxLevel], Loc[kMaxLevel], L0part, total;   // byte offsets
+};
+
+Layout layout(int L) {
+  Layout lo{};
+  size_t off = 0;
+  for (int l = 0; l < L; ++l) {
+    const size_t n = (size_t)(8 << l) * (8 << l) * (8 << l);
+    lo.M[l] = off;
+    off += n * NC * 8;
+    lo.Loc[l] = off;
+    off += n * NC * 8;
+  }
+  lo.L0part = off;
+  off += (size_t)8 * NC * 512 * 8;
+  lo.total = off;
+  return lo;
+}
+
+bool valid_level(int L) { return L >= 1 && L <= kMaxLevel; }
+
+int ensure_weights() {
+  static int done_mask = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 31 && (done_mask >> dev & 1)) return TB_OK;
+  static double w[11 * 11 * 11][4];
+  for (int z = -5; z <= 5; ++z)
+    for (int y = -5; y <= 5; ++y)
+      for (int x = -5; x <= 5; ++x) {
+        double *e = w[((z + 5) * 11 + (y + 5)) * 11 + (x + 5)];
+        const double r2 = double(x * x + y * y + z * z);
+        if (r2 == 0.0) {
+          e[0] = e[1] = e[2] = e[3] = 0.0;
+          continue;
+        }
+        const double r1 = 1.0 / std::sqrt(r2);
+        const double r3 = r1 / r2;
+        e[0] = r1;
+        e[1] = x * r3;
+        e[2] = y * r3;
+        e[3] = z * r3;
+      }
+  const int r = tb::rc(cudaMemcpyToSymbol(c_w, w, sizeof w));
+  if (r == TB_OK && dev < 31) done_mask |= 1 << dev;
+  return r;
+}
+
+using EncodeTiled = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                 const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                 const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                 CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int encoder(EncodeTiled *fn) {
+  static EncodeTiled enc = nullptr;
+  if (!enc) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    const int r = tb::rc(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (r != TB_OK) return r;
+    if (!p || q != cudaDriverEntryPointSuccess) return TB_E_INVALID;
+    enc = reinterpret_cast<EncodeTiled>(p);
+  }
+  *fn = enc;
+  return TB_OK;
+}
+
+int make_params(int L, double *work, Params *P) {
+  EncodeTiled enc = nullptr;
+  int r = encoder(&enc);
+  if (r != TB_OK) return r;
+  const Layout lo = layout(L);
+  char *base = reinterpret_cast<char *>(work);
+  *P = Params{};
+  P->L = L;
+  P->L0part = reinterpret_cast<double *>(base + lo.L0part);
+  for (int l = 0; l < L; ++l) {
+    P->M[l] = reinterpret_cast<double *>(base + lo.M[l]);
+    P->Loc[l] = reinterpret_cast<double *>(base + lo.Loc[l]);
+    const cuuint64_t N = (cuuint64_t)(8 << l);
+    const cuuint64_t dims[4] = {N, N, N, (cuuint64_t)NC};
+    const cuuint64_t strides[3] = {N * 8, N * N * 8, N * N * N * 8};
+    const cuuint32_t box[4] = {8, 8, 8, (cuuint32_t)NC};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    if (enc(&P->maps[l], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, P->M[l], dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return TB_E_INVALID;
+  }
+  return TB_OK;
+}
+
+inline cudaStream_t strm(tb_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+}  // namespace
+
+extern "C" {
+
+int tb_fmm_workspace_bytes(int max_level, uint64_t *bytes) {
+  if (!bytes || !valid_level(max_level)) return TB_E_INVALID;
+  *bytes = layout(max_level).total;
+  return TB_OK;
+}
+
+int tb_fmm_upward(tb_stream_t s, int max_level, const double *rho, double *work) {
+  if (!rho || !work || !valid_level(max_level)) return TB_E_INVALID;
+  const Layout lo = layout(max_level);
+  char *base = reinterpret_cast<char *>(work);
+  for (int l = max_level - 1; l >= 0; --l) {
+    const int Np = 8 << l;
+    const int64_t npar = (int64_t)Np * Np * Np;
+    const int64_t blocks = (npar + 31) / 32;   // 8 warps x 4 parents
+    const double hc = 1.0 / double(2 * Np);
+    const double *child = l == max_level - 1 ? nullptr
+                                             : reinterpret_cast<const double *>(base + lo.M[l + 1]);
+    k_fmm_up<<<(unsigned)blocks, 256, 0, strm(s)>>>(l == max_level - 1 ? rho : nullptr, child,
+                                                 reinterpret_cast<double *>(base + lo.M[l]), Np,
+                                                 hc);
+  }
+  return tb::last_error();
+}
+
+int tb_fmm_m2l(tb_stream_t s, int max_level, double *work) {
+  if (!work || !valid_level(max_level)) return TB_E_INVALID;
+  Params P;
+  int r = make_params(max_level, work, &P);
+  if (r != TB_OK) return r;
+  static bool attr = false;
+  if (!attr) {
+    r = tb::rc(cudaFuncSetAttribute(k_fmm_m2l, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kM2LSmem));
+    if (r != TB_OK) return r;
+    attr = true;
+  }
+  int jobs = 8;
+  for (int l = 1; l < max_level; ++l) jobs += 1 << (3 * l);
+  k_fmm_m2l<<<jobs, kM2LThreads, kM2LSmem, strm(s)>>>(P);
+  return tb::last_error();
+}
+
+int tb_fmm_downward(tb_stream_t s, int max_level, double *work) {
+  if (!work || !valid_level(max_level)) return TB_E_INVALID;
+  const Layout lo = layout(max_level);
+  char *base = reinterpret_cast<char *>(work);
+  for (int l = 0; l < max_level; ++l) {
+    const int N = 8 << l;
+    const int64_t n = (int64_t)N * N * N;
+    double *Lc = reinterpret_cast<double *>(base + lo.Loc[l]);
+    const double *Lp = l ? reinterpret_cast<const double *>(base + lo.Loc[l - 1]) : nullptr;
+    const double *part = l ? nullptr : reinterpret_cast<const double *>(base + lo.L0part);
+    k_fmm_down<<<(unsigned)((n + 255) / 256), 256, 0, strm(s)>>>(Lp, Lc, part, N, 1.0 / N);
+  }
+  return tb::last_error();
+}
+
+int tb_fmm_leaf(tb_stream_t s, int max_level, const double *rho, const double *work,
+                double *out) {
+  if (!rho || !out || !valid_level(max_level) || !work) return TB_E_INVALID;
+  int r = ensure_weights();
+  if (r != TB_OK) return r;
+  static bool attr = false;
+  if (!attr) {
+    r = tb::rc(cudaFuncSetAttribute(k_fmm_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kLeafSmem));
+    if (r != TB_OK) return r;
+    attr = true;
+  }
+  const Layout lo = layout(max_level);
+  const double *Lpar =
+      reinterpret_cast<const double *>(reinterpret_cast<const char *>(work) + lo.Loc[max_level - 1]);
+  const int N = 8 << max_level;
+  const int tiles = (N / kTX) * (N / kTY) * (N / kTZ);
+  k_fmm_leaf<<<tiles, kLeafThreads, kLeafSmem, strm(s)>>>(rho, Lpar, out, N, 1.0 / N);
+  return tb::last_error();
+}
+
+int tb_fmm_solve(tb_stream_t s, int max_level, const double *rho, double *work, double *out) {
+  int r = tb_fmm_upward(s, max_level, rho, work);
+  if (r == TB_OK) r = tb_fmm_m2l(s, max_level, work);
+  if (r == TB_OK) r = tb_fmm_downward(s, max_level, work);
+  if (r == TB_OK) r = tb_fmm_leaf(s, max_level, rho, work, out);
+  return r;
+}
+
+}  // extern "C"
