@@ -8,24 +8,28 @@
 // bit — FMAs and rsqrt are used freely here.
 //
 // Layout (one device workspace, tb_fmm_workspace_bytes):
-//   for level l in [0, L): Mhat_l [20][N_l^3], Loc_l [20][N_l^3]   (N_l = 8*2^l,
-//   lattices z,y,x with x fastest); L0part [8][20][512].
+//   for level l in [0, L): Mhat_l [N_l^3][22], Loc_l [N_l^3][20] (N_l = 8*2^l,
+//   cells z,y,x with x fastest, one record per cell), Dtab_l [33][912] (l >= 1);
+//   L0part [8][512][20].
 //   Mhat holds the raw Cartesian moments pre-multiplied by the M2L source
-//   coefficient -(-1)^m mult(B)/m!, so the interaction is a pure FMA chain.
+//   coefficient -(-1)^m mult(B)/m! (2 zero pads), so the interaction is a pure
+//   FMA chain; Dtab_l holds, per stencil stage, the derivative tensors of the
+//   27 distinct child offsets (zero for near pairs).
 //
 // Kernels
 //   k_fmm_up    P2M+M2M, one level per launch: 8 lanes = the 8 children of a
-//               parent; shifted moments are summed with xor-shuffles (the
-//               warp-level multipole sums).
+//               parent; shifted moments are summed by an 8-lane xor-shuffle
+//               reduce-scatter (the warp-level multipole sums).
 //   k_fmm_m2l   multipole interactions of ALL levels in ONE launch (a CTA per
 //               level-l sub-grid, heaviest level first; level 0 split over 8
 //               CTAs). The interaction stencil is walked as 33 parent-near
-//               offsets P: for each, the 8^3 x 20 source block at 2P is staged
-//               by one 4-D TMA load (OOB = zero mass: the isolated boundary),
+//               offsets P: for each, the 8^3 x 22 source block at 2P is staged
+//               by one 4-D TMA load (OOB = zero mass: the isolated boundary)
+//               plus a bulk copy of that stage's 27 derivative tensors,
 //               double-buffered on mbarriers; each thread (one target cell)
-//               takes the 8 children of its parent's neighbour P, builds the
-//               1/r derivative tensor D(R) to order 3 and contracts it with the
-//               source moments (84 FMAs).
+//               takes the 8 children of its parent's neighbour P and contracts
+//               their moments with the tensor of its offset (LDS.128 pairs,
+//               84 FMAs, no branch: near pairs have D = 0).
 //   k_fmm_down  L2L, one level per launch (level 0: sums the 8 partials).
 //   k_fmm_leaf  monopole interactions at the leaves: a 264-point stencil whose
 //               weights 1/|q|, q/|q|^3 depend only on the integer offset q; a
@@ -110,12 +114,13 @@ struct Table {
   int n;
 };
 
-// M2L: L[t] += Mhat[s] * D[merge(t,s)]   (t, s, b = D index)
+// M2L: L[t] += Mhat[s] * D[merge(t,s)]   (t, s, b = D index). Source-major
+// order: consecutive FMAs update different accumulators (ILP).
 constexpr Table<84> make_m2l() {
   Table<84> T{};
   int k = 0;
-  for (int t = 0; t < NC; ++t)
-    for (int s = 0; s < NC; ++s)
+  for (int s = 0; s < NC; ++s)
+    for (int t = 0; t < NC; ++t)
       if (kComps[t].n + kComps[s].n <= 3) T.v[k++] = Term{t, s, merge(t, s), 1};
   T.n = k;
   return T;
@@ -234,21 +239,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
-// One 4-D TMA box {8,8,8,20} (x, y, z, component) of a level's moments.
-__device__ __forceinline__ void tma_load_block(const CUtensorMap *map, double *dst,
-                                               uint64_t *bar, int x, int y, int z) {
-  constexpr uint32_t bytes = 8 * 8 * 8 * NC * 8;
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes "
-      "[%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(0),
-      "r"(smem_u32(bar))
-      : "memory");
-}
-
 // The 33 parent-near offsets (|P|^2 <= 4), x fastest — same order as
 // oracle/fmm_oracle.py PNEAR.
 struct PTab {
@@ -274,16 +264,69 @@ __constant__ PTab c_pnear = make_ptab();
 // (1/|q|, qx/|q|^3, qy/|q|^3, qz/|q|^3); q = 0 -> 0 (the self term).
 __constant__ double c_w[11 * 11 * 11][4];
 
+// Per-component M2L source scale for runtime component indices.
+struct ScaleTab {
+  double v[NC];
+};
+constexpr ScaleTab make_scales() {
+  ScaleTab T{};
+  for (int k = 0; k < NC; ++k) T.v[k] = m2l_scale(k);
+  return T;
+}
+__constant__ ScaleTab c_m2lscale = make_scales();
+
+// Moment records are padded to 22 doubles (176 B): the 4 cells a warp reads
+// per LDS.128 (stride 2 cells = 22 chunks) land on distinct bank groups.
+constexpr int MS = 22;
+// Per-stage D table: the 27 offsets e = o - c + 1 in {0,1,2}^3 at 16-byte
+// chunk strides 17 / 50 / 156 (distinct mod 8 for the 8 octants of a warp).
+constexpr int kDX = 17, kDY = 50, kDZ = 156;
+constexpr int kDChunks = 2 * kDZ + 2 * kDY + 2 * kDX + NC / 2;   // 456
+constexpr int kDStage = 2 * kDChunks;                            // 912 doubles
+constexpr int kMStage = 512 * MS;                                // 11264 doubles
+constexpr int kStage = kMStage + kDStage;                        // 97,408 B
+constexpr uint32_t kMBytes = kMStage * 8, kDBytes = kDStage * 8;
+
 struct Params {
-  CUtensorMap maps[kMaxLevel];     // level l moments, 4-D {N,N,N,20}
-  double *M[kMaxLevel];
-  double *Loc[kMaxLevel];
-  double *L0part;
+  CUtensorMap maps[kMaxLevel];     // level l moment records, 4-D {22,N,N,N}
+  double *Loc[kMaxLevel];          // [N^3][20]
+  const double *Dtab[kMaxLevel];   // [33][912], levels >= 1
+  double *L0part;                  // [8][512][20]
   int L;                           // max_level (leaves); multipole levels 0..L-1
 };
 
 // ---------------------------------------------------------------- upward
-// Parents at lattice Np from children (rho leaves when rho != nullptr).
+// 8-lane reduce-scatter of v[20] (xor 4, 2, 1): lane c ends up owning
+// components [first, first + cnt) in out[].
+__device__ __forceinline__ void reduce_scatter8(const double (&v)[NC], int c, double (&out)[3],
+                                                int &first, int &cnt) {
+  const bool b2 = c & 4, b1 = c & 2, b0 = c & 1;
+  double w[10], x[5];
+#pragma unroll
+  for (int k = 0; k < 10; ++k) {
+    const double send = b2 ? v[k] : v[10 + k];
+    const double keep = b2 ? v[10 + k] : v[k];
+    w[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const double send = b1 ? w[k] : w[5 + k];
+    const double keep = b1 ? w[5 + k] : w[k];
+    x[k] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double hi = k + 3 < 5 ? x[k + 3] : 0.0;
+    const double send = b0 ? x[k] : hi;
+    const double keep = b0 ? hi : x[k];
+    out[k] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+  }
+  first = (b2 ? 10 : 0) + (b1 ? 5 : 0) + (b0 ? 3 : 0);
+  cnt = b0 ? 2 : 3;
+}
+
+// Parents at lattice Np from their 8 children: leaves (rho) or a finer
+// level's moment records. 8 lanes = the children of one parent.
 __global__ void __launch_bounds__(256) k_fmm_up(const double *__restrict__ rho,
                                                 const double *__restrict__ child,
                                                 double *__restrict__ parent, int Np,
@@ -296,51 +339,113 @@ __global__ void __launch_bounds__(256) k_fmm_up(const double *__restrict__ rho,
   const int px = (int)(pp % Np), py = (int)((pp / Np) % Np), pz = (int)(pp / ((int64_t)Np * Np));
   const int cx = c & 1, cy = (c >> 1) & 1, cz = c >> 2;
   const int Nc = 2 * Np;
-  const int64_t nch = (int64_t)Nc * Nc * Nc;
   const int64_t cf = ((int64_t)(2 * pz + cz) * Nc + (2 * py + cy)) * Nc + (2 * px + cx);
   double mono[NC];
   monomials<false>((cx - 0.5) * hc, (cy - 0.5) * hc, (cz - 0.5) * hc, mono);
-  double out[NC];
+  double v[NC];
   if (rho) {
-    const double m = valid ? rho[cf] * (hc * hc * hc) : 0.0;
-    unroll<NC>([&](auto K) { out[K] = m * mono[K]; });
+    const double m = valid ? __ldg(rho + cf) * (hc * hc * hc) : 0.0;
+    unroll<NC>([&](auto K) { v[K] = m * mono[K]; });
   } else {
     double Mc[NC];
+    const double2 *rec = reinterpret_cast<const double2 *>(child + cf * MS);
+#pragma unroll
+    for (int k = 0; k < NC / 2; ++k) {
+      const double2 a = valid ? __ldg(rec + k) : make_double2(0.0, 0.0);
+      Mc[2 * k] = a.x;
+      Mc[2 * k + 1] = a.y;
+    }
     unroll<NC>([&](auto K) {
       constexpr double inv = 1.0 / m2l_scale(K);
-      Mc[K] = valid ? child[K * nch + cf] * inv : 0.0;
-      out[K] = 0.0;
+      Mc[K] = Mc[K] * inv;
+      v[K] = 0.0;
     });
     unroll<kM2M.n>([&](auto E) {
       constexpr Term T = kM2M.v[E];
-      out[T.t] = fma(T.c * Mc[T.s], mono[T.b], out[T.t]);
+      if constexpr (T.c == 1)
+        v[T.t] = fma(Mc[T.s], mono[T.b], v[T.t]);
+      else
+        v[T.t] = fma(double(T.c) * Mc[T.s], mono[T.b], v[T.t]);
     });
   }
-  // the 8 children's shifted moments -> the parent's (xor butterfly)
-  unroll<NC>([&](auto K) {
-    double v = out[K];
-    v += __shfl_xor_sync(0xffffffffu, v, 1);
-    v += __shfl_xor_sync(0xffffffffu, v, 2);
-    v += __shfl_xor_sync(0xffffffffu, v, 4);
-    constexpr double sc = m2l_scale(K);
-    if (valid && (K & 7) == c) parent[K * npar + pidx] = v * sc;
-  });
+  double out[3];
+  int first, cnt;
+  reduce_scatter8(v, c, out, first, cnt);
+  if (valid) {
+    double *rec = parent + pidx * MS;
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      if (k < cnt) rec[first + k] = out[k] * c_m2lscale.v[first + k];
+    if (c == 0) {
+      rec[NC] = 0.0;
+      rec[NC + 1] = 0.0;
+    }
+  }
+}
+
+// --------------------------------------------------------- M2L D tables
+// Dtab[level][stage k][entry e] = D(q h) with q = (e - 1) - 2 P_k, or 0 where
+// the pair is near (|q|^2 <= 4): those children then contribute nothing and
+// the interaction loop needs no branch.
+struct TabPtrs {
+  double *p[kMaxLevel];
+};
+__global__ void __launch_bounds__(32) k_fmm_dtab(const TabPtrs T) {
+  const int k = blockIdx.x, lev = blockIdx.y + 1, e = threadIdx.x;
+  double *tab = T.p[lev] + (size_t)k * kDStage;
+  for (int i = e; i < kDStage; i += 32) tab[i] = 0.0;
+  __syncwarp();
+  if (e >= 27) return;
+  const int ex = e % 3, ey = (e / 3) % 3, ez = e / 9;
+  const int qx = ex - 1 - 2 * c_pnear.p[k][0], qy = ey - 1 - 2 * c_pnear.p[k][1],
+            qz = ez - 1 - 2 * c_pnear.p[k][2];
+  if (qx * qx + qy * qy + qz * qz <= 4) return;
+  const double h = 1.0 / double(8 << lev);
+  double D[NC];
+  d_tensor(qx * h, qy * h, qz * h, D);
+  double *dst = tab + 2 * (ex * kDX + ey * kDY + ez * kDZ);
+#pragma unroll
+  for (int i = 0; i < NC; ++i) dst[i] = D[i];
 }
 
 // ------------------------------------------------------------------- M2L
 constexpr int kM2LThreads = 512;
-constexpr int kBlock = 8 * 8 * 8;                 // doubles per component per stage
-constexpr int kStage = kBlock * NC;               // 10240 doubles = 80 KB
-constexpr int kM2LSmem = 2 * kStage * 8;          // 160 KB
+constexpr int kM2LSmem = 2 * kStage * 8;          // 194,816 B
 
-__device__ __forceinline__ void contract(double (&L)[NC], const double *Ms, int off,
+__device__ __forceinline__ void load20(const double *p, double (&v)[NC]) {
+  const double2 *q = reinterpret_cast<const double2 *>(p);
+#pragma unroll
+  for (int k = 0; k < NC / 2; ++k) {
+    const double2 a = q[k];
+    v[2 * k] = a.x;
+    v[2 * k + 1] = a.y;
+  }
+}
+
+__device__ __forceinline__ void contract(double (&L)[NC], const double (&M)[NC],
                                          const double (&D)[NC]) {
-  double M[NC];
-  unroll<NC>([&](auto K) { M[K] = Ms[K * kBlock + off]; });
   unroll<kM2L.n>([&](auto E) {
     constexpr Term T = kM2L.v[E];
     L[T.t] = fma(M[T.s], D[T.b], L[T.t]);
   });
+}
+
+__device__ __forceinline__ void issue_stage(const Params &P, int lev, double *dst,
+                                            uint64_t *bar, int k, int X0, int Y0, int Z0) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(kMBytes + kDBytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(&P.maps[lev])), "r"(0), "r"(X0 + 2 * c_pnear.p[k][0]),
+      "r"(Y0 + 2 * c_pnear.p[k][1]), "r"(Z0 + 2 * c_pnear.p[k][2]), "r"(smem_u32(bar))
+      : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst + kMStage)),
+      "l"(P.Dtab[lev] + (size_t)k * kDStage), "r"(kDBytes), "r"(smem_u32(bar))
+      : "memory");
 }
 
 __global__ void __launch_bounds__(kM2LThreads, 1) k_fmm_m2l(const __grid_constant__ Params P) {
@@ -370,71 +475,79 @@ __global__ void __launch_bounds__(kM2LThreads, 1) k_fmm_m2l(const __grid_constan
   double L[NC];
 #pragma unroll
   for (int k = 0; k < NC; ++k) L[k] = 0.0;
-  const double h = 1.0 / double(8 << lev);
-  const CUtensorMap *map = &P.maps[lev];
 
   if (lev == 0) {
     // level-0 slab `job`: all 512 targets against the sources with z == job
     if (t == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      tma_load_block(map, sm, &bar[0], 0, 0, 0);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                       smem_u32(&bar[0])),
+                   "r"(kMBytes)
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes "
+          "[%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(sm)),
+          "l"(reinterpret_cast<uint64_t>(&P.maps[0])), "r"(0), "r"(0), "r"(0), "r"(0),
+          "r"(smem_u32(&bar[0]))
+          : "memory");
     }
     mbar_wait(&bar[0], 0);
+    const double h = 1.0 / 8.0;
     const int jz = job;
 #pragma unroll 1
     for (int jy = 0; jy < 8; ++jy)
-#pragma unroll 2
+#pragma unroll 1
       for (int jx = 0; jx < 8; ++jx) {
         const int qx = lx - jx, qy = ly - jy, qz = lz - jz;
         if (qx * qx + qy * qy + qz * qz > 4) {
-          double D[NC];
+          double D[NC], M[NC];
           d_tensor(qx * h, qy * h, qz * h, D);
-          contract(L, sm, (jz * 8 + jy) * 8 + jx, D);
+          load20(sm + ((jz * 8 + jy) * 8 + jx) * MS, M);
+          contract(L, M, D);
         }
       }
-    double *dst = P.L0part + (size_t)job * NC * 512 + (lz * 8 + ly) * 8 + lx;
+    double2 *dst = reinterpret_cast<double2 *>(P.L0part + ((size_t)job * 512 +
+                                                            (lz * 8 + ly) * 8 + lx) * NC);
 #pragma unroll
-    for (int k = 0; k < NC; ++k) dst[k * 512] = L[k];
+    for (int k = 0; k < NC / 2; ++k) dst[k] = make_double2(L[2 * k], L[2 * k + 1]);
     return;
   }
 
   const int nb = 1 << lev;
-  const int bx = sub % nb, by = (sub / nb) % nb, bz = sub / (nb * nb);
-  const int X0 = 8 * bx, Y0 = 8 * by, Z0 = 8 * bz;
+  const int X0 = 8 * (sub % nb), Y0 = 8 * ((sub / nb) % nb), Z0 = 8 * (sub / (nb * nb));
   if (t == 0) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    for (int s = 0; s < 2; ++s)
-      tma_load_block(map, sm + s * kStage, &bar[s], X0 + 2 * c_pnear.p[s][0],
-                     Y0 + 2 * c_pnear.p[s][1], Z0 + 2 * c_pnear.p[s][2]);
+    issue_stage(P, lev, sm, &bar[0], 0, X0, Y0, Z0);
+    issue_stage(P, lev, sm + kStage, &bar[1], 1, X0, Y0, Z0);
   }
+  // lane-dependent parts of the source cell and of the D-table entry
+  const int cbase = ((2 * pz) * 8 + 2 * py) * 8 + 2 * px;
+  const int dbase = (ox + 1) * kDX + (oy + 1) * kDY + (oz + 1) * kDZ;
 #pragma unroll 1
   for (int k = 0; k < 33; ++k) {
     const int buf = k & 1;
     mbar_wait(&bar[buf], (k >> 1) & 1);
     const double *Ms = sm + buf * kStage;
-    const int Px = c_pnear.p[k][0], Py = c_pnear.p[k][1], Pz = c_pnear.p[k][2];
+    const double *Ds = Ms + kMStage;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const int cx = c & 1, cy = (c >> 1) & 1, cz = c >> 2;
-      const int qx = ox - 2 * Px - cx, qy = oy - 2 * Py - cy, qz = oz - 2 * Pz - cz;
-      if (qx * qx + qy * qy + qz * qz > 4) {
-        double D[NC];
-        d_tensor(qx * h, qy * h, qz * h, D);
-        contract(L, Ms, ((2 * pz + cz) * 8 + (2 * py + cy)) * 8 + (2 * px + cx), D);
-      }
+      double M[NC], D[NC];
+      load20(Ms + (cbase + (cz * 8 + cy) * 8 + cx) * MS, M);
+      load20(Ds + 2 * (dbase - cx * kDX - cy * kDY - cz * kDZ), D);
+      contract(L, M, D);
     }
     __syncthreads();            // every thread is done with this buffer
     if (t == 0 && k + 2 < 33) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      tma_load_block(map, sm + buf * kStage, &bar[buf], X0 + 2 * c_pnear.p[k + 2][0],
-                     Y0 + 2 * c_pnear.p[k + 2][1], Z0 + 2 * c_pnear.p[k + 2][2]);
+      issue_stage(P, lev, sm + buf * kStage, &bar[buf], k + 2, X0, Y0, Z0);
     }
   }
   const int N = 8 << lev;
-  const size_t ncell = (size_t)N * N * N;
-  double *dst = P.Loc[lev] + ((size_t)(Z0 + lz) * N + (Y0 + ly)) * N + (X0 + lx);
+  double2 *dst = reinterpret_cast<double2 *>(
+      P.Loc[lev] + (((size_t)(Z0 + lz) * N + (Y0 + ly)) * N + (X0 + lx)) * NC);
 #pragma unroll
-  for (int k = 0; k < NC; ++k) dst[k * ncell] = L[k];
+  for (int k = 0; k < NC / 2; ++k) dst[k] = make_double2(L[2 * k], L[2 * k + 1]);
 }
 
 // ------------------------------------------------------------------ L2L
@@ -445,30 +558,32 @@ __global__ void __launch_bounds__(256) k_fmm_down(const double *__restrict__ Lp,
   const int64_t n = (int64_t)N * N * N;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  double out[NC];
   if (L0part) {   // level 0: sum the 8 slab partials in a fixed order
 #pragma unroll
-    for (int k = 0; k < NC; ++k) {
-      double v = 0.0;
-      for (int s = 0; s < 8; ++s) v += L0part[((size_t)s * NC + k) * 512 + i];
-      Lc[k * n + i] = v;
+    for (int k = 0; k < NC; ++k) out[k] = 0.0;
+    for (int s = 0; s < 8; ++s) {
+      double v[NC];
+      load20(L0part + ((size_t)s * 512 + i) * NC, v);
+#pragma unroll
+      for (int k = 0; k < NC; ++k) out[k] += v[k];
     }
-    return;
+  } else {
+    const int x = (int)(i % N), y = (int)((i / N) % N), z = (int)(i / ((int64_t)N * N));
+    const int Nq = N / 2;
+    const int64_t pi = ((int64_t)(z >> 1) * Nq + (y >> 1)) * Nq + (x >> 1);
+    double mono[NC], Lpar[NC];
+    monomials<true>(((x & 1) - 0.5) * h, ((y & 1) - 0.5) * h, ((z & 1) - 0.5) * h, mono);
+    load20(Lp + pi * NC, Lpar);
+    load20(Lc + i * NC, out);
+    unroll<kL2L.n>([&](auto E) {
+      constexpr Term T = kL2L.v[E];
+      out[T.t] = fma(Lpar[T.s], mono[T.b], out[T.t]);
+    });
   }
-  const int x = (int)(i % N), y = (int)((i / N) % N), z = (int)(i / ((int64_t)N * N));
-  const int Nq = N / 2;
-  const int64_t np = (int64_t)Nq * Nq * Nq;
-  const int64_t pi = ((int64_t)(z >> 1) * Nq + (y >> 1)) * Nq + (x >> 1);
-  double mono[NC], Lpar[NC], out[NC];
-  monomials<true>(((x & 1) - 0.5) * h, ((y & 1) - 0.5) * h, ((z & 1) - 0.5) * h, mono);
-  unroll<NC>([&](auto K) {
-    Lpar[K] = Lp[K * np + pi];
-    out[K] = Lc[K * n + i];
-  });
-  unroll<kL2L.n>([&](auto E) {
-    constexpr Term T = kL2L.v[E];
-    out[T.t] = fma(Lpar[T.s], mono[T.b], out[T.t]);
-  });
-  unroll<NC>([&](auto K) { Lc[K * n + i] = out[K]; });
+  double2 *dst = reinterpret_cast<double2 *>(Lc + i * NC);
+#pragma unroll
+  for (int k = 0; k < NC / 2; ++k) dst[k] = make_double2(out[2 * k], out[2 * k + 1]);
 }
 
 // ------------------------------------------------------------ leaf (P2P)
@@ -488,18 +603,20 @@ __global__ void __launch_bounds__(kLeafThreads, 2)
   const int X0 = (tile % ntx) * kTX, Y0 = ((tile / ntx) % nty) * kTY,
             Z0 = (tile / (ntx * nty)) * kTZ;
   // ---- stage rho over [X0-4, X0+12) x [Y0-4, Y0+12) x [Z0-4, Z0+20), split by
-  //      parity: S[c][z'][y'][x'] with coordinate = 2*primed + c
-  for (int r = w; r < 16 * 24; r += kLeafThreads / 32) {
-    const int ry = r % 16, rz = r / 16;
-    if (lane < 16) {
-      const int gx = X0 - 4 + lane, gy = Y0 - 4 + ry, gz = Z0 - 4 + rz;
-      double v = 0.0;
-      if (gx >= 0 && gx < N && gy >= 0 && gy < N && gz >= 0 && gz < N)
-        v = __ldg(rho + ((size_t)gz * N + gy) * N + gx);
-      const int c = (lane & 1) | ((ry & 1) << 1) | ((rz & 1) << 2);
-      S[c * kPar + ((rz >> 1) * kSY + (ry >> 1)) * kSX + (lane >> 1)] = v;
-    }
+  //      parity: S[c][z'][y'][x'] with coordinate = 2*primed + c; 8-byte
+  //      cp.async (all in flight at once), zero-filled outside the domain
+  for (int e = t; e < 16 * 16 * 24; e += kLeafThreads) {
+    const int rx = e & 15, ry = (e >> 4) & 15, rz = e >> 8;
+    const int gx = X0 - 4 + rx, gy = Y0 - 4 + ry, gz = Z0 - 4 + rz;
+    const bool in = gx >= 0 && gx < N && gy >= 0 && gy < N && gz >= 0 && gz < N;
+    const double *src = in ? rho + ((size_t)gz * N + gy) * N + gx : rho;
+    const int c = (rx & 1) | ((ry & 1) << 1) | ((rz & 1) << 2);
+    double *dst = S + c * kPar + ((rz >> 1) * kSY + (ry >> 1)) * kSX + (rx >> 1);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src),
+                 "r"(in ? 8 : 0)
+                 : "memory");
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   // ---- warp = child octant o; lane = (px, py, pz low bit); 4 targets over pz
   const int ox = w & 1, oy = (w >> 1) & 1, oz = w >> 2;
@@ -533,7 +650,7 @@ __global__ void __launch_bounds__(kLeafThreads, 2)
   double mono[NC];
   monomials<true>((ox - 0.5) * h, (oy - 0.5) * h, (oz - 0.5) * h, mono);
   const int Nq = N / 2;
-  const size_t np = (size_t)Nq * Nq * Nq, n = (size_t)N * N * N;
+  const size_t n = (size_t)N * N * N;
   const double h2 = h * h;
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
@@ -543,7 +660,13 @@ __global__ void __launch_bounds__(kLeafThreads, 2)
     if (Lpar) {
       const size_t pi = ((size_t)(z >> 1) * Nq + (y >> 1)) * Nq + (x >> 1);
       double Lp[NC];
-      unroll<NC>([&](auto K) { Lp[K] = __ldg(Lpar + K * np + pi); });
+      const double2 *rec = reinterpret_cast<const double2 *>(Lpar + pi * NC);
+#pragma unroll
+      for (int k = 0; k < NC / 2; ++k) {
+        const double2 a = __ldg(rec + k);
+        Lp[2 * k] = a.x;
+        Lp[2 * k + 1] = a.y;
+      }
       unroll<kL2L.n>([&](auto E) {
         constexpr Term T = kL2L.v[E];
         if constexpr (T.t == 0) phi = fma(Lp[T.s], mono[T.b], phi);
@@ -560,7 +683,7 @@ __global__ void __launch_bounds__(kLeafThreads, 2)
 
 // ------------------------------------------------------------------ host
 struct Layout {
-  size_t M[kMaxLevel], Loc[kMaxLevel], L0part, total;   // byte offsets
+  size_t M[kMaxLevel], Loc[kMaxLevel], Dtab[kMaxLevel], L0part, total;   // byte offsets
 };
 
 Layout layout(int L) {
@@ -569,12 +692,14 @@ Layout layout(int L) {
   for (int l = 0; l < L; ++l) {
     const size_t n = (size_t)(8 << l) * (8 << l) * (8 << l);
     lo.M[l] = off;
-    off += n * NC * 8;
+    off += n * MS * 8;
     lo.Loc[l] = off;
     off += n * NC * 8;
+    lo.Dtab[l] = off;
+    if (l) off += (size_t)33 * kDStage * 8;
   }
   lo.L0part = off;
-  off += (size_t)8 * NC * 512 * 8;
+  off += (size_t)8 * 512 * NC * 8;
   lo.total = off;
   return lo;
 }
@@ -618,7 +743,8 @@ int encoder(EncodeTiled *fn) {
   if (!enc) {
     void *p = nullptr;
     cudaDriverEntryPointQueryResult q;
-    const int r = tb::rc(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    const int r =
+        tb::rc(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
     if (r != TB_OK) return r;
     if (!p || q != cudaDriverEntryPointSuccess) return TB_E_INVALID;
     enc = reinterpret_cast<EncodeTiled>(p);
@@ -637,14 +763,15 @@ int make_params(int L, double *work, Params *P) {
   P->L = L;
   P->L0part = reinterpret_cast<double *>(base + lo.L0part);
   for (int l = 0; l < L; ++l) {
-    P->M[l] = reinterpret_cast<double *>(base + lo.M[l]);
+    double *M = reinterpret_cast<double *>(base + lo.M[l]);
     P->Loc[l] = reinterpret_cast<double *>(base + lo.Loc[l]);
+    P->Dtab[l] = reinterpret_cast<const double *>(base + lo.Dtab[l]);
     const cuuint64_t N = (cuuint64_t)(8 << l);
-    const cuuint64_t dims[4] = {N, N, N, (cuuint64_t)NC};
-    const cuuint64_t strides[3] = {N * 8, N * N * 8, N * N * N * 8};
-    const cuuint32_t box[4] = {8, 8, 8, (cuuint32_t)NC};
+    const cuuint64_t dims[4] = {(cuuint64_t)MS, N, N, N};
+    const cuuint64_t strides[3] = {MS * 8, MS * 8 * N, MS * 8 * N * N};
+    const cuuint32_t box[4] = {(cuuint32_t)MS, 8, 8, 8};
     const cuuint32_t estr[4] = {1, 1, 1, 1};
-    if (enc(&P->maps[l], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, P->M[l], dims, strides, box, estr,
+    if (enc(&P->maps[l], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, M, dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return TB_E_INVALID;
@@ -673,11 +800,11 @@ int tb_fmm_upward(tb_stream_t s, int max_level, const double *rho, double *work)
     const int64_t npar = (int64_t)Np * Np * Np;
     const int64_t blocks = (npar + 31) / 32;   // 8 warps x 4 parents
     const double hc = 1.0 / double(2 * Np);
-    const double *child = l == max_level - 1 ? nullptr
-                                             : reinterpret_cast<const double *>(base + lo.M[l + 1]);
-    k_fmm_up<<<(unsigned)blocks, 256, 0, strm(s)>>>(l == max_level - 1 ? rho : nullptr, child,
-                                                 reinterpret_cast<double *>(base + lo.M[l]), Np,
-                                                 hc);
+    const double *child =
+        l == max_level - 1 ? nullptr : reinterpret_cast<const double *>(base + lo.M[l + 1]);
+    k_fmm_up<<<(unsigned)blocks, 256, 0, strm(s)>>>(
+        l == max_level - 1 ? rho : nullptr, child, reinterpret_cast<double *>(base + lo.M[l]),
+        Np, hc);
   }
   return tb::last_error();
 }
@@ -693,6 +820,11 @@ int tb_fmm_m2l(tb_stream_t s, int max_level, double *work) {
                                     kM2LSmem));
     if (r != TB_OK) return r;
     attr = true;
+  }
+  if (max_level > 1) {
+    TabPtrs T{};
+    for (int l = 1; l < max_level; ++l) T.p[l] = const_cast<double *>(P.Dtab[l]);
+    k_fmm_dtab<<<dim3(33, max_level - 1), 32, 0, strm(s)>>>(T);
   }
   int jobs = 8;
   for (int l = 1; l < max_level; ++l) jobs += 1 << (3 * l);
@@ -728,8 +860,8 @@ int tb_fmm_leaf(tb_stream_t s, int max_level, const double *rho, const double *w
     attr = true;
   }
   const Layout lo = layout(max_level);
-  const double *Lpar =
-      reinterpret_cast<const double *>(reinterpret_cast<const char *>(work) + lo.Loc[max_level - 1]);
+  const double *Lpar = reinterpret_cast<const double *>(reinterpret_cast<const char *>(work) +
+                                                        lo.Loc[max_level - 1]);
   const int N = 8 << max_level;
   const int tiles = (N / kTX) * (N / kTY) * (N / kTZ);
   k_fmm_leaf<<<tiles, kLeafThreads, kLeafSmem, strm(s)>>>(rho, Lpar, out, N, 1.0 / N);

@@ -56,13 +56,15 @@ def test_fmm_upward_moments_vs_oracle():
     scale = np.array([(1.0 if len(B) % 2 else -1.0) * f.mult(B) / math.factorial(len(B))
                       for B in f.COMPS])
     off = 0
-    for lev in range(L):
+    for lev in range(L):                        # workspace: [M_l [n][22], Loc_l [n][20], Dtab_l]
         n = (8 << lev) ** 3
-        got = work[off:off + 20 * n].reshape(20, 8 << lev, 8 << lev, 8 << lev)
+        rec = work[off:off + 22 * n].reshape(8 << lev, 8 << lev, 8 << lev, 22)
+        got = np.moveaxis(rec[..., :20], -1, 0)
+        assert np.all(rec[..., 20:] == 0.0)
         want = Ms[lev] * scale[:, None, None, None]
         mag = np.abs(want).max(axis=(1, 2, 3), keepdims=True)
         assert np.all(np.abs(got - want) <= 1e-13 * mag + 1e-300), lev
-        off += 40 * n
+        off += 42 * n + (33 * 912 if lev else 0)
 
 
 @pytest.mark.parametrize("L", [3, 4])
