@@ -202,6 +202,147 @@ def machine_ablation(subgrids=512, steps=5, repeats=3):
     return out
 
 
+HYDRO_BYTES_PER_SUBGRID = 5 * 12 ** 3 * 8 + 5 * 8 ** 3 * 8 + 8   # U in, dU/dt + amax out
+M2L_FMA, LEAF_FMA = 84, 4     # algorithmic FP64 FMAs per interaction (K7)
+
+
+def fp64_peak():
+    """Measured FP64 issue rate (profiles/fp64_peak.json, tb_fp64_probe)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as fh:
+            return json.load(fh)["dfma_instr_per_s"], "measured (tb_fp64_probe)"
+    except (OSError, ValueError, KeyError):
+        return 64 * 148 * 1.965e9, "nominal 64 DFMA/clk/SM x 148 SMs x 1965 MHz"
+
+
+def fmm_interactions(L):
+    """Algorithmic interaction counts of the FMM at max_level L: (M2L pairs of
+    levels 0..L-1 on the interaction lists, leaf monopole pairs)."""
+    import itertools
+    pnear = [p for p in itertools.product(range(-2, 3), repeat=3) if sum(x * x for x in p) <= 4]
+    ch = list(itertools.product((0, 1), repeat=3))
+
+    def inside(v, n):
+        return 0 <= v < n
+
+    m2l = 0
+    # level 0: every far pair of the 8^3 root lattice
+    g = list(itertools.product(range(8), repeat=3))
+    m2l += sum(1 for a in g for b in g if sum((a[k] - b[k]) ** 2 for k in range(3)) > 4)
+    for lev in range(1, L):
+        n = 8 << lev
+        # per parent position along an axis the in-range count factorises only
+        # approximately; count exactly over one axis-symmetric sweep
+        tot = 0
+        for o in ch:
+            for P in pnear:
+                for c in ch:
+                    q = [o[k] - 2 * P[k] - c[k] for k in range(3)]
+                    if sum(x * x for x in q) <= 4:
+                        continue
+                    cnt = 1
+                    for k in range(3):   # targets along axis k whose partner is in range
+                        cnt *= sum(1 for i in range(o[k], n, 2) if inside(i - q[k], n))
+                    tot += cnt
+        m2l += tot
+    nl = 8 << L
+    leaf = 0
+    for o in ch:
+        for P in pnear:
+            for c in ch:
+                q = [o[k] - 2 * P[k] - c[k] for k in range(3)]
+                if q == [0, 0, 0]:
+                    continue
+                cnt = 1
+                for k in range(3):
+                    cnt *= sum(1 for i in range(o[k], nl, 2) if inside(i - q[k], nl))
+                leaf += cnt
+    return m2l, leaf
+
+
+def north_star_kernels(dev, reps=20):
+    """BASELINE configs 2 and 3 on the north_star's hydro (K6) and FMM (K7)
+    kernels — PARITY UNPINNED (self-authored specs, oracle/hydro_oracle.py,
+    oracle/fmm_oracle.py; the reference has neither). CUDA events on the
+    launching stream, L2 flushed before every timed launch."""
+    import torch
+    from paper_2303_08058_b200 import hydro
+    from paper_2303_08058_b200.gravity import GravitySolver, rotating_star_density
+    peaks, _ = measured_peaks()
+    hbm = float(peaks.get("hbm_gbs", FALLBACK_HBM_GBS))
+    f64, f64_src = fp64_peak()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    out = {}
+    # K6: hydro reconstruct+flux, 4096 sub-grids (config 2)
+    S = 4096
+    I, dx = hydro.rotating_star(S, device=dev)
+    U = hydro.with_ghosts(I)
+    du = torch.empty((S, 5, 8, 8, 8), dtype=torch.float64, device=dev)
+    am = torch.empty(S, dtype=torch.float64, device=dev)
+    for _ in range(3):
+        hydro.hydro_flux(U, dx, out=du, amax=am)
+    tot = 0.0
+    for _ in range(reps):
+        flush.fill_(1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        hydro.hydro_flux(U, dx, out=du, amax=am)
+        b.record()
+        torch.cuda.synchronize()
+        tot += a.elapsed_time(b)
+    ms = tot / reps
+    gbs = S * HYDRO_BYTES_PER_SUBGRID / (ms * 1e-3) / 1e9
+    out["hydro_k6"] = {
+        "config": "BASELINE config 2: hydro reconstruct+flux, 4096 synthetic 8^3 sub-grids "
+                  "with 2-cell ghost layers (rotating star), 1 B200",
+        "kernel": "k_hydro_flux", "ms": ms, "cells_per_s": S * 512 / (ms * 1e-3),
+        "roofline": {"bound": "fp64 (divide/sqrt-heavy; see profiles)", "hbm_achieved_gbs": gbs,
+                     "hbm_frac": gbs / hbm,
+                     "algorithmic_bytes_per_launch": S * HYDRO_BYTES_PER_SUBGRID},
+        "parity": "unpinned (self-authored spec; bit-exact to oracle/hydro_oracle.py)"}
+    # K7: FMM gravity, max_level 4 (config 3)
+    L = 4
+    rho = rotating_star_density(L, device=dev)
+    gs = GravitySolver(L, dev)
+    for _ in range(3):
+        gs.solve(rho)
+    names = ["upward", "m2l", "downward", "leaf"]
+    acc = dict.fromkeys(names + ["solve"], 0.0)
+    for _ in range(reps):
+        flush.fill_(1)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        ev[0].record()
+        gs.upward(rho)
+        ev[1].record()
+        gs.m2l()
+        ev[2].record()
+        gs.downward()
+        ev[3].record()
+        gs.leaf(rho)
+        ev[4].record()
+        torch.cuda.synchronize()
+        for i, k in enumerate(names):
+            acc[k] += ev[i].elapsed_time(ev[i + 1])
+        acc["solve"] += ev[0].elapsed_time(ev[4])
+    ms = {k: v / reps for k, v in acc.items()}
+    nm, nl = fmm_interactions(L)
+    m2l_rate = nm * M2L_FMA / (ms["m2l"] * 1e-3)
+    leaf_rate = nl * LEAF_FMA / (ms["leaf"] * 1e-3)
+    cells = (8 << L) ** 3
+    out["fmm_k7"] = {
+        "config": "BASELINE config 3: FMM multipole (M2L, levels 0-3) + monopole (leaf) "
+                  "interaction kernels, rotating star max_level 4 (2,097,152 leaf cells), 1 B200",
+        "ms": ms, "cells_per_s": cells / (ms["solve"] * 1e-3),
+        "interactions": {"m2l": nm, "leaf": nl},
+        "roofline": {"bound": "fp64", "unit": "DFMA/s", "peak": f64, "peak_source": f64_src,
+                     "m2l_achieved": m2l_rate, "m2l_frac": m2l_rate / f64,
+                     "leaf_achieved": leaf_rate, "leaf_frac": leaf_rate / f64,
+                     "algorithmic_fma_per_interaction": {"m2l": M2L_FMA, "leaf": LEAF_FMA}},
+        "gpu_launches_per_solve": 2 * L + 2,
+        "parity": "unpinned (self-authored spec; 1e-10 relative to oracle/fmm_oracle.py)"}
+    return out
+
+
 def run_reference_arm(args, workload_key, rank, world):
     if rank != 0:
         return 0
@@ -266,6 +407,8 @@ def main(argv=None):
                     help="all ranks on cuda:0 (with --dist-backend gloo: code-path test)")
     ap.add_argument("--no-ablation", action="store_true",
                     help="skip the polling/host-task/fence machine ablation")
+    ap.add_argument("--no-kernels", action="store_true",
+                    help="skip the hydro (K6) / FMM (K7) lines of configs 2 and 3")
     ap.add_argument("--spw", type=int, default=0,
                     help="K2 sub-grids per warp per CTA (0 = one persistent wave)")
     args = ap.parse_args(argv)
@@ -387,6 +530,9 @@ def main(argv=None):
         ablation = None
         if not args.no_ablation:
             ablation = machine_ablation()
+        kernels = None
+        if not args.no_kernels:
+            kernels = north_star_kernels(dev)
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             v, cores, nsteps, el = cpu_reference_sample(per_gpu, args.cpu_budget)
@@ -426,6 +572,7 @@ def main(argv=None):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "ablation": ablation,
+            "north_star_kernels": kernels,
             "gpu_launches": (1 if world == 1 else 2) * args.steps,
             "clocks": clocks,
             "wall_s_timed_region": wall,

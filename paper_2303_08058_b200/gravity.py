@@ -87,3 +87,14 @@ def fmm_gravity(rho: torch.Tensor, max_level: Optional[int] = None) -> torch.Ten
     lev = max_level if max_level is not None else (n // 8).bit_length() - 1
     s = GravitySolver(lev, rho.device)
     return s.solve(rho).clone()
+
+
+def rotating_star_density(max_level: int, device=None) -> torch.Tensor:
+    """The synthetic rotating star's density (the hydro generator's bump on a
+    1e-3 floor) as an [N, N, N] leaf lattice, N = 8 * 2^max_level, on the
+    isolated unit cube (tests check it against the oracle's generator)."""
+    N = 8 << max_level
+    c = (torch.arange(N, dtype=torch.float64, device=device) + 0.5) / N - 0.5
+    z, y, x = torch.meshgrid(c, c, c, indexing="ij")
+    r = torch.sqrt(x * x + y * y + z * z)
+    return (1e-3 + torch.clamp(1.0 - (r / 0.35) ** 2, min=0.0) ** 1.5).contiguous()

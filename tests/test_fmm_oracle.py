@@ -105,3 +105,11 @@ def test_mirror_symmetry():
     assert np.allclose(out[0], flipped[0], rtol=1e-12, atol=0)
     assert np.allclose(out[1], -flipped[1], rtol=1e-9, atol=1e-12 * np.abs(out[1]).max())
     assert np.allclose(out[2], flipped[2], rtol=1e-9, atol=1e-12 * np.abs(out[2]).max())
+
+
+def test_product_density_matches_the_oracle_generator():
+    pytest.importorskip("torch")
+    from paper_2303_08058_b200.gravity import rotating_star_density
+    for L in (1, 2):
+        np.testing.assert_allclose(rotating_star_density(L).numpy(),
+                                   f.rotating_star_density(L), rtol=1e-15, atol=0)

@@ -56,3 +56,15 @@ def test_positive_pressure_and_signal_speed():
     assert (p > 0).all() and (rho > 0).all()
     _, a = h.hydro_flux(h.with_ghosts(I), dx, 5 / 3)
     assert (a > 0).all()
+
+
+def test_product_synthetic_inputs_match_the_oracle_generator():
+    torch = pytest.importorskip("torch")
+    from paper_2303_08058_b200 import hydro
+    for s in (1, 8, 27):
+        I, dx = h.rotating_star(s)
+        It, dxt = hydro.rotating_star(s)
+        assert dx == dxt
+        np.testing.assert_allclose(It.numpy(), I, rtol=1e-15, atol=1e-15)
+        np.testing.assert_array_equal(hydro.with_ghosts(torch.from_numpy(I)).numpy(),
+                                      h.with_ghosts(I))
