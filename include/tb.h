@@ -222,6 +222,27 @@ int tb_acc_allreduce_p2p(tb_stream_t s, int64_t *local_acc, int64_t *const *peer
 int tb_hydro_flux(tb_stream_t s, const double *U, double *dudt, double *amax,
                   int64_t nsub, double dx, double gamma);
 
+/* K6 on a ghost-padded global lattice (the coupled step's layout):
+ * Up [5][n+4][n+4][n+4] (2-cell ghost layer already filled, e.g. by
+ * tb_star_pad); sub-grid s = (bz*nb + by)*nb + bx (nb = n/8) is staged by one
+ * 4-D TMA box; dudt [nb^3][5][8][8][8], amax [nb^3] as tb_hydro_flux. */
+int tb_hydro_flux_lattice(tb_stream_t s, const double *Up, int64_t n, double *dudt,
+                          double *amax, double dx, double gamma);
+
+/* The coupled rotating-star step (PARITY UNPINNED; spec oracle/star_oracle.py):
+ * U [5][n][n][n] lattice (rho, sx, sy, sz, E), periodic hydro, isolated FMM
+ * gravity. tb_star_pad fills Up with the periodic ghost layer; tb_star_cfl
+ * writes dt = cfl*dx/max(amax) to device memory; tb_star_stage applies
+ * L(U) = dU/dt + (0, rho g, s.g) with g = rows 1..3 of the FMM output:
+ * stage 1: Unew = Uc + dt L(Uc); stage 2: Unew = 0.5 (U0 + (Uc + dt L(Uc)))
+ * (Unew may alias U0). No FMA: matches the oracle's rounding. */
+int tb_star_pad(tb_stream_t s, const double *U, int64_t n, double *Up);
+int tb_star_cfl(tb_stream_t s, const double *amax, int64_t nsub, double dx, double cfl,
+                double *dt);
+int tb_star_stage(tb_stream_t s, int stage, const double *U0, const double *Uc,
+                  const double *dudt, const double *g, const double *dt, int64_t n,
+                  double *Unew);
+
 /* K7 (north_star "FMM monopole/multipole stencil-interaction kernels",
  * BASELINE config 3; PARITY UNPINNED — no gravity exists in the reference,
  * the spec is oracle/fmm_oracle.py, matched to 1e-10

@@ -1,0 +1,70 @@
+"""numpy oracle for the coupled rotating-star step — TEST INFRASTRUCTURE.
+
+PARITY UNPINNED: the reference has no physics. This is the
+north_star's "full rotating-star step" as a SELF-AUTHORED spec composed of
+the two self-authored kernels (oracle/hydro_oracle.py, oracle/fmm_oracle.py):
+
+* state U [5, N, N, N] (rho, sx, sy, sz, E) on the unit cube, N = 8 * 2^L
+  (the octree's leaf level), sub-grid s = (bz*n + by)*n + bx of 8^3 cells;
+* hydro: periodic 2-cell ghost layers, dU/dt and per-sub-grid amax;
+* gravity: FMM of rho with isolated boundary -> g;
+* L(U) = dU/dt + (0, rho gx, rho gy, rho gz, (sx gx + sy gy) + sz gz);
+* dt = (cfl * dx) / max(amax) from the stage-1 state;
+* Heun / SSP-RK2: U1 = U + dt L(U);  U' = 0.5 * (U + (U1 + dt L(U1))).
+
+Properties (tests/test_star_oracle.py): total mass conserved to round-off;
+a uniform gas at rest stays at rest up to gravity; GPU per cell within 1e-10.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import fmm_oracle as fo
+from . import hydro_oracle as ho
+
+NF, NI = 5, 8
+
+
+def subgrids_to_lattice(S: np.ndarray) -> np.ndarray:
+    """[n^3, F, 8, 8, 8] -> [F, N, N, N]."""
+    s, F = S.shape[:2]
+    n = round(s ** (1 / 3))
+    g = S.reshape(n, n, n, F, NI, NI, NI).transpose(3, 0, 4, 1, 5, 2, 6)
+    return np.ascontiguousarray(g.reshape(F, n * NI, n * NI, n * NI))
+
+
+def lattice_to_subgrids(U: np.ndarray) -> np.ndarray:
+    F, N = U.shape[0], U.shape[1]
+    n = N // NI
+    g = U.reshape(F, n, NI, n, NI, n, NI).transpose(1, 3, 5, 0, 2, 4, 6)
+    return np.ascontiguousarray(g.reshape(n ** 3, F, NI, NI, NI))
+
+
+def initial_state(max_level: int, gamma: float = 5.0 / 3.0, omega: float = 0.3):
+    I, dx = ho.rotating_star(8 ** max_level, gamma, omega)
+    return subgrids_to_lattice(I), dx
+
+
+def rhs(U: np.ndarray, max_level: int, gamma: float):
+    N = U.shape[1]
+    dx = 1.0 / N
+    du, amax = ho.hydro_flux(ho.with_ghosts(lattice_to_subgrids(U)), dx, gamma)
+    du = subgrids_to_lattice(du)
+    g = fo.solve(U[0], max_level)[1:]
+    L = du.copy()
+    L[1] = du[1] + U[0] * g[0]
+    L[2] = du[2] + U[0] * g[1]
+    L[3] = du[3] + U[0] * g[2]
+    L[4] = du[4] + ((U[1] * g[0] + U[2] * g[1]) + U[3] * g[2])
+    return L, amax
+
+
+def step(U: np.ndarray, max_level: int, gamma: float = 5.0 / 3.0, cfl: float = 0.4):
+    """One SSP-RK2 step -> (U', dt)."""
+    dx = 1.0 / U.shape[1]
+    L1, amax = rhs(U, max_level, gamma)
+    dt = (cfl * dx) / amax.max()
+    U1 = U + dt * L1
+    L2, _ = rhs(U1, max_level, gamma)
+    return 0.5 * (U + (U1 + dt * L2)), dt

@@ -15,7 +15,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libtb.so")
-SOURCES = ["tb_kernels.cu", "tb_runtime.cu", "tb_machine.cu", "tb_hydro.cu", "tb_probe.cu", "tb_fmm.cu"]
+SOURCES = ["tb_kernels.cu", "tb_runtime.cu", "tb_machine.cu", "tb_hydro.cu", "tb_probe.cu", "tb_fmm.cu", "tb_star.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -733,30 +733,7 @@ int ensure_weights() {
   return r;
 }
 
-using EncodeTiled = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
-                                 const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
-                                 const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                 CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-int encoder(EncodeTiled *fn) {
-  static EncodeTiled enc = nullptr;
-  if (!enc) {
-    void *p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    const int r =
-        tb::rc(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
-    if (r != TB_OK) return r;
-    if (!p || q != cudaDriverEntryPointSuccess) return TB_E_INVALID;
-    enc = reinterpret_cast<EncodeTiled>(p);
-  }
-  *fn = enc;
-  return TB_OK;
-}
-
 int make_params(int L, double *work, Params *P) {
-  EncodeTiled enc = nullptr;
-  int r = encoder(&enc);
-  if (r != TB_OK) return r;
   const Layout lo = layout(L);
   char *base = reinterpret_cast<char *>(work);
   *P = Params{};
@@ -766,15 +743,12 @@ int make_params(int L, double *work, Params *P) {
     double *M = reinterpret_cast<double *>(base + lo.M[l]);
     P->Loc[l] = reinterpret_cast<double *>(base + lo.Loc[l]);
     P->Dtab[l] = reinterpret_cast<const double *>(base + lo.Dtab[l]);
-    const cuuint64_t N = (cuuint64_t)(8 << l);
-    const cuuint64_t dims[4] = {(cuuint64_t)MS, N, N, N};
-    const cuuint64_t strides[3] = {MS * 8, MS * 8 * N, MS * 8 * N * N};
-    const cuuint32_t box[4] = {(cuuint32_t)MS, 8, 8, 8};
-    const cuuint32_t estr[4] = {1, 1, 1, 1};
-    if (enc(&P->maps[l], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, M, dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return TB_E_INVALID;
+    const uint64_t N = (uint64_t)(8 << l);
+    const uint64_t dims[4] = {(uint64_t)MS, N, N, N};
+    const uint64_t strides[3] = {MS * 8, MS * 8 * N, MS * 8 * N * N};
+    const uint32_t box[4] = {(uint32_t)MS, 8, 8, 8};
+    const int r = tb::encode_tiled(&P->maps[l], 4, M, dims, strides, box);
+    if (r != TB_OK) return r;
   }
   return TB_OK;
 }

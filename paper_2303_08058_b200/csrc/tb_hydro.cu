@@ -71,9 +71,16 @@ __device__ __forceinline__ double minmod(double dl, double dr) {
   return __dmul_rn(dl, dr) <= 0.0 ? 0.0 : pick;
 }
 
+// LATTICE = false: U is [nsub][5][12][12][12] (ghosted sub-grids), staged by
+// one 1-D bulk copy. LATTICE = true: U is a ghost-padded global lattice
+// [5][N+4][N+4][N+4] described by `map`; sub-grid s (x fastest, nb per edge)
+// is staged by one 4-D TMA box {12,12,12,5} at (8 bx, 8 by, 8 bz, 0) — the
+// same shared-memory layout, no per-sub-grid ghost copies in HBM.
+template <bool LATTICE>
 __global__ void __launch_bounds__(kThreads, 2)
-    k_hydro_flux(const double *__restrict__ U, double *__restrict__ dudt,
-                 double *__restrict__ amax_out, int64_t nsub, double dx, double gamma) {
+    k_hydro_flux(const double *__restrict__ U, const __grid_constant__ CUtensorMap map, int nb,
+                 double *__restrict__ dudt, double *__restrict__ amax_out, int64_t nsub,
+                 double dx, double gamma) {
   extern __shared__ __align__(128) double sm[];
   double *W = sm;                        // [5][1728] primitives (staged U)
   double *Fb = sm + NF * NCELL;          // [5][576] one direction's face fluxes
@@ -96,11 +103,21 @@ __global__ void __launch_bounds__(kThreads, 2)
                        smem_u32(&bar)),
                    "r"(bytes)
                    : "memory");
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], "
-          "%2, [%3];" ::"r"(smem_u32(W)),
-          "l"(U + s * (int64_t)(NF * NCELL)), "r"(bytes), "r"(smem_u32(&bar))
-          : "memory");
+      if constexpr (LATTICE) {
+        const int bx = (int)(s % nb), by = (int)((s / nb) % nb), bz = (int)(s / ((int64_t)nb * nb));
+        asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes "
+            "[%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(W)),
+            "l"(reinterpret_cast<uint64_t>(&map)), "r"(8 * bx), "r"(8 * by), "r"(8 * bz), "r"(0),
+            "r"(smem_u32(&bar))
+            : "memory");
+      } else {
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], "
+            "%2, [%3];" ::"r"(smem_u32(W)),
+            "l"(U + s * (int64_t)(NF * NCELL)), "r"(bytes), "r"(smem_u32(&bar))
+            : "memory");
+      }
     }
     asm volatile(
         "{\n\t.reg .pred p;\nHW_%=:\n\t"
@@ -223,6 +240,25 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
 }
 
+template <bool LATTICE>
+int launch(tb_stream_t s, const double *U, const CUtensorMap &map, int nb, double *dudt,
+           double *amax, int64_t nsub, double dx, double gamma) {
+  static int occ = 0;
+  if (!occ) {
+    cudaFuncSetAttribute(k_hydro_flux<LATTICE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kSmem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hydro_flux<LATTICE>, kThreads,
+                                                      kSmem) != cudaSuccess ||
+        occ < 1)
+      occ = 1;
+  }
+  int64_t blocks = (int64_t)tb::sm_count() * occ;
+  if (blocks > nsub) blocks = nsub;
+  k_hydro_flux<LATTICE><<<(int)blocks, kThreads, kSmem, reinterpret_cast<cudaStream_t>(s)>>>(
+      U, map, nb, dudt, amax, nsub, dx, gamma);
+  return tb::last_error();
+}
+
 }  // namespace
 
 extern "C" int tb_hydro_flux(tb_stream_t s, const double *U, double *dudt, double *amax,
@@ -231,17 +267,22 @@ extern "C" int tb_hydro_flux(tb_stream_t s, const double *U, double *dudt, doubl
     return TB_E_INVALID;
   if (nsub == 0) return TB_OK;
   if (reinterpret_cast<uintptr_t>(U) & 15) return TB_E_INVALID;
-  static int occ = 0;
-  if (!occ) {
-    cudaFuncSetAttribute(k_hydro_flux, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hydro_flux, kThreads, kSmem) !=
-            cudaSuccess ||
-        occ < 1)
-      occ = 1;
-  }
-  int64_t blocks = (int64_t)tb::sm_count() * occ;
-  if (blocks > nsub) blocks = nsub;
-  k_hydro_flux<<<(int)blocks, kThreads, kSmem, reinterpret_cast<cudaStream_t>(s)>>>(
-      U, dudt, amax, nsub, dx, gamma);
-  return tb::last_error();
+  CUtensorMap unused{};
+  return launch<false>(s, U, unused, 0, dudt, amax, nsub, dx, gamma);
+}
+
+extern "C" int tb_hydro_flux_lattice(tb_stream_t s, const double *Up, int64_t n, double *dudt,
+                                     double *amax, double dx, double gamma) {
+  if (!Up || !dudt || !amax || n < 8 || n % 8 || !(dx > 0.0) || !(gamma > 1.0))
+    return TB_E_INVALID;
+  if (reinterpret_cast<uintptr_t>(Up) & 15) return TB_E_INVALID;
+  const uint64_t P = (uint64_t)n + 2 * NG;
+  const uint64_t dims[4] = {P, P, P, (uint64_t)NF};
+  const uint64_t strides[3] = {P * 8, P * P * 8, P * P * P * 8};
+  const uint32_t box[4] = {NT, NT, NT, NF};
+  CUtensorMap map;
+  const int r = tb::encode_tiled(&map, 4, const_cast<double *>(Up), dims, strides, box);
+  if (r != TB_OK) return r;
+  const int nb = (int)(n / NI);
+  return launch<true>(s, Up, map, nb, dudt, amax, (int64_t)nb * nb * nb, dx, gamma);
 }

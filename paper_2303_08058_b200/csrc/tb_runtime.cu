@@ -174,6 +174,37 @@ int sm_count() {
   return v;
 }
 
+int encode_tiled(CUtensorMap *map, int rank, void *base, const uint64_t *dims,
+                 const uint64_t *strides_bytes, const uint32_t *box) {
+  using Fn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                          const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                          const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                          CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Fn enc = nullptr;
+  if (!enc) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    const int r = rc(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (r != TB_OK) return r;
+    if (!p || q != cudaDriverEntryPointSuccess) return TB_E_INVALID;
+    enc = reinterpret_cast<Fn>(p);
+  }
+  cuuint64_t d[5], st[4];
+  cuuint32_t b[5], e[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    b[i] = box[i];
+    e[i] = 1;
+    if (i + 1 < rank) st[i] = strides_bytes[i];
+  }
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)rank, base, d, st, b, e,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS
+             ? TB_OK
+             : TB_E_INVALID;
+}
+
 }  // namespace tb
 
 using namespace tb;

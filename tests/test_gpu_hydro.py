@@ -41,3 +41,24 @@ def test_hydro_flux_uniform_and_conservation_at_c2_size():
         Uu[:, f] = v
     duu, _ = hydro_flux(Uu, 0.1)
     assert (duu == 0).all()
+
+
+@pytest.mark.parametrize("s", [8, 64])
+def test_lattice_tma_variant_equals_ghosted_variant(s):
+    """tb_hydro_flux_lattice (4-D TMA boxes from the periodic-padded global
+    lattice) == tb_hydro_flux on materialised ghosted sub-grids, bit for bit."""
+    from paper_2303_08058_b200 import _native as N
+    from paper_2303_08058_b200.hydro import hydro_flux
+    from paper_2303_08058_b200.star import subgrids_to_lattice
+    I, dx = h.rotating_star(s)
+    want, wa = hydro_flux(torch.from_numpy(h.with_ghosts(I)).cuda(), dx)
+    U = subgrids_to_lattice(torch.from_numpy(I)).cuda()
+    n = U.shape[1]
+    Up = torch.empty((5, n + 4, n + 4, n + 4), dtype=torch.float64, device="cuda")
+    du = torch.empty_like(want)
+    am = torch.empty_like(wa)
+    st = torch.cuda.current_stream().cuda_stream
+    N.call("tb_star_pad", st, U.data_ptr(), n, Up.data_ptr())
+    N.call("tb_hydro_flux_lattice", st, Up.data_ptr(), n, du.data_ptr(), am.data_ptr(), dx,
+           5 / 3)
+    assert torch.equal(du, want) and torch.equal(am, wa)
