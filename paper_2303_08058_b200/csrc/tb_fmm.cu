@@ -8,28 +8,30 @@
 // bit — FMAs and rsqrt are used freely here.
 //
 // Layout (one device workspace, tb_fmm_workspace_bytes):
-//   for level l in [0, L): Mhat_l [N_l^3][22], Loc_l [N_l^3][20] (N_l = 8*2^l,
-//   cells z,y,x with x fastest, one record per cell), Dtab_l [33][912] (l >= 1);
-//   L0part [8][512][20].
+//   for level l in [0, L): Mhat_l [N_l^3][20], Mred_l [N_l^3][18], Loc_l
+//   [N_l^3][20] (N_l = 8*2^l, cells z,y,x with x fastest, one record per cell),
+//   Dtab_l [33][912] (l >= 1); L0part [8][512][20].
 //   Mhat holds the raw Cartesian moments pre-multiplied by the M2L source
-//   coefficient -(-1)^m mult(B)/m! (2 zero pads), so the interaction is a pure
-//   FMA chain; Dtab_l holds, per stencil stage, the derivative tensors of the
-//   27 distinct child offsets (zero for near pairs).
+//   coefficient -(-1)^m mult(B)/m! (M2M input); Mred their traceless
+//   reduction to 16 moments + 2 zero pads (M2L input), so the interaction is
+//   a pure FMA chain; Dtab_l holds, per stencil stage, the derivative tensors
+//   of the 27 distinct child offsets (zero for near pairs).
 //
 // Kernels
-//   k_fmm_up    P2M+M2M, one level per launch: 8 lanes = the 8 children of a
-//               parent; shifted moments are summed by an 8-lane xor-shuffle
-//               reduce-scatter (the warp-level multipole sums).
+//   k_fmm_up    P2M+M2M, one level per launch, one thread per parent: child
+//               offsets are +-h/2 per axis, so the multipole sums are signed
+//               sums of the children (compile-time signs), no shuffles.
 //   k_fmm_m2l   multipole interactions of ALL levels in ONE launch (a CTA per
 //               level-l sub-grid, heaviest level first; level 0 split over 8
 //               CTAs). The interaction stencil is walked as 33 parent-near
-//               offsets P: for each, the 8^3 x 22 source block at 2P is staged
+//               offsets P: for each, the 8^3 x 18 source block at 2P is staged
 //               by one 4-D TMA load (OOB = zero mass: the isolated boundary)
 //               plus a bulk copy of that stage's 27 derivative tensors,
 //               double-buffered on mbarriers; each thread (one target cell)
 //               takes the 8 children of its parent's neighbour P and contracts
 //               their moments with the tensor of its offset (LDS.128 pairs,
-//               84 FMAs, no branch: near pairs have D = 0).
+//               70 FMAs on the traceless reduction, no branch: near pairs
+//               have D = 0).
 //   k_fmm_down  L2L, one level per launch (level 0: sums the 8 partials).
 //   k_fmm_leaf  monopole interactions at the leaves: a 264-point stencil whose
 //               weights 1/|q|, q/|q|^3 depend only on the integer offset q; a
@@ -170,6 +172,27 @@ constexpr auto kL2L = make_l2l();
 constexpr auto kM2M = make_m2m();
 static_assert(kM2L.n == 84 && kL2L.n == 84 && kM2M.n == 84, "term tables");
 
+// Traceless reduction. The derivative tensors of 1/r are traceless
+// (D_{..zz} = -D_{..xx} - D_{..yy}), so (i) a source's zz-containing moments
+// fold into reduced moments (M'xx = Mxx - Mzz, M'xxx = Mxxx - Mxzz, ...), 16
+// instead of 20, and (ii) the local expansions are traceless too, so only
+// their 16 independent components (no zz index pair) are accumulated and the
+// other 4 are rebuilt at the end: 70 FMAs per pair instead of 84.
+constexpr int kRed[16] = {0, 1, 2, 3, 4, 5, 6, 7, 8, 10, 11, 12, 13, 14, 16, 17};
+constexpr Table<84> make_m2l_red() {
+  Table<84> T{};
+  int k = 0;
+  for (int r = 0; r < 16; ++r)
+    for (int q = 0; q < 16; ++q) {
+      const int t = kRed[q], s = kRed[r];
+      if (kComps[t].n + kComps[s].n <= 3) T.v[k++] = Term{t, r, merge(t, s), 1};
+    }
+  T.n = k;
+  return T;
+}
+constexpr auto kM2LRed = make_m2l_red();
+static_assert(kM2LRed.n == 70, "reduced M2L table");
+
 template <typename F, int... K>
 __device__ __forceinline__ void unroll_impl(F &&f, std::integer_sequence<int, K...>) {
   (f(std::integral_constant<int, K>{}), ...);
@@ -264,31 +287,21 @@ __constant__ PTab c_pnear = make_ptab();
 // (1/|q|, qx/|q|^3, qy/|q|^3, qz/|q|^3); q = 0 -> 0 (the self term).
 __constant__ double c_w[11 * 11 * 11][4];
 
-// Per-component M2L source scale for runtime component indices.
-struct ScaleTab {
-  double v[NC];
-};
-constexpr ScaleTab make_scales() {
-  ScaleTab T{};
-  for (int k = 0; k < NC; ++k) T.v[k] = m2l_scale(k);
-  return T;
-}
-__constant__ ScaleTab c_m2lscale = make_scales();
-
-// Moment records are padded to 22 doubles (176 B): the 4 cells a warp reads
-// per LDS.128 (stride 2 cells = 22 chunks) land on distinct bank groups.
-constexpr int MS = 22;
+// Reduced moment records (the M2L's source) hold 16 moments padded to 18
+// doubles (144 B): the 4 cells a warp reads per LDS.128 (stride 2 cells = 18
+// chunks) land on distinct bank groups. Raw records ([N^3][20]) feed M2M.
+constexpr int MS = 18;
 // Per-stage D table: the 27 offsets e = o - c + 1 in {0,1,2}^3 at 16-byte
 // chunk strides 17 / 50 / 156 (distinct mod 8 for the 8 octants of a warp).
 constexpr int kDX = 17, kDY = 50, kDZ = 156;
 constexpr int kDChunks = 2 * kDZ + 2 * kDY + 2 * kDX + NC / 2;   // 456
 constexpr int kDStage = 2 * kDChunks;                            // 912 doubles
-constexpr int kMStage = 512 * MS;                                // 11264 doubles
-constexpr int kStage = kMStage + kDStage;                        // 97,408 B
+constexpr int kMStage = 512 * MS;                                // 9216 doubles
+constexpr int kStage = kMStage + kDStage;                        // 81,024 B
 constexpr uint32_t kMBytes = kMStage * 8, kDBytes = kDStage * 8;
 
 struct Params {
-  CUtensorMap maps[kMaxLevel];     // level l moment records, 4-D {22,N,N,N}
+  CUtensorMap maps[kMaxLevel];     // level l reduced moment records, 4-D {18,N,N,N}
   double *Loc[kMaxLevel];          // [N^3][20]
   const double *Dtab[kMaxLevel];   // [33][912], levels >= 1
   double *L0part;                  // [8][512][20]
@@ -296,91 +309,90 @@ struct Params {
 };
 
 // ---------------------------------------------------------------- upward
-// 8-lane reduce-scatter of v[20] (xor 4, 2, 1): lane c ends up owning
-// components [first, first + cnt) in out[].
-__device__ __forceinline__ void reduce_scatter8(const double (&v)[NC], int c, double (&out)[3],
-                                                int &first, int &cnt) {
-  const bool b2 = c & 4, b1 = c & 2, b0 = c & 1;
-  double w[10], x[5];
-#pragma unroll
-  for (int k = 0; k < 10; ++k) {
-    const double send = b2 ? v[k] : v[10 + k];
-    const double keep = b2 ? v[10 + k] : v[k];
-    w[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-  }
-#pragma unroll
-  for (int k = 0; k < 5; ++k) {
-    const double send = b1 ? w[k] : w[5 + k];
-    const double keep = b1 ? w[5 + k] : w[k];
-    x[k] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-  }
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    const double hi = k + 3 < 5 ? x[k + 3] : 0.0;
-    const double send = b0 ? x[k] : hi;
-    const double keep = b0 ? hi : x[k];
-    out[k] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
-  }
-  first = (b2 ? 10 : 0) + (b1 ? 5 : 0) + (b0 ? 3 : 0);
-  cnt = b0 ? 2 : 3;
+// One thread per parent cell. Child c sits at d = (s_x, s_y, s_z) h/2 from
+// the parent's centre (s_a = 2 c_a - 1), so every monomial d^b is a
+// compile-time sign times (h/2)^|b|: for leaf children (monopoles) each
+// moment is a signed sum of the 8 child masses; for finer-level children the
+// exact M2M shift is 84 FMAs per child with folded signs. The thread writes
+// its parent's raw (pre-scaled) record and the traceless-reduced record.
+template <int C>
+constexpr double child_sign(int b) {
+  double v = 1.0;
+  for (int q = 0; q < kComps[b].n; ++q) v *= ((C >> kComps[b].a[q]) & 1) ? 1.0 : -1.0;
+  return v;
 }
 
-// Parents at lattice Np from their 8 children: leaves (rho) or a finer
-// level's moment records. 8 lanes = the children of one parent.
 __global__ void __launch_bounds__(256) k_fmm_up(const double *__restrict__ rho,
                                                 const double *__restrict__ child,
-                                                double *__restrict__ parent, int Np,
+                                                double *__restrict__ parent,
+                                                double *__restrict__ parent_red, int Np,
                                                 double hc) {
-  const int lane = threadIdx.x & 31, c = lane & 7, g = lane >> 3;
   const int64_t npar = (int64_t)Np * Np * Np;
-  const int64_t pidx = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 4 + g;
-  const bool valid = pidx < npar;
-  const int64_t pp = valid ? pidx : 0;
-  const int px = (int)(pp % Np), py = (int)((pp / Np) % Np), pz = (int)(pp / ((int64_t)Np * Np));
-  const int cx = c & 1, cy = (c >> 1) & 1, cz = c >> 2;
+  const int64_t pidx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pidx >= npar) return;
+  const int px = (int)(pidx % Np), py = (int)((pidx / Np) % Np),
+            pz = (int)(pidx / ((int64_t)Np * Np));
   const int Nc = 2 * Np;
-  const int64_t cf = ((int64_t)(2 * pz + cz) * Nc + (2 * py + cy)) * Nc + (2 * px + cx);
-  double mono[NC];
-  monomials<false>((cx - 0.5) * hc, (cy - 0.5) * hc, (cz - 0.5) * hc, mono);
-  double v[NC];
+  const double h2 = 0.5 * hc;
+  const double hp[4] = {1.0, h2, h2 * h2, h2 * h2 * h2};
+  double M[NC];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) M[k] = 0.0;
   if (rho) {
-    const double m = valid ? __ldg(rho + cf) * (hc * hc * hc) : 0.0;
-    unroll<NC>([&](auto K) { v[K] = m * mono[K]; });
+    const double vol = hc * hc * hc;
+    double m[8];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {      // r = (cz, cy); x pair by one 16-B load
+      const int cy = r & 1, cz = r >> 1;
+      const double2 v = __ldg(reinterpret_cast<const double2 *>(
+          rho + ((int64_t)(2 * pz + cz) * Nc + (2 * py + cy)) * Nc + 2 * px));
+      m[2 * r] = v.x * vol;
+      m[2 * r + 1] = v.y * vol;
+    }
+    unroll<8>([&](auto C) {
+      unroll<NC>([&](auto K) {
+        constexpr double sg = child_sign<decltype(C)::value>(K);
+        M[K] = sg > 0 ? M[K] + m[C] : M[K] - m[C];
+      });
+    });
+    unroll<NC>([&](auto K) { M[K] = M[K] * hp[kComps[K].n]; });
   } else {
-    double Mc[NC];
-    const double2 *rec = reinterpret_cast<const double2 *>(child + cf * MS);
+    unroll<8>([&](auto C) {
+      constexpr int Cv = decltype(C)::value;
+      constexpr int cx = Cv & 1, cy = (Cv >> 1) & 1, cz = Cv >> 2;
+      const double2 *rec = reinterpret_cast<const double2 *>(
+          child + (((int64_t)(2 * pz + cz) * Nc + (2 * py + cy)) * Nc + (2 * px + cx)) * NC);
+      double Mc[NC];
 #pragma unroll
-    for (int k = 0; k < NC / 2; ++k) {
-      const double2 a = valid ? __ldg(rec + k) : make_double2(0.0, 0.0);
-      Mc[2 * k] = a.x;
-      Mc[2 * k + 1] = a.y;
-    }
-    unroll<NC>([&](auto K) {
-      constexpr double inv = 1.0 / m2l_scale(K);
-      Mc[K] = Mc[K] * inv;
-      v[K] = 0.0;
-    });
-    unroll<kM2M.n>([&](auto E) {
-      constexpr Term T = kM2M.v[E];
-      if constexpr (T.c == 1)
-        v[T.t] = fma(Mc[T.s], mono[T.b], v[T.t]);
-      else
-        v[T.t] = fma(double(T.c) * Mc[T.s], mono[T.b], v[T.t]);
+      for (int k = 0; k < NC / 2; ++k) {
+        const double2 a = __ldg(rec + k);
+        Mc[2 * k] = a.x;
+        Mc[2 * k + 1] = a.y;
+      }
+      unroll<kM2M.n>([&](auto E) {
+        constexpr Term T = kM2M.v[E];
+        // child raw records are pre-scaled: undo the source scale here
+        constexpr double coef = T.c * child_sign<decltype(C)::value>(T.b) / m2l_scale(T.s);
+        M[T.t] = fma(coef * Mc[T.s], hp[kComps[T.b].n], M[T.t]);
+      });
     });
   }
-  double out[3];
-  int first, cnt;
-  reduce_scatter8(v, c, out, first, cnt);
-  if (valid) {
-    double *rec = parent + pidx * MS;
+  unroll<NC>([&](auto K) {
+    constexpr double sc = m2l_scale(K);
+    M[K] = M[K] * sc;
+  });
+  double2 *raw = reinterpret_cast<double2 *>(parent + pidx * NC);
 #pragma unroll
-    for (int k = 0; k < 3; ++k)
-      if (k < cnt) rec[first + k] = out[k] * c_m2lscale.v[first + k];
-    if (c == 0) {
-      rec[NC] = 0.0;
-      rec[NC + 1] = 0.0;
-    }
-  }
+  for (int k = 0; k < NC / 2; ++k) raw[k] = make_double2(M[2 * k], M[2 * k + 1]);
+  // traceless reduction (see kRed): fold the zz-containing moments
+  const double red[MS] = {M[0],          M[1],          M[2],          M[3],
+                          M[4] - M[9],   M[5],          M[6],          M[7] - M[9],
+                          M[8],          M[10] - M[15], M[11] - M[18], M[12] - M[19],
+                          M[13] - M[15], M[14],         M[16] - M[18], M[17] - M[19],
+                          0.0,           0.0};
+  double2 *rd = reinterpret_cast<double2 *>(parent_red + pidx * MS);
+#pragma unroll
+  for (int k = 0; k < MS / 2; ++k) rd[k] = make_double2(red[2 * k], red[2 * k + 1]);
 }
 
 // --------------------------------------------------------- M2L D tables
@@ -410,7 +422,7 @@ __global__ void __launch_bounds__(32) k_fmm_dtab(const TabPtrs T) {
 
 // ------------------------------------------------------------------- M2L
 constexpr int kM2LThreads = 512;
-constexpr int kM2LSmem = 2 * kStage * 8;          // 194,816 B
+constexpr int kM2LSmem = 2 * kStage * 8;          // 162,048 B
 
 __device__ __forceinline__ void load20(const double *p, double (&v)[NC]) {
   const double2 *q = reinterpret_cast<const double2 *>(p);
@@ -422,12 +434,31 @@ __device__ __forceinline__ void load20(const double *p, double (&v)[NC]) {
   }
 }
 
-__device__ __forceinline__ void contract(double (&L)[NC], const double (&M)[NC],
+__device__ __forceinline__ void load16(const double *p, double (&v)[16]) {
+  const double2 *q = reinterpret_cast<const double2 *>(p);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const double2 a = q[k];
+    v[2 * k] = a.x;
+    v[2 * k + 1] = a.y;
+  }
+}
+
+// L (independent components) += reduced source moments x D: 70 FMAs.
+__device__ __forceinline__ void contract(double (&L)[NC], const double (&M)[16],
                                          const double (&D)[NC]) {
-  unroll<kM2L.n>([&](auto E) {
-    constexpr Term T = kM2L.v[E];
+  unroll<kM2LRed.n>([&](auto E) {
+    constexpr Term T = kM2LRed.v[E];
     L[T.t] = fma(M[T.s], D[T.b], L[T.t]);
   });
+}
+
+// Rebuild the 4 dependent components of a traceless local expansion.
+__device__ __forceinline__ void untrace(double (&L)[NC]) {
+  L[9] = -(L[4] + L[7]);
+  L[15] = -(L[10] + L[13]);
+  L[18] = -(L[11] + L[16]);
+  L[19] = -(L[12] + L[17]);
 }
 
 __device__ __forceinline__ void issue_stage(const Params &P, int lev, double *dst,
@@ -500,12 +531,13 @@ __global__ void __launch_bounds__(kM2LThreads, 1) k_fmm_m2l(const __grid_constan
       for (int jx = 0; jx < 8; ++jx) {
         const int qx = lx - jx, qy = ly - jy, qz = lz - jz;
         if (qx * qx + qy * qy + qz * qz > 4) {
-          double D[NC], M[NC];
+          double D[NC], M[16];
           d_tensor(qx * h, qy * h, qz * h, D);
-          load20(sm + ((jz * 8 + jy) * 8 + jx) * MS, M);
+          load16(sm + ((jz * 8 + jy) * 8 + jx) * MS, M);
           contract(L, M, D);
         }
       }
+    untrace(L);
     double2 *dst = reinterpret_cast<double2 *>(P.L0part + ((size_t)job * 512 +
                                                             (lz * 8 + ly) * 8 + lx) * NC);
 #pragma unroll
@@ -532,8 +564,8 @@ __global__ void __launch_bounds__(kM2LThreads, 1) k_fmm_m2l(const __grid_constan
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const int cx = c & 1, cy = (c >> 1) & 1, cz = c >> 2;
-      double M[NC], D[NC];
-      load20(Ms + (cbase + (cz * 8 + cy) * 8 + cx) * MS, M);
+      double M[16], D[NC];
+      load16(Ms + (cbase + (cz * 8 + cy) * 8 + cx) * MS, M);
       load20(Ds + 2 * (dbase - cx * kDX - cy * kDY - cz * kDZ), D);
       contract(L, M, D);
     }
@@ -543,6 +575,7 @@ __global__ void __launch_bounds__(kM2LThreads, 1) k_fmm_m2l(const __grid_constan
       issue_stage(P, lev, sm + buf * kStage, &bar[buf], k + 2, X0, Y0, Z0);
     }
   }
+  untrace(L);
   const int N = 8 << lev;
   double2 *dst = reinterpret_cast<double2 *>(
       P.Loc[lev] + (((size_t)(Z0 + lz) * N + (Y0 + ly)) * N + (X0 + lx)) * NC);
@@ -683,7 +716,8 @@ __global__ void __launch_bounds__(kLeafThreads, 2)
 
 // ------------------------------------------------------------------ host
 struct Layout {
-  size_t M[kMaxLevel], Loc[kMaxLevel], Dtab[kMaxLevel], L0part, total;   // byte offsets
+  size_t M[kMaxLevel], Mred[kMaxLevel], Loc[kMaxLevel], Dtab[kMaxLevel], L0part,
+      total;   // byte offsets
 };
 
 Layout layout(int L) {
@@ -692,6 +726,8 @@ Layout layout(int L) {
   for (int l = 0; l < L; ++l) {
     const size_t n = (size_t)(8 << l) * (8 << l) * (8 << l);
     lo.M[l] = off;
+    off += n * NC * 8;
+    lo.Mred[l] = off;
     off += n * MS * 8;
     lo.Loc[l] = off;
     off += n * NC * 8;
@@ -740,7 +776,7 @@ int make_params(int L, double *work, Params *P) {
   P->L = L;
   P->L0part = reinterpret_cast<double *>(base + lo.L0part);
   for (int l = 0; l < L; ++l) {
-    double *M = reinterpret_cast<double *>(base + lo.M[l]);
+    double *M = reinterpret_cast<double *>(base + lo.Mred[l]);
     P->Loc[l] = reinterpret_cast<double *>(base + lo.Loc[l]);
     P->Dtab[l] = reinterpret_cast<const double *>(base + lo.Dtab[l]);
     const uint64_t N = (uint64_t)(8 << l);
@@ -772,13 +808,13 @@ int tb_fmm_upward(tb_stream_t s, int max_level, const double *rho, double *work)
   for (int l = max_level - 1; l >= 0; --l) {
     const int Np = 8 << l;
     const int64_t npar = (int64_t)Np * Np * Np;
-    const int64_t blocks = (npar + 31) / 32;   // 8 warps x 4 parents
+    const int64_t blocks = (npar + 255) / 256;   // one thread per parent
     const double hc = 1.0 / double(2 * Np);
     const double *child =
         l == max_level - 1 ? nullptr : reinterpret_cast<const double *>(base + lo.M[l + 1]);
     k_fmm_up<<<(unsigned)blocks, 256, 0, strm(s)>>>(
         l == max_level - 1 ? rho : nullptr, child, reinterpret_cast<double *>(base + lo.M[l]),
-        Np, hc);
+        reinterpret_cast<double *>(base + lo.Mred[l]), Np, hc);
   }
   return tb::last_error();
 }

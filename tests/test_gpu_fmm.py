@@ -56,15 +56,21 @@ def test_fmm_upward_moments_vs_oracle():
     scale = np.array([(1.0 if len(B) % 2 else -1.0) * f.mult(B) / math.factorial(len(B))
                       for B in f.COMPS])
     off = 0
-    for lev in range(L):                        # workspace: [M_l [n][22], Loc_l [n][20], Dtab_l]
+    for lev in range(L):      # workspace: [Mhat_l [n][20], Mred_l [n][18], Loc_l [n][20], Dtab_l]
         n = (8 << lev) ** 3
-        rec = work[off:off + 22 * n].reshape(8 << lev, 8 << lev, 8 << lev, 22)
-        got = np.moveaxis(rec[..., :20], -1, 0)
-        assert np.all(rec[..., 20:] == 0.0)
+        got = np.moveaxis(work[off:off + 20 * n].reshape((8 << lev,) * 3 + (20,)), -1, 0)
         want = Ms[lev] * scale[:, None, None, None]
         mag = np.abs(want).max(axis=(1, 2, 3), keepdims=True)
         assert np.all(np.abs(got - want) <= 1e-13 * mag + 1e-300), lev
-        off += 42 * n + (33 * 912 if lev else 0)
+        red = work[off + 20 * n:off + 38 * n].reshape(n, 18)
+        w = want.reshape(20, n)
+        # traceless reduction: zz-containing moments folded into xx, yy, xxx, ...
+        exp = np.stack([w[0], w[1], w[2], w[3], w[4] - w[9], w[5], w[6], w[7] - w[9], w[8],
+                        w[10] - w[15], w[11] - w[18], w[12] - w[19], w[13] - w[15], w[14],
+                        w[16] - w[18], w[17] - w[19]], axis=1)
+        assert np.all(np.abs(red[:, :16] - exp) <= 1e-13 * np.abs(w).max() + 1e-300), lev
+        assert np.all(red[:, 16:] == 0.0)
+        off += 58 * n + (33 * 912 if lev else 0)
 
 
 @pytest.mark.parametrize("L", [3, 4])
