@@ -346,6 +346,34 @@ def north_star_kernels(dev, reps=20):
     return out
 
 
+def hydro_machine_ablation(subgrids=512, steps=8, repeats=3):
+    """The paper's experiment shape on the north_star hydro kernel (PAPER.md:
+    762-782: per-sub-grid hydro tasks, aggregated launches): the native
+    machine with K6 tasks (tb_machine_run_hydro; parity unpinned, bit-exact
+    to oracle/hydro_oracle.py euler_step), 32 executors x max 8, 8 workers,
+    POLLING vs HOSTTASK vs FENCE; median of `repeats` of the mean step time
+    over steps 3..N."""
+    from paper_2303_08058_b200.bridge import IntegrationMode
+    from paper_2303_08058_b200.hydro import rotating_star
+    from paper_2303_08058_b200.native_machine import run_native_hydro
+    I = rotating_star(subgrids)[0].numpy()
+    out = {"config": f"native machine, hydro (K6) tasks, {subgrids} sub-grids x {steps} "
+                     f"steps, 8 workers, 32 executors, max 8 aggregated, median of {repeats}"}
+    finals = set()
+    for mode in IntegrationMode:
+        ms = []
+        for _ in range(repeats):
+            per, U = run_native_hydro(I, steps, workers=8, executors=32, max_agg=8, mode=mode)
+            ms.append(statistics.fmean(m.wall_ms for m in per[2:]))
+            finals.add(hash(U.tobytes()))
+        out[f"{mode.value}_ms_per_step"] = statistics.median(ms)
+        out[f"{mode.value}_mean_batch"] = per[-1].mean_batch
+    out["speedup_polling_vs_fence"] = out["fence_ms_per_step"] / out["polling_ms_per_step"]
+    out["speedup_hosttask_vs_fence"] = out["fence_ms_per_step"] / out["hosttask_ms_per_step"]
+    out["results_identical"] = len(finals) == 1
+    return out
+
+
 def run_reference_arm(args, workload_key, rank, world):
     if rank != 0:
         return 0
@@ -558,6 +586,7 @@ def main(argv=None):
         ablation = None
         if not args.no_ablation:
             ablation = machine_ablation()
+            ablation["hydro_machine"] = hydro_machine_ablation()
         kernels = None
         if not args.no_kernels:
             kernels = north_star_kernels(dev)

@@ -342,6 +342,25 @@ typedef struct {             /* StepMetrics (src/miniapp.py:103-113)         */
 int tb_machine_run(const tb_machine_config *cfg, double *checksum,
                    tb_machine_step *steps_out, double *cells_out);
 
+/* One aggregated hydro batch (the Octo-Tiger use of src/executors.py:257-284,
+ * PAPER.md:762-773): H2D(din <- hin: nsub ghosted sub-grids [5][12^3]) ;
+ * K6 ; D2H(hout <- dout: dU/dt [nsub][5][512] then amax [nsub]) ; record
+ * *done. din/dout device, hin/hout pinned host. */
+int tb_agg_launch_hydro(tb_stream_t s, double *din, const double *hin, int64_t nsub,
+                        double *dout, double *hout, double dx, double gamma,
+                        tb_event_t *done);
+
+/* The same machine on the north_star's hydro kernel (PARITY UNPINNED; spec
+ * oracle/hydro_oracle.py euler_step): per step, one task per task_subgrids
+ * sub-grids builds their periodic ghost layers on the host and schedules a
+ * K6 request on its executor (aggregated up to max_agg per launch, completed
+ * by cfg->mode); then dt = cfl*dx/max(amax) and U += dt*dU/dt (host tasks).
+ * subgrids must be a cube n^3 (sub-grid order x fastest); chains,
+ * kernels_per_chain, inject_barriers, barrier_elision are ignored.
+ * U_in/U_out: [subgrids][5][8][8][8]; piece = exact sum of all rho. */
+int tb_machine_run_hydro(const tb_machine_config *cfg, const double *U_in, double *U_out,
+                         double cfl, double gamma, tb_machine_step *steps_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -177,3 +177,14 @@ def with_ghosts(interior: np.ndarray):
                                                   by * NI:by * NI + NT,
                                                   bx * NI:bx * NI + NT]
     return out
+
+
+def euler_step(I: np.ndarray, gamma: float = 5.0 / 3.0, cfl: float = 0.4):
+    """One forward-Euler hydro step of the periodic sub-grid lattice (the
+    native machine's hydro workload, tb_machine_run_hydro): dt =
+    (cfl * dx) / max(amax); I' = I + dt * dU/dt. Returns (I', dt)."""
+    n = lattice_shape(I.shape[0])
+    dx = 1.0 / (n * NI)
+    du, amax = hydro_flux(with_ghosts(I), dx, gamma)
+    dt = (cfl * dx) / amax.max()
+    return I + dt * du, dt

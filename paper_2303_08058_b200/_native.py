@@ -137,6 +137,8 @@ SIGNATURES = {
     "tb_htq_close": [_u64],
     "tb_htq_destroy": [_u64],
     "tb_machine_run": [_vp, _vp, _vp, _vp],
+    "tb_agg_launch_hydro": [_u64, _vp, _vp, _i64, _vp, _vp, _dbl, _dbl, _pu64],
+    "tb_machine_run_hydro": [_vp, _vp, _vp, _dbl, _dbl, _vp],
     "tb_ipc_get_handle": [_vp, _vp, _pu64],
     "tb_ipc_open_handle": [_vp, _pvp],
     "tb_ipc_close": [_vp],
@@ -157,7 +159,7 @@ SIGNATURES = {
 BLOCKING = {"tb_init", "tb_device_sync", "tb_stream_sync", "tb_event_wait",
             "tb_htq_next", "tb_htq_destroy", "tb_malloc", "tb_free",
             "tb_host_alloc", "tb_host_free", "tb_stream_destroy",
-            "tb_memcpy_h2d", "tb_memcpy_d2h", "tb_poll_drain", "tb_machine_run",
+            "tb_memcpy_h2d", "tb_memcpy_d2h", "tb_poll_drain", "tb_machine_run", "tb_machine_run_hydro",
             "tb_fp64_probe"}
 
 _lock = threading.Lock()

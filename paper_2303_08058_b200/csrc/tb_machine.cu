@@ -308,6 +308,9 @@ class HostTasks {
 // ---------------------------------------------------------------- machine --
 constexpr int kCells = TB_CELLS;
 constexpr int kFace = TB_FACE;
+constexpr int64_t kGhosted = 5 * 1728;      // one ghosted hydro sub-grid [5][12^3]
+constexpr int64_t kInterior = 5 * 512;      // its dU/dt [5][8^3]
+constexpr int64_t kHydroOut = kInterior + 1;   // + amax
 
 struct Machine;
 struct SubTask;
@@ -382,6 +385,13 @@ struct Machine {
   std::atomic<int64_t> launches{0}, transfers{0}, event_waits{0}, full{0}, idle{0},
       members{0}, kernels{0};
   int error = TB_OK;
+  // hydro workload (tb_machine_run_hydro)
+  bool hydro = false;
+  int64_t nb = 0;                  // sub-grids per lattice edge
+  double dx = 0.0, gamma = 0.0, dt = 0.0;
+  std::vector<double> U;           // [S][5][512] interior state
+  std::vector<double> dudt;        // [S][5][512]
+  std::vector<double> amax;        // [S]
 };
 
 Staging *staging_alloc(Machine *m, size_t bytes) {
@@ -400,6 +410,11 @@ Staging *staging_alloc(Machine *m, size_t bytes) {
   std::lock_guard<std::mutex> g(m->staging_mu);
   m->staging_all.push_back(s);
   return s;
+}
+
+size_t hydro_staging_bytes(const Machine *m) {
+  return sizeof(double) * (size_t)(m->cfg.max_agg * m->cfg.task_subgrids) *
+         (size_t)(kGhosted + kHydroOut);
 }
 
 void staging_release(Machine *m, Staging *s) {
@@ -427,20 +442,36 @@ void bridge(Machine *m, Executor *ex, cudaEvent_t ev, Task cont) {
 }
 
 void resume_task(void *p);
+void hydro_resume(void *p);
 
 void batch_done(void *p) {   // AggregationExecutor finish (src/executors.py:286-301)
   Batch *b = static_cast<Batch *>(p);
   Machine *m = b->ex->m;
-  int64_t off = 0;
-  for (const Req &r : b->members) {
-    std::memcpy(r.dst, b->staging->host + off, sizeof(double) * r.n);
-    off += r.n;
+  if (m->hydro) {   // scatter each member's dU/dt rows and amax entries
+    int64_t total = 0;
+    for (const Req &r : b->members) total += r.n;
+    const int64_t nsub = total / kGhosted;
+    const double *du = b->staging->host + total, *am = du + nsub * kInterior;
+    int64_t o = 0;
+    for (const Req &r : b->members) {
+      const int64_t k = r.n / kGhosted;
+      std::memcpy(r.dst, du + o * kInterior, sizeof(double) * k * kInterior);
+      std::memcpy(r.dst + k * kInterior, am + o, sizeof(double) * k);
+      o += k;
+    }
+  } else {
+    int64_t off = 0;
+    for (const Req &r : b->members) {
+      std::memcpy(r.dst, b->staging->host + off, sizeof(double) * r.n);
+      off += r.n;
+    }
   }
   staging_release(m, b->staging);
   m->launches.fetch_add(1, std::memory_order_relaxed);
   m->members.fetch_add((int64_t)b->members.size(), std::memory_order_relaxed);
   (b->idle ? m->idle : m->full).fetch_add(1, std::memory_order_relaxed);
-  for (const Req &r : b->members) m->pool->push(Task{resume_task, r.task});
+  for (const Req &r : b->members)
+    m->pool->push(Task{m->hydro ? hydro_resume : resume_task, r.task});
   batch_release(b);
 }
 
@@ -450,7 +481,10 @@ void launch(Batch *b, bool idle) {   // src/executors.py:257-284 as one launch
   b->idle = idle;
   int64_t total = 0;
   for (const Req &r : b->members) total += r.n;
-  const size_t bytes = sizeof(double) * total;
+  // hydro: staging = [ghosted inputs | dU/dt + amax outputs], one size class
+  // (a full batch) so buffers are always reused; the ring keeps the
+  // reference BufferPool's exact-size buckets (src/executors.py:86-121)
+  const size_t bytes = m->hydro ? hydro_staging_bytes(m) : sizeof(double) * total;
   b->staging = staging_alloc(m, bytes);
   int64_t off = 0;
   for (const Req &r : b->members) {
@@ -459,7 +493,12 @@ void launch(Batch *b, bool idle) {   // src/executors.py:257-284 as one launch
   }
   tb_event_t ev = 0;
   const int do_barrier = m->cfg.inject_barriers && !m->cfg.barrier_elision;
-  const int rc = tb_agg_launch(reinterpret_cast<tb_stream_t>(ex->stream), TB_OP_KIND, b->kind,
+  const int rc =
+      m->hydro ? tb_agg_launch_hydro(reinterpret_cast<tb_stream_t>(ex->stream), b->staging->dev,
+                                     b->staging->host, total / kGhosted,
+                                     b->staging->dev + total, b->staging->host + total, m->dx,
+                                     m->gamma, &ev)
+               : tb_agg_launch(reinterpret_cast<tb_stream_t>(ex->stream), TB_OP_KIND, b->kind,
                                0.0, 0.0, b->staging->dev, b->staging->host, bytes, do_barrier,
                                &ev);
   if (rc != TB_OK) m->error = rc;
@@ -574,6 +613,69 @@ void resume_task(void *p) {   // next round, or write-back + post-process
     std::lock_guard<std::mutex> g(m->done_mu);
     m->done_cv.notify_all();
   }
+}
+
+// ------------------------------------------------------- hydro workload --
+// Host ghost exchange: sub-grid g's [5][12][12][12] block from the periodic
+// lattice of interiors (what Octo-Tiger's HPX channels provide), row by row.
+void ghost_fill(const Machine *m, int64_t g, double *out) {
+  const int64_t n = m->nb, N = 8 * n;
+  const int64_t bx = g % n, by = (g / n) % n, bz = g / (n * n);
+  for (int f = 0; f < 5; ++f)
+    for (int k = 0; k < 12; ++k) {
+      const int64_t Z = (8 * bz - 2 + k + N) % N;
+      for (int j = 0; j < 12; ++j) {
+        const int64_t Y = (8 * by - 2 + j + N) % N;
+        double *row = out + ((f * 12 + k) * 12 + j) * 12;
+        const int64_t sb = ((Z / 8) * n + Y / 8) * n;
+        const int64_t lrow = ((int64_t)f * 8 + Z % 8) * 64 + (Y % 8) * 8;
+        // x: 2 ghosts from the left neighbour, 8 interior, 2 from the right
+        const int64_t xl = (bx - 1 + n) % n, xr = (bx + 1) % n;
+        const double *L = m->U.data() + (sb + xl) * kInterior + lrow;
+        const double *C = m->U.data() + (sb + bx) * kInterior + lrow;
+        const double *R = m->U.data() + (sb + xr) * kInterior + lrow;
+        row[0] = L[6];
+        row[1] = L[7];
+        std::memcpy(row + 2, C, 8 * sizeof(double));
+        row[10] = R[0];
+        row[11] = R[1];
+      }
+    }
+}
+
+void hydro_done(Machine *m) {
+  if (m->remaining.fetch_sub(1) == 1) {
+    std::lock_guard<std::mutex> g(m->done_mu);
+    m->done_cv.notify_all();
+  }
+}
+
+void hydro_resume(void *p) {   // outputs landed in t->b: keep dU/dt and amax
+  SubTask *t = static_cast<SubTask *>(p);
+  Machine *m = t->m;
+  std::memcpy(m->dudt.data() + t->lo * kInterior, t->b.data(),
+              sizeof(double) * t->n * kInterior);
+  std::memcpy(m->amax.data() + t->lo, t->b.data() + t->n * kInterior, sizeof(double) * t->n);
+  hydro_done(m);
+}
+
+void hydro_start(void *p) {    // ghost exchange + one K6 request
+  SubTask *t = static_cast<SubTask *>(p);
+  for (int64_t k = 0; k < t->n; ++k) ghost_fill(t->m, t->lo + k, t->a.data() + k * kGhosted);
+  schedule(t->ex, 0, t->a.data(), t->b.data(), t->n * kGhosted, t);
+}
+
+void hydro_update(void *p) {   // U += dt * dU/dt (two roundings, as the oracle)
+  SubTask *t = static_cast<SubTask *>(p);
+  Machine *m = t->m;
+  double *u = m->U.data() + t->lo * kInterior;
+  const double *du = m->dudt.data() + t->lo * kInterior;
+  const double dt = m->dt;
+  for (int64_t i = 0; i < t->n * kInterior; ++i) {
+    const volatile double inc = dt * du[i];   // no contraction into an FMA
+    u[i] = u[i] + inc;
+  }
+  hydro_done(m);
 }
 
 // exact sum (== math.fsum): 32-bit digits in int64 limbs, half-even rounding
@@ -733,6 +835,104 @@ extern "C" int tb_machine_run(const tb_machine_config *cfg_in, double *checksum,
     cudaFreeHost(s->host);
     cudaFree(s->dev);
     delete s;
+  }
+  const int err = tb::rc(cudaGetLastError());
+  return m.error != TB_OK ? m.error : err;
+}
+
+extern "C" int tb_machine_run_hydro(const tb_machine_config *cfg_in, const double *U_in,
+                                    double *U_out, double cfl, double gamma,
+                                    tb_machine_step *steps_out) {
+  if (!cfg_in || !U_in || !(cfl > 0.0) || !(gamma > 1.0)) return TB_E_INVALID;
+  const tb_machine_config &c = *cfg_in;
+  int64_t nb = 1;
+  while (nb * nb * nb < c.subgrids) ++nb;
+  if (c.subgrids < 1 || nb * nb * nb != c.subgrids || c.steps < 0 || c.workers < 1 ||
+      c.executors < 1 || c.max_agg < 1 || c.task_subgrids < 1 || c.mode < TB_MODE_POLLING ||
+      c.mode > TB_MODE_FENCE)
+    return TB_E_INVALID;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  Machine m;
+  m.cfg = c;
+  m.hydro = true;
+  m.nb = nb;
+  m.dx = 1.0 / (8.0 * (double)nb);
+  m.gamma = gamma;
+  const int64_t S = c.subgrids;
+  m.U.assign(U_in, U_in + S * kInterior);
+  m.dudt.resize(S * kInterior);
+  m.amax.resize(S);
+  m.pool.reset(new Pool((int)c.workers, dev, 1234));
+  m.poller.reset(new Poller(m.pool.get()));
+  if (c.mode == TB_MODE_POLLING) m.pool->set_idle_hook(&Poller::hook, m.poller.get());
+  m.hosttasks.reset(new HostTasks(m.pool.get(), (int)std::max<int64_t>(1, c.hosttask_threads),
+                                  dev, 4));
+  for (int64_t e = 0; e < c.executors; ++e) {
+    auto ex = std::make_unique<Executor>();
+    ex->m = &m;
+    ex->id = (int)e;
+    cudaStreamCreateWithFlags(&ex->stream, cudaStreamNonBlocking);
+    m.execs.push_back(std::move(ex));
+  }
+  for (int64_t lo = 0; lo < S; lo += c.task_subgrids) {
+    auto t = std::make_unique<SubTask>();
+    t->m = &m;
+    t->lo = lo;
+    t->n = std::min<int64_t>(c.task_subgrids, S - lo);
+    t->ex = m.execs[(size_t)((lo / c.task_subgrids) % c.executors)].get();
+    t->a.resize(t->n * kGhosted);
+    t->b.resize(t->n * kHydroOut);
+    m.tasks.push_back(std::move(t));
+  }
+  {  // pre-allocate the pinned/device staging pool (two full batches per stream)
+    std::vector<Staging *> warm;
+    for (int64_t i = 0; i < 2 * c.executors; ++i) warm.push_back(staging_alloc(&m, hydro_staging_bytes(&m)));
+    for (Staging *st : warm) staging_release(&m, st);
+  }
+  std::vector<double> rho(S * 512);
+  for (int64_t step = 0; step < c.steps; ++step) {
+    const int64_t k0 = m.kernels, t0n = m.transfers, w0 = m.event_waits, f0 = m.full,
+                  i0 = m.idle, mb0 = m.members;
+    const auto t0 = Clock::now();
+    for (int phase = 0; phase < 2; ++phase) {   // fluxes, then the update
+      m.remaining.store((int64_t)m.tasks.size());
+      for (auto &t : m.tasks) m.pool->push(Task{phase ? hydro_update : hydro_start, t.get()});
+      std::unique_lock<std::mutex> lk(m.done_mu);
+      m.done_cv.wait(lk, [&] { return m.remaining.load() == 0; });
+      if (phase == 0) {
+        double am = m.amax[0];
+        for (int64_t g = 1; g < S; ++g) am = m.amax[g] > am ? m.amax[g] : am;
+        m.dt = (cfl * m.dx) / am;
+      }
+    }
+    const auto t1 = Clock::now();
+    for (int64_t g = 0; g < S; ++g)
+      std::memcpy(rho.data() + g * 512, m.U.data() + g * kInterior, 512 * sizeof(double));
+    if (steps_out) {
+      tb_machine_step &o = steps_out[step];
+      o.wall_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+      o.dt = m.dt;
+      o.piece = exact_sum(rho.data(), S * 512);
+      o.launches = m.kernels - k0;
+      o.transfers = m.transfers - t0n;
+      o.event_waits = m.event_waits - w0;
+      o.full = m.full - f0;
+      o.idle = m.idle - i0;
+      o.members = m.members - mb0;
+    }
+  }
+  if (U_out) std::memcpy(U_out, m.U.data(), sizeof(double) * S * kInterior);
+  m.pool->stop();
+  m.hosttasks.reset();
+  for (auto &ex : m.execs) {
+    cudaStreamSynchronize(ex->stream);
+    cudaStreamDestroy(ex->stream);
+  }
+  for (Staging *st : m.staging_all) {
+    cudaFreeHost(st->host);
+    cudaFree(st->dev);
+    delete st;
   }
   const int err = tb::rc(cudaGetLastError());
   return m.error != TB_OK ? m.error : err;

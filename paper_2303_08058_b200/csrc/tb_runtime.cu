@@ -437,6 +437,19 @@ int tb_agg_launch(tb_stream_t s, int op, int kind, double c1, double c2,
   return r;
 }
 
+int tb_agg_launch_hydro(tb_stream_t s, double *din, const double *hin, int64_t nsub,
+                        double *dout, double *hout, double dx, double gamma,
+                        tb_event_t *done) {
+  if (!din || !hin || !dout || !hout || !done || nsub < 1) return TB_E_INVALID;
+  ensure_device();
+  const size_t in_bytes = (size_t)nsub * 5 * 1728 * 8, out_bytes = (size_t)nsub * (5 * 512 + 1) * 8;
+  int r = tb_memcpy_h2d(s, din, hin, in_bytes);
+  if (r == TB_OK) r = tb_hydro_flux(s, din, dout, dout + nsub * 5 * 512, nsub, dx, gamma);
+  if (r == TB_OK) r = tb_memcpy_d2h(s, hout, dout, out_bytes);
+  if (r == TB_OK) r = tb_event_record(s, done);
+  return r;
+}
+
 // ---------------------------------------------------------- poll registry
 int tb_poll_create(tb_poll_t *reg) {
   if (!reg) return TB_E_INVALID;

@@ -64,3 +64,32 @@ def run_native(subgrids: int, steps: int, workers: int = 8, executors: int = 32,
         per_step[-1].mean_batch = o.members / max(o.full + o.idle, 1)
     return ScenarioResult(per_step=per_step, checksum=cs.value,
                           dts=[o.dt for o in out[:steps]]), cells
+
+
+def run_native_hydro(state: np.ndarray, steps: int, workers: int = 8, executors: int = 32,
+                     max_agg: int = 8, mode: IntegrationMode = IntegrationMode.POLLING,
+                     task_subgrids: int = 1, hosttask_threads: int = 2, device: int = 0,
+                     cfl: float = 0.4, gamma: float = 5.0 / 3.0):
+    """The machine on the north_star's hydro kernel (tb_machine_run_hydro):
+    per step one task per ``task_subgrids`` sub-grids does the periodic ghost
+    exchange on the host and schedules an aggregated K6 request; completion
+    by ``mode``; then the forward-Euler update. ``state``: [S, 5, 8, 8, 8]
+    float64 (S = n^3). Returns (per-step StepMetrics, final state)."""
+    N.init(device)
+    st = np.ascontiguousarray(state, dtype=np.float64)
+    S = st.shape[0]
+    cfg = MachineConfig(S, steps, 0, 1, workers, executors, max_agg, _MODES[mode], 0, 0,
+                        task_subgrids, hosttask_threads)
+    out = (MachineStep * max(steps, 1))()
+    final = np.empty_like(st)
+    N.call("tb_machine_run_hydro", ctypes.addressof(cfg), st.ctypes.data, final.ctypes.data,
+           float(cfl), float(gamma), ctypes.addressof(out))
+    per_step = []
+    for k in range(steps):
+        o = out[k]
+        m = StepMetrics(wall_ms=o.wall_ms, dt=o.dt, checksum_piece=o.piece, launches=o.launches,
+                        transfers=o.transfers, batch_sizes=[], reasons_full=o.full,
+                        reasons_idle=o.idle, event_waits=o.event_waits)
+        m.mean_batch = o.members / max(o.full + o.idle, 1)
+        per_step.append(m)
+    return per_step, final
