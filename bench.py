@@ -206,7 +206,7 @@ def machine_ablation(subgrids=512, steps=5, repeats=3):
 
 
 HYDRO_BYTES_PER_SUBGRID = 5 * 12 ** 3 * 8 + 5 * 8 ** 3 * 8 + 8   # U in, dU/dt + amax out
-M2L_FMA, LEAF_FMA = 84, 4     # algorithmic FP64 FMAs per interaction (K7)
+M2L_FMA, LEAF_FMA = 70, 4     # algorithmic FP64 FMAs per interaction (traceless M2L, K7)
 
 
 def fp64_peak():
