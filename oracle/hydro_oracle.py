@@ -16,15 +16,16 @@ layer, i.e. 12^3 cells):
 
 * layout U[s, f, k, j, i], f in (rho, sx, sy, sz, E), i fastest, float64;
 * ideal gas, gamma given; primitives per cell, in this exact order:
-  vx = sx/rho; vy = sy/rho; vz = sz/rho;
+  irho = 1/rho; vx = sx*irho; vy = sy*irho; vz = sz*irho;
   ke = 0.5 * ((sx*vx + sy*vy) + sz*vz); p = (gamma - 1) * (E - ke);
+  (one divide per cell; the reciprocals 1/(gamma-1) and 1/dx are formed once)
 * piecewise-linear reconstruction of (rho, vx, vy, vz, p) along each
   direction with the minmod limiter: dl = q[c]-q[c-1], dr = q[c+1]-q[c];
   slope = 0 if dl*dr <= 0 else (dl if |dl| < |dr| else dr);
   face values q[c] +/- 0.5*slope;
 * at each face: left state = cell c's "+" value, right state = cell c+1's "-"
   value; per state (direction d with normal velocity vn):
-  cs = sqrt(gamma*p/rho); e = p/(gamma-1) + 0.5*rho*((vx*vx + vy*vy) + vz*vz);
+  cs = sqrt((gamma*p)/rho); e = p*(1/(gamma-1)) + 0.5*rho*((vx*vx + vy*vy) + vz*vz);
   U = (rho, rho*vx, rho*vy, rho*vz, e); F = (rho*vn, rho*vx*vn [+p if d==x],
   rho*vy*vn [+p if d==y], rho*vz*vn [+p if d==z], (e+p)*vn) with momentum
   flux components computed as (rho*v_comp)*vn then + p on the normal one;
@@ -34,7 +35,7 @@ layer, i.e. 12^3 cells):
   (0.5*(FL+FR)) - ((0.5*a)*(UR-UL));
 * update of interior cell c: du = (Fx[c+1/2]-Fx[c-1/2]);
   du = du + (Fy[c+1/2]-Fy[c-1/2]); du = du + (Fz[c+1/2]-Fz[c-1/2]);
-  dUdt = -(du / dx);
+  dUdt = -(du * (1/dx));
 * per sub-grid: amax = max over all its faces of a (the CFL signal speed).
 """
 
@@ -50,9 +51,10 @@ NF = 5                      # rho, sx, sy, sz, E
 
 def primitives(U: np.ndarray, gamma: float):
     rho, sx, sy, sz, E = (U[:, f] for f in range(NF))
-    vx = sx / rho
-    vy = sy / rho
-    vz = sz / rho
+    irho = 1.0 / rho
+    vx = sx * irho
+    vy = sy * irho
+    vz = sz * irho
     ke = 0.5 * ((sx * vx + sy * vy) + sz * vz)
     p = (gamma - 1.0) * (E - ke)
     return rho, vx, vy, vz, p
@@ -65,7 +67,7 @@ def _minmod(dl, dr):
 
 def _state(rho, vx, vy, vz, p, gamma, d):
     cs = np.sqrt((gamma * p) / rho)
-    e = p / (gamma - 1.0) + 0.5 * rho * ((vx * vx + vy * vy) + vz * vz)
+    e = p * (1.0 / (gamma - 1.0)) + 0.5 * rho * ((vx * vx + vy * vy) + vz * vz)
     vn = (vx, vy, vz)[d]
     mx, my, mz = rho * vx, rho * vy, rho * vz
     U = (rho, mx, my, mz, e)
@@ -129,7 +131,7 @@ def hydro_flux(U: np.ndarray, dx: float, gamma: float):
             parts.append(hi - lo)
         diff = np.stack(parts, axis=1)
         du = diff if du is None else du + diff
-    return -(du / dx), amax
+    return -(du * (1.0 / dx)), amax
 
 
 # ------------------------------------------------------- synthetic inputs --

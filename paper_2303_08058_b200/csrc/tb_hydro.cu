@@ -38,12 +38,12 @@ struct State {
 
 // Left/right state -> conserved vector, flux along d, signal speed |vn|+cs.
 __device__ __forceinline__ void face_state(double rho, double vx, double vy, double vz,
-                                           double p, double gamma, double gm1, int d,
+                                           double p, double gamma, double igm1, int d,
                                            State &s) {
   const double cs = __dsqrt_rn(__ddiv_rn(__dmul_rn(gamma, p), rho));
   const double vv = __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)),
                               __dmul_rn(vz, vz));
-  const double e = __dadd_rn(__ddiv_rn(p, gm1), __dmul_rn(__dmul_rn(0.5, rho), vv));
+  const double e = __dadd_rn(__dmul_rn(p, igm1), __dmul_rn(__dmul_rn(0.5, rho), vv));
   const double vn = d == 0 ? vx : (d == 1 ? vy : vz);
   const double mx = __dmul_rn(rho, vx), my = __dmul_rn(rho, vy), mz = __dmul_rn(rho, vz);
   s.u[0] = rho;
@@ -88,6 +88,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   __shared__ double s_amax[kThreads / 32];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const double gm1 = __dadd_rn(gamma, -1.0);
+  const double igm1 = __ddiv_rn(1.0, gm1), idx = __ddiv_rn(1.0, dx);
   if (t == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -129,7 +130,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int c = t; c < NCELL; c += kThreads) {
       const double rho = W[c], sx = W[NCELL + c], sy = W[2 * NCELL + c],
                    sz = W[3 * NCELL + c], E = W[4 * NCELL + c];
-      const double vx = __ddiv_rn(sx, rho), vy = __ddiv_rn(sy, rho), vz = __ddiv_rn(sz, rho);
+      const double ir = __ddiv_rn(1.0, rho);
+      const double vx = __dmul_rn(sx, ir), vy = __dmul_rn(sy, ir), vz = __dmul_rn(sz, ir);
       const double ke = __dmul_rn(
           0.5, __dadd_rn(__dadd_rn(__dmul_rn(sx, vx), __dmul_rn(sy, vy)), __dmul_rn(sz, vz)));
       W[NCELL + c] = vx;
@@ -176,8 +178,8 @@ __global__ void __launch_bounds__(kThreads, 2)
           qR[v] = __dadd_rn(qp, -__dmul_rn(0.5, s1));
         }
         State L, R;
-        face_state(qL[0], qL[1], qL[2], qL[3], qL[4], gamma, gm1, d, L);
-        face_state(qR[0], qR[1], qR[2], qR[3], qR[4], gamma, gm1, d, R);
+        face_state(qL[0], qL[1], qL[2], qL[3], qL[4], gamma, igm1, d, L);
+        face_state(qR[0], qR[1], qR[2], qR[3], qR[4], gamma, igm1, d, R);
         const double a = fmax(L.a, R.a);
         amax = fmax(amax, a);
         const double ha = __dmul_rn(0.5, a);
@@ -226,7 +228,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int m = 0; m < kCellsPerThread; ++m)
 #pragma unroll
       for (int v = 0; v < NF; ++v)
-        out[v * (NI * NI * NI) + t + kThreads * m] = -__ddiv_rn(du[v][m], dx);
+        out[v * (NI * NI * NI) + t + kThreads * m] = -__dmul_rn(du[v][m], idx);
     // ---- max signal speed of the sub-grid ---------------------------------
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
