@@ -261,6 +261,30 @@ int tb_fmm_leaf(tb_stream_t s, int max_level, const double *rho, const double *w
                 double *out);
 int tb_fmm_solve(tb_stream_t s, int max_level, const double *rho, double *work, double *out);
 
+/* The same solve split over `ranks` devices by z-slabs of the leaf lattice
+ * (ranks a power of two, N/ranks a multiple of 16; the single-device calls
+ * above are ranks = 1). Levels >= lp are partitioned (this rank keeps
+ * N_l/ranks planes; reduced moment records carry 4 halo planes per side that
+ * the caller fills from the z-neighbours — zero at the domain boundary —
+ * between upward and m2l); levels < lp are replicated: the caller all-gathers
+ * the raw and reduced records of level lp-1 (each rank computes its own
+ * slab of it in tb_fmm_slab_upward), then tb_fmm_slab_coarse builds the
+ * coarser levels. The workspace must be zeroed once (halo planes).
+ * info (tb_fmm_slab_layout, 8 words): byte offsets of the level's raw
+ * records [nzr][N][N][20], reduced records [nzr+2 halo][N][N][18] and local
+ * expansions [nz][N][N][20]; N; nz (planes kept); z0 (global plane of local
+ * plane 0); halo; lp. Leaves: rho points at this rank's first leaf plane,
+ * planes [zmin, zmax) relative to it are readable; out [4][nz][N][N]. */
+int tb_fmm_slab_workspace_bytes(int max_level, int ranks, uint64_t *bytes);
+int tb_fmm_slab_layout(int max_level, int ranks, int rank, int level, uint64_t *info);
+int tb_fmm_slab_upward(tb_stream_t s, int max_level, int ranks, int rank, const double *rho,
+                       double *work);
+int tb_fmm_slab_coarse(tb_stream_t s, int max_level, int ranks, int rank, double *work);
+int tb_fmm_slab_m2l(tb_stream_t s, int max_level, int ranks, int rank, double *work);
+int tb_fmm_slab_downward(tb_stream_t s, int max_level, int ranks, int rank, double *work);
+int tb_fmm_slab_leaf(tb_stream_t s, int max_level, int ranks, int rank, const double *rho,
+                     int zmin, int zmax, const double *work, double *out);
+
 /* FP64 issue-rate probe (roofline denominator; no reference counterpart):
  * runs one FP64 instruction type on 8 independent chains per thread over a
  * full grid on the current device and returns thread-instructions/s and the

@@ -155,6 +155,13 @@ SIGNATURES = {
     "tb_fmm_downward": [_u64, _int, _vp],
     "tb_fmm_leaf": [_u64, _int, _vp, _vp, _vp],
     "tb_fmm_solve": [_u64, _int, _vp, _vp, _vp],
+    "tb_fmm_slab_workspace_bytes": [_int, _int, _pu64],
+    "tb_fmm_slab_layout": [_int, _int, _int, _int, _pu64],
+    "tb_fmm_slab_upward": [_u64, _int, _int, _int, _vp, _vp],
+    "tb_fmm_slab_coarse": [_u64, _int, _int, _int, _vp],
+    "tb_fmm_slab_m2l": [_u64, _int, _int, _int, _vp],
+    "tb_fmm_slab_downward": [_u64, _int, _int, _int, _vp],
+    "tb_fmm_slab_leaf": [_u64, _int, _int, _int, _vp, _int, _int, _vp, _vp],
 }
 BLOCKING = {"tb_init", "tb_device_sync", "tb_stream_sync", "tb_event_wait",
             "tb_htq_next", "tb_htq_destroy", "tb_malloc", "tb_free",

@@ -301,10 +301,12 @@ constexpr int kStage = kMStage + kDStage;                        // 81,024 B
 constexpr uint32_t kMBytes = kMStage * 8, kDBytes = kDStage * 8;
 
 struct Params {
-  CUtensorMap maps[kMaxLevel];     // level l reduced moment records, 4-D {18,N,N,N}
-  double *Loc[kMaxLevel];          // [N^3][20]
+  CUtensorMap maps[kMaxLevel];     // level l reduced records, 4-D {18, N, N, nz + 2 halo}
+  double *Loc[kMaxLevel];          // [nz][N][N][20] (this rank's planes)
   const double *Dtab[kMaxLevel];   // [33][912], levels >= 1
   double *L0part;                  // [8][512][20]
+  int nbz[kMaxLevel];              // this rank's sub-grid planes (N/8 when replicated)
+  int zoff[kMaxLevel];             // halo planes below plane 0 in the reduced records
   int L;                           // max_level (leaves); multipole levels 0..L-1
 };
 
@@ -326,8 +328,9 @@ __global__ void __launch_bounds__(256) k_fmm_up(const double *__restrict__ rho,
                                                 const double *__restrict__ child,
                                                 double *__restrict__ parent,
                                                 double *__restrict__ parent_red, int Np,
-                                                double hc) {
-  const int64_t npar = (int64_t)Np * Np * Np;
+                                                int Npz, double hc) {
+  // parents: Np x Np x Npz (this rank's planes); all pointers at local plane 0
+  const int64_t npar = (int64_t)Np * Np * Npz;
   const int64_t pidx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (pidx >= npar) return;
   const int px = (int)(pidx % Np), py = (int)((pidx / Np) % Np),
@@ -489,7 +492,7 @@ __global__ void __launch_bounds__(kM2LThreads, 1) k_fmm_m2l(const __grid_constan
   // decode the job: levels L-1 .. 1 (8^l sub-grids each), then 8 level-0 slabs
   int job = blockIdx.x, lev = 0, sub = 0;
   for (int l = P.L - 1; l >= 1; --l) {
-    const int cnt = 1 << (3 * l);
+    const int cnt = (1 << (2 * l)) * P.nbz[l];
     if (job < cnt) {
       lev = l;
       sub = job;
@@ -547,10 +550,11 @@ __global__ void __launch_bounds__(kM2LThreads, 1) k_fmm_m2l(const __grid_constan
 
   const int nb = 1 << lev;
   const int X0 = 8 * (sub % nb), Y0 = 8 * ((sub / nb) % nb), Z0 = 8 * (sub / (nb * nb));
+  const int ZT = Z0 + P.zoff[lev];     // TMA z of the sub-grid in the halo'd records
   if (t == 0) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    issue_stage(P, lev, sm, &bar[0], 0, X0, Y0, Z0);
-    issue_stage(P, lev, sm + kStage, &bar[1], 1, X0, Y0, Z0);
+    issue_stage(P, lev, sm, &bar[0], 0, X0, Y0, ZT);
+    issue_stage(P, lev, sm + kStage, &bar[1], 1, X0, Y0, ZT);
   }
   // lane-dependent parts of the source cell and of the D-table entry
   const int cbase = ((2 * pz) * 8 + 2 * py) * 8 + 2 * px;
@@ -572,7 +576,7 @@ __global__ void __launch_bounds__(kM2LThreads, 1) k_fmm_m2l(const __grid_constan
     __syncthreads();            // every thread is done with this buffer
     if (t == 0 && k + 2 < 33) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue_stage(P, lev, sm + buf * kStage, &bar[buf], k + 2, X0, Y0, Z0);
+      issue_stage(P, lev, sm + buf * kStage, &bar[buf], k + 2, X0, Y0, ZT);
     }
   }
   untrace(L);
@@ -584,11 +588,13 @@ __global__ void __launch_bounds__(kM2LThreads, 1) k_fmm_m2l(const __grid_constan
 }
 
 // ------------------------------------------------------------------ L2L
+// Child cells: N x N x nzc (this rank's planes, global plane z0c + local);
+// the parent array's local plane 0 is global plane z0p (0 when replicated).
 __global__ void __launch_bounds__(256) k_fmm_down(const double *__restrict__ Lp,
                                                   double *__restrict__ Lc,
                                                   const double *__restrict__ L0part, int N,
-                                                  double h) {
-  const int64_t n = (int64_t)N * N * N;
+                                                  int nzc, int z0c, int z0p, double h) {
+  const int64_t n = (int64_t)N * N * nzc;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double out[NC];
@@ -604,7 +610,8 @@ __global__ void __launch_bounds__(256) k_fmm_down(const double *__restrict__ Lp,
   } else {
     const int x = (int)(i % N), y = (int)((i / N) % N), z = (int)(i / ((int64_t)N * N));
     const int Nq = N / 2;
-    const int64_t pi = ((int64_t)(z >> 1) * Nq + (y >> 1)) * Nq + (x >> 1);
+    const int pz = ((z0c + z) >> 1) - z0p;
+    const int64_t pi = ((int64_t)pz * Nq + (y >> 1)) * Nq + (x >> 1);
     double mono[NC], Lpar[NC];
     monomials<true>(((x & 1) - 0.5) * h, ((y & 1) - 0.5) * h, ((z & 1) - 0.5) * h, mono);
     load20(Lp + pi * NC, Lpar);
@@ -626,9 +633,13 @@ constexpr int kSX = 12, kSY = 8, kSZ = (kTZ + 8) / 2;   // per-parity staged ext
 constexpr int kPar = kSX * kSY * kSZ;                    // x' padded 8 -> 12 (banks)
 constexpr int kLeafSmem = 8 * kPar * 8;                  // 73,728 B
 
+// Leaves: N x N x nz (this rank's planes). rho points at local plane 0 and
+// its planes [zmin, zmax) are readable (a halo of exchanged planes, or just
+// [0, N) on one device); the rest reads as zero (isolated boundary).
 __global__ void __launch_bounds__(kLeafThreads, 2)
-    k_fmm_leaf(const double *__restrict__ rho, const double *__restrict__ Lpar,
-               double *__restrict__ out, int N, double h) {
+    k_fmm_leaf(const double *__restrict__ rho, int zmin, int zmax,
+               const double *__restrict__ Lpar, double *__restrict__ out, int N, int nz,
+               double h) {
   extern __shared__ __align__(128) double S[];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const int ntx = N / kTX, nty = N / kTY;
@@ -641,8 +652,8 @@ __global__ void __launch_bounds__(kLeafThreads, 2)
   for (int e = t; e < 16 * 16 * 24; e += kLeafThreads) {
     const int rx = e & 15, ry = (e >> 4) & 15, rz = e >> 8;
     const int gx = X0 - 4 + rx, gy = Y0 - 4 + ry, gz = Z0 - 4 + rz;
-    const bool in = gx >= 0 && gx < N && gy >= 0 && gy < N && gz >= 0 && gz < N;
-    const double *src = in ? rho + ((size_t)gz * N + gy) * N + gx : rho;
+    const bool in = gx >= 0 && gx < N && gy >= 0 && gy < N && gz >= zmin && gz < zmax;
+    const double *src = in ? rho + ((int64_t)gz * N + gy) * N + gx : rho;
     const int c = (rx & 1) | ((ry & 1) << 1) | ((rz & 1) << 2);
     double *dst = S + c * kPar + ((rz >> 1) * kSY + (ry >> 1)) * kSX + (rx >> 1);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src),
@@ -683,7 +694,7 @@ __global__ void __launch_bounds__(kLeafThreads, 2)
   double mono[NC];
   monomials<true>((ox - 0.5) * h, (oy - 0.5) * h, (oz - 0.5) * h, mono);
   const int Nq = N / 2;
-  const size_t n = (size_t)N * N * N;
+  const size_t n = (size_t)N * N * nz;
   const double h2 = h * h;
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
@@ -715,22 +726,59 @@ __global__ void __launch_bounds__(kLeafThreads, 2)
 }
 
 // ------------------------------------------------------------------ host
+// Slab geometry for `ranks` devices, each owning N/ranks leaf planes in z.
+// Levels l >= lp are partitioned: this rank keeps its nz_l = N_l/ranks planes
+// (z0_l = rank * nz_l) and the reduced records carry 4 halo planes on each
+// side (zero, or the neighbours' planes after an exchange). Levels < lp are
+// replicated: full lattices on every rank; level lp-1 is assembled by an
+// all-gather of the ranks' slabs (each computes its own from level lp), the
+// coarser ones are then computed redundantly. One rank: lp = 1, nothing to
+// exchange, the halos stay zero (= the isolated boundary).
+struct Geom {
+  int L, R, r, lp;
+  int n[kMaxLevel + 1], nz[kMaxLevel + 1], z0[kMaxLevel + 1], halo[kMaxLevel + 1];
+};
+
+constexpr int kHalo = 4;
+
+bool make_geom(int L, int R, int r, Geom *g) {
+  if (L < 1 || L > kMaxLevel || R < 1 || (R & (R - 1)) || r < 0 || r >= R) return false;
+  const int N = 8 << L;
+  if (N / R < 16 || N % (16 * R)) return false;   // leaf tiles are 16 planes deep
+  g->L = L;
+  g->R = R;
+  g->r = r;
+  g->lp = 1;
+  while (g->lp < L && (8 << g->lp) / R < 8) ++g->lp;
+  for (int l = 0; l <= L; ++l) {
+    g->n[l] = 8 << l;
+    const bool part = l >= g->lp;
+    g->nz[l] = part ? g->n[l] / R : g->n[l];
+    g->z0[l] = part ? r * g->nz[l] : 0;
+    g->halo[l] = part && l < L ? kHalo : 0;
+  }
+  return true;
+}
+
 struct Layout {
   size_t M[kMaxLevel], Mred[kMaxLevel], Loc[kMaxLevel], Dtab[kMaxLevel], L0part,
       total;   // byte offsets
 };
 
-Layout layout(int L) {
+Layout layout(const Geom &g) {
   Layout lo{};
   size_t off = 0;
-  for (int l = 0; l < L; ++l) {
-    const size_t n = (size_t)(8 << l) * (8 << l) * (8 << l);
+  for (int l = 0; l < g.L; ++l) {
+    const size_t plane = (size_t)g.n[l] * g.n[l];
+    // the gathered level keeps full raw/reduced records (its slab is computed
+    // locally, the rest arrives by all-gather)
+    const size_t nzr = (l == g.lp - 1) ? (size_t)g.n[l] : (size_t)g.nz[l];
     lo.M[l] = off;
-    off += n * NC * 8;
+    off += plane * nzr * NC * 8;
     lo.Mred[l] = off;
-    off += n * MS * 8;
+    off += plane * (nzr + 2 * g.halo[l]) * MS * 8;
     lo.Loc[l] = off;
-    off += n * NC * 8;
+    off += plane * g.nz[l] * NC * 8;
     lo.Dtab[l] = off;
     if (l) off += (size_t)33 * kDStage * 8;
   }
@@ -739,8 +787,6 @@ Layout layout(int L) {
   lo.total = off;
   return lo;
 }
-
-bool valid_level(int L) { return L >= 1 && L <= kMaxLevel; }
 
 int ensure_weights() {
   static int done_mask = 0;
@@ -769,18 +815,21 @@ int ensure_weights() {
   return r;
 }
 
-int make_params(int L, double *work, Params *P) {
-  const Layout lo = layout(L);
+int make_params(const Geom &g, double *work, Params *P) {
+  const Layout lo = layout(g);
   char *base = reinterpret_cast<char *>(work);
   *P = Params{};
-  P->L = L;
+  P->L = g.L;
   P->L0part = reinterpret_cast<double *>(base + lo.L0part);
-  for (int l = 0; l < L; ++l) {
+  for (int l = 0; l < g.L; ++l) {
     double *M = reinterpret_cast<double *>(base + lo.Mred[l]);
     P->Loc[l] = reinterpret_cast<double *>(base + lo.Loc[l]);
     P->Dtab[l] = reinterpret_cast<const double *>(base + lo.Dtab[l]);
-    const uint64_t N = (uint64_t)(8 << l);
-    const uint64_t dims[4] = {(uint64_t)MS, N, N, N};
+    P->nbz[l] = g.nz[l] / 8;
+    P->zoff[l] = g.halo[l];
+    const uint64_t N = (uint64_t)g.n[l];
+    const uint64_t planes = (uint64_t)((l == g.lp - 1) ? g.n[l] : g.nz[l]) + 2 * g.halo[l];
+    const uint64_t dims[4] = {(uint64_t)MS, N, N, planes};
     const uint64_t strides[3] = {MS * 8, MS * 8 * N, MS * 8 * N * N};
     const uint32_t box[4] = {(uint32_t)MS, 8, 8, 8};
     const int r = tb::encode_tiled(&P->maps[l], 4, M, dims, strides, box);
@@ -791,38 +840,79 @@ int make_params(int L, double *work, Params *P) {
 
 inline cudaStream_t strm(tb_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// parents of level l from level l+1 (or from the leaves when l == L-1)
+void launch_up(tb_stream_t s, const Geom &g, const Layout &lo, char *base, const double *rho,
+               int l) {
+  const int Np = g.n[l];
+  // parent planes computed here: this rank's slab (the gathered level too)
+  const int npz = (l >= g.lp - 1 && g.R > 1) ? g.nz[l + 1] / 2 : g.nz[l];
+  const int pz0 = (l == g.lp - 1) ? g.z0[l + 1] / 2 : 0;   // local plane in the array
+  const size_t plane = (size_t)Np * Np;
+  double *raw = reinterpret_cast<double *>(base + lo.M[l]) + plane * pz0 * NC;
+  double *red = reinterpret_cast<double *>(base + lo.Mred[l]) + plane * (pz0 + g.halo[l]) * MS;
+  const double *child =
+      l == g.L - 1 ? nullptr : reinterpret_cast<const double *>(base + lo.M[l + 1]);
+  const int64_t npar = (int64_t)plane * npz;
+  k_fmm_up<<<(unsigned)((npar + 255) / 256), 256, 0, strm(s)>>>(
+      l == g.L - 1 ? rho : nullptr, child, raw, red, Np, npz, 1.0 / double(2 * Np));
+}
+
 }  // namespace
 
 extern "C" {
 
-int tb_fmm_workspace_bytes(int max_level, uint64_t *bytes) {
-  if (!bytes || !valid_level(max_level)) return TB_E_INVALID;
-  *bytes = layout(max_level).total;
+int tb_fmm_slab_workspace_bytes(int max_level, int ranks, uint64_t *bytes) {
+  Geom g;
+  if (!bytes || !make_geom(max_level, ranks, 0, &g)) return TB_E_INVALID;
+  *bytes = layout(g).total;
   return TB_OK;
 }
 
-int tb_fmm_upward(tb_stream_t s, int max_level, const double *rho, double *work) {
-  if (!rho || !work || !valid_level(max_level)) return TB_E_INVALID;
-  const Layout lo = layout(max_level);
+int tb_fmm_slab_layout(int max_level, int ranks, int rank, int level, uint64_t *info) {
+  Geom g;
+  if (!info || !make_geom(max_level, ranks, rank, &g) || level < 0 || level > max_level)
+    return TB_E_INVALID;
+  const Layout lo = layout(g);
+  const bool multipole = level < max_level;
+  info[0] = multipole ? lo.M[level] : 0;
+  info[1] = multipole ? lo.Mred[level] : 0;
+  info[2] = multipole ? lo.Loc[level] : 0;
+  info[3] = (uint64_t)g.n[level];
+  info[4] = (uint64_t)g.nz[level];
+  info[5] = (uint64_t)g.z0[level];
+  info[6] = (uint64_t)g.halo[level];
+  info[7] = (uint64_t)g.lp;
+  return TB_OK;
+}
+
+int tb_fmm_slab_upward(tb_stream_t s, int max_level, int ranks, int rank, const double *rho,
+                       double *work) {
+  Geom g;
+  if (!rho || !work || !make_geom(max_level, ranks, rank, &g)) return TB_E_INVALID;
+  const Layout lo = layout(g);
   char *base = reinterpret_cast<char *>(work);
-  for (int l = max_level - 1; l >= 0; --l) {
-    const int Np = 8 << l;
-    const int64_t npar = (int64_t)Np * Np * Np;
-    const int64_t blocks = (npar + 255) / 256;   // one thread per parent
-    const double hc = 1.0 / double(2 * Np);
-    const double *child =
-        l == max_level - 1 ? nullptr : reinterpret_cast<const double *>(base + lo.M[l + 1]);
-    k_fmm_up<<<(unsigned)blocks, 256, 0, strm(s)>>>(
-        l == max_level - 1 ? rho : nullptr, child, reinterpret_cast<double *>(base + lo.M[l]),
-        reinterpret_cast<double *>(base + lo.Mred[l]), Np, hc);
-  }
+  // one rank: every level; several: the partitioned levels and this rank's
+  // slab of the gathered level lp-1 (tb_fmm_slab_coarse does the rest)
+  const int stop = ranks == 1 ? 0 : g.lp - 1;
+  for (int l = max_level - 1; l >= stop; --l) launch_up(s, g, lo, base, rho, l);
   return tb::last_error();
 }
 
-int tb_fmm_m2l(tb_stream_t s, int max_level, double *work) {
-  if (!work || !valid_level(max_level)) return TB_E_INVALID;
+int tb_fmm_slab_coarse(tb_stream_t s, int max_level, int ranks, int rank, double *work) {
+  Geom g;
+  if (!work || !make_geom(max_level, ranks, rank, &g)) return TB_E_INVALID;
+  if (ranks == 1) return TB_OK;
+  const Layout lo = layout(g);
+  char *base = reinterpret_cast<char *>(work);
+  for (int l = g.lp - 2; l >= 0; --l) launch_up(s, g, lo, base, nullptr, l);
+  return tb::last_error();
+}
+
+int tb_fmm_slab_m2l(tb_stream_t s, int max_level, int ranks, int rank, double *work) {
+  Geom g;
+  if (!work || !make_geom(max_level, ranks, rank, &g)) return TB_E_INVALID;
   Params P;
-  int r = make_params(max_level, work, &P);
+  int r = make_params(g, work, &P);
   if (r != TB_OK) return r;
   static bool attr = false;
   if (!attr) {
@@ -837,29 +927,34 @@ int tb_fmm_m2l(tb_stream_t s, int max_level, double *work) {
     k_fmm_dtab<<<dim3(33, max_level - 1), 32, 0, strm(s)>>>(T);
   }
   int jobs = 8;
-  for (int l = 1; l < max_level; ++l) jobs += 1 << (3 * l);
+  for (int l = 1; l < max_level; ++l) jobs += (1 << (2 * l)) * P.nbz[l];
   k_fmm_m2l<<<jobs, kM2LThreads, kM2LSmem, strm(s)>>>(P);
   return tb::last_error();
 }
 
-int tb_fmm_downward(tb_stream_t s, int max_level, double *work) {
-  if (!work || !valid_level(max_level)) return TB_E_INVALID;
-  const Layout lo = layout(max_level);
+int tb_fmm_slab_downward(tb_stream_t s, int max_level, int ranks, int rank, double *work) {
+  Geom g;
+  if (!work || !make_geom(max_level, ranks, rank, &g)) return TB_E_INVALID;
+  const Layout lo = layout(g);
   char *base = reinterpret_cast<char *>(work);
   for (int l = 0; l < max_level; ++l) {
-    const int N = 8 << l;
-    const int64_t n = (int64_t)N * N * N;
+    const int N = g.n[l];
+    const int64_t n = (int64_t)N * N * g.nz[l];
     double *Lc = reinterpret_cast<double *>(base + lo.Loc[l]);
     const double *Lp = l ? reinterpret_cast<const double *>(base + lo.Loc[l - 1]) : nullptr;
     const double *part = l ? nullptr : reinterpret_cast<const double *>(base + lo.L0part);
-    k_fmm_down<<<(unsigned)((n + 255) / 256), 256, 0, strm(s)>>>(Lp, Lc, part, N, 1.0 / N);
+    k_fmm_down<<<(unsigned)((n + 255) / 256), 256, 0, strm(s)>>>(
+        Lp, Lc, part, N, g.nz[l], g.z0[l], l ? g.z0[l - 1] : 0, 1.0 / N);
   }
   return tb::last_error();
 }
 
-int tb_fmm_leaf(tb_stream_t s, int max_level, const double *rho, const double *work,
-                double *out) {
-  if (!rho || !out || !valid_level(max_level) || !work) return TB_E_INVALID;
+int tb_fmm_slab_leaf(tb_stream_t s, int max_level, int ranks, int rank, const double *rho,
+                     int zmin, int zmax, const double *work, double *out) {
+  Geom g;
+  if (!rho || !out || !work || !make_geom(max_level, ranks, rank, &g) || zmin > 0 ||
+      zmax < g.nz[max_level])
+    return TB_E_INVALID;
   int r = ensure_weights();
   if (r != TB_OK) return r;
   static bool attr = false;
@@ -869,13 +964,36 @@ int tb_fmm_leaf(tb_stream_t s, int max_level, const double *rho, const double *w
     if (r != TB_OK) return r;
     attr = true;
   }
-  const Layout lo = layout(max_level);
+  const Layout lo = layout(g);
   const double *Lpar = reinterpret_cast<const double *>(reinterpret_cast<const char *>(work) +
                                                         lo.Loc[max_level - 1]);
-  const int N = 8 << max_level;
-  const int tiles = (N / kTX) * (N / kTY) * (N / kTZ);
-  k_fmm_leaf<<<tiles, kLeafThreads, kLeafSmem, strm(s)>>>(rho, Lpar, out, N, 1.0 / N);
+  const int N = g.n[max_level], nz = g.nz[max_level];
+  const int tiles = (N / kTX) * (N / kTY) * (nz / kTZ);
+  k_fmm_leaf<<<tiles, kLeafThreads, kLeafSmem, strm(s)>>>(rho, zmin, zmax, Lpar, out, N, nz,
+                                                          1.0 / N);
   return tb::last_error();
+}
+
+// ---- one device (the slab API with one rank) -----------------------------
+int tb_fmm_workspace_bytes(int max_level, uint64_t *bytes) {
+  return tb_fmm_slab_workspace_bytes(max_level, 1, bytes);
+}
+
+int tb_fmm_upward(tb_stream_t s, int max_level, const double *rho, double *work) {
+  return tb_fmm_slab_upward(s, max_level, 1, 0, rho, work);
+}
+
+int tb_fmm_m2l(tb_stream_t s, int max_level, double *work) {
+  return tb_fmm_slab_m2l(s, max_level, 1, 0, work);
+}
+
+int tb_fmm_downward(tb_stream_t s, int max_level, double *work) {
+  return tb_fmm_slab_downward(s, max_level, 1, 0, work);
+}
+
+int tb_fmm_leaf(tb_stream_t s, int max_level, const double *rho, const double *work,
+                double *out) {
+  return tb_fmm_slab_leaf(s, max_level, 1, 0, rho, 0, 8 << max_level, work, out);
 }
 
 int tb_fmm_solve(tb_stream_t s, int max_level, const double *rho, double *work, double *out) {

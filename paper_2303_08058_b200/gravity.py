@@ -43,7 +43,9 @@ class GravitySolver:
             raise RuntimeError("GravitySolver needs a CUDA device (no CPU fallback)")
         N.init(self.device.index or 0)
         nbytes = workspace_bytes(max_level)
-        self.work = torch.empty(nbytes // 8, dtype=torch.float64, device=self.device)
+        # zeroed once: the halo planes of the partitioned levels' moment
+        # records stay zero on one device (= the isolated boundary)
+        self.work = torch.zeros(nbytes // 8, dtype=torch.float64, device=self.device)
         self.out = torch.empty((4, self.n, self.n, self.n), dtype=torch.float64,
                                device=self.device)
 

@@ -55,22 +55,27 @@ def test_fmm_upward_moments_vs_oracle():
     Ms = f.upward(rho, L)
     scale = np.array([(1.0 if len(B) % 2 else -1.0) * f.mult(B) / math.factorial(len(B))
                       for B in f.COMPS])
-    off = 0
-    for lev in range(L):      # workspace: [Mhat_l [n][20], Mred_l [n][18], Loc_l [n][20], Dtab_l]
-        n = (8 << lev) ** 3
-        got = np.moveaxis(work[off:off + 20 * n].reshape((8 << lev,) * 3 + (20,)), -1, 0)
+    import ctypes
+    from paper_2303_08058_b200 import _native as N
+    info = (ctypes.c_uint64 * 8)()
+    for lev in range(L):
+        N.call("tb_fmm_slab_layout", L, 1, 0, lev, info)
+        raw_off, red_off, n, halo = info[0] // 8, info[1] // 8, info[3], info[6]
+        cells = n ** 3
+        got = np.moveaxis(work[raw_off:raw_off + 20 * cells].reshape((n,) * 3 + (20,)), -1, 0)
         want = Ms[lev] * scale[:, None, None, None]
         mag = np.abs(want).max(axis=(1, 2, 3), keepdims=True)
         assert np.all(np.abs(got - want) <= 1e-13 * mag + 1e-300), lev
-        red = work[off + 20 * n:off + 38 * n].reshape(n, 18)
-        w = want.reshape(20, n)
+        recs = work[red_off:red_off + 18 * n * n * (n + 2 * halo)].reshape(-1, 18)
+        assert np.all(recs[:n * n * halo] == 0.0) and np.all(recs[n * n * (n + halo):] == 0.0)
+        red = recs[n * n * halo:n * n * (n + halo)]
+        w = want.reshape(20, cells)
         # traceless reduction: zz-containing moments folded into xx, yy, xxx, ...
         exp = np.stack([w[0], w[1], w[2], w[3], w[4] - w[9], w[5], w[6], w[7] - w[9], w[8],
                         w[10] - w[15], w[11] - w[18], w[12] - w[19], w[13] - w[15], w[14],
                         w[16] - w[18], w[17] - w[19]], axis=1)
         assert np.all(np.abs(red[:, :16] - exp) <= 1e-13 * np.abs(w).max() + 1e-300), lev
         assert np.all(red[:, 16:] == 0.0)
-        off += 58 * n + (33 * 912 if lev else 0)
 
 
 @pytest.mark.parametrize("L", [3, 4])
