@@ -225,9 +225,10 @@ int tb_hydro_flux(tb_stream_t s, const double *U, double *dudt, double *amax,
 /* K6 on a ghost-padded global lattice (the coupled step's layout):
  * Up [5][n+4][n+4][n+4] (2-cell ghost layer already filled, e.g. by
  * tb_star_pad); sub-grid s = (bz*nb + by)*nb + bx (nb = n/8) is staged by one
- * 4-D TMA box; dudt [nb^3][5][8][8][8], amax [nb^3] as tb_hydro_flux. */
-int tb_hydro_flux_lattice(tb_stream_t s, const double *Up, int64_t n, double *dudt,
-                          double *amax, double dx, double gamma);
+ * 4-D TMA box; dudt [nb^3][5][8][8][8], amax [nb^3] as tb_hydro_flux. A z-slab
+ * of nz planes (Up [5][nz+4][n+4][n+4]) gives nb*nb*nz/8 sub-grids. */
+int tb_hydro_flux_lattice(tb_stream_t s, const double *Up, int64_t n, int64_t nz,
+                          double *dudt, double *amax, double dx, double gamma);
 
 /* The coupled rotating-star step (PARITY UNPINNED; spec oracle/star_oracle.py):
  * U [5][n][n][n] lattice (rho, sx, sy, sz, E), periodic hydro, isolated FMM
@@ -237,10 +238,14 @@ int tb_hydro_flux_lattice(tb_stream_t s, const double *Up, int64_t n, double *du
  * stage 1: Unew = Uc + dt L(Uc); stage 2: Unew = 0.5 (U0 + (Uc + dt L(Uc)))
  * (Unew may alias U0). No FMA: matches the oracle's rounding. */
 int tb_star_pad(tb_stream_t s, const double *U, int64_t n, double *Up);
+/* Slab of nz planes: lo/hi = the 2 planes below/above from the z-neighbours
+ * ([5][2][n][n]; both null = wrap inside the slab). */
+int tb_star_pad_slab(tb_stream_t s, const double *U, int64_t n, int64_t nz, const double *lo,
+                     const double *hi, double *Up);
 int tb_star_cfl(tb_stream_t s, const double *amax, int64_t nsub, double dx, double cfl,
                 double *dt);
 int tb_star_stage(tb_stream_t s, int stage, const double *U0, const double *Uc,
-                  const double *dudt, const double *g, const double *dt, int64_t n,
+                  const double *dudt, const double *g, const double *dt, int64_t n, int64_t nz,
                   double *Unew);
 
 /* K7 (north_star "FMM monopole/multipole stencil-interaction kernels",

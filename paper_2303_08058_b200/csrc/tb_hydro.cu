@@ -273,18 +273,19 @@ extern "C" int tb_hydro_flux(tb_stream_t s, const double *U, double *dudt, doubl
   return launch<false>(s, U, unused, 0, dudt, amax, nsub, dx, gamma);
 }
 
-extern "C" int tb_hydro_flux_lattice(tb_stream_t s, const double *Up, int64_t n, double *dudt,
-                                     double *amax, double dx, double gamma) {
-  if (!Up || !dudt || !amax || n < 8 || n % 8 || !(dx > 0.0) || !(gamma > 1.0))
+extern "C" int tb_hydro_flux_lattice(tb_stream_t s, const double *Up, int64_t n, int64_t nz,
+                                     double *dudt, double *amax, double dx, double gamma) {
+  if (!Up || !dudt || !amax || n < 8 || n % 8 || nz < 8 || nz % 8 || !(dx > 0.0) ||
+      !(gamma > 1.0))
     return TB_E_INVALID;
   if (reinterpret_cast<uintptr_t>(Up) & 15) return TB_E_INVALID;
-  const uint64_t P = (uint64_t)n + 2 * NG;
-  const uint64_t dims[4] = {P, P, P, (uint64_t)NF};
-  const uint64_t strides[3] = {P * 8, P * P * 8, P * P * P * 8};
+  const uint64_t P = (uint64_t)n + 2 * NG, Pz = (uint64_t)nz + 2 * NG;
+  const uint64_t dims[4] = {P, P, Pz, (uint64_t)NF};
+  const uint64_t strides[3] = {P * 8, P * P * 8, P * P * Pz * 8};
   const uint32_t box[4] = {NT, NT, NT, NF};
   CUtensorMap map;
   const int r = tb::encode_tiled(&map, 4, const_cast<double *>(Up), dims, strides, box);
   if (r != TB_OK) return r;
   const int nb = (int)(n / NI);
-  return launch<true>(s, Up, map, nb, dudt, amax, (int64_t)nb * nb * nb, dx, gamma);
+  return launch<true>(s, Up, map, nb, dudt, amax, (int64_t)nb * nb * (nz / NI), dx, gamma);
 }

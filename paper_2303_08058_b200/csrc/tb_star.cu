@@ -26,16 +26,33 @@ namespace {
 
 constexpr int NF = 5, NG = 2;
 
+// U [5][nz][n][n] (a slab, or the whole lattice) -> Up [5][nz+4][n+4][n+4]:
+// x, y wrap periodically inside the slab; z takes the 2 planes below / above
+// from lo / hi ([5][2][n][n], the z-neighbours' planes) or, when they are
+// null (one device), wraps inside the slab.
 __global__ void __launch_bounds__(256) k_star_pad(const double *__restrict__ U,
-                                                  double *__restrict__ Up, int n) {
-  const int P = n + 2 * NG;
-  const int64_t total = (int64_t)NF * P * P * P;
+                                                  const double *__restrict__ lo,
+                                                  const double *__restrict__ hi,
+                                                  double *__restrict__ Up, int n, int nz) {
+  const int P = n + 2 * NG, Pz = nz + 2 * NG;
+  const int64_t plane = (int64_t)n * n;
+  const int64_t total = (int64_t)NF * P * P * Pz;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const int x = (int)(e % P), y = (int)((e / P) % P), z = (int)((e / ((int64_t)P * P)) % P);
-    const int f = (int)(e / ((int64_t)P * P * P));
-    const int sx = (x - NG + n) % n, sy = (y - NG + n) % n, sz = (z - NG + n) % n;
-    Up[e] = __ldg(U + (((int64_t)f * n + sz) * n + sy) * n + sx);
+    const int x = (int)(e % P), y = (int)((e / P) % P), z = (int)((e / ((int64_t)P * P)) % Pz);
+    const int f = (int)(e / ((int64_t)P * P * Pz));
+    const int sx = (x - NG + n) % n, sy = (y - NG + n) % n, zl = z - NG;
+    const int64_t in_plane = (int64_t)sy * n + sx;
+    double v;
+    if (zl >= 0 && zl < nz)
+      v = __ldg(U + ((int64_t)f * nz + zl) * plane + in_plane);
+    else if (!lo)
+      v = __ldg(U + ((int64_t)f * nz + (zl + nz) % nz) * plane + in_plane);
+    else if (zl < 0)
+      v = __ldg(lo + ((int64_t)f * NG + (zl + NG)) * plane + in_plane);
+    else
+      v = __ldg(hi + ((int64_t)f * NG + (zl - nz)) * plane + in_plane);
+    Up[e] = v;
   }
 }
 
@@ -65,8 +82,8 @@ __global__ void __launch_bounds__(256) k_star_stage(const double *__restrict__ U
                                                     const double *__restrict__ dudt,
                                                     const double *__restrict__ g,
                                                     const double *__restrict__ dtp, int n,
-                                                    double *__restrict__ Unew) {
-  const int64_t ncell = (int64_t)n * n * n;
+                                                    int nz, double *__restrict__ Unew) {
+  const int64_t ncell = (int64_t)n * n * nz;   // this slab's cells
   const int nb = n / 8;
   const double dt = *dtp;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ncell;
@@ -107,11 +124,17 @@ inline unsigned grid_for(int64_t n, int threads) {
 
 extern "C" {
 
-int tb_star_pad(tb_stream_t s, const double *U, int64_t n, double *Up) {
-  if (!U || !Up || n < 8 || n % 8) return TB_E_INVALID;
-  const int64_t P = n + 2 * NG;
-  k_star_pad<<<grid_for(NF * P * P * P, 256), 256, 0, strm(s)>>>(U, Up, (int)n);
+int tb_star_pad_slab(tb_stream_t s, const double *U, int64_t n, int64_t nz, const double *lo,
+                     const double *hi, double *Up) {
+  if (!U || !Up || n < 8 || n % 8 || nz < 8 || nz % 8 || (!lo != !hi)) return TB_E_INVALID;
+  const int64_t P = n + 2 * NG, Pz = nz + 2 * NG;
+  k_star_pad<<<grid_for(NF * P * P * Pz, 256), 256, 0, strm(s)>>>(U, lo, hi, Up, (int)n,
+                                                                  (int)nz);
   return tb::last_error();
+}
+
+int tb_star_pad(tb_stream_t s, const double *U, int64_t n, double *Up) {
+  return tb_star_pad_slab(s, U, n, n, nullptr, nullptr, Up);
 }
 
 int tb_star_cfl(tb_stream_t s, const double *amax, int64_t nsub, double dx, double cfl,
@@ -122,18 +145,18 @@ int tb_star_cfl(tb_stream_t s, const double *amax, int64_t nsub, double dx, doub
 }
 
 int tb_star_stage(tb_stream_t s, int stage, const double *U0, const double *Uc,
-                  const double *dudt, const double *g, const double *dt, int64_t n,
+                  const double *dudt, const double *g, const double *dt, int64_t n, int64_t nz,
                   double *Unew) {
-  if (!Uc || !dudt || !g || !dt || !Unew || n < 8 || n % 8 || (stage != 1 && stage != 2) ||
-      (stage == 2 && !U0))
+  if (!Uc || !dudt || !g || !dt || !Unew || n < 8 || n % 8 || nz < 8 || nz % 8 ||
+      (stage != 1 && stage != 2) || (stage == 2 && !U0))
     return TB_E_INVALID;
-  const int64_t cells = n * n * n;
+  const int64_t cells = n * n * nz;
   if (stage == 1)
     k_star_stage<1><<<grid_for(cells, 256), 256, 0, strm(s)>>>(U0, Uc, dudt, g, dt, (int)n,
-                                                                Unew);
+                                                                (int)nz, Unew);
   else
     k_star_stage<2><<<grid_for(cells, 256), 256, 0, strm(s)>>>(U0, Uc, dudt, g, dt, (int)n,
-                                                                Unew);
+                                                                (int)nz, Unew);
   return tb::last_error();
 }
 

@@ -67,8 +67,8 @@ class RotatingStarStep:
     def _rhs(self, Uc: torch.Tensor) -> None:
         s = self._s()
         N.call("tb_star_pad", s, Uc.data_ptr(), self.n, self.Up.data_ptr())
-        N.call("tb_hydro_flux_lattice", s, self.Up.data_ptr(), self.n, self.dudt.data_ptr(),
-               self.amax.data_ptr(), self.dx, self.gamma)
+        N.call("tb_hydro_flux_lattice", s, self.Up.data_ptr(), self.n, self.n,
+               self.dudt.data_ptr(), self.amax.data_ptr(), self.dx, self.gamma)
         self.gravity.solve(Uc[0])
 
     def _g(self) -> int:
@@ -80,10 +80,10 @@ class RotatingStarStep:
         N.call("tb_star_cfl", s, self.amax.data_ptr(), self.nsub, self.dx, self.cfl,
                self.dt.data_ptr())
         N.call("tb_star_stage", s, 1, None, self.U.data_ptr(), self.dudt.data_ptr(), self._g(),
-               self.dt.data_ptr(), self.n, self.U1.data_ptr())
+               self.dt.data_ptr(), self.n, self.n, self.U1.data_ptr())
         self._rhs(self.U1)
         N.call("tb_star_stage", s, 2, self.U.data_ptr(), self.U1.data_ptr(),
-               self.dudt.data_ptr(), self._g(), self.dt.data_ptr(), self.n,
+               self.dudt.data_ptr(), self._g(), self.dt.data_ptr(), self.n, self.n,
                self.U.data_ptr())
         self.time.add_(self.dt)
 

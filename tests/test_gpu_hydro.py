@@ -59,6 +59,6 @@ def test_lattice_tma_variant_equals_ghosted_variant(s):
     am = torch.empty_like(wa)
     st = torch.cuda.current_stream().cuda_stream
     N.call("tb_star_pad", st, U.data_ptr(), n, Up.data_ptr())
-    N.call("tb_hydro_flux_lattice", st, Up.data_ptr(), n, du.data_ptr(), am.data_ptr(), dx,
+    N.call("tb_hydro_flux_lattice", st, Up.data_ptr(), n, n, du.data_ptr(), am.data_ptr(), dx,
            5 / 3)
     assert torch.equal(du, want) and torch.equal(am, wa)
