@@ -399,6 +399,46 @@ def hydro_machine_ablation(subgrids=512, steps=8, repeats=3):
     return out
 
 
+def star_dist_bench(dev, rank, world, L=5, steps=5):
+    """The rotating-star step at max_level 5 split into z-slabs over the
+    job's ranks (StarSlab + DistDriver: NCCL halo planes of state and
+    multipole records, all-gathered coarse level, MIN-reduced dt); strong
+    scaling, CUDA events, max over ranks. Parity unpinned; bit-identical to
+    the single-device step (tests/test_gpu_star_dist.py)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2303_08058_b200.hydro import rotating_star
+    from paper_2303_08058_b200.star import subgrids_to_lattice
+    from paper_2303_08058_b200.star_dist import DistDriver, StarSlab, split_state
+    U = subgrids_to_lattice(rotating_star(8 ** L, device=dev)[0])
+    slab = StarSlab(L, world, rank, split_state(U, world)[rank])
+    del U
+    drv = DistDriver(slab)
+    for _ in range(2):
+        drv.step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(steps):
+        drv.step()
+    b.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([a.elapsed_time(b) / steps], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = t.item()
+    cells = (8 << L) ** 3
+    backend = dist.get_backend()
+    return {"config": f"rotating-star step, max_level {L} ({cells} cells) in {world} z-slabs "
+                      f"(one per rank, {backend}): halo planes of the state and of each "
+                      "partitioned FMM level's multipole records, all-gathered coarse level, "
+                      "MIN dt" + ("" if backend == "nccl" else
+                                  " [non-NCCL: host-staged code-path test, not a timing]"),
+            "ms_per_step": ms, "cells_per_s": cells / (ms * 1e-3), "scaling": "strong",
+            "n_gpus": world,
+            "parity": "unpinned (self-authored spec); bit-identical to the one-device step"}
+
+
 def run_reference_arm(args, workload_key, rank, world):
     if rank != 0:
         return 0
@@ -592,6 +632,9 @@ def main(argv=None):
                "api": "RingStepper.step_host (pinned H2D | K2 | D2H pipelined "
                       "over chunks on 3 streams, chained across steps)"}
 
+    star_dist = None
+    if world > 1 and not args.no_kernels:
+        star_dist = star_dist_bench(dev, rank, world)
     if rank == 0:
         peaks, peak_kind = measured_peaks()
         hbm = float(peaks.get("hbm_gbs", FALLBACK_HBM_GBS))
@@ -615,6 +658,8 @@ def main(argv=None):
         kernels = None
         if not args.no_kernels:
             kernels = north_star_kernels(dev)
+            if star_dist is not None:
+                kernels["star_step_dist"] = star_dist
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             v, cores, nsteps, el = cpu_reference_sample(per_gpu, args.cpu_budget)

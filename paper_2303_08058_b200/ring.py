@@ -254,6 +254,22 @@ class RingStepper:
         return dist.batch_isend_irecv(ops)
 
     def _exchange(self, send_left: torch.Tensor, send_right: torch.Tensor) -> None:
+        import torch.distributed as dist
+        if send_left.is_cuda and dist.get_backend(self.group) != "nccl":
+            # gloo cannot send device memory: stage the 64-byte faces on the host
+            left = (self.rank - 1) % self.world
+            right = (self.rank + 1) % self.world
+            sl, sr = send_left.cpu(), send_right.cpu()
+            h0, h1 = torch.empty_like(sl), torch.empty_like(sr)
+            ops = [dist.P2POp(dist.isend, sl, left, self.group),
+                   dist.P2POp(dist.irecv, h1, right, self.group),
+                   dist.P2POp(dist.isend, sr, right, self.group),
+                   dist.P2POp(dist.irecv, h0, left, self.group)]
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+            self.halo[0].copy_(h0)
+            self.halo[1].copy_(h1)
+            return
         for req in self._exchange_start(send_left, send_right):
             req.wait()
 
