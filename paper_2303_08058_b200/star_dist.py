@@ -104,23 +104,16 @@ class StarSlab:
 
     # ------------------------------------------------------------- phases --
     def _rhs(self, Uc: torch.Tensor) -> Iterator[tuple]:
+        """One right-hand side. Exchanges are posted ("halo", "allgather") and
+        awaited ("wait") only where their data is consumed, so on NCCL the
+        state halo flies under the FMM upward pass and the multipole halos /
+        gather under the hydro pad + flux."""
         s, n, nz = self._s(), self.n, self.nz
         self.send_lo.copy_(Uc[:, :4])
         self.send_hi.copy_(Uc[:, nz - 4:])
         yield ("halo", self.send_lo, self.send_hi, self.recv_lo, self.recv_hi, True)
-        # hydro on the slab: 2 ghost planes from each neighbour (periodic)
-        lo2 = self.recv_lo[:, 2:].contiguous()
-        hi2 = self.recv_hi[:, :2].contiguous()
-        N.call("tb_star_pad_slab", s, Uc.data_ptr(), n, nz, lo2.data_ptr(), hi2.data_ptr(),
-               self.Up.data_ptr())
-        N.call("tb_hydro_flux_lattice", s, self.Up.data_ptr(), n, nz, self.dudt.data_ptr(),
-               self.amax.data_ptr(), self.dx, self.gamma)
-        # gravity: rho with 4 halo planes (zero beyond the isolated domain)
-        if self.r > 0:
-            self.rho_h[:4].copy_(self.recv_lo[0])
+        # gravity upward pass: local planes only
         self.rho_h[4:4 + nz].copy_(Uc[0])
-        if self.r < self.R - 1:
-            self.rho_h[4 + nz:].copy_(self.recv_hi[0])
         rho = self.rho_h.data_ptr() + 4 * n * n * 8
         N.call("tb_fmm_slab_upward", s, self.L, self.R, self.r, rho, self.work.data_ptr())
         for level in range(self.lp, self.L):
@@ -130,6 +123,21 @@ class StarSlab:
         if self.R > 1:
             for full, a, b in self._gathered():
                 yield ("allgather", full, a, b)
+        yield ("wait", 0)                 # the state halo (posted first)
+        # hydro on the slab: 2 ghost planes from each neighbour (periodic)
+        lo2 = self.recv_lo[:, 2:].contiguous()
+        hi2 = self.recv_hi[:, :2].contiguous()
+        N.call("tb_star_pad_slab", s, Uc.data_ptr(), n, nz, lo2.data_ptr(), hi2.data_ptr(),
+               self.Up.data_ptr())
+        N.call("tb_hydro_flux_lattice", s, self.Up.data_ptr(), n, nz, self.dudt.data_ptr(),
+               self.amax.data_ptr(), self.dx, self.gamma)
+        # rho halo for the leaf stencil (zero beyond the isolated domain)
+        if self.r > 0:
+            self.rho_h[:4].copy_(self.recv_lo[0])
+        if self.r < self.R - 1:
+            self.rho_h[4 + nz:].copy_(self.recv_hi[0])
+        yield ("wait", None)              # everything else
+        if self.R > 1:
             N.call("tb_fmm_slab_coarse", s, self.L, self.R, self.r, self.work.data_ptr())
         N.call("tb_fmm_slab_m2l", s, self.L, self.R, self.r, self.work.data_ptr())
         N.call("tb_fmm_slab_downward", s, self.L, self.R, self.r, self.work.data_ptr())
@@ -144,6 +152,7 @@ class StarSlab:
         N.call("tb_star_cfl", s, self.amax.data_ptr(), self.nsub, self.dx, self.cfl,
                self.dt.data_ptr())
         yield ("min", self.dt)
+        yield ("wait", None)
         N.call("tb_star_stage", s, 1, None, self.U.data_ptr(), self.dudt.data_ptr(), g,
                self.dt.data_ptr(), n, nz, self.U1.data_ptr())
         yield from self._rhs(self.U1)
@@ -189,7 +198,7 @@ class VirtualCluster:
             m = torch.stack([q[1] for q in reqs]).min(dim=0).values
             for q in reqs:
                 q[1].copy_(m)
-        else:
+        elif kind != "wait":              # copies above complete in stream order
             raise ValueError(kind)
 
     def step(self) -> None:
@@ -218,6 +227,7 @@ class DistDriver:
         self.dist, self.slab, self.group = dist, slab, group
         self.R, self.r = slab.R, slab.r
         self.host = dist.get_backend(group) != "nccl"
+        self.pending: list = []
 
     def _h(self, t: torch.Tensor) -> torch.Tensor:
         return t.cpu() if self.host else t
@@ -232,8 +242,10 @@ class DistDriver:
         below, above = (r - 1) % R, (r + 1) % R
         has_below, has_above = periodic or r > 0, periodic or r < R - 1
         s_lo, s_hi = self._h(send_lo.contiguous()), self._h(send_hi.contiguous())
-        r_lo = torch.empty_like(s_lo) if has_below else None
-        r_hi = torch.empty_like(s_hi) if has_above else None
+        # NCCL receives straight into the (contiguous) targets; host staging
+        # copies them in when the exchange is awaited
+        r_lo = (recv_lo if not self.host else torch.empty_like(s_lo)) if has_below else None
+        r_hi = (recv_hi if not self.host else torch.empty_like(s_hi)) if has_above else None
         ops = []
         # sends (lo down, hi up), receives (hi from above, lo from below): with
         # two ranks both neighbours coincide and issue order pairs them up
@@ -245,23 +257,36 @@ class DistDriver:
             ops.append(dist.P2POp(dist.irecv, r_hi, above, self.group))
         if has_below:
             ops.append(dist.P2POp(dist.irecv, r_lo, below, self.group))
-        for w in dist.batch_isend_irecv(ops):
-            w.wait()
-        if has_below:
-            recv_lo.copy_(r_lo)
-        if has_above:
-            recv_hi.copy_(r_hi)
+        works = dist.batch_isend_irecv(ops)
+        copies = []
+        if self.host:
+            if has_below:
+                copies.append((recv_lo, r_lo))
+            if has_above:
+                copies.append((recv_hi, r_hi))
+        self.pending.append((works, copies, (s_lo, s_hi)))
 
     def _allgather(self, full, a, b) -> None:
         if self.R == 1:
             return
         dist = self.dist
         if not self.host:
-            dist.all_gather_into_tensor(full, full[a:b].clone(), group=self.group)
+            src = full[a:b].clone()
+            w = dist.all_gather_into_tensor(full, src, group=self.group, async_op=True)
+            self.pending.append(([w], [], (src,)))
             return
         parts = [torch.empty(b - a, dtype=full.dtype) for _ in range(self.R)]
-        dist.all_gather(parts, full[a:b].cpu(), group=self.group)
-        full.copy_(torch.cat(parts))
+        w = dist.all_gather(parts, full[a:b].cpu(), group=self.group, async_op=True)
+        self.pending.append(([w], [(full, parts)], ()))
+
+    def _wait(self, first_only: bool) -> None:
+        todo = self.pending[:1] if first_only else self.pending
+        for works, copies, _ in todo:
+            for w in works:
+                w.wait()
+            for dst, src in copies:
+                dst.copy_(torch.cat(src) if isinstance(src, list) else src)
+        self.pending = self.pending[1:] if first_only else []
 
     def _min(self, t) -> None:
         if self.R == 1:
@@ -272,6 +297,7 @@ class DistDriver:
             t.copy_(h)
 
     def step(self) -> None:
+        self.pending = []
         for req in self.slab.step_gen():
             kind = req[0]
             if kind == "halo":
@@ -280,3 +306,6 @@ class DistDriver:
                 self._allgather(*req[1:])
             elif kind == "min":
                 self._min(req[1])
+            elif kind == "wait":
+                self._wait(first_only=req[1] == 0)
+        self._wait(first_only=False)

@@ -64,6 +64,13 @@ class _FakeSlab:
         self.R, self.r = R, r
 
 
+def test_virtual_wait_is_a_no_op():
+    from paper_2303_08058_b200.star_dist import VirtualCluster
+    vc = VirtualCluster.__new__(VirtualCluster)
+    vc.ranks = 2
+    vc._service([("wait", 0), ("wait", 0)])
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -81,9 +88,11 @@ def _worker(rank, world, port, q):
         for periodic in (True, False):
             _, lo, hi, rlo, rhi, _ = _reqs(world, "halo", periodic)[rank]
             drv._halo(lo, hi, rlo, rhi, periodic)
+            drv._wait(first_only=False)
             res[periodic] = (rlo.clone(), rhi.clone())
         _, full, a, b = _reqs(world, "allgather")[rank]
         drv._allgather(full, a, b)
+        drv._wait(first_only=False)
         m = _reqs(world, "min")[rank][1]
         drv._min(m)
         q.put((rank, res, full, m.item()))
