@@ -304,7 +304,23 @@ struct StepArgs {
   int64_t *acc;
   double *piece, *dt, *checksum;   // fused finalize outputs (single device)
   int finalize;
+  // deferred finalize: the grid's last CTA rounds the PREVIOUS step's
+  // accumulator (prev_acc -> prev_piece, prev_dt, checksum += piece, reset)
+  // while the others stream this step; no ticket, no serial tail
+  int64_t *prev_acc;
+  double *prev_piece, *prev_dt;
+  int finalizer;
 };
+
+// The finalizer CTA of a deferred-finalize launch; returns true if this CTA
+// was it (it does nothing else).
+__device__ void warp_finalize(int64_t *acc, double *piece, double *dt,
+                              double *checksum, int reset);
+__device__ __forceinline__ bool finalizer_cta(const StepArgs &a) {
+  if (!a.finalizer || blockIdx.x != gridDim.x - 1) return false;
+  if (threadIdx.x < 32) warp_finalize(a.prev_acc, a.prev_piece, a.prev_dt, a.checksum, 1);
+  return true;
+}
 
 template <int CHAINS, int KPC>
 __device__ __forceinline__ void run_chains(double (&v)[16], int chains, int kpc) {
@@ -346,10 +362,58 @@ __device__ __forceinline__ double load_face(const StepArgs &a, int64_t g, int la
   return 0.0;
 }
 
+// Lane 0's register window over the exact accumulator: the sums of one
+// warp's sub-grids mostly share their 3-digit limb window, so their digits
+// are added in registers and reach the shared limbs (3 atomics) only when the
+// window moves and at the end. Signed 64-bit digit sums cannot overflow
+// (< 2^31 additions of 32-bit digits).
+struct AccCache {
+  int limb = -1;
+  long long d0 = 0, d1 = 0, d2 = 0;
+  __device__ __forceinline__ void flush(unsigned long long *limbs) {
+    if (limb < 0) return;
+    if (d0) atomicAdd(limbs + limb, (unsigned long long)d0);
+    if (d1) atomicAdd(limbs + limb + 1, (unsigned long long)d1);
+    if (d2) atomicAdd(limbs + limb + 2, (unsigned long long)d2);
+    limb = -1;
+    d0 = d1 = d2 = 0;
+  }
+  __device__ __forceinline__ void add(unsigned long long *limbs, double x) {
+    if (x == 0.0) return;
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
+    const int ex = (int)((bits >> 52) & 0x7ff);
+    unsigned long long mant = bits & ((1ULL << 52) - 1);
+    int p = 0;
+    if (ex != 0) {
+      mant |= 1ULL << 52;
+      p = ex - 1;
+    }
+    const int l = p >> 5, off = p & 31;
+    const unsigned long long lo = mant << off;
+    const unsigned long long hi = off ? (mant >> (64 - off)) : 0ULL;
+    const long long e0 = (long long)(lo & 0xffffffffULL), e1 = (long long)(lo >> 32),
+                    e2 = (long long)hi;
+    if (l != limb) {
+      flush(limbs);
+      limb = l;
+    }
+    if ((long long)bits < 0) {
+      d0 -= e0;
+      d1 -= e1;
+      d2 -= e2;
+    } else {
+      d0 += e0;
+      d1 += e1;
+      d2 += e2;
+    }
+  }
+};
+
 template <int CHAINS, int KPC>
 __device__ __forceinline__ void subgrid_body(const StepArgs &a, int64_t g, int lane,
                                              double (&v)[16], double face,
-                                             unsigned long long *s_limbs, double &wmin) {
+                                             unsigned long long *s_limbs, double &wmin,
+                                             AccCache &cache) {
   const int r = lane & 7;
   // Ghost fold against the previous generation: cells 0..7 are lanes 0..7 at
   // i = 0; cells 504..511 are lanes 24..31 at i = 15. Add rounds; *0.5 exact.
@@ -377,8 +441,8 @@ __device__ __forceinline__ void subgrid_body(const StepArgs &a, int64_t g, int l
   if (lane == 0) {
     if (a.sums) a.sums[g] = s;
     if (a.mins) a.mins[g] = m;
-    if (a.acc) acc_add_digits(s_limbs, s);
   }
+  if (a.acc && lane == 0) cache.add(s_limbs, s);
   wmin = fmin(wmin, m);
 }
 
@@ -386,9 +450,11 @@ __device__ __forceinline__ void subgrid_body(const StepArgs &a, int64_t g, int l
 // last CTA to finish (threadfence + ticket) closes the step with one warp.
 __device__ __forceinline__ void step_epilogue(const StepArgs &a,
                                               unsigned long long *s_limbs,
-                                              long long *s_min, double wmin) {
+                                              long long *s_min, double wmin,
+                                              AccCache *cache = nullptr) {
   if (!a.acc) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (cache && lane == 0) cache->flush(s_limbs);
   if (lane == 0) s_min[warp] = min_key(wmin);
   __syncthreads();                    // the CTA's limbs and warp minima are in smem
   if (warp != 0) return;              // warp 0 publishes; the rest retire now
@@ -423,6 +489,7 @@ template <int CHAINS, int KPC, bool PF, int MINB = 1>
 __global__ void __launch_bounds__(kStepThreads, MINB) k_step(StepArgs a) {
   __shared__ unsigned long long s_limbs[TB_ACC_LIMBS];
   __shared__ long long s_min[kStepWarps];
+  if (finalizer_cta(a)) return;
   if (a.acc) {
     for (int i = threadIdx.x; i < TB_ACC_LIMBS; i += blockDim.x) s_limbs[i] = 0ULL;
     __syncthreads();
@@ -430,8 +497,9 @@ __global__ void __launch_bounds__(kStepThreads, MINB) k_step(StepArgs a) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int lane_off = 128 * (lane >> 3) + (lane & 7);
-  const int64_t gstride = (int64_t)gridDim.x * kStepWarps;
+  const int64_t gstride = (int64_t)(gridDim.x - a.finalizer) * kStepWarps;
   double wmin = CUDART_INF;
+  AccCache cache;
   int64_t g = (int64_t)blockIdx.x * kStepWarps + warp;
   if (PF) {
     double nxt[16], nface = 0.0;
@@ -453,7 +521,7 @@ __global__ void __launch_bounds__(kStepThreads, MINB) k_step(StepArgs a) {
         for (int i = 0; i < 16; ++i) nxt[i] = ld_stream(src + 8 * i);
         nface = load_face(a, gn, lane);
       }
-      subgrid_body<CHAINS, KPC>(a, g, lane, v, face, s_limbs, wmin);
+      subgrid_body<CHAINS, KPC>(a, g, lane, v, face, s_limbs, wmin, cache);
     }
   } else {
     for (; g < a.n; g += gstride) {
@@ -462,10 +530,10 @@ __global__ void __launch_bounds__(kStepThreads, MINB) k_step(StepArgs a) {
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] = ld_stream(src + 8 * i);
       const double face = load_face(a, g, lane);
-      subgrid_body<CHAINS, KPC>(a, g, lane, v, face, s_limbs, wmin);
+      subgrid_body<CHAINS, KPC>(a, g, lane, v, face, s_limbs, wmin, cache);
     }
   }
-  step_epilogue(a, s_limbs, s_min, wmin);
+  step_epilogue(a, s_limbs, s_min, wmin, &cache);
 }
 
 // K2c: a warp PAIR per sub-grid, 8 cells per lane (half the registers of
@@ -501,6 +569,7 @@ __global__ void __launch_bounds__(kStepThreads, 6) k_step_pair(StepArgs a) {
   __shared__ unsigned long long s_limbs[TB_ACC_LIMBS];
   __shared__ long long s_min[kStepWarps];
   __shared__ double s_pair[2][kStepWarps / 2][2][2];   // [parity][pair][q][sum,min]
+  if (finalizer_cta(a)) return;
   if (a.acc) {
     for (int i = threadIdx.x; i < TB_ACC_LIMBS; i += blockDim.x) s_limbs[i] = 0ULL;
     __syncthreads();
@@ -515,7 +584,7 @@ __global__ void __launch_bounds__(kStepThreads, 6) k_step_pair(StepArgs a) {
   double wmin = CUDART_INF;
   int it = 0;
   for (int64_t g = (int64_t)blockIdx.x * kPairs + pair; g < a.n;
-       g += (int64_t)gridDim.x * kPairs, ++it) {
+       g += (int64_t)(gridDim.x - a.finalizer) * kPairs, ++it) {
     const double *src = a.old + g * TB_CELLS + lane_off;
     double v[8];
 #pragma unroll
@@ -609,6 +678,7 @@ __global__ void __launch_bounds__(kStepThreads) k_step_bulk(StepArgs a) {
   __shared__ __align__(8) uint64_t bars[kStepWarps][kStages];
   __shared__ unsigned long long s_limbs[TB_ACC_LIMBS];
   __shared__ long long s_min[kStepWarps];
+  if (finalizer_cta(a)) return;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < TB_ACC_LIMBS; i += blockDim.x) s_limbs[i] = 0ULL;
@@ -617,7 +687,7 @@ __global__ void __launch_bounds__(kStepThreads) k_step_bulk(StepArgs a) {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
   double *slots = ring + (size_t)warp * kStages * kSlot;
-  const int64_t gstride = (int64_t)gridDim.x * kStepWarps;
+  const int64_t gstride = (int64_t)(gridDim.x - a.finalizer) * kStepWarps;
   const int64_t g0 = (int64_t)blockIdx.x * kStepWarps + warp;
   if (lane == 0) {
 #pragma unroll
@@ -627,6 +697,7 @@ __global__ void __launch_bounds__(kStepThreads) k_step_bulk(StepArgs a) {
     }
   }
   double wmin = CUDART_INF;
+  AccCache cache;
   int it = 0;
   for (int64_t g = g0; g < a.n; g += gstride, ++it) {
     const int s = it % kStages;
@@ -646,9 +717,9 @@ __global__ void __launch_bounds__(kStepThreads) k_step_bulk(StepArgs a) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       bulk_load_subgrid(slots + s * kSlot, a.old + gn * TB_CELLS, &bars[warp][s]);
     }
-    subgrid_body<CHAINS, KPC>(a, g, lane, v, face, s_limbs, wmin);
+    subgrid_body<CHAINS, KPC>(a, g, lane, v, face, s_limbs, wmin, cache);
   }
-  step_epilogue(a, s_limbs, s_min, wmin);
+  step_epilogue(a, s_limbs, s_min, wmin, &cache);
 }
 
 int g_step_impl = TB_STEP_AUTO;
@@ -656,7 +727,19 @@ int g_step_spw = 0;   // sub-grids per warp per CTA; 0 = persistent (one wave)
 
 // CTAs for n sub-grids: one resident wave (occ CTAs per SM) by default, or
 // ceil(n / (warps * spw)) CTAs so the hardware scheduler balances the tail.
-inline int step_grid(int64_t n, int occ) {
+inline int step_grid_streaming(int64_t n, int occ);
+// + the finalizer CTA when it is used (kept co-resident: at most occ*SMs CTAs)
+inline int step_grid(int64_t n, int occ, int finalizer = 0) {
+  int b = step_grid_streaming(n, occ);
+  if (finalizer) {
+    const int cap = tb::sm_count() * occ;
+    if (b >= cap && cap > 1) b = cap - 1;
+    b += 1;
+  }
+  return b;
+}
+
+inline int step_grid_streaming(int64_t n, int occ) {
   if (g_step_spw > 0) {
     int64_t b = (n + (int64_t)kStepWarps * g_step_spw - 1) / ((int64_t)kStepWarps * g_step_spw);
     return (int)(b < 1 ? 1 : (b > (1LL << 30) ? (1LL << 30) : b));
@@ -692,7 +775,7 @@ void launch_bulk(cudaStream_t st, const StepArgs &a) {
     occ = occupancy(k_step_bulk<CHAINS, KPC, STAGES>, bulk_smem(STAGES));
   }
   k_step_bulk<CHAINS, KPC, STAGES>
-      <<<step_grid(a.n, occ), kStepThreads, bulk_smem(STAGES), st>>>(a);
+      <<<step_grid(a.n, occ, a.finalizer), kStepThreads, bulk_smem(STAGES), st>>>(a);
 }
 
 int launch_step(cudaStream_t st, StepArgs a) {
@@ -723,24 +806,24 @@ int launch_step(cudaStream_t st, StepArgs a) {
     static int occ_f = 0, occ_g = 0;
     if (fixed) {
       if (!occ_f) occ_f = occupancy(k_step<3, 5, true>, 0);
-      const int blocks = step_grid(a.n, occ_f);
+      const int blocks = step_grid(a.n, occ_f, a.finalizer);
       k_step<3, 5, true><<<blocks, kStepThreads, 0, st>>>(a);
     } else {
       if (!occ_g) occ_g = occupancy(k_step<0, 0, true>, 0);
-      const int blocks = step_grid(a.n, occ_g);
+      const int blocks = step_grid(a.n, occ_g, a.finalizer);
       k_step<0, 0, true><<<blocks, kStepThreads, 0, st>>>(a);
     }
   } else if (g_step_impl == TB_STEP_LEAN && fixed) {
     // registers capped at 48 (5 CTAs = 40 warps per SM; a few spill slots)
     static int occ = 0;
     if (!occ) occ = occupancy(k_step<3, 5, false, 5>, 0);
-    k_step<3, 5, false, 5><<<step_grid(a.n, occ), kStepThreads, 0, st>>>(a);
+    k_step<3, 5, false, 5><<<step_grid(a.n, occ, a.finalizer), kStepThreads, 0, st>>>(a);
   } else if (g_step_impl == TB_STEP_PAIR) {
     // a warp pair per sub-grid: the grid helper counts pairs as "warps"
     static int occ_f = 0, occ_g = 0;
     int &occ = fixed ? occ_f : occ_g;
     if (!occ) occ = fixed ? occupancy(k_step_pair<3, 5>, 0) : occupancy(k_step_pair<0, 0>, 0);
-    const int blocks = step_grid(2 * a.n, occ);
+    const int blocks = step_grid(2 * a.n, occ, a.finalizer);
     if (fixed)
       k_step_pair<3, 5><<<blocks, kStepThreads, 0, st>>>(a);
     else
@@ -749,11 +832,11 @@ int launch_step(cudaStream_t st, StepArgs a) {
     static int occ_f = 0, occ_g = 0;
     if (fixed) {
       if (!occ_f) occ_f = occupancy(k_step<3, 5, false>, 0);
-      const int blocks = step_grid(a.n, occ_f);
+      const int blocks = step_grid(a.n, occ_f, a.finalizer);
       k_step<3, 5, false><<<blocks, kStepThreads, 0, st>>>(a);
     } else {
       if (!occ_g) occ_g = occupancy(k_step<0, 0, false>, 0);
-      const int blocks = step_grid(a.n, occ_g);
+      const int blocks = step_grid(a.n, occ_g, a.finalizer);
       k_step<0, 0, false><<<blocks, kStepThreads, 0, st>>>(a);
     }
   }
@@ -888,7 +971,7 @@ static int step_args(StepArgs *a, const double *old, double *out, int64_t n,
   if (n > 0 && (!old || !out || old == out || !left_face || !right_face))
     return TB_E_INVALID;
   *a = StepArgs{old, out, n, left_face, right_face, chains, kpc, mins, sums, acc,
-                nullptr, nullptr, nullptr, 0};
+                nullptr, nullptr, nullptr, 0, nullptr, nullptr, nullptr, 0};
   return TB_OK;
 }
 
@@ -917,6 +1000,28 @@ int tb_step_final(tb_stream_t s, const double *old, double *out, int64_t n,
   a.dt = dt;
   a.checksum = checksum;
   a.finalize = 1;
+  return launch_step(reinterpret_cast<cudaStream_t>(s), a);
+}
+
+int tb_step_deferred(tb_stream_t s, const double *old, double *out, int64_t n,
+                     const double *left_face, const double *right_face, int chains,
+                     int kernels_per_chain, double *mins, double *sums, int64_t *acc,
+                     int64_t *prev_acc, double *prev_piece, double *prev_dt,
+                     double *checksum) {
+  StepArgs a;
+  int r = step_args(&a, old, out, n, left_face, right_face, chains, kernels_per_chain,
+                    mins, sums, acc);
+  if (r != TB_OK) return r;
+  if (!acc || acc == prev_acc) return TB_E_INVALID;
+  if (n == 0) return prev_acc ? tb_acc_finalize(s, prev_acc, prev_piece, prev_dt, checksum, 1)
+                              : TB_OK;
+  if (prev_acc) {
+    a.prev_acc = prev_acc;
+    a.prev_piece = prev_piece;
+    a.prev_dt = prev_dt;
+    a.checksum = checksum;
+    a.finalizer = 1;
+  }
   return launch_step(reinterpret_cast<cudaStream_t>(s), a);
 }
 

@@ -98,6 +98,12 @@ class CudaRingOps:
                _ptr(left_face), _ptr(right_face), chains, kpc, _ptr(mins), _ptr(sums),
                _ptr(acc), _ptr(piece), _ptr(dt), _ptr(checksum))
 
+    def step_deferred(self, old, out, left_face, right_face, chains, kpc, acc, prev_acc,
+                      prev_piece, prev_dt, checksum, mins=None, sums=None) -> None:
+        N.call("tb_step_deferred", self.stream(), _ptr(old), _ptr(out), old.shape[0],
+               _ptr(left_face), _ptr(right_face), chains, kpc, _ptr(mins), _ptr(sums),
+               _ptr(acc), _ptr(prev_acc), _ptr(prev_piece), _ptr(prev_dt), _ptr(checksum))
+
     def acc_reset(self, acc) -> None:
         N.call("tb_acc_reset", self.stream(), _ptr(acc))
 
@@ -156,6 +162,13 @@ class RingStepper:
         self._host_prev = None
         self.ops.init_cells(self.state[0], subgrids, self.lo)
         self.ops.acc_reset(self.acc)
+        # single device, back to back: step k accumulates into accd[k & 1] and
+        # step k+1's launch closes it (tb_step_deferred); `pending` = the step
+        # whose accumulator still awaits that
+        self.accd = torch.zeros((2, N.TB_ACC_WORDS), dtype=torch.int64, device=device)
+        self.ops.acc_reset(self.accd[0])
+        self.ops.acc_reset(self.accd[1])
+        self._pending: Optional[int] = None
         # Multi-GPU halo: "p2p" maps the ring neighbours' state buffers (CUDA
         # IPC) so K2 reads the ghost faces straight from their HBM; "nccl"
         # sends them with NCCL P2P; "auto" tries p2p, else nccl.
@@ -313,7 +326,16 @@ class RingStepper:
             lf, rf = old[n - 1, CELLS - FACE:], old[0, :FACE]   # ring wraps locally
             if kernel_events is not None:
                 kernel_events[0].record()
-            if hasattr(self.ops, "step_final"):
+            if hasattr(self.ops, "step_deferred"):
+                p = self._pending
+                self.ops.step_deferred(
+                    old, out, lf, rf, self.chains, self.kpc, self.accd[k & 1],
+                    None if p is None else self.accd[p & 1],
+                    None if p is None else self.pieces[p:p + 1],
+                    None if p is None else self.dts[p:p + 1], self.checksum,
+                    self.mins, self.sums)
+                self._pending = k
+            elif hasattr(self.ops, "step_final"):
                 self.ops.step_final(old, out, lf, rf, self.chains, self.kpc, self.acc,
                                     self.pieces[k:k + 1], self.dts[k:k + 1],
                                     self.checksum, self.mins, self.sums)
@@ -367,6 +389,15 @@ class RingStepper:
         if kernel_events is not None:
             kernel_events[1].record()
 
+    def flush(self) -> None:
+        """Close the last device step's deferred accumulator (its piece, dt
+        and checksum contribution are then final)."""
+        p = self._pending
+        if p is not None:
+            self.ops.acc_finalize(self.accd[p & 1], self.pieces[p:p + 1], self.dts[p:p + 1],
+                                  self.checksum)
+            self._pending = None
+
     def run(self, steps: int) -> RingResult:
         k0 = self.steps_done
         for _ in range(steps):
@@ -397,6 +428,7 @@ class RingStepper:
             raise RuntimeError("max_steps exceeded; raise max_steps")
         if not isinstance(self.ops, CudaRingOps):
             raise RuntimeError("step_host needs the CUDA ops")
+        self.flush()          # a preceding device step's checksum piece comes first
         dev = self.device
         main = torch.cuda.current_stream(dev)
         if self._streams is None:
@@ -485,6 +517,7 @@ class RingStepper:
             torch.cuda.current_stream(self.device).wait_stream(self._streams[1])
 
     def result(self, first_step: int = 0) -> RingResult:
+        self.flush()
         k = self.steps_done
         return RingResult(checksum=float(self.checksum.item()),
                           dts=self.dts[first_step:k].tolist(),
