@@ -178,18 +178,22 @@ int tb_step_final(tb_stream_t s, const double *old, double *out, int64_t n,
                   const double *left_face, const double *right_face, int chains,
                   int kernels_per_chain, double *mins, double *sums, int64_t *acc,
                   double *piece, double *dt, double *checksum);
-/* tb_step with the previous step closed inside this launch (single device,
- * back-to-back steps): one extra CTA rounds prev_acc exactly as
- * tb_acc_finalize(..., reset=1) would (prev_piece, prev_dt, *checksum +=
- * prev_piece) while the others stream this step into acc — the rounding
- * leaves the step's critical path. Accumulators alternate (acc != prev_acc);
- * prev_acc = NULL on the first step; the last step is closed with
- * tb_acc_finalize. */
+/* Back-to-back single-device steps with the exact close off the critical
+ * path: this launch only writes each sub-grid's pairwise sum and min (sums,
+ * mins: [n], required — the reference's per-sub-grid outputs,
+ * src/miniapp.py:133), and one extra CTA reduces the PREVIOUS step's
+ * (prev_sums, prev_mins) — exact sum == math.fsum, min — through the scratch
+ * accumulator acc into prev_piece / prev_dt and *checksum += prev_piece while
+ * the other CTAs stream. prev_sums = NULL on the first step; sums/mins must
+ * alternate between two buffers; tb_step_close closes the last step (one
+ * CTA). */
 int tb_step_deferred(tb_stream_t s, const double *old, double *out, int64_t n,
                      const double *left_face, const double *right_face, int chains,
-                     int kernels_per_chain, double *mins, double *sums, int64_t *acc,
-                     int64_t *prev_acc, double *prev_piece, double *prev_dt,
-                     double *checksum);
+                     int kernels_per_chain, double *sums, double *mins,
+                     const double *prev_sums, const double *prev_mins, int64_t *acc,
+                     double *prev_piece, double *prev_dt, double *checksum);
+int tb_step_close(tb_stream_t s, const double *sums, const double *mins, int64_t n,
+                  int64_t *acc, double *piece, double *dt, double *checksum);
 /* Zero an accumulator (limbs = 0, min = +inf). */
 int tb_acc_reset(tb_stream_t s, int64_t *acc);
 /* Exact sum of n doubles into acc (the reduction half of tb_step). */

@@ -122,7 +122,8 @@ SIGNATURES = {
     "tb_step_final": [_u64, _vp, _vp, _i64, _vp, _vp, _int, _int, _vp, _vp, _vp, _vp, _vp,
                       _vp],
     "tb_step_deferred": [_u64, _vp, _vp, _i64, _vp, _vp, _int, _int, _vp, _vp, _vp, _vp, _vp,
-                         _vp, _vp],
+                         _vp, _vp, _vp],
+    "tb_step_close": [_u64, _vp, _vp, _i64, _vp, _vp, _vp, _vp],
     "tb_acc_reset": [_u64, _vp],
     "tb_acc_add": [_u64, _vp, _i64, _vp],
     "tb_acc_finalize": [_u64, _vp, _vp, _vp, _vp, _int],

@@ -280,6 +280,38 @@ __global__ void k_acc_finalize(int64_t *acc, double *piece, double *dt,
   if (threadIdx.x < 32) warp_finalize(acc, piece, dt, checksum, reset);
 }
 
+__device__ void warp_acc_flush_strided(const double *sums, int64_t first, int64_t stride,
+                                       int64_t n, unsigned long long *limbs);
+
+// Close a step from its per-sub-grid (sum, min) in one standalone launch
+// (tb_step_close: the last step of a deferred run): exact digits of every
+// sum, min of the mins, then the one-warp correctly rounded result ==
+// math.fsum of the sums and the min-tree dt (src/miniapp.py:138-171).
+__global__ void __launch_bounds__(256) k_step_close(const double *sums, const double *mins,
+                                                    int64_t n, int64_t *acc, double *piece,
+                                                    double *dt, double *checksum) {
+  __shared__ unsigned long long c_limbs[TB_ACC_LIMBS];
+  __shared__ long long c_min;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  for (int i = t; i < TB_ACC_LIMBS; i += blockDim.x) c_limbs[i] = 0ULL;
+  if (t == 0) c_min = kKeyInf;
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  // warp w takes sums w, w + nw, ... (32 at a time, warp-merged digits)
+  warp_acc_flush_strided(sums, warp, nw, n, c_limbs);
+  double m = CUDART_INF;
+  for (int64_t i = t; i < n; i += blockDim.x) m = fmin(m, __ldcg(mins + i));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) atomicMin(&c_min, min_key(m));
+  __syncthreads();
+  for (int i = t; i < TB_ACC_WORDS; i += blockDim.x)
+    acc[i] = i < TB_ACC_LIMBS ? (long long)c_limbs[i] : (i == TB_ACC_MIN_WORD ? c_min : 0);
+  __threadfence_block();
+  __syncthreads();
+  if (t < 32) warp_finalize(acc, piece, dt, checksum, 1);
+}
+
 // ------------------------------------------------------------------ K2 --
 constexpr int kStepThreads = 256;
 constexpr int kStepWarps = kStepThreads / 32;
@@ -304,21 +336,35 @@ struct StepArgs {
   int64_t *acc;
   double *piece, *dt, *checksum;   // fused finalize outputs (single device)
   int finalize;
-  // deferred finalize: the grid's last CTA rounds the PREVIOUS step's
-  // accumulator (prev_acc -> prev_piece, prev_dt, checksum += piece, reset)
-  // while the others stream this step; no ticket, no serial tail
+  // deferred close: this launch writes only per-sub-grid (sum, min); every
+  // streaming warp folds its share of the PREVIOUS step's (prev_sums,
+  // prev_mins) exactly into prev_acc early in the launch, and the grid's
+  // extra last CTA waits for all shares and rounds them into prev_piece /
+  // prev_dt, checksum += piece
   int64_t *prev_acc;
+  const double *prev_sums, *prev_mins;
   double *prev_piece, *prev_dt;
   int finalizer;
 };
 
-// The finalizer CTA of a deferred-finalize launch; returns true if this CTA
-// was it (it does nothing else).
 __device__ void warp_finalize(int64_t *acc, double *piece, double *dt,
                               double *checksum, int reset);
+__device__ __forceinline__ long long ld_acquire_s64(const int64_t *p) {
+  long long v;
+  asm volatile("ld.acquire.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// The deferred close's extra CTA (returns true if this CTA is it): waits for
+// every streaming CTA's share of the previous step (the count word), then
+// rounds. The shares arrive early in the launch, so this is off the step's
+// critical path.
 __device__ __forceinline__ bool finalizer_cta(const StepArgs &a) {
   if (!a.finalizer || blockIdx.x != gridDim.x - 1) return false;
-  if (threadIdx.x < 32) warp_finalize(a.prev_acc, a.prev_piece, a.prev_dt, a.checksum, 1);
+  if (threadIdx.x < 32) {
+    const long long want = (long long)gridDim.x - 1;
+    while (ld_acquire_s64(a.prev_acc + TB_ACC_COUNT_WORD) < want) __nanosleep(256);
+    warp_finalize(a.prev_acc, a.prev_piece, a.prev_dt, a.checksum, 1);
+  }
   return true;
 }
 
@@ -362,58 +408,161 @@ __device__ __forceinline__ double load_face(const StepArgs &a, int64_t g, int la
   return 0.0;
 }
 
-// Lane 0's register window over the exact accumulator: the sums of one
-// warp's sub-grids mostly share their 3-digit limb window, so their digits
-// are added in registers and reach the shared limbs (3 atomics) only when the
-// window moves and at the end. Signed 64-bit digit sums cannot overflow
-// (< 2^31 additions of 32-bit digits).
-struct AccCache {
-  int limb = -1;
-  long long d0 = 0, d1 = 0, d2 = 0;
-  __device__ __forceinline__ void flush(unsigned long long *limbs) {
-    if (limb < 0) return;
-    if (d0) atomicAdd(limbs + limb, (unsigned long long)d0);
-    if (d1) atomicAdd(limbs + limb + 1, (unsigned long long)d1);
-    if (d2) atomicAdd(limbs + limb + 2, (unsigned long long)d2);
-    limb = -1;
-    d0 = d1 = d2 = 0;
-  }
-  __device__ __forceinline__ void add(unsigned long long *limbs, double x) {
-    if (x == 0.0) return;
-    const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
-    const int ex = (int)((bits >> 52) & 0x7ff);
-    unsigned long long mant = bits & ((1ULL << 52) - 1);
-    int p = 0;
-    if (ex != 0) {
-      mant |= 1ULL << 52;
-      p = ex - 1;
-    }
-    const int l = p >> 5, off = p & 31;
-    const unsigned long long lo = mant << off;
-    const unsigned long long hi = off ? (mant >> (64 - off)) : 0ULL;
-    const long long e0 = (long long)(lo & 0xffffffffULL), e1 = (long long)(lo >> 32),
-                    e2 = (long long)hi;
-    if (l != limb) {
-      flush(limbs);
-      limb = l;
-    }
-    if ((long long)bits < 0) {
-      d0 -= e0;
-      d1 -= e1;
-      d2 -= e2;
-    } else {
-      d0 += e0;
-      d1 += e1;
-      d2 += e2;
-    }
-  }
+// Exact accumulation off the per-sub-grid path: lane 0 parks each sub-grid's
+// sum in its warp's shared buffer (one store); every kSumBuf sub-grids and at
+// the end the warp converts 32 sums at a time in parallel and, when they share
+// their 3-digit window (the common case), warp-reduces the digits so lane 0
+// issues just 3 shared atomics.
+constexpr int kSumBuf = 64;
+
+struct SumBuf {
+  int cnt = 0;
 };
+
+__device__ __forceinline__ long long shfl_sum_s64(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ void warp_acc_flush(const double *sums, int cnt, unsigned long long *limbs) {
+  const int lane = threadIdx.x & 31;
+  for (int base = 0; base < cnt; base += 32) {
+    const double x = base + lane < cnt ? sums[base + lane] : 0.0;
+    int l = -1;
+    long long d0 = 0, d1 = 0, d2 = 0;
+    if (x != 0.0) {
+      const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
+      const int ex = (int)((bits >> 52) & 0x7ff);
+      unsigned long long mant = bits & ((1ULL << 52) - 1);
+      int p = 0;
+      if (ex != 0) {
+        mant |= 1ULL << 52;
+        p = ex - 1;
+      }
+      l = p >> 5;
+      const int off = p & 31;
+      const unsigned long long lo = mant << off;
+      const unsigned long long hi = off ? (mant >> (64 - off)) : 0ULL;
+      d0 = (long long)(lo & 0xffffffffULL);
+      d1 = (long long)(lo >> 32);
+      d2 = (long long)hi;
+      if ((long long)bits < 0) {
+        d0 = -d0;
+        d1 = -d1;
+        d2 = -d2;
+      }
+    }
+    const int lmax = __reduce_max_sync(0xffffffffu, l);
+    const bool same = __all_sync(0xffffffffu, l < 0 || l == lmax);
+    if (same) {
+      if (lmax < 0) continue;
+      d0 = shfl_sum_s64(d0);
+      d1 = shfl_sum_s64(d1);
+      d2 = shfl_sum_s64(d2);
+      if (lane == 0) {
+        if (d0) atomicAdd(limbs + lmax, (unsigned long long)d0);
+        if (d1) atomicAdd(limbs + lmax + 1, (unsigned long long)d1);
+        if (d2) atomicAdd(limbs + lmax + 2, (unsigned long long)d2);
+      }
+    } else if (l >= 0) {
+      if (d0) atomicAdd(limbs + l, (unsigned long long)d0);
+      if (d1) atomicAdd(limbs + l + 1, (unsigned long long)d1);
+      if (d2) atomicAdd(limbs + l + 2, (unsigned long long)d2);
+    }
+  }
+}
+
+// warp_acc_flush over sums[first + k*stride], k = 0.. while < n
+__device__ void warp_acc_flush_strided(const double *sums, int64_t first, int64_t stride,
+                                       int64_t n, unsigned long long *limbs) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = first; base < n; base += 32 * stride) {
+    const int64_t i = base + lane * stride;
+    const double x = i < n ? __ldcg(sums + i) : 0.0;
+    int l = -1;
+    long long d0 = 0, d1 = 0, d2 = 0;
+    if (x != 0.0) {
+      const unsigned long long bits = (unsigned long long)__double_as_longlong(x);
+      const int ex = (int)((bits >> 52) & 0x7ff);
+      unsigned long long mant = bits & ((1ULL << 52) - 1);
+      int p = 0;
+      if (ex != 0) {
+        mant |= 1ULL << 52;
+        p = ex - 1;
+      }
+      l = p >> 5;
+      const int off = p & 31;
+      const unsigned long long lo = mant << off;
+      const unsigned long long hi = off ? (mant >> (64 - off)) : 0ULL;
+      d0 = (long long)(lo & 0xffffffffULL);
+      d1 = (long long)(lo >> 32);
+      d2 = (long long)hi;
+      if ((long long)bits < 0) {
+        d0 = -d0;
+        d1 = -d1;
+        d2 = -d2;
+      }
+    }
+    const int lmax = __reduce_max_sync(0xffffffffu, l);
+    if (__all_sync(0xffffffffu, l < 0 || l == lmax)) {
+      if (lmax < 0) continue;
+      d0 = shfl_sum_s64(d0);
+      d1 = shfl_sum_s64(d1);
+      d2 = shfl_sum_s64(d2);
+      if (lane == 0) {
+        if (d0) atomicAdd(limbs + lmax, (unsigned long long)d0);
+        if (d1) atomicAdd(limbs + lmax + 1, (unsigned long long)d1);
+        if (d2) atomicAdd(limbs + lmax + 2, (unsigned long long)d2);
+      }
+    } else if (l >= 0) {
+      if (d0) atomicAdd(limbs + l, (unsigned long long)d0);
+      if (d1) atomicAdd(limbs + l + 1, (unsigned long long)d1);
+      if (d2) atomicAdd(limbs + l + 2, (unsigned long long)d2);
+    }
+  }
+}
+
+// A streaming warp's share of the previous step's close: the (sum, min) of
+// the sub-grids it also streams this step (same grid stride, a handful),
+// folded once its own pipeline runs. No CTA barrier (a warp may have no
+// sub-grids): the CTA's last warp to fold (s_min[1] = ticket, s_min[0] = min
+// key, both set at kernel start) adds the CTA's digits to prev_acc and
+// counts the CTA in for the waiting close CTA.
+__device__ __forceinline__ void fold_previous(const StepArgs &a, int64_t g0, int64_t gstride,
+                                              unsigned long long *s_limbs, long long *s_min) {
+  const int lane = threadIdx.x & 31;
+  warp_acc_flush_strided(a.prev_sums, g0, gstride, a.n, s_limbs);
+  double m = CUDART_INF;
+  for (int64_t g = g0 + lane * gstride; g < a.n; g += 32 * gstride)
+    m = fmin(m, __ldcg(a.prev_mins + g));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) atomicMin(&s_min[0], min_key(m));
+  __threadfence_block();
+  __syncwarp();
+  unsigned long long tk = 0;
+  if (lane == 0) tk = atomicAdd(reinterpret_cast<unsigned long long *>(&s_min[1]), 1ULL);
+  tk = __shfl_sync(0xffffffffu, tk, 0);
+  if (tk != (unsigned long long)(blockDim.x >> 5) - 1) return;
+  __threadfence_block();
+  for (int i = lane; i < TB_ACC_LIMBS; i += 32) {
+    const unsigned long long v = *reinterpret_cast<volatile unsigned long long *>(s_limbs + i);
+    if (v) atomicAdd(reinterpret_cast<unsigned long long *>(a.prev_acc) + i, v);
+  }
+  if (lane == 0) {
+    atomicMin(reinterpret_cast<long long *>(a.prev_acc) + TB_ACC_MIN_WORD,
+              *reinterpret_cast<volatile long long *>(&s_min[0]));
+    __threadfence();
+    atomicAdd(reinterpret_cast<unsigned long long *>(a.prev_acc) + TB_ACC_COUNT_WORD, 1ULL);
+  }
+}
 
 template <int CHAINS, int KPC>
 __device__ __forceinline__ void subgrid_body(const StepArgs &a, int64_t g, int lane,
                                              double (&v)[16], double face,
                                              unsigned long long *s_limbs, double &wmin,
-                                             AccCache &cache) {
+                                             double *wsums, SumBuf &sb) {
   const int r = lane & 7;
   // Ghost fold against the previous generation: cells 0..7 are lanes 0..7 at
   // i = 0; cells 504..511 are lanes 24..31 at i = 15. Add rounds; *0.5 exact.
@@ -442,7 +591,15 @@ __device__ __forceinline__ void subgrid_body(const StepArgs &a, int64_t g, int l
     if (a.sums) a.sums[g] = s;
     if (a.mins) a.mins[g] = m;
   }
-  if (a.acc && lane == 0) cache.add(s_limbs, s);
+  if (a.acc) {
+    if (lane == 0) wsums[sb.cnt] = s;
+    if (++sb.cnt == kSumBuf) {
+      __syncwarp();
+      warp_acc_flush(wsums, kSumBuf, s_limbs);
+      __syncwarp();
+      sb.cnt = 0;
+    }
+  }
   wmin = fmin(wmin, m);
 }
 
@@ -451,22 +608,26 @@ __device__ __forceinline__ void subgrid_body(const StepArgs &a, int64_t g, int l
 __device__ __forceinline__ void step_epilogue(const StepArgs &a,
                                               unsigned long long *s_limbs,
                                               long long *s_min, double wmin,
-                                              AccCache *cache = nullptr) {
+                                              double *wsums = nullptr, int nsums = 0) {
   if (!a.acc) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (cache && lane == 0) cache->flush(s_limbs);
+  if (wsums) {
+    __syncwarp();
+    warp_acc_flush(wsums, nsums, s_limbs);
+  }
   if (lane == 0) s_min[warp] = min_key(wmin);
   __syncthreads();                    // the CTA's limbs and warp minima are in smem
   if (warp != 0) return;              // warp 0 publishes; the rest retire now
   long long bm = s_min[0];
 #pragma unroll
   for (int w = 1; w < kStepWarps; ++w) bm = min(bm, s_min[w]);
+  int64_t *acc = a.acc;
   for (int i = lane; i < TB_ACC_LIMBS; i += 32) {
     const unsigned long long v = s_limbs[i];
-    if (v) atomicAdd(reinterpret_cast<unsigned long long *>(a.acc) + i, v);
+    if (v) atomicAdd(reinterpret_cast<unsigned long long *>(acc) + i, v);
   }
   if (lane == 0)
-    atomicMin(reinterpret_cast<long long *>(a.acc) + TB_ACC_MIN_WORD, bm);
+    atomicMin(reinterpret_cast<long long *>(acc) + TB_ACC_MIN_WORD, bm);
   if (!a.finalize) return;
   // Last-CTA ticket: each publishing lane fences its own atomics, then lane 0
   // takes a ticket; the CTA that draws gridDim.x-1 closes the step.
@@ -485,10 +646,11 @@ __device__ __forceinline__ void step_epilogue(const StepArgs &a,
 // K2a: direct loads into registers (ld.global.nc, no L1 allocate). With PF,
 // the next sub-grid's 16 values per lane are loaded before this one is
 // transformed (register double buffer: more MLP, fewer resident warps).
-template <int CHAINS, int KPC, bool PF, int MINB = 1>
+template <int CHAINS, int KPC, bool PF, int MINB = 4>
 __global__ void __launch_bounds__(kStepThreads, MINB) k_step(StepArgs a) {
   __shared__ unsigned long long s_limbs[TB_ACC_LIMBS];
   __shared__ long long s_min[kStepWarps];
+  __shared__ double s_sums[kStepWarps][kSumBuf];
   if (finalizer_cta(a)) return;
   if (a.acc) {
     for (int i = threadIdx.x; i < TB_ACC_LIMBS; i += blockDim.x) s_limbs[i] = 0ULL;
@@ -499,7 +661,7 @@ __global__ void __launch_bounds__(kStepThreads, MINB) k_step(StepArgs a) {
   const int lane_off = 128 * (lane >> 3) + (lane & 7);
   const int64_t gstride = (int64_t)(gridDim.x - a.finalizer) * kStepWarps;
   double wmin = CUDART_INF;
-  AccCache cache;
+  SumBuf sb;
   int64_t g = (int64_t)blockIdx.x * kStepWarps + warp;
   if (PF) {
     double nxt[16], nface = 0.0;
@@ -521,7 +683,7 @@ __global__ void __launch_bounds__(kStepThreads, MINB) k_step(StepArgs a) {
         for (int i = 0; i < 16; ++i) nxt[i] = ld_stream(src + 8 * i);
         nface = load_face(a, gn, lane);
       }
-      subgrid_body<CHAINS, KPC>(a, g, lane, v, face, s_limbs, wmin, cache);
+      subgrid_body<CHAINS, KPC>(a, g, lane, v, face, s_limbs, wmin, s_sums[warp], sb);
     }
   } else {
     for (; g < a.n; g += gstride) {
@@ -530,10 +692,10 @@ __global__ void __launch_bounds__(kStepThreads, MINB) k_step(StepArgs a) {
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] = ld_stream(src + 8 * i);
       const double face = load_face(a, g, lane);
-      subgrid_body<CHAINS, KPC>(a, g, lane, v, face, s_limbs, wmin, cache);
+      subgrid_body<CHAINS, KPC>(a, g, lane, v, face, s_limbs, wmin, s_sums[warp], sb);
     }
   }
-  step_epilogue(a, s_limbs, s_min, wmin, &cache);
+  step_epilogue(a, s_limbs, s_min, wmin, s_sums[warp], sb.cnt);
 }
 
 // K2c: a warp PAIR per sub-grid, 8 cells per lane (half the registers of
@@ -672,16 +834,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
 }
 
 template <int CHAINS, int KPC, int STAGES>
-__global__ void __launch_bounds__(kStepThreads) k_step_bulk(StepArgs a) {
+// 4 CTAs per SM (64 registers)
+__global__ void __launch_bounds__(kStepThreads, 4) k_step_bulk(StepArgs a) {
   constexpr int kStages = STAGES;
   extern __shared__ __align__(128) double ring[];   // [warps][stages][padded 512]
   __shared__ __align__(8) uint64_t bars[kStepWarps][kStages];
   __shared__ unsigned long long s_limbs[TB_ACC_LIMBS];
   __shared__ long long s_min[kStepWarps];
+  __shared__ double s_sums[kStepWarps][kSumBuf];
   if (finalizer_cta(a)) return;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < TB_ACC_LIMBS; i += blockDim.x) s_limbs[i] = 0ULL;
+  if (threadIdx.x == 0) {   // the deferred fold's min key and warp ticket
+    s_min[0] = kKeyInf;
+    s_min[1] = 0;
+  }
   if (lane == 0)
     for (int s = 0; s < kStages; ++s) mbar_init(&bars[warp][s], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -696,8 +864,11 @@ __global__ void __launch_bounds__(kStepThreads) k_step_bulk(StepArgs a) {
       if (g < a.n) bulk_load_subgrid(slots + s * kSlot, a.old + g * TB_CELLS, &bars[warp][s]);
     }
   }
+  // deferred close: fold the previous step's share under the first bulk
+  // copy's latency
+  if (a.finalizer) fold_previous(a, g0, gstride, s_limbs, s_min);
   double wmin = CUDART_INF;
-  AccCache cache;
+  SumBuf sb;
   int it = 0;
   for (int64_t g = g0; g < a.n; g += gstride, ++it) {
     const int s = it % kStages;
@@ -717,9 +888,9 @@ __global__ void __launch_bounds__(kStepThreads) k_step_bulk(StepArgs a) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       bulk_load_subgrid(slots + s * kSlot, a.old + gn * TB_CELLS, &bars[warp][s]);
     }
-    subgrid_body<CHAINS, KPC>(a, g, lane, v, face, s_limbs, wmin, cache);
+    subgrid_body<CHAINS, KPC>(a, g, lane, v, face, s_limbs, wmin, s_sums[warp], sb);
   }
-  step_epilogue(a, s_limbs, s_min, wmin, &cache);
+  step_epilogue(a, s_limbs, s_min, wmin, s_sums[warp], sb.cnt);
 }
 
 int g_step_impl = TB_STEP_AUTO;
@@ -971,7 +1142,7 @@ static int step_args(StepArgs *a, const double *old, double *out, int64_t n,
   if (n > 0 && (!old || !out || old == out || !left_face || !right_face))
     return TB_E_INVALID;
   *a = StepArgs{old, out, n, left_face, right_face, chains, kpc, mins, sums, acc,
-                nullptr, nullptr, nullptr, 0, nullptr, nullptr, nullptr, 0};
+                nullptr, nullptr, nullptr, 0, nullptr, nullptr, nullptr, nullptr, nullptr, 0};
   return TB_OK;
 }
 
@@ -1003,26 +1174,50 @@ int tb_step_final(tb_stream_t s, const double *old, double *out, int64_t n,
   return launch_step(reinterpret_cast<cudaStream_t>(s), a);
 }
 
+int tb_step_close(tb_stream_t s, const double *sums, const double *mins, int64_t n,
+                  int64_t *acc, double *piece, double *dt, double *checksum) {
+  if (!acc || n < 0 || (n > 0 && (!sums || !mins))) return TB_E_INVALID;
+  k_step_close<<<1, 256, 0, reinterpret_cast<cudaStream_t>(s)>>>(sums, mins, n, acc, piece,
+                                                                 dt, checksum);
+  return tb::last_error();
+}
+
 int tb_step_deferred(tb_stream_t s, const double *old, double *out, int64_t n,
                      const double *left_face, const double *right_face, int chains,
-                     int kernels_per_chain, double *mins, double *sums, int64_t *acc,
-                     int64_t *prev_acc, double *prev_piece, double *prev_dt,
-                     double *checksum) {
+                     int kernels_per_chain, double *sums, double *mins,
+                     const double *prev_sums, const double *prev_mins, int64_t *acc,
+                     double *prev_piece, double *prev_dt, double *checksum) {
   StepArgs a;
   int r = step_args(&a, old, out, n, left_face, right_face, chains, kernels_per_chain,
-                    mins, sums, acc);
+                    mins, sums, nullptr);
   if (r != TB_OK) return r;
-  if (!acc || acc == prev_acc) return TB_E_INVALID;
-  if (n == 0) return prev_acc ? tb_acc_finalize(s, prev_acc, prev_piece, prev_dt, checksum, 1)
-                              : TB_OK;
-  if (prev_acc) {
-    a.prev_acc = prev_acc;
-    a.prev_piece = prev_piece;
-    a.prev_dt = prev_dt;
-    a.checksum = checksum;
-    a.finalizer = 1;
+  if (n > 0 && (!sums || !mins)) return TB_E_INVALID;
+  if (prev_sums && (!prev_mins || !acc || prev_sums == sums)) return TB_E_INVALID;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
+  if (n == 0)
+    return prev_sums ? tb_step_close(s, prev_sums, prev_mins, 0, acc, prev_piece, prev_dt,
+                                     checksum)
+                     : TB_OK;
+  if (!prev_sums) return launch_step(st, a);
+  if ((reinterpret_cast<uintptr_t>(old) & 15) != 0) {
+    // the in-launch close lives in the bulk-copy kernel only
+    r = launch_step(st, a);
+    return r == TB_OK ? tb_step_close(s, prev_sums, prev_mins, n, acc, prev_piece, prev_dt,
+                                      checksum)
+                      : r;
   }
-  return launch_step(reinterpret_cast<cudaStream_t>(s), a);
+  a.prev_acc = acc;
+  a.prev_sums = prev_sums;
+  a.prev_mins = prev_mins;
+  a.prev_piece = prev_piece;
+  a.prev_dt = prev_dt;
+  a.checksum = checksum;
+  a.finalizer = 1;
+  if (chains == 3 && kernels_per_chain == 5)
+    launch_bulk<3, 5, 1>(st, a);
+  else
+    launch_bulk<0, 0, 1>(st, a);
+  return tb::last_error();
 }
 
 int tb_acc_reset(tb_stream_t s, int64_t *acc) {

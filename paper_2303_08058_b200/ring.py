@@ -98,11 +98,16 @@ class CudaRingOps:
                _ptr(left_face), _ptr(right_face), chains, kpc, _ptr(mins), _ptr(sums),
                _ptr(acc), _ptr(piece), _ptr(dt), _ptr(checksum))
 
-    def step_deferred(self, old, out, left_face, right_face, chains, kpc, acc, prev_acc,
-                      prev_piece, prev_dt, checksum, mins=None, sums=None) -> None:
+    def step_deferred(self, old, out, left_face, right_face, chains, kpc, sums, mins,
+                      prev_sums, prev_mins, acc, prev_piece, prev_dt, checksum) -> None:
         N.call("tb_step_deferred", self.stream(), _ptr(old), _ptr(out), old.shape[0],
-               _ptr(left_face), _ptr(right_face), chains, kpc, _ptr(mins), _ptr(sums),
-               _ptr(acc), _ptr(prev_acc), _ptr(prev_piece), _ptr(prev_dt), _ptr(checksum))
+               _ptr(left_face), _ptr(right_face), chains, kpc, _ptr(sums), _ptr(mins),
+               _ptr(prev_sums), _ptr(prev_mins), _ptr(acc), _ptr(prev_piece), _ptr(prev_dt),
+               _ptr(checksum))
+
+    def step_close(self, sums, mins, acc, piece, dt, checksum) -> None:
+        N.call("tb_step_close", self.stream(), _ptr(sums), _ptr(mins), sums.shape[0],
+               _ptr(acc), _ptr(piece), _ptr(dt), _ptr(checksum))
 
     def acc_reset(self, acc) -> None:
         N.call("tb_acc_reset", self.stream(), _ptr(acc))
@@ -162,13 +167,13 @@ class RingStepper:
         self._host_prev = None
         self.ops.init_cells(self.state[0], subgrids, self.lo)
         self.ops.acc_reset(self.acc)
-        # single device, back to back: step k accumulates into accd[k & 1] and
-        # step k+1's launch closes it (tb_step_deferred); `pending` = the step
-        # whose accumulator still awaits that
-        self.accd = torch.zeros((2, N.TB_ACC_WORDS), dtype=torch.int64, device=device)
-        self.ops.acc_reset(self.accd[0])
-        self.ops.acc_reset(self.accd[1])
+        # single device, back to back: step k writes per-sub-grid (sum, min)
+        # into parity k & 1 and step k+1's launch closes it exactly
+        # (tb_step_deferred); `pending` = the step still awaiting that
+        self.dsums = torch.zeros((2, n), **f64)
+        self.dmins = torch.zeros((2, n), **f64)
         self._pending: Optional[int] = None
+        self._collect = collect_subgrid_stats
         # Multi-GPU halo: "p2p" maps the ring neighbours' state buffers (CUDA
         # IPC) so K2 reads the ghost faces straight from their HBM; "nccl"
         # sends them with NCCL P2P; "auto" tries p2p, else nccl.
@@ -329,12 +334,14 @@ class RingStepper:
             if hasattr(self.ops, "step_deferred"):
                 p = self._pending
                 self.ops.step_deferred(
-                    old, out, lf, rf, self.chains, self.kpc, self.accd[k & 1],
-                    None if p is None else self.accd[p & 1],
+                    old, out, lf, rf, self.chains, self.kpc, self.dsums[k & 1],
+                    self.dmins[k & 1], None if p is None else self.dsums[p & 1],
+                    None if p is None else self.dmins[p & 1], self.acc,
                     None if p is None else self.pieces[p:p + 1],
-                    None if p is None else self.dts[p:p + 1], self.checksum,
-                    self.mins, self.sums)
+                    None if p is None else self.dts[p:p + 1], self.checksum)
                 self._pending = k
+                if self._collect:
+                    self.sums, self.mins = self.dsums[k & 1], self.dmins[k & 1]
             elif hasattr(self.ops, "step_final"):
                 self.ops.step_final(old, out, lf, rf, self.chains, self.kpc, self.acc,
                                     self.pieces[k:k + 1], self.dts[k:k + 1],
@@ -394,8 +401,8 @@ class RingStepper:
         and checksum contribution are then final)."""
         p = self._pending
         if p is not None:
-            self.ops.acc_finalize(self.accd[p & 1], self.pieces[p:p + 1], self.dts[p:p + 1],
-                                  self.checksum)
+            self.ops.step_close(self.dsums[p & 1], self.dmins[p & 1], self.acc,
+                                self.pieces[p:p + 1], self.dts[p:p + 1], self.checksum)
             self._pending = None
 
     def run(self, steps: int) -> RingResult:

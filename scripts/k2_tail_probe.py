@@ -22,12 +22,12 @@ def main():
     N.call("tb_init_cells", s, st[0].data_ptr(), n, 0, n)
     acc = torch.zeros(N.TB_ACC_WORDS, dtype=torch.int64, device=dev)
     N.call("tb_acc_reset", s, acc.data_ptr())
-    accd = torch.zeros((2, N.TB_ACC_WORDS), dtype=torch.int64, device=dev)
-    N.call("tb_acc_reset", s, accd[0].data_ptr())
-    N.call("tb_acc_reset", s, accd[1].data_ptr())
+    ds = torch.zeros((2, n), dtype=torch.float64, device=dev)
+    dm = torch.zeros((2, n), dtype=torch.float64, device=dev)
+    sacc = torch.zeros(N.TB_ACC_WORDS, dtype=torch.int64, device=dev)
     out = torch.zeros(3, dtype=torch.float64, device=dev)
     res = {}
-    for mode in ("final", "acc_only", "no_acc", "deferred") * 3:
+    for mode in ("final", "no_acc", "sums_only", "deferred") * 3:
         def launch(k):
             o, w = st[k & 1], st[(k + 1) & 1]
             lf, rf = o[-1, -8:].data_ptr(), o[0, :8].data_ptr()
@@ -36,9 +36,14 @@ def main():
                        None, acc.data_ptr(), out[0:1].data_ptr(), out[1:2].data_ptr(),
                        out[2:3].data_ptr())
             elif mode == "deferred":
-                N.call("tb_step_deferred", s, o.data_ptr(), w.data_ptr(), n, lf, rf, 3, 5, None,
-                       None, accd[k & 1].data_ptr(), accd[(k - 1) & 1].data_ptr() if k else None,
+                N.call("tb_step_deferred", s, o.data_ptr(), w.data_ptr(), n, lf, rf, 3, 5,
+                       ds[k & 1].data_ptr(), dm[k & 1].data_ptr(),
+                       ds[(k - 1) & 1].data_ptr() if k else None,
+                       dm[(k - 1) & 1].data_ptr() if k else None, sacc.data_ptr(),
                        out[0:1].data_ptr(), out[1:2].data_ptr(), out[2:3].data_ptr())
+            elif mode == "sums_only":
+                N.call("tb_step", s, o.data_ptr(), w.data_ptr(), n, lf, rf, 3, 5,
+                       dm[k & 1].data_ptr(), ds[k & 1].data_ptr(), None)
             elif mode == "acc_only":
                 N.call("tb_step", s, o.data_ptr(), w.data_ptr(), n, lf, rf, 3, 5, None, None,
                        acc.data_ptr())
