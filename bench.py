@@ -551,9 +551,8 @@ def main(argv=None):
     # Headline: steps back to back, no L2 flush. Each step reads the previous
     # step's 128 MiB output (> the 126 MB L2) from the start while its tail is
     # the most recently written, so nothing is re-read from L2: ncu
-    # --cache-control none on back-to-back launches measures 134.7 MB DRAM
-    # reads per launch (the whole input), L2 hit rate 1.7 %
-    # (profiles/r01_k2_back_to_back.txt). At N = 1 one launch per step, so the
+    # --cache-control none on back-to-back launches measures 135 MB DRAM
+    # reads per launch (the whole input; profiles/r01_k2_back_to_back.txt). At N = 1 one launch per step, so the
     # outer events also time K2; at N > 1 K2 is bracketed per step.
     per_step_k2 = world > 1
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -679,8 +678,9 @@ def main(argv=None):
                                      ("nccl all_reduce" if world > 1 else "in-kernel")),
                        "l2": "no flush: steps back to back, inputs larger than L2 (each step "
                              "reads the previous step's 128 MiB output; 126 MB L2; ncu "
-                             "--cache-control none: 134.7 MB DRAM reads per launch, L2 hit "
-                             "rate 1.7 %); the flushed number is l2_flushed_per_step"},
+                             "--cache-control none: 135 MB DRAM reads per launch = the whole "
+                             "input, profiles/r01_k2_back_to_back.txt); the flushed number "
+                             "is l2_flushed_per_step"},
             "l2_flushed_per_step": {
                 "ms_per_step": flushed_step_ms, "value": cells_total / (flushed_step_ms * 1e-3),
                 "k2_ms": flushed_k2_ms,

@@ -185,8 +185,8 @@ int tb_step_final(tb_stream_t s, const double *old, double *out, int64_t n,
  * (prev_sums, prev_mins) — exact sum == math.fsum, min — through the scratch
  * accumulator acc into prev_piece / prev_dt and *checksum += prev_piece while
  * the other CTAs stream. prev_sums = NULL on the first step; sums/mins must
- * alternate between two buffers; tb_step_close closes the last step (one
- * CTA). */
+ * alternate between two buffers; tb_step_close closes the last step (acc
+ * reset on entry, as after every close). */
 int tb_step_deferred(tb_stream_t s, const double *old, double *out, int64_t n,
                      const double *left_face, const double *right_face, int chains,
                      int kernels_per_chain, double *sums, double *mins,

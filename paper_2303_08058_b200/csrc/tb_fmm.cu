@@ -424,7 +424,8 @@ __global__ void __launch_bounds__(32) k_fmm_dtab(const TabPtrs T) {
 }
 
 // ------------------------------------------------------------------- M2L
-constexpr int kM2LThreads = 512;
+constexpr int kT = 2;                             // targets per thread
+constexpr int kM2LThreads = 512 / kT;
 constexpr int kM2LSmem = 2 * kStage * 8;          // 162,048 B
 
 __device__ __forceinline__ void load20(const double *p, double (&v)[NC]) {
@@ -485,10 +486,16 @@ __device__ __forceinline__ void issue_stage(const Params &P, int lev, double *ds
 __global__ void __launch_bounds__(kM2LThreads, 1) k_fmm_m2l(const __grid_constant__ Params P) {
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t bar[2];
+  // thread = (octant, parent x) x two parents 2 planes apart in z: both
+  // targets share the octant, hence every derivative tensor D (one load
+  // feeds 2 x 70 FMAs); the source records differ
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const int ox = lane & 1, oy = (lane >> 1) & 1, oz = (lane >> 2) & 1;
-  const int px = lane >> 3, py = w & 3, pz = w >> 2;
-  const int lx = 2 * px + ox, ly = 2 * py + oy, lz = 2 * pz + oz;   // target in sub-grid
+  const int px = lane >> 3, py = w & 3, pzb = w >> 2;
+  const int lx = 2 * px + ox, ly = 2 * py + oy;
+  int lz[kT];
+#pragma unroll
+  for (int r = 0; r < kT; ++r) lz[r] = 2 * (pzb + 2 * r) + oz;
   // decode the job: levels L-1 .. 1 (8^l sub-grids each), then 8 level-0 slabs
   int job = blockIdx.x, lev = 0, sub = 0;
   for (int l = P.L - 1; l >= 1; --l) {
@@ -506,9 +513,11 @@ __global__ void __launch_bounds__(kM2LThreads, 1) k_fmm_m2l(const __grid_constan
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  double L[NC];
+  double L[kT][NC];
 #pragma unroll
-  for (int k = 0; k < NC; ++k) L[k] = 0.0;
+  for (int r = 0; r < kT; ++r)
+#pragma unroll
+    for (int k = 0; k < NC; ++k) L[r][k] = 0.0;
 
   if (lev == 0) {
     // level-0 slab `job`: all 512 targets against the sources with z == job
@@ -528,23 +537,26 @@ __global__ void __launch_bounds__(kM2LThreads, 1) k_fmm_m2l(const __grid_constan
     mbar_wait(&bar[0], 0);
     const double h = 1.0 / 8.0;
     const int jz = job;
-#pragma unroll 1
-    for (int jy = 0; jy < 8; ++jy)
-#pragma unroll 1
-      for (int jx = 0; jx < 8; ++jx) {
-        const int qx = lx - jx, qy = ly - jy, qz = lz - jz;
-        if (qx * qx + qy * qy + qz * qz > 4) {
-          double D[NC], M[16];
-          d_tensor(qx * h, qy * h, qz * h, D);
-          load16(sm + ((jz * 8 + jy) * 8 + jx) * MS, M);
-          contract(L, M, D);
-        }
-      }
-    untrace(L);
-    double2 *dst = reinterpret_cast<double2 *>(P.L0part + ((size_t)job * 512 +
-                                                            (lz * 8 + ly) * 8 + lx) * NC);
 #pragma unroll
-    for (int k = 0; k < NC / 2; ++k) dst[k] = make_double2(L[2 * k], L[2 * k + 1]);
+    for (int r = 0; r < kT; ++r) {
+#pragma unroll 1
+      for (int jy = 0; jy < 8; ++jy)
+#pragma unroll 1
+        for (int jx = 0; jx < 8; ++jx) {
+          const int qx = lx - jx, qy = ly - jy, qz = lz[r] - jz;
+          if (qx * qx + qy * qy + qz * qz > 4) {
+            double D[NC], M[16];
+            d_tensor(qx * h, qy * h, qz * h, D);
+            load16(sm + ((jz * 8 + jy) * 8 + jx) * MS, M);
+            contract(L[r], M, D);
+          }
+        }
+      untrace(L[r]);
+      double2 *dst = reinterpret_cast<double2 *>(
+          P.L0part + ((size_t)job * 512 + (lz[r] * 8 + ly) * 8 + lx) * NC);
+#pragma unroll
+      for (int k = 0; k < NC / 2; ++k) dst[k] = make_double2(L[r][2 * k], L[r][2 * k + 1]);
+    }
     return;
   }
 
@@ -557,7 +569,7 @@ __global__ void __launch_bounds__(kM2LThreads, 1) k_fmm_m2l(const __grid_constan
     issue_stage(P, lev, sm + kStage, &bar[1], 1, X0, Y0, ZT);
   }
   // lane-dependent parts of the source cell and of the D-table entry
-  const int cbase = ((2 * pz) * 8 + 2 * py) * 8 + 2 * px;
+  const int cbase = ((2 * pzb) * 8 + 2 * py) * 8 + 2 * px;   // target 0; target 1 is +256
   const int dbase = (ox + 1) * kDX + (oy + 1) * kDY + (oz + 1) * kDZ;
 #pragma unroll 1
   for (int k = 0; k < 33; ++k) {
@@ -568,10 +580,14 @@ __global__ void __launch_bounds__(kM2LThreads, 1) k_fmm_m2l(const __grid_constan
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       const int cx = c & 1, cy = (c >> 1) & 1, cz = c >> 2;
-      double M[16], D[NC];
-      load16(Ms + (cbase + (cz * 8 + cy) * 8 + cx) * MS, M);
+      double D[NC];
       load20(Ds + 2 * (dbase - cx * kDX - cy * kDY - cz * kDZ), D);
-      contract(L, M, D);
+#pragma unroll
+      for (int r = 0; r < kT; ++r) {
+        double M[16];
+        load16(Ms + (cbase + 256 * r + (cz * 8 + cy) * 8 + cx) * MS, M);
+        contract(L[r], M, D);
+      }
     }
     __syncthreads();            // every thread is done with this buffer
     if (t == 0 && k + 2 < 33) {
@@ -579,12 +595,15 @@ __global__ void __launch_bounds__(kM2LThreads, 1) k_fmm_m2l(const __grid_constan
       issue_stage(P, lev, sm + buf * kStage, &bar[buf], k + 2, X0, Y0, ZT);
     }
   }
-  untrace(L);
   const int N = 8 << lev;
-  double2 *dst = reinterpret_cast<double2 *>(
-      P.Loc[lev] + (((size_t)(Z0 + lz) * N + (Y0 + ly)) * N + (X0 + lx)) * NC);
 #pragma unroll
-  for (int k = 0; k < NC / 2; ++k) dst[k] = make_double2(L[2 * k], L[2 * k + 1]);
+  for (int r = 0; r < kT; ++r) {
+    untrace(L[r]);
+    double2 *dst = reinterpret_cast<double2 *>(
+        P.Loc[lev] + (((size_t)(Z0 + lz[r]) * N + (Y0 + ly)) * N + (X0 + lx)) * NC);
+#pragma unroll
+    for (int k = 0; k < NC / 2; ++k) dst[k] = make_double2(L[r][2 * k], L[r][2 * k + 1]);
+  }
 }
 
 // ------------------------------------------------------------------ L2L

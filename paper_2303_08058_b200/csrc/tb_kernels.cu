@@ -284,9 +284,10 @@ __device__ void warp_acc_flush_strided(const double *sums, int64_t first, int64_
                                        int64_t n, unsigned long long *limbs);
 
 // Close a step from its per-sub-grid (sum, min) in one standalone launch
-// (tb_step_close: the last step of a deferred run): exact digits of every
-// sum, min of the mins, then the one-warp correctly rounded result ==
-// math.fsum of the sums and the min-tree dt (src/miniapp.py:138-171).
+// (tb_step_close: the last step of a deferred run): every CTA folds a slice
+// (exact digits, warp-merged windows; min of the mins) into acc, and the last
+// CTA to finish rounds — == math.fsum of the sums and the min-tree dt
+// (src/miniapp.py:138-171). acc must be reset (it is reset again after).
 __global__ void __launch_bounds__(256) k_step_close(const double *sums, const double *mins,
                                                     int64_t n, int64_t *acc, double *piece,
                                                     double *dt, double *checksum) {
@@ -296,20 +297,32 @@ __global__ void __launch_bounds__(256) k_step_close(const double *sums, const do
   for (int i = t; i < TB_ACC_LIMBS; i += blockDim.x) c_limbs[i] = 0ULL;
   if (t == 0) c_min = kKeyInf;
   __syncthreads();
-  const int nw = blockDim.x >> 5;
-  // warp w takes sums w, w + nw, ... (32 at a time, warp-merged digits)
-  warp_acc_flush_strided(sums, warp, nw, n, c_limbs);
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  warp_acc_flush_strided(sums, gw, nw, n, c_limbs);
   double m = CUDART_INF;
-  for (int64_t i = t; i < n; i += blockDim.x) m = fmin(m, __ldcg(mins + i));
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + t; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = fmin(m, __ldcg(mins + i));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, o));
   if (lane == 0) atomicMin(&c_min, min_key(m));
   __syncthreads();
-  for (int i = t; i < TB_ACC_WORDS; i += blockDim.x)
-    acc[i] = i < TB_ACC_LIMBS ? (long long)c_limbs[i] : (i == TB_ACC_MIN_WORD ? c_min : 0);
-  __threadfence_block();
-  __syncthreads();
-  if (t < 32) warp_finalize(acc, piece, dt, checksum, 1);
+  if (warp != 0) return;
+  for (int i = lane; i < TB_ACC_LIMBS; i += 32) {
+    const unsigned long long v = c_limbs[i];
+    if (v) atomicAdd(reinterpret_cast<unsigned long long *>(acc) + i, v);
+  }
+  if (lane == 0) atomicMin(reinterpret_cast<long long *>(acc) + TB_ACC_MIN_WORD, c_min);
+  __threadfence();
+  __syncwarp();
+  unsigned long long tk = 0;
+  if (lane == 0)
+    tk = atomicAdd(reinterpret_cast<unsigned long long *>(acc) + TB_ACC_COUNT_WORD, 1ULL);
+  tk = __shfl_sync(0xffffffffu, tk, 0);
+  if (tk == (unsigned long long)gridDim.x - 1) {
+    __threadfence();
+    warp_finalize(acc, piece, dt, checksum, 1);
+  }
 }
 
 // ------------------------------------------------------------------ K2 --
@@ -1177,8 +1190,12 @@ int tb_step_final(tb_stream_t s, const double *old, double *out, int64_t n,
 int tb_step_close(tb_stream_t s, const double *sums, const double *mins, int64_t n,
                   int64_t *acc, double *piece, double *dt, double *checksum) {
   if (!acc || n < 0 || (n > 0 && (!sums || !mins))) return TB_E_INVALID;
-  k_step_close<<<1, 256, 0, reinterpret_cast<cudaStream_t>(s)>>>(sums, mins, n, acc, piece,
-                                                                 dt, checksum);
+  int64_t blocks = (n + 2047) / 2048;   // >= 8 values per thread
+  const int64_t cap = (int64_t)tb::sm_count() * 2;
+  if (blocks < 1) blocks = 1;
+  if (blocks > cap) blocks = cap;
+  k_step_close<<<(unsigned)blocks, 256, 0, reinterpret_cast<cudaStream_t>(s)>>>(
+      sums, mins, n, acc, piece, dt, checksum);
   return tb::last_error();
 }
 
