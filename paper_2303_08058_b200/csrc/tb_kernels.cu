@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "../../include/tb.h"
 #include "tb_internal.h"
@@ -855,6 +856,13 @@ __global__ void __launch_bounds__(kStepThreads, 4) k_step_bulk(StepArgs a) {
   __shared__ unsigned long long s_limbs[TB_ACC_LIMBS];
   __shared__ long long s_min[kStepWarps];
   __shared__ double s_sums[kStepWarps][kSumBuf];
+  // Programmatic dependent launch: the next step's grid is released now (all
+  // CTAs of this one-wave grid are resident), so its CTAs take the SM slots
+  // ours free and wait here — everything below reads the previous step's
+  // output, so nothing runs before the previous grid has completed and
+  // flushed. A no-op when launched without the attribute.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (finalizer_cta(a)) return;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -907,6 +915,11 @@ __global__ void __launch_bounds__(kStepThreads, 4) k_step_bulk(StepArgs a) {
 }
 
 int g_step_impl = TB_STEP_AUTO;
+// programmatic dependent launch of consecutive steps (TB_STEP_PDL=0 disables)
+const bool g_step_pdl = [] {
+  const char *e = getenv("TB_STEP_PDL");
+  return !(e && e[0] == '0');
+}();
 int g_step_spw = 0;   // sub-grids per warp per CTA; 0 = persistent (one wave)
 
 // CTAs for n sub-grids: one resident wave (occ CTAs per SM) by default, or
@@ -958,8 +971,17 @@ void launch_bulk(cudaStream_t st, const StepArgs &a) {
                          cudaFuncAttributeMaxDynamicSharedMemorySize, bulk_smem(STAGES));
     occ = occupancy(k_step_bulk<CHAINS, KPC, STAGES>, bulk_smem(STAGES));
   }
-  k_step_bulk<CHAINS, KPC, STAGES>
-      <<<step_grid(a.n, occ, a.finalizer), kStepThreads, bulk_smem(STAGES), st>>>(a);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)step_grid(a.n, occ, a.finalizer));
+  cfg.blockDim = dim3(kStepThreads);
+  cfg.dynamicSmemBytes = bulk_smem(STAGES);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = g_step_pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k_step_bulk<CHAINS, KPC, STAGES>, a);
 }
 
 int launch_step(cudaStream_t st, StepArgs a) {
@@ -972,9 +994,6 @@ int launch_step(cudaStream_t st, StepArgs a) {
   if (g_step_impl == TB_STEP_AUTO && aligned && fixed) {
     launch_bulk<3, 5, 1>(st, a);
     return tb::last_error();
-  }
-  if (a.finalize && a.acc) {
-    // ticket counter must start at 0 (reset by acc_reset / finalize)
   }
   if (bulk) {
     if (fixed)
