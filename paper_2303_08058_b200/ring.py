@@ -182,13 +182,11 @@ class RingStepper:
         if world > 1 and halo not in ("auto", "p2p", "nccl"):
             raise ValueError(f"unknown halo mode {halo!r}")
         if world > 1 and halo != "nccl" and isinstance(self.ops, CudaRingOps):
-            try:
-                self._peers = self._map_peers()
+            self._peers, err = self._map_peers()
+            if self._peers is not None:
                 self.halo_mode = "p2p"
-            except Exception:
-                if halo == "p2p":
-                    raise
-                self._peers = None
+            elif halo == "p2p":
+                raise RuntimeError(f"peer-memory halo unavailable: {err}")
 
     @staticmethod
     def _export(t: torch.Tensor):
@@ -202,16 +200,29 @@ class RingStepper:
     def _map_peers(self):
         """Exchange IPC handles with every rank; map the ring neighbours' two
         state generations (peer-memory halo) and every rank's reduction
-        accumulators (peer-memory all-reduce)."""
+        accumulators (peer-memory all-reduce).
+
+        Collective and all-or-nothing: every rank runs the same two
+        all-gathers whatever fails locally, and the mapping is kept only when
+        every rank succeeded, so all ranks take the same halo path. Returns
+        (peers, None) or (None, the first local error)."""
         import ctypes
 
         import torch.distributed as dist
-        # two parities of the cross-rank accumulator (see tb_acc_allreduce_p2p)
-        self.gacc = torch.zeros((2, N.TB_ACC_WORDS), dtype=torch.int64, device=self.device)
-        self.gacc[:, N.TB_ACC_MIN_WORD] = 0x7FF0000000000000      # key(+inf)
-        mine = ([self._export(t) for t in self.state], self.n, self._export(self.gacc))
+        err = None
+        mine = None
+        try:
+            # two parities of the cross-rank accumulator (tb_acc_allreduce_p2p)
+            self.gacc = torch.zeros((2, N.TB_ACC_WORDS), dtype=torch.int64,
+                                    device=self.device)
+            self.gacc[:, N.TB_ACC_MIN_WORD] = 0x7FF0000000000000      # key(+inf)
+            mine = ([self._export(t) for t in self.state], self.n, self._export(self.gacc))
+        except Exception as e:          # noqa: BLE001 — reported after agreement
+            err = e
         table = [None] * self.world
         dist.all_gather_object(table, mine, group=self.group)
+        if any(t is None for t in table):
+            return None, err or "a peer could not export its buffers"
         opened = {}
 
         def open_handle(handle, offset):
@@ -221,21 +232,33 @@ class RingStepper:
             opened.setdefault(base.value, 0)
             return base.value, base.value + offset
 
-        left, right = (self.rank - 1) % self.world, (self.rank + 1) % self.world
-        state = {}
-        for peer in sorted({left, right}):
-            state[peer] = ([open_handle(h, off) for h, off in table[peer][0]], table[peer][1])
-        row = self.gacc.stride(0) * self.gacc.element_size()
-        tab = [[0] * self.world for _ in range(2)]
-        for p in range(self.world):
-            if p == self.rank:
-                base_ptr = self.gacc.data_ptr()
-            else:
-                base_ptr = open_handle(*table[p][2])[1]
-            for parity in range(2):
-                tab[parity][p] = base_ptr + parity * row
-        self.peer_tab = torch.tensor(tab, dtype=torch.int64, device=self.device)
-        return {"left": state[left], "right": state[right], "bases": list(opened)}
+        peers = None
+        try:
+            left, right = (self.rank - 1) % self.world, (self.rank + 1) % self.world
+            state = {}
+            for peer in sorted({left, right}):
+                state[peer] = ([open_handle(h, off) for h, off in table[peer][0]],
+                               table[peer][1])
+            row = self.gacc.stride(0) * self.gacc.element_size()
+            tab = [[0] * self.world for _ in range(2)]
+            for p in range(self.world):
+                if p == self.rank:
+                    base_ptr = self.gacc.data_ptr()
+                else:
+                    base_ptr = open_handle(*table[p][2])[1]
+                for parity in range(2):
+                    tab[parity][p] = base_ptr + parity * row
+            self.peer_tab = torch.tensor(tab, dtype=torch.int64, device=self.device)
+            peers = {"left": state[left], "right": state[right], "bases": list(opened)}
+        except Exception as e:          # noqa: BLE001 — reported after agreement
+            err = e
+        ok = [None] * self.world
+        dist.all_gather_object(ok, peers is not None, group=self.group)
+        if not all(ok):
+            for base in opened:
+                N.call("tb_ipc_close", base)
+            return None, err or "a peer could not map its neighbours' buffers"
+        return peers, None
 
     def close(self) -> None:
         """Unmap neighbours' buffers (p2p halo)."""

@@ -120,3 +120,64 @@ def test_ring_partition_balanced_and_contiguous():
             assert max(sizes) - min(sizes) <= 1
     with pytest.raises(ValueError):
         ring_partition(1, 2, 0)
+
+
+class _PeerStub:
+    """The attributes RingStepper._map_peers reads, on CPU (tests only)."""
+
+    def __init__(self, rank, world, fail):
+        self.rank, self.world, self.group = rank, world, None
+        self.device = torch.device("cpu")
+        self.state = [torch.zeros(4, 512, dtype=torch.float64) for _ in range(2)]
+        self.n = 4
+        self.fail = fail
+
+    def _export(self, t):
+        if self.fail == ("export", self.rank):
+            raise RuntimeError("export failed")
+        return bytes(N.TB_IPC_HANDLE_BYTES), 0
+
+
+def _map_worker(rank, world, port, fail, q):
+    import paper_2303_08058_b200.ring as ring
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    calls = []
+
+    def fake_call(name, *args):
+        calls.append(name)
+        if name == "tb_ipc_open_handle":
+            if fail == ("open", rank):
+                raise RuntimeError("open failed")
+            args[1]._obj.value = 0x1000 * (len(calls) + 1)
+        return 0
+
+    ring.N.call = fake_call
+    try:
+        peers, err = RingStepper._map_peers(_PeerStub(rank, world, fail))
+        q.put((rank, peers is not None, calls.count("tb_ipc_open_handle"),
+               calls.count("tb_ipc_close")))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fail", [None, ("export", 1), ("open", 1), ("open", 0)])
+def test_peer_mapping_is_all_or_nothing(fail):
+    """A rank whose IPC export or open fails must not leave the others on the
+    peer-memory halo: every rank takes the same path (ring.py _map_peers)."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_map_worker, args=(r, world, port, fail, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert {ok for _, ok, _, _ in outs} == {fail is None}
+    for rank, ok, opens, closes in outs:
+        # every successful open is closed again when any rank failed
+        assert closes == (0 if ok else (opens if fail != ("open", rank) else opens - 1))
