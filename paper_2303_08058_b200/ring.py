@@ -182,7 +182,11 @@ class RingStepper:
         if world > 1 and halo not in ("auto", "p2p", "nccl"):
             raise ValueError(f"unknown halo mode {halo!r}")
         if world > 1 and halo != "nccl" and isinstance(self.ops, CudaRingOps):
-            self._peers, err = self._map_peers()
+            import torch.distributed as dist
+            if dist.is_available() and dist.is_initialized():
+                self._peers, err = self._map_peers()
+            else:
+                err = "no process group to exchange IPC handles over"
             if self._peers is not None:
                 self.halo_mode = "p2p"
             elif halo == "p2p":
