@@ -30,29 +30,50 @@ constexpr int NF = 5, NG = 2;
 // x, y wrap periodically inside the slab; z takes the 2 planes below / above
 // from lo / hi ([5][2][n][n], the z-neighbours' planes) or, when they are
 // null (one device), wraps inside the slab.
+// One warp per padded row (f, z, y): the source row is resolved once, then
+// the row is copied as 16-byte pairs — the shift by NG = 2 cells keeps both
+// sides 16-byte aligned (n even, rows of n + 4 doubles): pair 0 is the left
+// ghost pair (cells n-2, n-1), pairs 1..n/2 the row, pair n/2+1 the right
+// ghost pair (cells 0, 1).
 __global__ void __launch_bounds__(256) k_star_pad(const double *__restrict__ U,
                                                   const double *__restrict__ lo,
                                                   const double *__restrict__ hi,
                                                   double *__restrict__ Up, int n, int nz) {
   const int P = n + 2 * NG, Pz = nz + 2 * NG;
   const int64_t plane = (int64_t)n * n;
-  const int64_t total = (int64_t)NF * P * P * Pz;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int x = (int)(e % P), y = (int)((e / P) % P), z = (int)((e / ((int64_t)P * P)) % Pz);
-    const int f = (int)(e / ((int64_t)P * P * Pz));
-    const int sx = (x - NG + n) % n, sy = (y - NG + n) % n, zl = z - NG;
-    const int64_t in_plane = (int64_t)sy * n + sx;
-    double v;
+  const int64_t rows = (int64_t)NF * Pz * P;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int pairs = n / 2 + 2;
+  for (int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < rows;
+       row += warps) {
+    const int y = (int)(row % P), z = (int)((row / P) % Pz), f = (int)(row / ((int64_t)P * Pz));
+    const int sy = (y - NG + n) % n, zl = z - NG;
+    const double *src;
     if (zl >= 0 && zl < nz)
-      v = __ldg(U + ((int64_t)f * nz + zl) * plane + in_plane);
+      src = U + ((int64_t)f * nz + zl) * plane;
     else if (!lo)
-      v = __ldg(U + ((int64_t)f * nz + (zl + nz) % nz) * plane + in_plane);
+      src = U + ((int64_t)f * nz + (zl + nz) % nz) * plane;
     else if (zl < 0)
-      v = __ldg(lo + ((int64_t)f * NG + (zl + NG)) * plane + in_plane);
+      src = lo + ((int64_t)f * NG + (zl + NG)) * plane;
     else
-      v = __ldg(hi + ((int64_t)f * NG + (zl - nz)) * plane + in_plane);
-    Up[e] = v;
+      src = hi + ((int64_t)f * NG + (zl - nz)) * plane;
+    const double2 *s2 = reinterpret_cast<const double2 *>(src + (int64_t)sy * n);
+    double2 *d2 = reinterpret_cast<double2 *>(Up + row * P);
+    for (int j0 = 0; j0 < pairs; j0 += 4 * 32) {   // 4 loads in flight per lane
+      double2 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = j0 + u * 32 + lane;
+        const int k = j == 0 ? n / 2 - 1 : (j == pairs - 1 ? 0 : j - 1);
+        if (j < pairs) v[u] = __ldg(s2 + k);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = j0 + u * 32 + lane;
+        if (j < pairs) d2[j] = v[u];
+      }
+    }
   }
 }
 
@@ -128,8 +149,8 @@ int tb_star_pad_slab(tb_stream_t s, const double *U, int64_t n, int64_t nz, cons
                      const double *hi, double *Up) {
   if (!U || !Up || n < 8 || n % 8 || nz < 8 || nz % 8 || (!lo != !hi)) return TB_E_INVALID;
   const int64_t P = n + 2 * NG, Pz = nz + 2 * NG;
-  k_star_pad<<<grid_for(NF * P * P * Pz, 256), 256, 0, strm(s)>>>(U, lo, hi, Up, (int)n,
-                                                                  (int)nz);
+  k_star_pad<<<grid_for(NF * P * Pz * 32, 256), 256, 0, strm(s)>>>(U, lo, hi, Up, (int)n,
+                                                                   (int)nz);
   return tb::last_error();
 }
 

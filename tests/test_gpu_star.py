@@ -53,3 +53,28 @@ def test_star_conserves_mass_at_max_level_4():
     assert abs(m1 - m0) <= 1e-13 * m0
     assert torch.isfinite(st.U).all()
     assert st.dt.item() > 0
+
+
+@pytest.mark.parametrize("n,nz,halo", [(8, 8, False), (16, 16, False), (24, 8, True),
+                                       (16, 32, True), (40, 16, False)])
+def test_pad_is_exact(n, nz, halo):
+    """tb_star_pad_slab: x, y periodic, z from the neighbours' planes (or
+    periodic without them) — an exact copy, checked against numpy."""
+    from paper_2303_08058_b200 import _native as N
+    dev = torch.device("cuda", 0)
+    g = torch.Generator().manual_seed(n * 100 + nz)
+    U = torch.rand((5, nz, n, n), dtype=torch.float64, generator=g)
+    lo = torch.rand((5, 2, n, n), dtype=torch.float64, generator=g)
+    hi = torch.rand((5, 2, n, n), dtype=torch.float64, generator=g)
+    Up = torch.full((5, nz + 4, n + 4, n + 4), float("nan"), dtype=torch.float64, device=dev)
+    Ud, lod, hid = U.to(dev), lo.to(dev), hi.to(dev)
+    N.call("tb_star_pad_slab", 0, Ud.data_ptr(), n, nz, lod.data_ptr() if halo else None,
+           hid.data_ptr() if halo else None, Up.data_ptr())
+    torch.cuda.synchronize()
+    u = U.numpy()
+    if halo:
+        u = np.concatenate([lo.numpy(), u, hi.numpy()], axis=1)
+        want = np.pad(u, ((0, 0), (0, 0), (2, 2), (2, 2)), mode="wrap")
+    else:
+        want = np.pad(u, ((0, 0), (2, 2), (2, 2), (2, 2)), mode="wrap")
+    np.testing.assert_array_equal(Up.cpu().numpy(), want)
