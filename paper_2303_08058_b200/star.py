@@ -35,7 +35,7 @@ class RotatingStarStep:
 
     def __init__(self, max_level: int, gamma: float = 5.0 / 3.0, cfl: float = 0.4,
                  omega: float = 0.3, device: Optional[torch.device] = None,
-                 state: Optional[torch.Tensor] = None):
+                 state: Optional[torch.Tensor] = None, concurrent: bool = True):
         self.device = torch.device(device) if device is not None else torch.device("cuda")
         if self.device.type != "cuda":
             raise RuntimeError("RotatingStarStep needs a CUDA device (no CPU fallback)")
@@ -60,16 +60,28 @@ class RotatingStarStep:
         self.time = torch.zeros(1, **f64)
         self.gravity = GravitySolver(max_level, self.device)
         self._graph = None
+        self._concurrent = concurrent
+        self._side = torch.cuda.Stream(self.device) if concurrent else None
 
     def _s(self) -> int:
         return torch.cuda.current_stream(self.device).cuda_stream
 
     def _rhs(self, Uc: torch.Tensor) -> None:
-        s = self._s()
+        # hydro (pad + K6) and gravity (K7) both only read Uc: the hydro
+        # branch runs on a side stream so it fills the SMs the FMM's coarse
+        # levels leave idle (fork/join by events; captured as graph branches)
+        main = torch.cuda.current_stream(self.device)
+        if self._concurrent:
+            self._side.wait_stream(main)
+            s = self._side.cuda_stream
+        else:
+            s = main.cuda_stream
         N.call("tb_star_pad", s, Uc.data_ptr(), self.n, self.Up.data_ptr())
         N.call("tb_hydro_flux_lattice", s, self.Up.data_ptr(), self.n, self.n,
                self.dudt.data_ptr(), self.amax.data_ptr(), self.dx, self.gamma)
         self.gravity.solve(Uc[0])
+        if self._concurrent:
+            main.wait_stream(self._side)
 
     def _g(self) -> int:
         return self.gravity.out.data_ptr() + self.n ** 3 * 8     # rows 1..3 of [4][N^3]

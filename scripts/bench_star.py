@@ -28,7 +28,8 @@ def timed(st, steps, graph):
 def main():
     L = int(sys.argv[1]) if len(sys.argv) > 1 else 5
     steps = int(sys.argv[2]) if len(sys.argv) > 2 else 10
-    st = RotatingStarStep(L)
+    concurrent = not (len(sys.argv) > 3 and sys.argv[3] == "serial")
+    st = RotatingStarStep(L, concurrent=concurrent)
     m0, _, e0 = st.totals()
     eager = timed(st, steps, False)
     graph = timed(st, steps, True)
@@ -37,6 +38,7 @@ def main():
     print(json.dumps({
         "workload": f"rotating star step (hydro + FMM gravity, SSP-RK2), max_level {L}, "
                     f"{cells} cells",
+        "hydro_branch": "side stream" if concurrent else "serial",
         "ms_per_step_eager": eager, "ms_per_step_graph": graph,
         "cells_per_s": cells / (min(eager, graph) * 1e-3),
         "launches_per_step": st.launches_per_step(),
