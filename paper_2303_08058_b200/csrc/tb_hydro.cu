@@ -26,7 +26,7 @@ constexpr int NCELL = NT * NT * NT;            // 1728
 constexpr int NFACE = (NI + 1) * NI * NI;      // 576 faces per direction
 constexpr int kThreads = 256;
 constexpr int kCellsPerThread = NI * NI * NI / kThreads;   // 2
-constexpr int kSmem = (NF * NCELL + NF * NFACE) * 8;       // 92,160 B
+constexpr int kSmem = (NF * NCELL + 2 * NF * NFACE) * 8;   // 115,200 B (2 CTAs/SM)
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                  double dx, double gamma) {
   extern __shared__ __align__(128) double sm[];
   double *W = sm;                        // [5][1728] primitives (staged U)
-  double *Fb = sm + NF * NCELL;          // [5][576] one direction's face fluxes
+  double *Fb0 = sm + NF * NCELL;         // [2][5][576] face fluxes, by direction parity
   __shared__ __align__(8) uint64_t bar;
   __shared__ double s_amax[kThreads / 32];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -94,32 +94,32 @@ __global__ void __launch_bounds__(kThreads, 2)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  // stage sub-grid s (one bulk copy / TMA box of 69,120 B) into W
+  auto issue = [&](int64_t s) {
+    const uint32_t bytes = NF * NCELL * 8;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar)),
+                 "r"(bytes)
+                 : "memory");
+    if constexpr (LATTICE) {
+      const int bx = (int)(s % nb), by = (int)((s / nb) % nb), bz = (int)(s / ((int64_t)nb * nb));
+      asm volatile(
+          "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes "
+          "[%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(W)),
+          "l"(reinterpret_cast<uint64_t>(&map)), "r"(8 * bx), "r"(8 * by), "r"(8 * bz), "r"(0),
+          "r"(smem_u32(&bar))
+          : "memory");
+    } else {
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], "
+          "%2, [%3];" ::"r"(smem_u32(W)),
+          "l"(U + s * (int64_t)(NF * NCELL)), "r"(bytes), "r"(smem_u32(&bar))
+          : "memory");
+    }
+  };
+  if (t == 0 && blockIdx.x < nsub) issue(blockIdx.x);
   uint32_t phase = 0;
   for (int64_t s = blockIdx.x; s < nsub; s += gridDim.x, phase ^= 1) {
-    // ---- stage the ghosted sub-grid (one bulk copy of 69,120 B) ----------
-    if (t == 0) {
-      const uint32_t bytes = NF * NCELL * 8;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                       smem_u32(&bar)),
-                   "r"(bytes)
-                   : "memory");
-      if constexpr (LATTICE) {
-        const int bx = (int)(s % nb), by = (int)((s / nb) % nb), bz = (int)(s / ((int64_t)nb * nb));
-        asm volatile(
-            "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes "
-            "[%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(W)),
-            "l"(reinterpret_cast<uint64_t>(&map)), "r"(8 * bx), "r"(8 * by), "r"(8 * bz), "r"(0),
-            "r"(smem_u32(&bar))
-            : "memory");
-      } else {
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], "
-            "%2, [%3];" ::"r"(smem_u32(W)),
-            "l"(U + s * (int64_t)(NF * NCELL)), "r"(bytes), "r"(smem_u32(&bar))
-            : "memory");
-      }
-    }
     asm volatile(
         "{\n\t.reg .pred p;\nHW_%=:\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
@@ -127,6 +127,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         "r"(phase)
         : "memory");
     // ---- conserved -> primitive, in place --------------------------------
+#pragma unroll 4
     for (int c = t; c < NCELL; c += kThreads) {
       const double rho = W[c], sx = W[NCELL + c], sy = W[2 * NCELL + c],
                    sz = W[3 * NCELL + c], E = W[4 * NCELL + c];
@@ -145,7 +146,11 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll 1
     for (int d = 0; d < 3; ++d) {
       const int stride = d == 0 ? 1 : (d == 1 ? NT : NT * NT);
+      // two flux buffers by direction parity: the fold of d and the faces of
+      // d + 1 need no barrier between them
+      double *Fb = Fb0 + (d & 1) * (NF * NFACE);
       // ---- face fluxes along d ------------------------------------------
+#pragma unroll 2
       for (int f = t; f < NFACE; f += kThreads) {
         // enumerate with the x-index fastest (stride-1 shared-memory reads)
         int c, ti, tj;   // c: face index along d (0..8); ti, tj: transverse
@@ -198,6 +203,9 @@ __global__ void __launch_bounds__(kThreads, 2)
                                           -__dmul_rn(ha, __dadd_rn(R.u[v], -L.u[v])));
       }
       __syncthreads();
+      // every face of this sub-grid is done with W: stream the next one in
+      // under the last fold, the output and the signal-speed reduction
+      if (d == 2 && t == 0 && s + gridDim.x < nsub) issue(s + gridDim.x);
       // ---- fold this direction's flux differences into the cells ----------
 #pragma unroll
       for (int m = 0; m < kCellsPerThread; ++m) {
@@ -220,7 +228,6 @@ __global__ void __launch_bounds__(kThreads, 2)
           du[v][m] = d == 0 ? diff : __dadd_rn(du[v][m], diff);
         }
       }
-      __syncthreads();
     }
     // ---- dU/dt = -(du / dx), coalesced ------------------------------------
     double *out = dudt + s * (int64_t)(NF * NI * NI * NI);

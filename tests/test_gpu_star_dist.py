@@ -55,7 +55,9 @@ def _worker(rank, world, port, L, steps, q):
         for _ in range(steps):
             drv.step()
         torch.cuda.synchronize()
-        q.put((rank, slab.U.cpu(), slab.time.item()))
+        # numpy travels by value (a shared torch tensor's file descriptor dies
+        # with this process if it exits before the parent has read it)
+        q.put((rank, slab.U.cpu().numpy(), slab.time.item()))
         dist.barrier()
     finally:
         dist.destroy_process_group()
@@ -87,6 +89,6 @@ def test_dist_driver_processes_equal_single_device(world, L):
     ref = RotatingStarStep(L, device=torch.device("cuda", 0))
     for _ in range(steps):
         ref.step()
-    got = torch.cat([o[1] for o in outs], dim=1)
+    got = torch.cat([torch.from_numpy(o[1]) for o in outs], dim=1)
     assert torch.equal(got, ref.U.cpu())
     assert all(o[2] == ref.time.item() for o in outs)

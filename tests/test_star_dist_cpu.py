@@ -95,7 +95,10 @@ def _worker(rank, world, port, q):
         drv._wait(first_only=False)
         m = _reqs(world, "min")[rank][1]
         drv._min(m)
-        q.put((rank, res, full, m.item()))
+        # numpy payloads travel by value (a torch tensor would be shared through
+        # a file descriptor that dies with this process if it exits first)
+        q.put((rank, {k: (a.numpy(), b.numpy()) for k, (a, b) in res.items()},
+               full.numpy().copy(), m.item()))
     finally:
         dist.destroy_process_group()
 
@@ -124,8 +127,8 @@ def test_dist_driver_matches_virtual_cluster(world):
         want = _reqs(world, "halo", periodic)
         vc._service(want)
         for r in range(world):
-            assert torch.equal(outs[r][1][periodic][0], want[r][3])
-            assert torch.equal(outs[r][1][periodic][1], want[r][4])
+            assert torch.equal(torch.from_numpy(outs[r][1][periodic][0]), want[r][3])
+            assert torch.equal(torch.from_numpy(outs[r][1][periodic][1]), want[r][4])
     gathered = torch.repeat_interleave(torch.arange(1.0, world + 1), 4)
-    assert all(torch.equal(o[2], gathered) for o in outs)
+    assert all(torch.equal(torch.from_numpy(o[2]), gathered) for o in outs)
     assert all(o[3] == 5.0 - (world - 1) for o in outs)
