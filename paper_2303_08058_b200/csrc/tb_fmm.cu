@@ -282,6 +282,18 @@ constexpr PTab make_ptab() {
   return T;
 }
 __constant__ PTab c_pnear = make_ptab();
+// P = (0,0,0): every child pair of it is near (|o - c|^2 <= 3), so its M2L
+// stage is all zero tensors — the M2L walks the other 32 stages only.
+constexpr int self_stage() {
+  const PTab T = make_ptab();
+  for (int k = 0; k < 33; ++k)
+    if (T.p[k][0] == 0 && T.p[k][1] == 0 && T.p[k][2] == 0) return k;
+  return -1;
+}
+constexpr int kSelfStage = self_stage();
+static_assert(kSelfStage == 16, "PNEAR order");
+constexpr int kM2LStages = 32;
+__host__ __device__ constexpr int m2l_stage(int s) { return s + (s >= kSelfStage); }
 
 // Leaf stencil weights by integer offset q = i - j in [-5,5]^3:
 // (1/|q|, qx/|q|^3, qy/|q|^3, qz/|q|^3); q = 0 -> 0 (the self term).
@@ -565,14 +577,14 @@ __global__ void __launch_bounds__(kM2LThreads, 1) k_fmm_m2l(const __grid_constan
   const int ZT = Z0 + P.zoff[lev];     // TMA z of the sub-grid in the halo'd records
   if (t == 0) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    issue_stage(P, lev, sm, &bar[0], 0, X0, Y0, ZT);
-    issue_stage(P, lev, sm + kStage, &bar[1], 1, X0, Y0, ZT);
+    issue_stage(P, lev, sm, &bar[0], m2l_stage(0), X0, Y0, ZT);
+    issue_stage(P, lev, sm + kStage, &bar[1], m2l_stage(1), X0, Y0, ZT);
   }
   // lane-dependent parts of the source cell and of the D-table entry
   const int cbase = ((2 * pzb) * 8 + 2 * py) * 8 + 2 * px;   // target 0; target 1 is +256
   const int dbase = (ox + 1) * kDX + (oy + 1) * kDY + (oz + 1) * kDZ;
 #pragma unroll 1
-  for (int k = 0; k < 33; ++k) {
+  for (int k = 0; k < kM2LStages; ++k) {
     const int buf = k & 1;
     mbar_wait(&bar[buf], (k >> 1) & 1);
     const double *Ms = sm + buf * kStage;
@@ -590,9 +602,9 @@ __global__ void __launch_bounds__(kM2LThreads, 1) k_fmm_m2l(const __grid_constan
       }
     }
     __syncthreads();            // every thread is done with this buffer
-    if (t == 0 && k + 2 < 33) {
+    if (t == 0 && k + 2 < kM2LStages) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue_stage(P, lev, sm + buf * kStage, &bar[buf], k + 2, X0, Y0, ZT);
+      issue_stage(P, lev, sm + buf * kStage, &bar[buf], m2l_stage(k + 2), X0, Y0, ZT);
     }
   }
   const int N = 8 << lev;
