@@ -659,10 +659,13 @@ __global__ void __launch_bounds__(256) k_fmm_down(const double *__restrict__ Lp,
 
 // ------------------------------------------------------------ leaf (P2P)
 constexpr int kLeafThreads = 256;
-constexpr int kTX = 8, kTY = 8, kTZ = 16;                // targets per CTA tile
-constexpr int kSX = 12, kSY = 8, kSZ = (kTZ + 8) / 2;   // per-parity staged extents
+// Each thread: one octant, 2 parent rows in y x 4 parent planes in z = 8
+// targets sharing every stencil weight (4 constant loads per 32 FMAs).
+constexpr int kRY = 2, kRZ = 4;
+constexpr int kTX = 8, kTY = 8 * kRY, kTZ = 16;          // targets per CTA tile
+constexpr int kSX = 12, kSY = (kTY + 8) / 2, kSZ = (kTZ + 8) / 2;   // per-parity extents
 constexpr int kPar = kSX * kSY * kSZ;                    // x' padded 8 -> 12 (banks)
-constexpr int kLeafSmem = 8 * kPar * 8;                  // 73,728 B
+constexpr int kLeafSmem = 8 * kPar * 8;                  // 110,592 B
 
 // Leaves: N x N x nz (this rank's planes). rho points at local plane 0 and
 // its planes [zmin, zmax) are readable (a halo of exchanged planes, or just
@@ -677,11 +680,12 @@ __global__ void __launch_bounds__(kLeafThreads, 2)
   const int tile = blockIdx.x;
   const int X0 = (tile % ntx) * kTX, Y0 = ((tile / ntx) % nty) * kTY,
             Z0 = (tile / (ntx * nty)) * kTZ;
-  // ---- stage rho over [X0-4, X0+12) x [Y0-4, Y0+12) x [Z0-4, Z0+20), split by
-  //      parity: S[c][z'][y'][x'] with coordinate = 2*primed + c; 8-byte
-  //      cp.async (all in flight at once), zero-filled outside the domain
-  for (int e = t; e < 16 * 16 * 24; e += kLeafThreads) {
-    const int rx = e & 15, ry = (e >> 4) & 15, rz = e >> 8;
+  // ---- stage rho over [X0-4, X0+kTX+4) x [Y0-4, Y0+kTY+4) x [Z0-4, Z0+kTZ+4),
+  //      split by parity: S[c][z'][y'][x'] with coordinate = 2*primed + c;
+  //      8-byte cp.async (all in flight at once), zero-filled outside the domain
+  constexpr int kEx = kTX + 8, kEy = kTY + 8, kEz = kTZ + 8;
+  for (int e = t; e < kEx * kEy * kEz; e += kLeafThreads) {
+    const int rx = e % kEx, ry = (e / kEx) % kEy, rz = e / (kEx * kEy);
     const int gx = X0 - 4 + rx, gy = Y0 - 4 + ry, gz = Z0 - 4 + rz;
     const bool in = gx >= 0 && gx < N && gy >= 0 && gy < N && gz >= zmin && gz < zmax;
     const double *src = in ? rho + ((int64_t)gz * N + gy) * N + gx : rho;
@@ -693,12 +697,13 @@ __global__ void __launch_bounds__(kLeafThreads, 2)
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
-  // ---- warp = child octant o; lane = (px, py, pz low bit); 4 targets over pz
+  // ---- warp = child octant o; lane = (px, py, pz low bit); targets over
+  //      (ry: py + 4 ry) x (r: pz = pzl + 2 r)
   const int ox = w & 1, oy = (w >> 1) & 1, oz = w >> 2;
   const int px = lane & 3, py = (lane >> 2) & 3, pzl = lane >> 4;
-  double acc[4][4];
+  double acc[kRY * kRZ][4];
 #pragma unroll
-  for (int r = 0; r < 4; ++r)
+  for (int r = 0; r < kRY * kRZ; ++r)
 #pragma unroll
     for (int k = 0; k < 4; ++k) acc[r][k] = 0.0;
 #pragma unroll 1
@@ -712,13 +717,16 @@ __global__ void __launch_bounds__(kLeafThreads, 2)
       const double w0 = c_w[wi][0], w1 = c_w[wi][1], w2 = c_w[wi][2], w3 = c_w[wi][3];
       const double *base = S + c * kPar + ((py + Py + 2) * kSX) + (px + Px + 2);
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const double m = base[(pzl + 2 * r + Pz + 2) * (kSX * kSY)];
-        acc[r][0] = fma(m, w0, acc[r][0]);
-        acc[r][1] = fma(m, w1, acc[r][1]);
-        acc[r][2] = fma(m, w2, acc[r][2]);
-        acc[r][3] = fma(m, w3, acc[r][3]);
-      }
+      for (int ry = 0; ry < kRY; ++ry)
+#pragma unroll
+        for (int r = 0; r < kRZ; ++r) {
+          const double m = base[(pzl + 2 * r + Pz + 2) * (kSX * kSY) + 4 * ry * kSX];
+          double(&a)[4] = acc[ry * kRZ + r];
+          a[0] = fma(m, w0, a[0]);
+          a[1] = fma(m, w1, a[1]);
+          a[2] = fma(m, w2, a[2]);
+          a[3] = fma(m, w3, a[3]);
+        }
     }
   }
   // ---- L2P from the parent's expansion (level L-1) and the output --------
@@ -728,10 +736,12 @@ __global__ void __launch_bounds__(kLeafThreads, 2)
   const size_t n = (size_t)N * N * nz;
   const double h2 = h * h;
 #pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int x = X0 + 2 * px + ox, y = Y0 + 2 * py + oy, z = Z0 + 2 * (pzl + 2 * r) + oz;
-    double phi = -h2 * acc[r][0];
-    double gr[3] = {h * acc[r][1], h * acc[r][2], h * acc[r][3]};
+  for (int rr = 0; rr < kRY * kRZ; ++rr) {
+    const int ry = rr / kRZ, r = rr % kRZ;
+    const int x = X0 + 2 * px + ox, y = Y0 + 2 * (py + 4 * ry) + oy,
+              z = Z0 + 2 * (pzl + 2 * r) + oz;
+    double phi = -h2 * acc[rr][0];
+    double gr[3] = {h * acc[rr][1], h * acc[rr][2], h * acc[rr][3]};
     if (Lpar) {
       const size_t pi = ((size_t)(z >> 1) * Nq + (y >> 1)) * Nq + (x >> 1);
       double Lp[NC];
