@@ -150,57 +150,69 @@ __global__ void __launch_bounds__(kThreads, 2)
       // d + 1 need no barrier between them
       double *Fb = Fb0 + (d & 1) * (NF * NFACE);
       // ---- face fluxes along d ------------------------------------------
-#pragma unroll 2
-      for (int f = t; f < NFACE; f += kThreads) {
-        // enumerate with the x-index fastest (stride-1 shared-memory reads)
-        int c, ti, tj;   // c: face index along d (0..8); ti, tj: transverse
-        int i, j, k;     // 12-grid coordinates of the face's left cell
+      // 192 threads, three consecutive faces of one line each: the 6 cells
+      // they read per field are loaded once and each interior slope (cells
+      // c0+1 .. c0+4) is formed once for the two faces that use it
+      if (t < 3 * NI * NI) {
+        int g, ti, tj;
         if (d == 0) {
-          c = f % 9;
-          ti = (f / 9) % NI;
-          tj = f / (9 * NI);
-          i = 1 + c, j = NG + ti, k = NG + tj;
-        } else if (d == 1) {
-          ti = f % NI;
-          c = (f / NI) % 9;
-          tj = f / (NI * 9);
-          i = NG + ti, j = 1 + c, k = NG + tj;
+          g = t % 3;
+          ti = (t / 3) % NI;
+          tj = t / (3 * NI);
         } else {
-          ti = f % NI;
-          tj = (f / NI) % NI;
-          c = f / (NI * NI);
-          i = NG + ti, j = NG + tj, k = 1 + c;
+          ti = t % NI;
+          g = (t / NI) % 3;
+          tj = t / (3 * NI);
         }
-        const int base = (k * NT + j) * NT + i;
-        double qL[NF], qR[NF];
+        const int c0 = 3 * g;
+        // 12-grid cell of the first face's left neighbour minus one (c0)
+        int base;
+        if (d == 0)
+          base = ((NG + tj) * NT + (NG + ti)) * NT + c0;
+        else if (d == 1)
+          base = ((NG + tj) * NT + c0) * NT + (NG + ti);
+        else
+          base = (c0 * NT + (NG + tj)) * NT + (NG + ti);
+        double qL[3][NF], qR[3][NF];
 #pragma unroll
         for (int v = 0; v < NF; ++v) {
           const double *w = W + v * NCELL + base;
-          const double qm = w[-stride], q0 = w[0], qp = w[stride], qpp = w[2 * stride];
-          const double s0 = minmod(__dadd_rn(q0, -qm), __dadd_rn(qp, -q0));
-          const double s1 = minmod(__dadd_rn(qp, -q0), __dadd_rn(qpp, -qp));
-          qL[v] = __dadd_rn(q0, __dmul_rn(0.5, s0));
-          qR[v] = __dadd_rn(qp, -__dmul_rn(0.5, s1));
-        }
-        State L, R;
-        face_state(qL[0], qL[1], qL[2], qL[3], qL[4], gamma, igm1, d, L);
-        face_state(qR[0], qR[1], qR[2], qR[3], qR[4], gamma, igm1, d, R);
-        const double a = fmax(L.a, R.a);
-        amax = fmax(amax, a);
-        const double ha = __dmul_rn(0.5, a);
-        // flux buffer index: (slow transverse, fast transverse, c) so the
-        // accumulation below reads lo/hi faces at a fixed layout per d
-        int idx;
-        if (d == 0)
-          idx = (tj * NI + ti) * 9 + c;          // (k, j, face i)
-        else if (d == 1)
-          idx = (tj * 9 + c) * NI + ti;          // (k, face j, i)
-        else
-          idx = (c * NI + tj) * NI + ti;         // (face k, j, i)
+          double q[6];
 #pragma unroll
-        for (int v = 0; v < NF; ++v)
-          Fb[v * NFACE + idx] = __dadd_rn(__dmul_rn(0.5, __dadd_rn(L.f[v], R.f[v])),
-                                          -__dmul_rn(ha, __dadd_rn(R.u[v], -L.u[v])));
+          for (int e = 0; e < 6; ++e) q[e] = w[e * stride];
+          double sl[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            sl[e] = minmod(__dadd_rn(q[e + 1], -q[e]), __dadd_rn(q[e + 2], -q[e + 1]));
+#pragma unroll
+          for (int cc = 0; cc < 3; ++cc) {
+            qL[cc][v] = __dadd_rn(q[cc + 1], __dmul_rn(0.5, sl[cc]));
+            qR[cc][v] = __dadd_rn(q[cc + 2], -__dmul_rn(0.5, sl[cc + 1]));
+          }
+        }
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) {
+          const int c = c0 + cc;
+          State L, R;
+          face_state(qL[cc][0], qL[cc][1], qL[cc][2], qL[cc][3], qL[cc][4], gamma, igm1, d, L);
+          face_state(qR[cc][0], qR[cc][1], qR[cc][2], qR[cc][3], qR[cc][4], gamma, igm1, d, R);
+          const double a = fmax(L.a, R.a);
+          amax = fmax(amax, a);
+          const double ha = __dmul_rn(0.5, a);
+          // flux buffer index: (slow transverse, fast transverse, c) so the
+          // accumulation below reads lo/hi faces at a fixed layout per d
+          int idx;
+          if (d == 0)
+            idx = (tj * NI + ti) * 9 + c;          // (k, j, face i)
+          else if (d == 1)
+            idx = (tj * 9 + c) * NI + ti;          // (k, face j, i)
+          else
+            idx = (c * NI + tj) * NI + ti;         // (face k, j, i)
+#pragma unroll
+          for (int v = 0; v < NF; ++v)
+            Fb[v * NFACE + idx] = __dadd_rn(__dmul_rn(0.5, __dadd_rn(L.f[v], R.f[v])),
+                                            -__dmul_rn(ha, __dadd_rn(R.u[v], -L.u[v])));
+        }
       }
       __syncthreads();
       // every face of this sub-grid is done with W: stream the next one in
