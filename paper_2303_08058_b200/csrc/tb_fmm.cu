@@ -342,9 +342,13 @@ __global__ void __launch_bounds__(256) k_fmm_up(const double *__restrict__ rho,
                                                 double *__restrict__ parent_red, int Np,
                                                 int Npz, double hc) {
   // parents: Np x Np x Npz (this rank's planes); all pointers at local plane 0
+  __shared__ __align__(16) double stage[256 * NC];   // the block's records
   const int64_t npar = (int64_t)Np * Np * Npz;
-  const int64_t pidx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (pidx >= npar) return;
+  const int64_t first = (int64_t)blockIdx.x * blockDim.x;
+  // a thread past the end recomputes the last parent (its record is not
+  // copied out) so every thread reaches the block's barriers
+  const int64_t pidx = min(first + threadIdx.x, npar - 1);
+  const int nrec = (int)min((int64_t)blockDim.x, npar - first);
   const int px = (int)(pidx % Np), py = (int)((pidx / Np) % Np),
             pz = (int)(pidx / ((int64_t)Np * Np));
   const int Nc = 2 * Np;
@@ -396,18 +400,27 @@ __global__ void __launch_bounds__(256) k_fmm_up(const double *__restrict__ rho,
     constexpr double sc = m2l_scale(K);
     M[K] = M[K] * sc;
   });
-  double2 *raw = reinterpret_cast<double2 *>(parent + pidx * NC);
+  // records leave through shared memory so each warp store instruction
+  // writes 512 contiguous bytes (a record per thread would be a 160-B stride)
+  const int t = threadIdx.x;
+  double2 *st2 = reinterpret_cast<double2 *>(stage);
 #pragma unroll
-  for (int k = 0; k < NC / 2; ++k) raw[k] = make_double2(M[2 * k], M[2 * k + 1]);
+  for (int k = 0; k < NC / 2; ++k) st2[t * (NC / 2) + k] = make_double2(M[2 * k], M[2 * k + 1]);
+  __syncthreads();
+  double2 *raw = reinterpret_cast<double2 *>(parent + first * NC);
+  for (int i = t; i < nrec * (NC / 2); i += blockDim.x) raw[i] = st2[i];
+  __syncthreads();
   // traceless reduction (see kRed): fold the zz-containing moments
   const double red[MS] = {M[0],          M[1],          M[2],          M[3],
                           M[4] - M[9],   M[5],          M[6],          M[7] - M[9],
                           M[8],          M[10] - M[15], M[11] - M[18], M[12] - M[19],
                           M[13] - M[15], M[14],         M[16] - M[18], M[17] - M[19],
                           0.0,           0.0};
-  double2 *rd = reinterpret_cast<double2 *>(parent_red + pidx * MS);
 #pragma unroll
-  for (int k = 0; k < MS / 2; ++k) rd[k] = make_double2(red[2 * k], red[2 * k + 1]);
+  for (int k = 0; k < MS / 2; ++k) st2[t * (MS / 2) + k] = make_double2(red[2 * k], red[2 * k + 1]);
+  __syncthreads();
+  double2 *rd = reinterpret_cast<double2 *>(parent_red + first * MS);
+  for (int i = t; i < nrec * (MS / 2); i += blockDim.x) rd[i] = st2[i];
 }
 
 // --------------------------------------------------------- M2L D tables
