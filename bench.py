@@ -48,6 +48,9 @@ WORKLOADS = {
 }
 METRIC = "sub-grid cells processed/sec (rotating star, FP64) at 1/2/4/8 B200 vs CPU ref"
 BYTES_PER_CELL = 8 + 8 + 0.25 + 0.03125   # 16.28 B/cell-step
+# FP64 instructions per cell-step: 15 x (DMUL + DADD), the
+# ghost fold (2 ops on 16 of 512 cells), one DADD of the pairwise sum, one min
+FP64_PER_CELL = 30 + 2 * 16 / 512 + 2
 GOLDEN_DEFAULTS = float.fromhex("0x1.df1096d8fa699p+20")   # run_reference(512, 15)
 FALLBACK_HBM_GBS = 6650.0
 AUTO_IMPL = "bulk1"    # what TB_STEP_AUTO launches for the aligned (3, 5) chain
@@ -703,8 +706,10 @@ def main(argv=None):
                                     "lean": "k_step<3,5,lean48>",
                                     "pair": "k_step_pair<3,5>",
                                     "bulk1": "k_step_bulk<3,5,1 stage>"}[
-                                        args.step_impl] + (" (tb_step_final: K2 + fused K4)"
-                                                           if world == 1 else " (tb_step)"),
+                                        args.step_impl] + (
+                                            " (tb_step_deferred: K2, the previous step's "
+                                            "exact close in its extra CTA)"
+                                            if world == 1 else " (tb_step)"),
                          "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm,
                          "traffic": traffic,
@@ -712,7 +717,15 @@ def main(argv=None):
                                          "(profiles/k2_traffic.json)",
                          "algorithmic_bytes_per_launch": n_local * 512 * BYTES_PER_CELL,
                          "peak_source": peak_kind,
-                         "bytes_per_cell": BYTES_PER_CELL, "k2_ms": k2_ms},
+                         "bytes_per_cell": BYTES_PER_CELL, "k2_ms": k2_ms,
+                         # the co-limit: 15 x (DMUL + DADD) + fold
+                         # + pairwise sum + min, FMA forbidden by parity
+                         "fp64": {"instr_per_cell": FP64_PER_CELL,
+                                  "achieved": FP64_PER_CELL * n_local * 512 / (k2_ms * 1e-3),
+                                  "peak": fp64_peak()[0], "peak_source": fp64_peak()[1],
+                                  "unit": "FP64 instr/s",
+                                  "frac": FP64_PER_CELL * n_local * 512 / (k2_ms * 1e-3)
+                                  / fp64_peak()[0]}},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "ablation": ablation,
