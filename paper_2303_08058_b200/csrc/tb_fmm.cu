@@ -33,15 +33,21 @@
 //               70 FMAs on the traceless reduction, no branch: near pairs
 //               have D = 0).
 //   k_fmm_down  L2L, one level per launch (level 0: sums the 8 partials).
-//   k_fmm_leaf  monopole interactions at the leaves: a 264-point stencil whose
-//               weights 1/|q|, q/|q|^3 depend only on the integer offset q; a
-//               warp owns one child octant so q is warp-uniform and the
-//               weights come from constant memory; the leaf densities are
-//               staged parity-split in shared memory (conflict-free). Then the
-//               parent's local expansion is evaluated at the leaf (L2P).
+//   k_fmm_leaf_mma  monopole interactions at the leaves on the FP64 tensor
+//               cores (default): a 264-point stencil whose weights 1/|q|,
+//               q/|q|^3 depend only on the integer offset q is, for the two
+//               octants of a parent that differ in x, a GEMM (rows = parents,
+//               K = source offsets, N = 4 components x 2 octants) done with
+//               mma.sync.m8n8k4.f64 on leaf densities staged parity-split in
+//               shared memory; then the parent's local expansion is evaluated
+//               at the leaf (L2P).
+//   k_fmm_leaf  the same on the DFMA pipe (TB_LEAF_MMA=0): a warp owns one
+//               octant so q is warp-uniform and the weights come from
+//               constant memory.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <cmath>
 #include <utility>
@@ -298,6 +304,9 @@ __host__ __device__ constexpr int m2l_stage(int s) { return s + (s >= kSelfStage
 // Leaf stencil weights by integer offset q = i - j in [-5,5]^3:
 // (1/|q|, qx/|q|^3, qy/|q|^3, qz/|q|^3); q = 0 -> 0 (the self term).
 __constant__ double c_w[11 * 11 * 11][4];
+// The same table in global memory for lane-divergent gathers (L1-resident).
+__device__ double g_w[11 * 11 * 11][4];
+
 
 // Reduced moment records (the M2L's source) hold 16 moments padded to 18
 // doubles (144 B): the 4 cells a warp reads per LDS.128 (stride 2 cells = 18
@@ -779,6 +788,131 @@ __global__ void __launch_bounds__(kLeafThreads, 2)
   }
 }
 
+// ----------------------------------------------- leaf on FP64 tensor cores
+// The leaf sum out[i][k] = sum_j m_j W(i - j)[k] is a GEMM per pair of
+// targets that share a parent p: rows = parents, K = the 264 source offsets
+// (P in PNEAR, child c), N = 4 components x 2 octants (o, o + e_x). Both
+// octants of a parent read the same sources j = 2(p + P) + c (one A
+// operand) and differ only in the weights W(o - 2P - c) (B), so every tensor
+// FMA is useful (the self term's weights are zero). One mma.sync.m8n8k4.f64
+// takes 8 x-consecutive parents as rows and 4 children (one z-half) of one
+// offset P as K: 33 x 2 = 66 K-chunks. A CTA (8 warps) covers 16 x 8 x 4
+// leaves: warp = (octant pair: oy, oz) x (parent plane in z); its 4 row
+// groups are the 4 parent rows in y.
+constexpr int kMX = 16, kMY = 8, kMZ = 4;                  // leaves per CTA tile
+constexpr int kMSX = 12, kMSY = 8, kMSZ = 6;               // per-parity staged extents
+constexpr int kMPar = kMSX * kMSY * kMSZ + 4;              // 580: planes 4 apart mod 16
+constexpr int kMAcc = kMX * kMY * kMZ * 4;                 // tile results [z][y][x][4]
+constexpr int kLeafMmaSmem = (8 * kMPar + kMAcc) * 8;      // 53,504 B
+
+__global__ void __launch_bounds__(256) k_fmm_leaf_mma(const double *__restrict__ rho, int zmin,
+                                                      int zmax, const double *__restrict__ Lpar,
+                                                      double *__restrict__ out, int N, int nz,
+                                                      double h) {
+  extern __shared__ __align__(128) double S[];
+  double *acc = S + 8 * kMPar;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int ntx = N / kMX, nty = N / kMY;
+  const int tile = blockIdx.x;
+  const int X0 = (tile % ntx) * kMX, Y0 = ((tile / ntx) % nty) * kMY,
+            Z0 = (tile / (ntx * nty)) * kMZ;
+  // ---- stage rho over [X0-4, X0+20) x [Y0-4, Y0+12) x [Z0-4, Z0+8), split by
+  //      parity as in k_fmm_leaf (zero outside the readable planes)
+  constexpr int kEx = 2 * kMSX, kEy = 2 * kMSY, kEz = 2 * kMSZ;
+  for (int e = t; e < kEx * kEy * kEz; e += 256) {
+    const int rx = e % kEx, ry = (e / kEx) % kEy, rz = e / (kEx * kEy);
+    const int gx = X0 - 4 + rx, gy = Y0 - 4 + ry, gz = Z0 - 4 + rz;
+    const bool in = gx >= 0 && gx < N && gy >= 0 && gy < N && gz >= zmin && gz < zmax;
+    const double *src = in ? rho + ((int64_t)gz * N + gy) * N + gx : rho;
+    const int c = (rx & 1) | ((ry & 1) << 1) | ((rz & 1) << 2);
+    double *dst = S + c * kMPar + ((rz >> 1) * kMSY + (ry >> 1)) * kMSX + (rx >> 1);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src),
+                 "r"(in ? 8 : 0)
+                 : "memory");
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  const int oy = w & 1, oz = (w >> 1) & 1, zsel = w >> 2;
+  const int kk = lane & 3, nn = lane >> 2;    // B fragment B[kk][nn]; A fragment A[nn][kk]
+  const int ox = nn >> 2, comp = nn & 3;      // B column nn: octant (ox, oy, oz), component
+  const int cx = kk & 1, cy = kk >> 1;
+  // per-lane bases; an offset P then adds -2 (121 Pz + 11 Py + Px) to the
+  // weight index and (Pz kMSY + Py) kMSX + Px to the source address
+  int wbase[2], abase[2];
+#pragma unroll
+  for (int hz = 0; hz < 2; ++hz) {
+    wbase[hz] = (((oz - hz + 5) * 11 + (oy - cy + 5)) * 11 + (ox - cx + 5)) * 4 + comp;
+    abase[hz] = (kk | (hz << 2)) * kMPar + ((zsel + 2) * kMSY + 2) * kMSX + (nn + 2);
+  }
+  const double *gw = &g_w[0][0];
+  double C[4][2];
+#pragma unroll
+  for (int g = 0; g < 4; ++g) C[g][0] = C[g][1] = 0.0;
+#pragma unroll 1
+  for (int k = 0; k < 33; ++k) {
+    const int Px = c_pnear.p[k][0], Py = c_pnear.p[k][1], Pz = c_pnear.p[k][2];
+    const int woff = -8 * ((Pz * 11 + Py) * 11 + Px);
+    const int aoff = (Pz * kMSY + Py) * kMSX + Px;
+#pragma unroll
+    for (int hz = 0; hz < 2; ++hz) {
+      const double b = __ldg(gw + wbase[hz] + woff);
+      const double *a0 = S + abase[hz] + aoff;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const double a = a0[g * kMSX];
+        asm volatile(
+            "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+            : "+d"(C[g][0]), "+d"(C[g][1])
+            : "d"(a), "d"(b));
+      }
+    }
+  }
+  // ---- C[g]: lane holds (row nn, columns 2kk, 2kk+1) -> tile results
+#pragma unroll
+  for (int g = 0; g < 4; ++g)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int col = 2 * kk + e, cox = col >> 2, k = col & 3;
+      const int x = 2 * nn + cox, y = 2 * g + oy, z = 2 * zsel + oz;
+      acc[((z * kMY + y) * kMX + x) * 4 + k] = C[g][e];
+    }
+  __syncthreads();
+  // ---- L2P from the parent's expansion and the output, x-fastest -------
+  const int Nq = N / 2;
+  const size_t n = (size_t)N * N * nz;
+  const double h2 = h * h;
+  for (int e = t; e < kMX * kMY * kMZ; e += 256) {
+    const int lx = e % kMX, ly = (e / kMX) % kMY, lz = e / (kMX * kMY);
+    const int x = X0 + lx, y = Y0 + ly, z = Z0 + lz;
+    const double *a = acc + e * 4;
+    double phi = -h2 * a[0];
+    double gr[3] = {h * a[1], h * a[2], h * a[3]};
+    if (Lpar) {
+      double mono[NC];
+      monomials<true>(((lx & 1) - 0.5) * h, ((ly & 1) - 0.5) * h, ((lz & 1) - 0.5) * h, mono);
+      const size_t pi = ((size_t)(z >> 1) * Nq + (y >> 1)) * Nq + (x >> 1);
+      double Lp[NC];
+      const double2 *rec = reinterpret_cast<const double2 *>(Lpar + pi * NC);
+#pragma unroll
+      for (int k = 0; k < NC / 2; ++k) {
+        const double2 v = __ldg(rec + k);
+        Lp[2 * k] = v.x;
+        Lp[2 * k + 1] = v.y;
+      }
+      unroll<kL2L.n>([&](auto E) {
+        constexpr Term T = kL2L.v[E];
+        if constexpr (T.t == 0) phi = fma(Lp[T.s], mono[T.b], phi);
+        if constexpr (T.t >= 1 && T.t <= 3) gr[T.t - 1] = fma(Lp[T.s], mono[T.b], gr[T.t - 1]);
+      });
+    }
+    const size_t i = ((size_t)z * N + y) * N + x;
+    out[i] = phi;
+    out[n + i] = -gr[0];
+    out[2 * n + i] = -gr[1];
+    out[3 * n + i] = -gr[2];
+  }
+}
+
 // ------------------------------------------------------------------ host
 // Slab geometry for `ranks` devices, each owning N/ranks leaf planes in z.
 // Levels l >= lp are partitioned: this rank keeps its nz_l = N_l/ranks planes
@@ -864,7 +998,8 @@ int ensure_weights() {
         e[2] = y * r3;
         e[3] = z * r3;
       }
-  const int r = tb::rc(cudaMemcpyToSymbol(c_w, w, sizeof w));
+  int r = tb::rc(cudaMemcpyToSymbol(c_w, w, sizeof w));
+  if (r == TB_OK) r = tb::rc(cudaMemcpyToSymbol(g_w, w, sizeof w));
   if (r == TB_OK && dev < 31) done_mask |= 1 << dev;
   return r;
 }
@@ -910,6 +1045,13 @@ void launch_up(tb_stream_t s, const Geom &g, const Layout &lo, char *base, const
   k_fmm_up<<<(unsigned)((npar + 255) / 256), 256, 0, strm(s)>>>(
       l == g.L - 1 ? rho : nullptr, child, raw, red, Np, npz, 1.0 / double(2 * Np));
 }
+
+// leaf variant: FP64 tensor cores (k_fmm_leaf_mma, default) or the DFMA
+// stencil (k_fmm_leaf, TB_LEAF_MMA=0)
+const bool g_leaf_mma = [] {
+  const char *e = getenv("TB_LEAF_MMA");
+  return !(e && e[0] == '0');
+}();
 
 }  // namespace
 
@@ -1022,6 +1164,20 @@ int tb_fmm_slab_leaf(tb_stream_t s, int max_level, int ranks, int rank, const do
   const double *Lpar = reinterpret_cast<const double *>(reinterpret_cast<const char *>(work) +
                                                         lo.Loc[max_level - 1]);
   const int N = g.n[max_level], nz = g.nz[max_level];
+  if (g_leaf_mma) {
+    static bool attr_mma = false;
+    if (!attr_mma) {
+      r = tb::rc(cudaFuncSetAttribute(k_fmm_leaf_mma,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kLeafMmaSmem));
+      if (r != TB_OK) return r;
+      attr_mma = true;
+    }
+    const int tiles = (N / kMX) * (N / kMY) * (nz / kMZ);
+    k_fmm_leaf_mma<<<tiles, 256, kLeafMmaSmem, strm(s)>>>(rho, zmin, zmax, Lpar, out, N, nz,
+                                                          1.0 / N);
+    return tb::last_error();
+  }
   const int tiles = (N / kTX) * (N / kTY) * (nz / kTZ);
   k_fmm_leaf<<<tiles, kLeafThreads, kLeafSmem, strm(s)>>>(rho, zmin, zmax, Lpar, out, N, nz,
                                                           1.0 / N);
