@@ -209,6 +209,26 @@ def machine_ablation(subgrids=512, steps=5, repeats=3):
 
 
 HYDRO_BYTES_PER_SUBGRID = 5 * 12 ** 3 * 8 + 5 * 8 ** 3 * 8 + 8   # U in, dU/dt + amax out
+
+def hydro_fp64_per_subgrid():
+    """FP64 instructions per sub-grid of the K6 spec (oracle/hydro_oracle.py),
+    an IEEE divide / square root counted as the 8-instruction sequence it
+    executes (tb_internal.h div_rn_fast / sqrt_rn_fast); the minmod compares
+    (2 per slope) and the signal-speed maxima (2 per face) counted too — they
+    issue on the FP64 pipe. DESIGN.md K6."""
+    cells, faces = 12 ** 3, 3 * 9 * 8 * 8
+    convert = 8 + 3 + 6 + 2                 # 1/rho, v = s/rho, ke, p
+    state = 1 + 8 + 8 + 5 + 4 + 3 + 4 + 1 + 2 + 1   # cs, |v|^2, e, m, momentum/energy flux, a
+    flux = 2 * state + 1 + 5 * 5            # two states, a/2, 5 x LLF combine
+    # minmod PLM: per line segment of N faces, N+1 slopes (2 DADD + DMUL) and
+    # 4 ops per face, per field; 192 segments of 2 and 64 of 3 per direction
+    recon = 3 * 5 * (192 * (3 * 3 + 2 * 4) + 64 * (4 * 3 + 3 * 4))
+    fold = 512 * 5 * (1 + 2 + 2) + 512 * 5  # flux differences + the 1/dx scaling
+    compares = 3 * 5 * (192 * 3 + 64 * 4) * 2 + faces * 2
+    return cells * convert + faces * flux + recon + fold + compares
+
+
+HYDRO_FP64_PER_SUBGRID = hydro_fp64_per_subgrid()
 M2L_FMA, LEAF_FMA = 70, 4     # algorithmic FP64 FMAs per interaction (traceless M2L, DESIGN.md K7)
 
 
@@ -304,6 +324,10 @@ def north_star_kernels(dev, reps=20):
         "kernel": "k_hydro_flux", "ms": ms, "cells_per_s": S * 512 / (ms * 1e-3),
         "roofline": {"bound": "fp64 (divide/sqrt-heavy; see profiles)", "hbm_achieved_gbs": gbs,
                      "hbm_frac": gbs / hbm,
+                     "fp64_instr_per_subgrid": HYDRO_FP64_PER_SUBGRID,
+                     "fp64_achieved": S * HYDRO_FP64_PER_SUBGRID / (ms * 1e-3),
+                     "fp64_peak": f64, "fp64_peak_source": f64_src,
+                     "fp64_frac": S * HYDRO_FP64_PER_SUBGRID / (ms * 1e-3) / f64,
                      "algorithmic_bytes_per_launch": S * HYDRO_BYTES_PER_SUBGRID},
         "parity": "unpinned (self-authored spec; bit-exact to oracle/hydro_oracle.py)"}
     # K7: FMM gravity, max_level 4 (config 3)

@@ -316,6 +316,14 @@ int tb_fmm_slab_leaf(tb_stream_t s, int max_level, int ranks, int rank, const do
 #define TB_PROBE_DMUL_DADD 3
 int tb_fp64_probe(int op, int64_t iters, double *instr_per_s, double *sm_mhz);
 
+/* The branch-free division / square-root fast paths the hydro kernel uses
+ * (no reference counterpart), exposed for testing: for i < n, q[i] = a[i] /
+ * b[i] and r[i] = sqrt(a[i]) through the fast path (the IEEE intrinsic where
+ * it flags); *slow_count += the flagged cases. The tests compare q and r
+ * bitwise with IEEE division and square root. Device pointers; enqueued on s. */
+int tb_divsqrt_fast(tb_stream_t s, const double *a, const double *b, int64_t n, double *q,
+                    double *r, unsigned long long *slow_count);
+
 /* -------------------------------------------------- poll registry -- */
 /* PollRegistry (src/runtime/polling.py:17-147): a lock-free MPSC inbox of
  * (event, token) and a poll-owned pending vector, drained by a single-entrant

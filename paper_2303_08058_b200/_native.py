@@ -148,6 +148,7 @@ SIGNATURES = {
     "tb_acc_allreduce_p2p": [_u64, _vp, _vp, _int, _vp, _vp, _vp, _vp],
     "tb_hydro_flux": [_u64, _vp, _vp, _vp, _i64, _dbl, _dbl],
     "tb_fp64_probe": [_int, _i64, _vp, _vp],
+    "tb_divsqrt_fast": [_u64, _vp, _vp, _i64, _vp, _vp, _vp],
     "tb_hydro_flux_lattice": [_u64, _vp, _i64, _i64, _vp, _vp, _dbl, _dbl],
     "tb_star_pad": [_u64, _vp, _i64, _vp],
     "tb_star_pad_slab": [_u64, _vp, _i64, _i64, _vp, _vp, _vp],

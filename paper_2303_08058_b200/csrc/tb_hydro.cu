@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "../../include/tb.h"
 #include "tb_internal.h"
@@ -26,6 +27,7 @@ constexpr int NCELL = NT * NT * NT;            // 1728
 constexpr int NFACE = (NI + 1) * NI * NI;      // 576 faces per direction
 constexpr int kThreads = 256;
 constexpr int kCellsPerThread = NI * NI * NI / kThreads;   // 2
+constexpr int kDefaultVariant = 13;
 constexpr int kSmem = (NF * NCELL + 2 * NF * NFACE) * 8;   // 115,200 B (2 CTAs/SM)
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -37,10 +39,15 @@ struct State {
 };
 
 // Left/right state -> conserved vector, flux along d, signal speed |vn|+cs.
+template <bool FAST>
 __device__ __forceinline__ void face_state(double rho, double vx, double vy, double vz,
                                            double p, double gamma, double igm1, int d,
-                                           State &s) {
-  const double cs = __dsqrt_rn(__ddiv_rn(__dmul_rn(gamma, p), rho));
+                                           State &s, bool &ok) {
+  double cs;
+  if constexpr (FAST)
+    cs = tb::sqrt_rn_fast(tb::div_rn_fast(__dmul_rn(gamma, p), rho, ok), ok);
+  else
+    cs = __dsqrt_rn(__ddiv_rn(__dmul_rn(gamma, p), rho));
   const double vv = __dadd_rn(__dadd_rn(__dmul_rn(vx, vx), __dmul_rn(vy, vy)),
                               __dmul_rn(vz, vz));
   const double e = __dadd_rn(__dmul_rn(p, igm1), __dmul_rn(__dmul_rn(0.5, rho), vv));
@@ -71,12 +78,92 @@ __device__ __forceinline__ double minmod(double dl, double dr) {
   return __dmul_rn(dl, dr) <= 0.0 ? 0.0 : pick;
 }
 
+// N consecutive faces c0 .. c0+N-1 of the line (ti, tj) along d: the N+3
+// cells they read per field are loaded once and each interior slope is formed
+// once for the two faces that use it. Face c lies between 12-grid cells c+1
+// and c+2 along d; its flux goes to Fb at a fixed (slow transverse, fast
+// transverse, face) layout per d.
+template <int N, bool FAST>
+__device__ __forceinline__ void face_segment_impl(const double *W, double *Fb, int d, int stride,
+                                                  int ti, int tj, int c0, double gamma,
+                                                  double igm1, double &amax, bool &ok) {
+  int base;
+  if (d == 0)
+    base = ((NG + tj) * NT + (NG + ti)) * NT + c0;
+  else if (d == 1)
+    base = ((NG + tj) * NT + c0) * NT + (NG + ti);
+  else
+    base = (c0 * NT + (NG + tj)) * NT + (NG + ti);
+  double qL[N][NF], qR[N][NF];
+#pragma unroll
+  for (int v = 0; v < NF; ++v) {
+    const double *w = W + v * NCELL + base;
+    double q[N + 3];
+#pragma unroll
+    for (int e = 0; e < N + 3; ++e) q[e] = w[e * stride];
+    double sl[N + 1];
+#pragma unroll
+    for (int e = 0; e < N + 1; ++e)
+      sl[e] = minmod(__dadd_rn(q[e + 1], -q[e]), __dadd_rn(q[e + 2], -q[e + 1]));
+#pragma unroll
+    for (int cc = 0; cc < N; ++cc) {
+      qL[cc][v] = __dadd_rn(q[cc + 1], __dmul_rn(0.5, sl[cc]));
+      qR[cc][v] = __dadd_rn(q[cc + 2], -__dmul_rn(0.5, sl[cc + 1]));
+    }
+  }
+#pragma unroll
+  for (int cc = 0; cc < N; ++cc) {
+    const int c = c0 + cc;
+    State L, R;
+    face_state<FAST>(qL[cc][0], qL[cc][1], qL[cc][2], qL[cc][3], qL[cc][4], gamma, igm1, d, L,
+                     ok);
+    face_state<FAST>(qR[cc][0], qR[cc][1], qR[cc][2], qR[cc][3], qR[cc][4], gamma, igm1, d, R,
+                     ok);
+    const double a = fmax(L.a, R.a);
+    amax = fmax(amax, a);
+    const double ha = __dmul_rn(0.5, a);
+    int idx;
+    if (d == 0)
+      idx = (tj * NI + ti) * 9 + c;          // (k, j, face i)
+    else if (d == 1)
+      idx = (tj * 9 + c) * NI + ti;          // (k, face j, i)
+    else
+      idx = (c * NI + tj) * NI + ti;         // (face k, j, i)
+#pragma unroll
+    for (int v = 0; v < NF; ++v)
+      Fb[v * NFACE + idx] = __dadd_rn(__dmul_rn(0.5, __dadd_rn(L.f[v], R.f[v])),
+                                      -__dmul_rn(ha, __dadd_rn(R.u[v], -L.u[v])));
+  }
+}
+
+// FAST: branch-free divide / square-root fast paths (tb_internal.h), so the
+// independent chains of a thread's faces interleave; a thread where any of
+// them flags (never for physical states) redoes its segment with the IEEE
+// intrinsics. Either way the fluxes are the intrinsics' bit for bit.
+template <int N, bool FAST>
+__device__ __forceinline__ void face_segment(const double *W, double *Fb, int d, int stride,
+                                             int ti, int tj, int c0, double gamma, double igm1,
+                                             double &amax) {
+  bool ok = true;
+  if constexpr (FAST) {
+    double am = amax;
+    face_segment_impl<N, true>(W, Fb, d, stride, ti, tj, c0, gamma, igm1, am, ok);
+    if (!ok) {
+      am = amax;
+      face_segment_impl<N, false>(W, Fb, d, stride, ti, tj, c0, gamma, igm1, am, ok);
+    }
+    amax = am;
+  } else {
+    face_segment_impl<N, false>(W, Fb, d, stride, ti, tj, c0, gamma, igm1, amax, ok);
+  }
+}
+
 // LATTICE = false: U is [nsub][5][12][12][12] (ghosted sub-grids), staged by
 // one 1-D bulk copy. LATTICE = true: U is a ghost-padded global lattice
 // [5][N+4][N+4][N+4] described by `map`; sub-grid s (x fastest, nb per edge)
 // is staged by one 4-D TMA box {12,12,12,5} at (8 bx, 8 by, 8 bz, 0) — the
 // same shared-memory layout, no per-sub-grid ghost copies in HBM.
-template <bool LATTICE>
+template <bool LATTICE, int V>
 __global__ void __launch_bounds__(kThreads, 2)
     k_hydro_flux(const double *__restrict__ U, const __grid_constant__ CUtensorMap map, int nb,
                  double *__restrict__ dudt, double *__restrict__ amax_out, int64_t nsub,
@@ -127,11 +214,10 @@ __global__ void __launch_bounds__(kThreads, 2)
         "r"(phase)
         : "memory");
     // ---- conserved -> primitive, in place --------------------------------
-#pragma unroll 4
-    for (int c = t; c < NCELL; c += kThreads) {
-      const double rho = W[c], sx = W[NCELL + c], sy = W[2 * NCELL + c],
-                   sz = W[3 * NCELL + c], E = W[4 * NCELL + c];
-      const double ir = __ddiv_rn(1.0, rho);
+    constexpr bool kFast = (V & 8) != 0;
+    auto to_primitive_ir = [&](int c, double ir) {
+      const double sx = W[NCELL + c], sy = W[2 * NCELL + c], sz = W[3 * NCELL + c],
+                   E = W[4 * NCELL + c];
       const double vx = __dmul_rn(sx, ir), vy = __dmul_rn(sy, ir), vz = __dmul_rn(sz, ir);
       const double ke = __dmul_rn(
           0.5, __dadd_rn(__dadd_rn(__dmul_rn(sx, vx), __dmul_rn(sy, vy)), __dmul_rn(sz, vz)));
@@ -139,11 +225,64 @@ __global__ void __launch_bounds__(kThreads, 2)
       W[2 * NCELL + c] = vy;
       W[3 * NCELL + c] = vz;
       W[4 * NCELL + c] = __dmul_rn(gm1, __dadd_rn(E, -ke));
+    };
+    auto to_primitive = [&](int c) { to_primitive_ir(c, __ddiv_rn(1.0, W[c])); };
+    if constexpr (V & 2) {
+      // only the 1280 cells a face reads: the interior and the 6 ghost slabs
+      // (2 x 8 x 8 each); the 448 edge/corner ghosts are never used
+#pragma unroll
+      for (int n = t; n < NI * NI * NI + 6 * 2 * NI * NI; n += kThreads) {
+        int x, y, z;
+        if (n < NI * NI * NI) {
+          x = NG + n % NI;
+          y = NG + (n / NI) % NI;
+          z = NG + n / (NI * NI);
+        } else {
+          const int r = n - NI * NI * NI, f = r >> 7, q = r & 127;
+          const int g = (f & 1) ? NG + NI + (q >> 6) : (q >> 6);
+          const int a = NG + (q & 7), b = NG + ((q >> 3) & 7);
+          const int ax = f >> 1;
+          x = ax == 0 ? g : a;
+          y = ax == 0 ? a : (ax == 1 ? g : b);
+          z = ax == 2 ? g : b;
+        }
+        to_primitive((z * NT + y) * NT + x);
+      }
+    } else if constexpr (kFast) {
+      // 4 cells at a time: their fast reciprocals interleave; a flagged group
+      // is redone with the intrinsic
+#pragma unroll 1
+      for (int c0 = t; c0 < NCELL; c0 += 4 * kThreads) {
+        double ir[4];
+        bool ok = true;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int c = c0 + u * kThreads;
+          ir[u] = tb::div_rn_fast(1.0, c < NCELL ? W[c] : 1.0, ok);
+        }
+        if (!ok) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int c = c0 + u * kThreads;
+            ir[u] = __ddiv_rn(1.0, c < NCELL ? W[c] : 1.0);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int c = c0 + u * kThreads;
+          if (c < NCELL) to_primitive_ir(c, ir[u]);
+        }
+      }
+    } else {
+#pragma unroll 4
+      for (int c = t; c < NCELL; c += kThreads) to_primitive(c);
     }
     __syncthreads();
     double du[NF][kCellsPerThread];
     double amax = -CUDART_INF;
-#pragma unroll 1
+    // bit 2: the direction loop unrolled (d compile-time in each copy)
+    constexpr int kUnrollD = (V & 4) ? 3 : 1;
+#pragma unroll kUnrollD
     for (int d = 0; d < 3; ++d) {
       const int stride = d == 0 ? 1 : (d == 1 ? NT : NT * NT);
       // two flux buffers by direction parity: the fold of d and the faces of
@@ -153,7 +292,27 @@ __global__ void __launch_bounds__(kThreads, 2)
       // 192 threads, three consecutive faces of one line each: the 6 cells
       // they read per field are loaded once and each interior slope (cells
       // c0+1 .. c0+4) is formed once for the two faces that use it
-      if (t < 3 * NI * NI) {
+      if constexpr (V & 1) {
+        // all 8 warps: warps 0-5 take two consecutive faces of a line
+        // (segments 0-1, 2-3, 4-5), warps 6-7 the last three (6-8)
+        if (t < 3 * NI * NI) {
+          int g, ti, tj;
+          if (d == 0) {
+            g = t % 3;
+            ti = (t / 3) % NI;
+            tj = t / (3 * NI);
+          } else {
+            ti = t % NI;
+            g = (t / NI) % 3;
+            tj = t / (3 * NI);
+          }
+          face_segment<2, kFast>(W, Fb, d, stride, ti, tj, 2 * g, gamma, igm1, amax);
+        } else {
+          const int u = t - 3 * NI * NI;
+          face_segment<3, kFast>(W, Fb, d, stride, u % NI, u / NI, 6, gamma, igm1, amax);
+        }
+      } else if (t < 3 * NI * NI) {
+        // 192 threads, three consecutive faces of one line each
         int g, ti, tj;
         if (d == 0) {
           g = t % 3;
@@ -164,55 +323,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           g = (t / NI) % 3;
           tj = t / (3 * NI);
         }
-        const int c0 = 3 * g;
-        // 12-grid cell of the first face's left neighbour minus one (c0)
-        int base;
-        if (d == 0)
-          base = ((NG + tj) * NT + (NG + ti)) * NT + c0;
-        else if (d == 1)
-          base = ((NG + tj) * NT + c0) * NT + (NG + ti);
-        else
-          base = (c0 * NT + (NG + tj)) * NT + (NG + ti);
-        double qL[3][NF], qR[3][NF];
-#pragma unroll
-        for (int v = 0; v < NF; ++v) {
-          const double *w = W + v * NCELL + base;
-          double q[6];
-#pragma unroll
-          for (int e = 0; e < 6; ++e) q[e] = w[e * stride];
-          double sl[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            sl[e] = minmod(__dadd_rn(q[e + 1], -q[e]), __dadd_rn(q[e + 2], -q[e + 1]));
-#pragma unroll
-          for (int cc = 0; cc < 3; ++cc) {
-            qL[cc][v] = __dadd_rn(q[cc + 1], __dmul_rn(0.5, sl[cc]));
-            qR[cc][v] = __dadd_rn(q[cc + 2], -__dmul_rn(0.5, sl[cc + 1]));
-          }
-        }
-#pragma unroll
-        for (int cc = 0; cc < 3; ++cc) {
-          const int c = c0 + cc;
-          State L, R;
-          face_state(qL[cc][0], qL[cc][1], qL[cc][2], qL[cc][3], qL[cc][4], gamma, igm1, d, L);
-          face_state(qR[cc][0], qR[cc][1], qR[cc][2], qR[cc][3], qR[cc][4], gamma, igm1, d, R);
-          const double a = fmax(L.a, R.a);
-          amax = fmax(amax, a);
-          const double ha = __dmul_rn(0.5, a);
-          // flux buffer index: (slow transverse, fast transverse, c) so the
-          // accumulation below reads lo/hi faces at a fixed layout per d
-          int idx;
-          if (d == 0)
-            idx = (tj * NI + ti) * 9 + c;          // (k, j, face i)
-          else if (d == 1)
-            idx = (tj * 9 + c) * NI + ti;          // (k, face j, i)
-          else
-            idx = (c * NI + tj) * NI + ti;         // (face k, j, i)
-#pragma unroll
-          for (int v = 0; v < NF; ++v)
-            Fb[v * NFACE + idx] = __dadd_rn(__dmul_rn(0.5, __dadd_rn(L.f[v], R.f[v])),
-                                            -__dmul_rn(ha, __dadd_rn(R.u[v], -L.u[v])));
-        }
+        face_segment<3, kFast>(W, Fb, d, stride, ti, tj, 3 * g, gamma, igm1, amax);
       }
       __syncthreads();
       // every face of this sub-grid is done with W: stream the next one in
@@ -261,23 +372,51 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
 }
 
-template <bool LATTICE>
-int launch(tb_stream_t s, const double *U, const CUtensorMap &map, int nb, double *dudt,
-           double *amax, int64_t nsub, double dx, double gamma) {
+template <bool LATTICE, int V>
+int launch_v(tb_stream_t s, const double *U, const CUtensorMap &map, int nb, double *dudt,
+             double *amax, int64_t nsub, double dx, double gamma) {
   static int occ = 0;
   if (!occ) {
-    cudaFuncSetAttribute(k_hydro_flux<LATTICE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_hydro_flux<LATTICE, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kSmem);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hydro_flux<LATTICE>, kThreads,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hydro_flux<LATTICE, V>, kThreads,
                                                       kSmem) != cudaSuccess ||
         occ < 1)
       occ = 1;
   }
   int64_t blocks = (int64_t)tb::sm_count() * occ;
   if (blocks > nsub) blocks = nsub;
-  k_hydro_flux<LATTICE><<<(int)blocks, kThreads, kSmem, reinterpret_cast<cudaStream_t>(s)>>>(
+  k_hydro_flux<LATTICE, V><<<(int)blocks, kThreads, kSmem, reinterpret_cast<cudaStream_t>(s)>>>(
       U, map, nb, dudt, amax, nsub, dx, gamma);
   return tb::last_error();
+}
+
+// TB_HYDRO_VARIANT (bit 0: all 8 warps on faces; bit 1: convert only the
+// cells a face reads; bit 2: direction loop unrolled; bit 3: branch-free
+// divide / square-root fast paths) selects the schedule; every variant is
+// bit-identical.
+int hydro_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("TB_HYDRO_VARIANT");
+    v = e ? (atoi(e) & 15) : kDefaultVariant;
+  }
+  return v;
+}
+
+template <bool LATTICE>
+int launch(tb_stream_t s, const double *U, const CUtensorMap &map, int nb, double *dudt,
+           double *amax, int64_t nsub, double dx, double gamma) {
+  switch (hydro_variant()) {
+    case 1: return launch_v<LATTICE, 1>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
+    case 2: return launch_v<LATTICE, 2>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
+    case 3: return launch_v<LATTICE, 3>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
+    case 4: return launch_v<LATTICE, 4>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
+    case 5: return launch_v<LATTICE, 5>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
+    case 9: return launch_v<LATTICE, 9>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
+    case 13: return launch_v<LATTICE, 13>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
+    default: return launch_v<LATTICE, 0>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
+  }
 }
 
 }  // namespace

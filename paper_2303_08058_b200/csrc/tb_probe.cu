@@ -38,7 +38,35 @@ __global__ void __launch_bounds__(256) k_fp64_probe(double *sink, int64_t iters,
   if (s == 1234.5) sink[threadIdx.x] = s;   // never true; keeps the chains live
 }
 
+// the fast paths with the intrinsic fallback where they flag, as K6 uses them
+__global__ void k_divsqrt_fast(const double *a, const double *b, int64_t n, double *q_out,
+                               double *r_out, unsigned long long *slow_count) {
+  unsigned long long slow = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    bool okd = true, oks = true;
+    double q = tb::div_rn_fast(a[i], b[i], okd);
+    double r = tb::sqrt_rn_fast(a[i], oks);
+    slow += !okd;
+    slow += !oks;
+    if (!okd) q = __ddiv_rn(a[i], b[i]);
+    if (!oks) r = __dsqrt_rn(a[i]);
+    q_out[i] = q;
+    r_out[i] = r;
+  }
+  atomicAdd(slow_count, slow);
+}
+
 }  // namespace
+
+extern "C" int tb_divsqrt_fast(tb_stream_t s, const double *a, const double *b, int64_t n,
+                               double *q, double *r, unsigned long long *slow_count) {
+  if (n < 0 || (n > 0 && (!a || !b || !q || !r)) || !slow_count) return TB_E_INVALID;
+  if (n == 0) return TB_OK;
+  k_divsqrt_fast<<<tb::sm_count() * 8, 256, 0, reinterpret_cast<cudaStream_t>(s)>>>(
+      a, b, n, q, r, slow_count);
+  return tb::last_error();
+}
 
 extern "C" int tb_fp64_probe(int op, int64_t iters, double *instr_per_s, double *sm_mhz) {
   if (!instr_per_s || iters <= 0 || op < TB_PROBE_DADD || op > TB_PROBE_DMUL_DADD)
