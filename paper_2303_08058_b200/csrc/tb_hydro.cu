@@ -25,9 +25,9 @@ namespace {
 constexpr int NG = 2, NI = 8, NT = 12, NF = 5;
 constexpr int NCELL = NT * NT * NT;            // 1728
 constexpr int NFACE = (NI + 1) * NI * NI;      // 576 faces per direction
-constexpr int kThreads = 256;
-constexpr int kCellsPerThread = NI * NI * NI / kThreads;   // 2
-constexpr int kDefaultVariant = 13;
+// threads per CTA: 256, or 320 with TB_HYDRO_VARIANT bit 4
+constexpr int threads_of(int v) { return (v & 16) ? 320 : 256; }
+constexpr int kDefaultVariant = 28;
 constexpr int kSmem = (NF * NCELL + 2 * NF * NFACE) * 8;   // 115,200 B (2 CTAs/SM)
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -164,7 +164,7 @@ __device__ __forceinline__ void face_segment(const double *W, double *Fb, int d,
 // is staged by one 4-D TMA box {12,12,12,5} at (8 bx, 8 by, 8 bz, 0) — the
 // same shared-memory layout, no per-sub-grid ghost copies in HBM.
 template <bool LATTICE, int V>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(threads_of(V), 2)
     k_hydro_flux(const double *__restrict__ U, const __grid_constant__ CUtensorMap map, int nb,
                  double *__restrict__ dudt, double *__restrict__ amax_out, int64_t nsub,
                  double dx, double gamma) {
@@ -172,6 +172,8 @@ __global__ void __launch_bounds__(kThreads, 2)
   double *W = sm;                        // [5][1728] primitives (staged U)
   double *Fb0 = sm + NF * NCELL;         // [2][5][576] face fluxes, by direction parity
   __shared__ __align__(8) uint64_t bar;
+  constexpr int kThreads = threads_of(V);
+  constexpr int kCellsPerThread = (NI * NI * NI + kThreads - 1) / kThreads;   // 2
   __shared__ double s_amax[kThreads / 32];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const double gm1 = __dadd_rn(gamma, -1.0);
@@ -292,7 +294,26 @@ __global__ void __launch_bounds__(kThreads, 2)
       // 192 threads, three consecutive faces of one line each: the 6 cells
       // they read per field are loaded once and each interior slope (cells
       // c0+1 .. c0+4) is formed once for the two faces that use it
-      if constexpr (V & 1) {
+      if constexpr (V & 16) {
+        // 10 warps: warps 0-7 take two consecutive faces of a line (segments
+        // 0-1, 2-3, 4-5, 6-7), warps 8-9 the last face (8)
+        if (t < 4 * NI * NI) {
+          int g, ti, tj;
+          if (d == 0) {
+            g = t % 4;
+            ti = (t / 4) % NI;
+            tj = t / (4 * NI);
+          } else {
+            ti = t % NI;
+            g = (t / NI) % 4;
+            tj = t / (4 * NI);
+          }
+          face_segment<2, kFast>(W, Fb, d, stride, ti, tj, 2 * g, gamma, igm1, amax);
+        } else {
+          const int u = t - 4 * NI * NI;
+          face_segment<1, kFast>(W, Fb, d, stride, u % NI, u / NI, 8, gamma, igm1, amax);
+        }
+      } else if constexpr (V & 1) {
         // all 8 warps: warps 0-5 take two consecutive faces of a line
         // (segments 0-1, 2-3, 4-5), warps 6-7 the last three (6-8)
         if (t < 3 * NI * NI) {
@@ -333,6 +354,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
       for (int m = 0; m < kCellsPerThread; ++m) {
         const int cell = t + kThreads * m;          // interior index (k, j, i)
+        if ((NI * NI * NI) % kThreads != 0 && cell >= NI * NI * NI) break;
         const int ci = cell % NI, cj = (cell / NI) % NI, ck = cell / (NI * NI);
         int lo, hi;
         if (d == 0) {
@@ -355,10 +377,12 @@ __global__ void __launch_bounds__(kThreads, 2)
     // ---- dU/dt = -(du / dx), coalesced ------------------------------------
     double *out = dudt + s * (int64_t)(NF * NI * NI * NI);
 #pragma unroll
-    for (int m = 0; m < kCellsPerThread; ++m)
+    for (int m = 0; m < kCellsPerThread; ++m) {
+      if ((NI * NI * NI) % kThreads != 0 && t + kThreads * m >= NI * NI * NI) break;
 #pragma unroll
       for (int v = 0; v < NF; ++v)
         out[v * (NI * NI * NI) + t + kThreads * m] = -__dmul_rn(du[v][m], idx);
+    }
     // ---- max signal speed of the sub-grid ---------------------------------
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
@@ -379,27 +403,28 @@ int launch_v(tb_stream_t s, const double *U, const CUtensorMap &map, int nb, dou
   if (!occ) {
     cudaFuncSetAttribute(k_hydro_flux<LATTICE, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kSmem);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hydro_flux<LATTICE, V>, kThreads,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_hydro_flux<LATTICE, V>, threads_of(V),
                                                       kSmem) != cudaSuccess ||
         occ < 1)
       occ = 1;
   }
   int64_t blocks = (int64_t)tb::sm_count() * occ;
   if (blocks > nsub) blocks = nsub;
-  k_hydro_flux<LATTICE, V><<<(int)blocks, kThreads, kSmem, reinterpret_cast<cudaStream_t>(s)>>>(
+  k_hydro_flux<LATTICE, V><<<(int)blocks, threads_of(V), kSmem, reinterpret_cast<cudaStream_t>(s)>>>(
       U, map, nb, dudt, amax, nsub, dx, gamma);
   return tb::last_error();
 }
 
 // TB_HYDRO_VARIANT (bit 0: all 8 warps on faces; bit 1: convert only the
 // cells a face reads; bit 2: direction loop unrolled; bit 3: branch-free
-// divide / square-root fast paths) selects the schedule; every variant is
+// divide / square-root fast paths; bit 4: 320 threads, 2-face segments and
+// one single face per line) selects the schedule; every variant is
 // bit-identical.
 int hydro_variant() {
   static int v = -1;
   if (v < 0) {
     const char *e = getenv("TB_HYDRO_VARIANT");
-    v = e ? (atoi(e) & 15) : kDefaultVariant;
+    v = e ? (atoi(e) & 31) : kDefaultVariant;
   }
   return v;
 }
@@ -415,6 +440,8 @@ int launch(tb_stream_t s, const double *U, const CUtensorMap &map, int nb, doubl
     case 5: return launch_v<LATTICE, 5>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
     case 9: return launch_v<LATTICE, 9>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
     case 13: return launch_v<LATTICE, 13>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
+    case 24: return launch_v<LATTICE, 24>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
+    case 28: return launch_v<LATTICE, 28>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
     default: return launch_v<LATTICE, 0>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
   }
 }
