@@ -27,7 +27,7 @@ constexpr int NCELL = NT * NT * NT;            // 1728
 constexpr int NFACE = (NI + 1) * NI * NI;      // 576 faces per direction
 // threads per CTA: 256, or 320 with TB_HYDRO_VARIANT bit 4
 constexpr int threads_of(int v) { return (v & 16) ? 320 : 256; }
-constexpr int kDefaultVariant = 28;
+constexpr int kDefaultVariant = 60;
 constexpr int kSmem = (NF * NCELL + 2 * NF * NFACE) * 8;   // 115,200 B (2 CTAs/SM)
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -140,7 +140,17 @@ __device__ __forceinline__ void face_segment_impl(const double *W, double *Fb, i
 // independent chains of a thread's faces interleave; a thread where any of
 // them flags (never for physical states) redoes its segment with the IEEE
 // intrinsics. Either way the fluxes are the intrinsics' bit for bit.
-template <int N, bool FAST>
+// the rare IEEE-intrinsic redo, out of line (keeps the hot loop compact)
+template <int N>
+__device__ __noinline__ double face_segment_slow(const double *W, double *Fb, int d, int stride,
+                                                 int ti, int tj, int c0, double gamma,
+                                                 double igm1, double amax) {
+  bool ok = true;
+  face_segment_impl<N, false>(W, Fb, d, stride, ti, tj, c0, gamma, igm1, amax, ok);
+  return amax;
+}
+
+template <int N, bool FAST, bool SLOW_OUT_OF_LINE = false>
 __device__ __forceinline__ void face_segment(const double *W, double *Fb, int d, int stride,
                                              int ti, int tj, int c0, double gamma, double igm1,
                                              double &amax) {
@@ -149,8 +159,12 @@ __device__ __forceinline__ void face_segment(const double *W, double *Fb, int d,
     double am = amax;
     face_segment_impl<N, true>(W, Fb, d, stride, ti, tj, c0, gamma, igm1, am, ok);
     if (!ok) {
-      am = amax;
-      face_segment_impl<N, false>(W, Fb, d, stride, ti, tj, c0, gamma, igm1, am, ok);
+      if constexpr (SLOW_OUT_OF_LINE) {
+        am = face_segment_slow<N>(W, Fb, d, stride, ti, tj, c0, gamma, igm1, amax);
+      } else {
+        am = amax;
+        face_segment_impl<N, false>(W, Fb, d, stride, ti, tj, c0, gamma, igm1, am, ok);
+      }
     }
     amax = am;
   } else {
@@ -217,6 +231,7 @@ __global__ void __launch_bounds__(threads_of(V), 2)
         : "memory");
     // ---- conserved -> primitive, in place --------------------------------
     constexpr bool kFast = (V & 8) != 0;
+    constexpr bool kSlowOut = (V & 32) != 0;
     auto to_primitive_ir = [&](int c, double ir) {
       const double sx = W[NCELL + c], sy = W[2 * NCELL + c], sz = W[3 * NCELL + c],
                    E = W[4 * NCELL + c];
@@ -232,8 +247,14 @@ __global__ void __launch_bounds__(threads_of(V), 2)
     if constexpr (V & 2) {
       // only the 1280 cells a face reads: the interior and the 6 ghost slabs
       // (2 x 8 x 8 each); the 448 edge/corner ghosts are never used
+      constexpr int kUsed = NI * NI * NI + 6 * 2 * NI * NI;
+      constexpr int kPer = (kUsed + kThreads - 1) / kThreads;
+      int cs[kPer];
+      double ir[kPer];
+      bool ok = true;
 #pragma unroll
-      for (int n = t; n < NI * NI * NI + 6 * 2 * NI * NI; n += kThreads) {
+      for (int u = 0; u < kPer; ++u) {
+        const int n = t + u * kThreads;
         int x, y, z;
         if (n < NI * NI * NI) {
           x = NG + n % NI;
@@ -248,8 +269,19 @@ __global__ void __launch_bounds__(threads_of(V), 2)
           y = ax == 0 ? a : (ax == 1 ? g : b);
           z = ax == 2 ? g : b;
         }
-        to_primitive((z * NT + y) * NT + x);
+        cs[u] = n < kUsed ? (z * NT + y) * NT + x : 0;
+        if constexpr (kFast)
+          ir[u] = tb::div_rn_fast(1.0, W[cs[u]], ok);
+        else
+          ir[u] = __ddiv_rn(1.0, W[cs[u]]);
       }
+      if (kFast && !ok) {
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) ir[u] = __ddiv_rn(1.0, W[cs[u]]);
+      }
+#pragma unroll
+      for (int u = 0; u < kPer; ++u)
+        if (kUsed % kThreads == 0 || t + u * kThreads < kUsed) to_primitive_ir(cs[u], ir[u]);
     } else if constexpr (kFast) {
       // 4 cells at a time: their fast reciprocals interleave; a flagged group
       // is redone with the intrinsic
@@ -308,10 +340,10 @@ __global__ void __launch_bounds__(threads_of(V), 2)
             g = (t / NI) % 4;
             tj = t / (4 * NI);
           }
-          face_segment<2, kFast>(W, Fb, d, stride, ti, tj, 2 * g, gamma, igm1, amax);
+          face_segment<2, kFast, kSlowOut>(W, Fb, d, stride, ti, tj, 2 * g, gamma, igm1, amax);
         } else {
           const int u = t - 4 * NI * NI;
-          face_segment<1, kFast>(W, Fb, d, stride, u % NI, u / NI, 8, gamma, igm1, amax);
+          face_segment<1, kFast, kSlowOut>(W, Fb, d, stride, u % NI, u / NI, 8, gamma, igm1, amax);
         }
       } else if constexpr (V & 1) {
         // all 8 warps: warps 0-5 take two consecutive faces of a line
@@ -327,10 +359,10 @@ __global__ void __launch_bounds__(threads_of(V), 2)
             g = (t / NI) % 3;
             tj = t / (3 * NI);
           }
-          face_segment<2, kFast>(W, Fb, d, stride, ti, tj, 2 * g, gamma, igm1, amax);
+          face_segment<2, kFast, kSlowOut>(W, Fb, d, stride, ti, tj, 2 * g, gamma, igm1, amax);
         } else {
           const int u = t - 3 * NI * NI;
-          face_segment<3, kFast>(W, Fb, d, stride, u % NI, u / NI, 6, gamma, igm1, amax);
+          face_segment<3, kFast, kSlowOut>(W, Fb, d, stride, u % NI, u / NI, 6, gamma, igm1, amax);
         }
       } else if (t < 3 * NI * NI) {
         // 192 threads, three consecutive faces of one line each
@@ -344,7 +376,7 @@ __global__ void __launch_bounds__(threads_of(V), 2)
           g = (t / NI) % 3;
           tj = t / (3 * NI);
         }
-        face_segment<3, kFast>(W, Fb, d, stride, ti, tj, 3 * g, gamma, igm1, amax);
+        face_segment<3, kFast, kSlowOut>(W, Fb, d, stride, ti, tj, 3 * g, gamma, igm1, amax);
       }
       __syncthreads();
       // every face of this sub-grid is done with W: stream the next one in
@@ -418,13 +450,14 @@ int launch_v(tb_stream_t s, const double *U, const CUtensorMap &map, int nb, dou
 // TB_HYDRO_VARIANT (bit 0: all 8 warps on faces; bit 1: convert only the
 // cells a face reads; bit 2: direction loop unrolled; bit 3: branch-free
 // divide / square-root fast paths; bit 4: 320 threads, 2-face segments and
-// one single face per line) selects the schedule; every variant is
+// one single face per line; bit 5: the fast paths' fallback out of line)
+// selects the schedule; every variant is
 // bit-identical.
 int hydro_variant() {
   static int v = -1;
   if (v < 0) {
     const char *e = getenv("TB_HYDRO_VARIANT");
-    v = e ? (atoi(e) & 31) : kDefaultVariant;
+    v = e ? (atoi(e) & 63) : kDefaultVariant;
   }
   return v;
 }
@@ -442,6 +475,9 @@ int launch(tb_stream_t s, const double *U, const CUtensorMap &map, int nb, doubl
     case 13: return launch_v<LATTICE, 13>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
     case 24: return launch_v<LATTICE, 24>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
     case 28: return launch_v<LATTICE, 28>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
+    case 30: return launch_v<LATTICE, 30>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
+    case 60: return launch_v<LATTICE, 60>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
+    case 62: return launch_v<LATTICE, 62>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
     default: return launch_v<LATTICE, 0>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
   }
 }
