@@ -666,7 +666,13 @@ def main(argv=None):
 
     star_dist = None
     if world > 1 and not args.no_kernels:
-        star_dist = star_dist_bench(dev, rank, world)
+        # a failure here must not cost the headline line (local errors, e.g.
+        # a slab geometry the rank count does not divide, raise before any
+        # collective of the step)
+        try:
+            star_dist = star_dist_bench(dev, rank, world)
+        except Exception as e:  # noqa: BLE001
+            star_dist = {"error": f"{type(e).__name__}: {e}"[:300]}
     if rank == 0:
         peaks, peak_kind = measured_peaks()
         hbm = float(peaks.get("hbm_gbs", FALLBACK_HBM_GBS))
