@@ -62,3 +62,41 @@ def test_lattice_tma_variant_equals_ghosted_variant(s):
     N.call("tb_hydro_flux_lattice", st, Up.data_ptr(), n, n, du.data_ptr(), am.data_ptr(), dx,
            5 / 3)
     assert torch.equal(du, want) and torch.equal(am, wa)
+
+
+def test_hydro_flux_bit_exact_over_several_subgrids_per_cta():
+    """700 sub-grids > 2 x the persistent grid (2 CTAs per SM): most CTAs run
+    the staged-prefetch loop two or three times."""
+    from paper_2303_08058_b200.hydro import hydro_flux
+    rng = np.random.default_rng(11)
+    I, dx = h.rotating_star(729)
+    I = I[:700] * (1 + 0.02 * rng.standard_normal(I[:700].shape))
+    I[:, 4] = np.abs(I[:, 4]) + 0.5
+    I[:, 0] = np.abs(I[:, 0]) + 1e-3
+    U = np.ascontiguousarray(h.with_ghosts(h.rotating_star(729)[0])[:700])
+    U[:, :, 2:10, 2:10, 2:10] = I
+    want, wa = h.hydro_flux(U, dx, 5 / 3)
+    got, ga = hydro_flux(torch.from_numpy(U).cuda(), dx, 5 / 3)
+    np.testing.assert_array_equal(got.cpu().numpy(), want)
+    np.testing.assert_array_equal(ga.cpu().numpy(), wa)
+
+
+def test_hydro_flux_fast_path_fallback_is_bit_exact():
+    """Cells at rest with pressure ~1e-300: gamma*p lies below the range the
+    branch-free divide accepts, so those faces take the IEEE-intrinsic redo
+    (tb_internal.h div_rn_fast / sqrt_rn_fast) — still bit-exact."""
+    from paper_2303_08058_b200.hydro import hydro_flux
+    rng = np.random.default_rng(12)
+    I, dx = h.rotating_star(8)
+    I = I * (1 + 0.05 * rng.standard_normal(I.shape))
+    I[:, 4] = np.abs(I[:, 4]) + 0.5
+    I[:, 0] = np.abs(I[:, 0]) + 1e-3
+    idx = rng.integers(0, 8, size=(40, 4))
+    for s, z, y, x in idx:
+        I[s, 1:4, z, y, x] = 0.0
+        I[s, 4, z, y, x] = 1.5e-300          # p = (gamma - 1) E = 1e-300
+    U = h.with_ghosts(I)
+    want, wa = h.hydro_flux(U, dx, 5 / 3)
+    got, ga = hydro_flux(torch.from_numpy(U).cuda(), dx, 5 / 3)
+    np.testing.assert_array_equal(got.cpu().numpy(), want)
+    np.testing.assert_array_equal(ga.cpu().numpy(), wa)
