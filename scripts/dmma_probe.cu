@@ -57,6 +57,38 @@ __global__ void k_smem(double *sink, int iters) {
   if (s == 12345.0) sink[threadIdx.x] = s;
 }
 
+// Pipe sharing: warps with MODE bit 0 run DMMA tiles, warps with bit 1 run
+// 8 independent DFMA chains; MODE 3 = half the warps each (warp parity).
+template <int MODE>
+__global__ void k_mix(double *sink, int iters) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const bool do_mma = MODE == 1 || (MODE == 3 && (w & 1) == 0);
+  double a = 1.0 + lane * 1e-3, b = 1.0 - lane * 1e-3;
+  double c[8][2];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) c[t][0] = c[t][1] = 1e-3 * t;
+  if (do_mma) {
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+        asm volatile(
+            "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+            : "+d"(c[t][0]), "+d"(c[t][1])
+            : "d"(a), "d"(b));
+    }
+  } else {
+    // 8 DFMAs per DMMA-equivalent step keep the instruction counts comparable
+    for (int it = 0; it < iters * 8; ++it) {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) c[t][0] = fma(c[t][0], a, b);
+    }
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) s += c[t][0] + c[t][1];
+  if (s == 12345.0) sink[threadIdx.x] = s;
+}
+
 int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -95,6 +127,31 @@ int main() {
     const double fmas = (double)blocks * (threads / 32) * iters * 4 * 256;
     printf("{\"smem_operands\": 1, \"threads\": %d, \"dmma_fma_per_s\": %.4g}\n", threads,
            fmas / (ms * 1e-3));
+  }
+  // pipe sharing: DMMA-only, DFMA-only and mixed at the same warp count;
+  // FMA rates per kind (a DMMA = 256 FMAs per warp, a DFMA = 32)
+  {
+    const int threads = 512, blocks = sms * 2, it = iters / 4;
+    auto run = [&](void (*kern)(double *, int)) {
+      kern<<<blocks, threads>>>(sink, it / 10);
+      cudaEvent_t e0, e1;
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0);
+      kern<<<blocks, threads>>>(sink, it);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0, e1);
+      return ms * 1e-3;
+    };
+    const double warps = (double)blocks * threads / 32;
+    const double per_warp = (double)it * 8 * 256;   // FMAs per warp in either mode
+    const double t1 = run(k_mix<1>), t2 = run(k_mix<2>), t3 = run(k_mix<3>);
+    printf("{\"pipe_sharing\": 1, \"dmma_only_fma_per_s\": %.4g, \"dfma_only_fma_per_s\": %.4g, "
+           "\"mixed_total_fma_per_s\": %.4g, \"mixed_s\": %.4g, \"dmma_only_s\": %.4g, "
+           "\"dfma_only_s\": %.4g}\n",
+           warps * per_warp / t1, warps * per_warp / t2, warps * per_warp / t3, t3, t1, t2);
   }
   return 0;
 }
