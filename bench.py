@@ -205,6 +205,21 @@ def machine_ablation(subgrids=512, steps=5, repeats=3):
         out[f"{mode.value}_ms_per_step"] = statistics.median(ms)
     out["speedup_polling_vs_fence"] = out["fence_ms_per_step"] / out["polling_ms_per_step"]
     out["speedup_hosttask_vs_fence"] = out["fence_ms_per_step"] / out["hosttask_ms_per_step"]
+    # the same machine with zero-copy batches: each batch kernel runs in place
+    # on its pinned staging buffer (one launch + one event per batch instead
+    # of H2D ; kernel ; D2H) — B200-side cost of a 4 KiB member is the PCIe
+    # round trip either way, the host saves two API calls per batch
+    zc = {}
+    for mode in (IntegrationMode.POLLING, IntegrationMode.FENCE):
+        ms = []
+        for _ in range(repeats):
+            res, _ = run_native(subgrids, steps, workers=8, executors=32, max_agg=8,
+                                mode=mode, zero_copy=True)
+            ms.append(statistics.fmean(res.step_ms[1:]))
+            checks.add(res.checksum.hex())
+        zc[f"{mode.value}_ms_per_step"] = statistics.median(ms)
+    zc["speedup_polling_vs_fence"] = zc["fence_ms_per_step"] / zc["polling_ms_per_step"]
+    out["zero_copy"] = zc
     out["checksums_identical"] = len(checks) == 1
     return out
 

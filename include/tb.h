@@ -383,6 +383,11 @@ typedef struct {
   int64_t barrier_elision;   /* drop those barriers                          */
   int64_t task_subgrids;     /* sub-grids per task (1 = reference structure) */
   int64_t hosttask_threads;  /* 2 */
+  int64_t zero_copy;         /* 0: the reference op sequence (H2D ; kernel ;
+                                D2H per batch). 1: the batch kernel runs in
+                                place on the pinned staging buffer (mapped
+                                host memory over PCIe): one launch + one event
+                                per batch, no copy ops (mini-app only).     */
 } tb_machine_config;
 
 typedef struct {             /* StepMetrics (src/miniapp.py:103-113)         */

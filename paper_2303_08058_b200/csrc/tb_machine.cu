@@ -493,6 +493,18 @@ void launch(Batch *b, bool idle) {   // src/executors.py:257-284 as one launch
   }
   tb_event_t ev = 0;
   const int do_barrier = m->cfg.inject_barriers && !m->cfg.barrier_elision;
+  if (m->cfg.zero_copy && !m->hydro) {
+    // the batch kernel in place on the pinned staging buffer (mapped host
+    // memory, read and written over PCIe): one launch + one event, no copies
+    const tb_stream_t st = reinterpret_cast<tb_stream_t>(ex->stream);
+    int rc = tb_launch(st, TB_OP_KIND, b->kind, 0.0, 0.0, b->staging->host, total);
+    if (rc == TB_OK && do_barrier) rc = tb_barrier(st);
+    if (rc == TB_OK) rc = tb_event_record(st, &ev);
+    if (rc != TB_OK) m->error = rc;
+    m->kernels.fetch_add(1, std::memory_order_relaxed);
+    bridge(m, ex, reinterpret_cast<cudaEvent_t>(ev), Task{batch_done, b});
+    return;
+  }
   const int rc =
       m->hydro ? tb_agg_launch_hydro(reinterpret_cast<tb_stream_t>(ex->stream), b->staging->dev,
                                      b->staging->host, total / kGhosted,

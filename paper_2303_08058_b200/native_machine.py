@@ -26,7 +26,7 @@ class MachineConfig(ctypes.Structure):
     _fields_ = [(name, ctypes.c_int64) for name in (
         "subgrids", "steps", "chains", "kernels_per_chain", "workers", "executors",
         "max_agg", "mode", "inject_barriers", "barrier_elision", "task_subgrids",
-        "hosttask_threads")]
+        "hosttask_threads", "zero_copy")]
 
 
 class MachineStep(ctypes.Structure):
@@ -41,12 +41,14 @@ def run_native(subgrids: int, steps: int, workers: int = 8, executors: int = 32,
                inject_barriers: bool = True, barrier_elision: bool = False,
                task_subgrids: int = 1, hosttask_threads: int = 2, device: int = 0,
                chains: int = 3, kernels_per_chain: int = 5,
-               return_cells: bool = False):
-    """Run the machine natively; returns (ScenarioResult, cells or None)."""
+               return_cells: bool = False, zero_copy: bool = False):
+    """Run the machine natively; returns (ScenarioResult, cells or None).
+    ``zero_copy``: each batch's kernel works in place on its pinned staging
+    buffer (one launch + one event per batch instead of H2D ; kernel ; D2H)."""
     N.init(device)
     cfg = MachineConfig(subgrids, steps, chains, kernels_per_chain, workers, executors,
                         max_agg, _MODES[mode], int(inject_barriers), int(barrier_elision),
-                        task_subgrids, hosttask_threads)
+                        task_subgrids, hosttask_threads, int(zero_copy))
     out = (MachineStep * max(steps, 1))()
     cs = ctypes.c_double(0.0)
     cells: Optional[np.ndarray] = None

@@ -77,3 +77,22 @@ def test_native_machine_repeated_runs_every_mode():
         for _ in range(3):
             res, _ = run_native(64, 3, workers=8, executors=8, max_agg=4, mode=mode)
             assert res.checksum == mo.run_reference(64, 3)[0]
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_native_machine_zero_copy_goldens(golden, mode):
+    """zero_copy: each batch kernel runs in place on its pinned staging buffer
+    (one launch + one event, no copy ops) — same goldens and cells."""
+    lit = golden["reference_test_literals"]
+    res, _ = run_native(4, 2, workers=2, executors=2, max_agg=8, mode=mode, zero_copy=True)
+    assert res.checksum == fx(lit["GOLDEN_4X2"])
+    assert res.dts == [fx(h) for h in lit["GOLDEN_4X2_DTS"]]
+    res, cells = run_native(16, 3, workers=4, executors=3, max_agg=4, mode=mode,
+                            return_cells=True, zero_copy=True)
+    assert res.checksum.hex() == golden["machine"]["16x3"]["checksum"]
+    want = np.load(__import__("conftest").TESTS + "/golden/cells.npz")["cells_16x3"]
+    np.testing.assert_array_equal(cells, want)
+    res, _ = run_native(8, 2, workers=2, executors=1, max_agg=1, mode=mode, zero_copy=True)
+    for m in res.per_step:
+        assert m.launches == 8 * 15 and m.transfers == 0
+    assert res.checksum == fx(lit["GOLDEN_8X2"])
