@@ -695,6 +695,9 @@ def main(argv=None):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
             st.load_cells(host_in)
+            if world > 1:       # peer-memory halos read the neighbours' new cells
+                torch.cuda.synchronize()
+                dist.barrier()
             st.run(SCENARIO_STEPS)                  # reads (checksum, dts) back
             host_out.copy_(st.cells, non_blocking=True)
             b.record()
