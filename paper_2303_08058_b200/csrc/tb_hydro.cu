@@ -244,45 +244,7 @@ __global__ void __launch_bounds__(threads_of(V), 2)
       W[4 * NCELL + c] = __dmul_rn(gm1, __dadd_rn(E, -ke));
     };
     auto to_primitive = [&](int c) { to_primitive_ir(c, __ddiv_rn(1.0, W[c])); };
-    if constexpr (V & 2) {
-      // only the 1280 cells a face reads: the interior and the 6 ghost slabs
-      // (2 x 8 x 8 each); the 448 edge/corner ghosts are never used
-      constexpr int kUsed = NI * NI * NI + 6 * 2 * NI * NI;
-      constexpr int kPer = (kUsed + kThreads - 1) / kThreads;
-      int cs[kPer];
-      double ir[kPer];
-      bool ok = true;
-#pragma unroll
-      for (int u = 0; u < kPer; ++u) {
-        const int n = t + u * kThreads;
-        int x, y, z;
-        if (n < NI * NI * NI) {
-          x = NG + n % NI;
-          y = NG + (n / NI) % NI;
-          z = NG + n / (NI * NI);
-        } else {
-          const int r = n - NI * NI * NI, f = r >> 7, q = r & 127;
-          const int g = (f & 1) ? NG + NI + (q >> 6) : (q >> 6);
-          const int a = NG + (q & 7), b = NG + ((q >> 3) & 7);
-          const int ax = f >> 1;
-          x = ax == 0 ? g : a;
-          y = ax == 0 ? a : (ax == 1 ? g : b);
-          z = ax == 2 ? g : b;
-        }
-        cs[u] = n < kUsed ? (z * NT + y) * NT + x : 0;
-        if constexpr (kFast)
-          ir[u] = tb::div_rn_fast(1.0, W[cs[u]], ok);
-        else
-          ir[u] = __ddiv_rn(1.0, W[cs[u]]);
-      }
-      if (kFast && !ok) {
-#pragma unroll
-        for (int u = 0; u < kPer; ++u) ir[u] = __ddiv_rn(1.0, W[cs[u]]);
-      }
-#pragma unroll
-      for (int u = 0; u < kPer; ++u)
-        if (kUsed % kThreads == 0 || t + u * kThreads < kUsed) to_primitive_ir(cs[u], ir[u]);
-    } else if constexpr (kFast) {
+    if constexpr (kFast) {
       // 4 cells at a time: their fast reciprocals interleave; a flagged group
       // is redone with the intrinsic
 #pragma unroll 1
@@ -447,12 +409,12 @@ int launch_v(tb_stream_t s, const double *U, const CUtensorMap &map, int nb, dou
   return tb::last_error();
 }
 
-// TB_HYDRO_VARIANT (bit 0: all 8 warps on faces; bit 1: convert only the
-// cells a face reads; bit 2: direction loop unrolled; bit 3: branch-free
-// divide / square-root fast paths; bit 4: 320 threads, 2-face segments and
-// one single face per line; bit 5: the fast paths' fallback out of line)
-// selects the schedule; every variant is
-// bit-identical.
+// TB_HYDRO_VARIANT selects the schedule (all bit-identical; K6 has
+// the A/B numbers): bit 0 = all warps on faces, bit 2 = direction loop
+// unrolled, bit 3 = branch-free divide / square-root fast paths, bit 4 = 320
+// threads (2-face segments + one single face per line), bit 5 = the fast
+// paths' fallback out of line. Built: 0 (the round's first schedule), 1, 9,
+// 13, 28 and 60 (default); the other measured variants were removed.
 int hydro_variant() {
   static int v = -1;
   if (v < 0) {
@@ -467,18 +429,12 @@ int launch(tb_stream_t s, const double *U, const CUtensorMap &map, int nb, doubl
            double *amax, int64_t nsub, double dx, double gamma) {
   switch (hydro_variant()) {
     case 1: return launch_v<LATTICE, 1>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
-    case 2: return launch_v<LATTICE, 2>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
-    case 3: return launch_v<LATTICE, 3>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
-    case 4: return launch_v<LATTICE, 4>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
-    case 5: return launch_v<LATTICE, 5>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
     case 9: return launch_v<LATTICE, 9>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
     case 13: return launch_v<LATTICE, 13>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
-    case 24: return launch_v<LATTICE, 24>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
     case 28: return launch_v<LATTICE, 28>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
-    case 30: return launch_v<LATTICE, 30>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
-    case 60: return launch_v<LATTICE, 60>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
-    case 62: return launch_v<LATTICE, 62>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
-    default: return launch_v<LATTICE, 0>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
+    case 0: return launch_v<LATTICE, 0>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
+    default: return launch_v<LATTICE, kDefaultVariant>(s, U, map, nb, dudt, amax, nsub, dx,
+                                                       gamma);
   }
 }
 
