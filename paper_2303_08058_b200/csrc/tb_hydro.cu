@@ -27,7 +27,7 @@ constexpr int NCELL = NT * NT * NT;            // 1728
 constexpr int NFACE = (NI + 1) * NI * NI;      // 576 faces per direction
 // threads per CTA: 256, or 320 with TB_HYDRO_VARIANT bit 4
 constexpr int threads_of(int v) { return (v & 16) ? 320 : 256; }
-constexpr int kDefaultVariant = 60;
+constexpr int kDefaultVariant = 124;
 constexpr int kSmem = (NF * NCELL + 2 * NF * NFACE) * 8;   // 115,200 B (2 CTAs/SM)
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -220,9 +220,27 @@ __global__ void __launch_bounds__(threads_of(V), 2)
           : "memory");
     }
   };
+  // bit 6: pull sub-grid s into L2 (no shared memory) when s - gridDim.x
+  // starts, so the later bulk copy into W streams from L2
+  auto prefetch_l2 = [&](int64_t s) {
+    if constexpr (LATTICE) {
+      const int bx = (int)(s % nb), by = (int)((s / nb) % nb), bz = (int)(s / ((int64_t)nb * nb));
+      asm volatile(
+          "cp.async.bulk.prefetch.tensor.4d.L2.global [%0, {%1, %2, %3, %4}];" ::"l"(
+              reinterpret_cast<uint64_t>(&map)),
+          "r"(8 * bx), "r"(8 * by), "r"(8 * bz), "r"(0)
+          : "memory");
+    } else {
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                       U + s * (int64_t)(NF * NCELL)),
+                   "r"((uint32_t)(NF * NCELL * 8))
+                   : "memory");
+    }
+  };
   if (t == 0 && blockIdx.x < nsub) issue(blockIdx.x);
   uint32_t phase = 0;
   for (int64_t s = blockIdx.x; s < nsub; s += gridDim.x, phase ^= 1) {
+    if ((V & 64) && t == 0 && s + gridDim.x < nsub) prefetch_l2(s + gridDim.x);
     asm volatile(
         "{\n\t.reg .pred p;\nHW_%=:\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
@@ -413,13 +431,14 @@ int launch_v(tb_stream_t s, const double *U, const CUtensorMap &map, int nb, dou
 // the A/B numbers): bit 0 = all warps on faces, bit 2 = direction loop
 // unrolled, bit 3 = branch-free divide / square-root fast paths, bit 4 = 320
 // threads (2-face segments + one single face per line), bit 5 = the fast
-// paths' fallback out of line. Built: 0 (the round's first schedule), 1, 9,
-// 13, 28 and 60 (default); the other measured variants were removed.
+// paths' fallback out of line, bit 6 = the next sub-grid prefetched into L2
+// when this one starts. Built: 0 (the round's first schedule), 1, 9, 13, 28,
+// 60 and 124 (default); the other measured variants were removed.
 int hydro_variant() {
   static int v = -1;
   if (v < 0) {
     const char *e = getenv("TB_HYDRO_VARIANT");
-    v = e ? (atoi(e) & 63) : kDefaultVariant;
+    v = e ? (atoi(e) & 127) : kDefaultVariant;
   }
   return v;
 }
@@ -433,6 +452,7 @@ int launch(tb_stream_t s, const double *U, const CUtensorMap &map, int nb, doubl
     case 13: return launch_v<LATTICE, 13>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
     case 28: return launch_v<LATTICE, 28>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
     case 0: return launch_v<LATTICE, 0>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
+    case 124: return launch_v<LATTICE, 124>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
     default: return launch_v<LATTICE, kDefaultVariant>(s, U, map, nb, dudt, amax, nsub, dx,
                                                        gamma);
   }
