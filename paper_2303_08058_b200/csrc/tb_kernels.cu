@@ -1092,7 +1092,16 @@ __global__ void k_acc_allreduce_p2p(int64_t *local_acc, int64_t *const *peer_acc
   if (lane == 0) {
     const unsigned long long *cnt =
         reinterpret_cast<const unsigned long long *>(my_acc) + TB_ACC_COUNT_WORD;
-    while (ld_acquire_sys_u64(cnt) < (unsigned long long)nranks) __nanosleep(200);
+    // a rank that never arrives (died, or launched a different step count)
+    // must not hang the job: after 30 s the kernel traps and the host sees
+    // a launch failure instead
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (ld_acquire_sys_u64(cnt) < (unsigned long long)nranks) {
+      __nanosleep(200);
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 30000000000ULL) __trap();
+    }
   }
   __syncwarp();
   __threadfence_system();
