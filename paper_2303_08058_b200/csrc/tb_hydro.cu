@@ -27,7 +27,7 @@ constexpr int NCELL = NT * NT * NT;            // 1728
 constexpr int NFACE = (NI + 1) * NI * NI;      // 576 faces per direction
 // threads per CTA: 256, or 320 with TB_HYDRO_VARIANT bit 4
 constexpr int threads_of(int v) { return (v & 16) ? 320 : 256; }
-constexpr int kDefaultVariant = 124;
+constexpr int kDefaultVariant = 252;
 constexpr int kSmem = (NF * NCELL + 2 * NF * NFACE) * 8;   // 115,200 B (2 CTAs/SM)
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -263,26 +263,28 @@ __global__ void __launch_bounds__(threads_of(V), 2)
     };
     auto to_primitive = [&](int c) { to_primitive_ir(c, __ddiv_rn(1.0, W[c])); };
     if constexpr (kFast) {
-      // 4 cells at a time: their fast reciprocals interleave; a flagged group
-      // is redone with the intrinsic
+      // kG cells at a time: their fast reciprocals interleave; a flagged
+      // group is redone with the intrinsic (bit 7: one group of 6 covers the
+      // 5.4 cells per thread of a 320-thread CTA in a single pass)
+      constexpr int kG = (V & 128) ? 6 : 4;
 #pragma unroll 1
-      for (int c0 = t; c0 < NCELL; c0 += 4 * kThreads) {
-        double ir[4];
+      for (int c0 = t; c0 < NCELL; c0 += kG * kThreads) {
+        double ir[kG];
         bool ok = true;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kG; ++u) {
           const int c = c0 + u * kThreads;
           ir[u] = tb::div_rn_fast(1.0, c < NCELL ? W[c] : 1.0, ok);
         }
         if (!ok) {
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < kG; ++u) {
             const int c = c0 + u * kThreads;
             ir[u] = __ddiv_rn(1.0, c < NCELL ? W[c] : 1.0);
           }
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kG; ++u) {
           const int c = c0 + u * kThreads;
           if (c < NCELL) to_primitive_ir(c, ir[u]);
         }
@@ -432,13 +434,14 @@ int launch_v(tb_stream_t s, const double *U, const CUtensorMap &map, int nb, dou
 // unrolled, bit 3 = branch-free divide / square-root fast paths, bit 4 = 320
 // threads (2-face segments + one single face per line), bit 5 = the fast
 // paths' fallback out of line, bit 6 = the next sub-grid prefetched into L2
-// when this one starts. Built: 0 (the round's first schedule), 1, 9, 13, 28,
-// 60 and 124 (default); the other measured variants were removed.
+// when this one starts, bit 7 = the conversion's reciprocals in one group of
+// 6 per thread. Built: 0 (the round's first schedule), 1, 9, 13, 28, 60, 124
+// and 252 (default); the other measured variants were removed.
 int hydro_variant() {
   static int v = -1;
   if (v < 0) {
     const char *e = getenv("TB_HYDRO_VARIANT");
-    v = e ? (atoi(e) & 127) : kDefaultVariant;
+    v = e ? (atoi(e) & 255) : kDefaultVariant;
   }
   return v;
 }
@@ -453,6 +456,7 @@ int launch(tb_stream_t s, const double *U, const CUtensorMap &map, int nb, doubl
     case 28: return launch_v<LATTICE, 28>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
     case 0: return launch_v<LATTICE, 0>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
     case 124: return launch_v<LATTICE, 124>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
+    case 252: return launch_v<LATTICE, 252>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
     default: return launch_v<LATTICE, kDefaultVariant>(s, U, map, nb, dudt, amax, nsub, dx,
                                                        gamma);
   }
