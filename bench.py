@@ -74,8 +74,15 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """SM clock + throttle reasons sampled DURING the timed region: NVML in a
-    background thread every 5 ms (falls back to ``nvidia-smi -lms 50``)."""
+    """SM clock + throttle reasons around and DURING the timed region.
+
+    NVML (``pynvml``) from a background thread every ~1 ms from before the
+    warm-up to after the timed region, each sample time-stamped, plus
+    samples taken on the launching thread while the timed launches are still
+    executing (the host returns from the asynchronous launches long before
+    the GPU finishes them, so those samples are genuinely under load) and
+    one synchronous sample right before and right after. Falls back to
+    ``nvidia-smi -lms 50``."""
 
     REASONS = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
                "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
@@ -84,11 +91,32 @@ class ClockSampler:
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
-        self.samples = []          # (sm_mhz, max_mhz, reasons bitmask)
+        self.samples = []          # (t, sm_mhz, mem_mhz, reasons bitmask)
         self._stop = None
         self._thread = None
         self._nvml = None
         self._proc = None
+        self.window = None         # (t0, t1) of the timed region
+        self.during = []           # samples taken while the timed launches ran
+        self.edges = {}            # "before"/"after" synchronous samples
+
+    def _read(self):
+        pynvml, h = self._nvml
+        return (time.perf_counter(), pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+                pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_MEM),
+                pynvml.nvmlDeviceGetCurrentClocksEventReasons(h))
+
+    def sample(self, into=None):
+        """One synchronous sample (appended to ``into`` or returned)."""
+        if self._nvml is None:
+            return None
+        try:
+            s = self._read()
+        except Exception:  # noqa: BLE001
+            return None
+        if into is not None:
+            into.append(s)
+        return s
 
     def start(self):
         import threading
@@ -97,6 +125,7 @@ class ClockSampler:
             pynvml.nvmlInit()
             h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
             self._nvml = (pynvml, h)
+            self._max = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
         except Exception:  # noqa: BLE001 - no NVML: use nvidia-smi
             self._nvml = None
         if self._nvml is None:
@@ -114,32 +143,36 @@ class ClockSampler:
         self._stop = threading.Event()
 
         def loop():
-            pynvml, h = self._nvml
-            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
             while not self._stop.is_set():
-                try:
-                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
-                    rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                    self.samples.append((sm, mx, rs))
-                except Exception:  # noqa: BLE001
-                    pass
-                self._stop.wait(0.005)
+                self.sample(self.samples)
+                self._stop.wait(0.001)
 
         self._thread = threading.Thread(target=loop, daemon=True)
         self._thread.start()
+
+    def _names(self, rows):
+        pynvml = self._nvml[0]
+        return sorted({name for *_, rs in rows for name, attr in self.REASONS.items()
+                       if rs & getattr(pynvml, attr, 0)})
 
     def stop(self):
         if self._nvml is not None:
             self._stop.set()
             self._thread.join(timeout=2)
-            pynvml = self._nvml[0]
-            names = sorted({name for _, _, rs in self.samples
-                            for name, attr in self.REASONS.items()
-                            if rs & getattr(pynvml, attr, 0)})
-            sm = [s for s, _, _ in self.samples]
+            t0, t1 = self.window if self.window else (float("-inf"), float("inf"))
+            inside = [s for s in self.samples if t0 <= s[0] <= t1] + self.during
+            near = [s for s in self.samples if t0 - 0.05 <= s[0] <= t1 + 0.05]
+            use = inside or near
+            sm = [s[1] for s in use]
             return {"sm_mhz": statistics.median(sm) if sm else None,
-                    "sm_max_mhz": max((m for _, m, _ in self.samples), default=None),
-                    "reasons": names, "samples": len(sm), "source": "nvml/5ms"}
+                    "sm_max_mhz": self._max,
+                    "mem_mhz": statistics.median(s[2] for s in use) if use else None,
+                    "reasons": self._names(use + list(self.edges.values())),
+                    "samples": len(inside), "samples_within_50ms": len(near),
+                    "before": self.edges.get("before", (None, None))[1],
+                    "after": self.edges.get("after", (None, None))[1],
+                    "source": "nvml: 1 ms thread + launching-thread samples while the "
+                              "timed launches run + before/after"}
         if self._proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no clock source"],
                     "samples": 0}
@@ -548,6 +581,9 @@ def main(argv=None):
                     help="skip the polling/host-task/fence machine ablation")
     ap.add_argument("--no-kernels", action="store_true",
                     help="skip the hydro (K6) / FMM (K7) lines of configs 2 and 3")
+    ap.add_argument("--warm-ms", type=float, default=250.0,
+                    help="minimum device time of back-to-back warm-up steps before the "
+                         "timed region (after the --warmup steps)")
     ap.add_argument("--spw", type=int, default=0,
                     help="K2 sub-grids per warp per CTA (0 = one persistent wave)")
     args = ap.parse_args(argv)
@@ -587,34 +623,56 @@ def main(argv=None):
     subgrids = per_gpu * world
     # (+ 4 scenario runs of SCENARIO_STEPS for e2e_scenario)
     total_steps = (args.warmup + args.steps + min(args.steps, 200) + args.e2e_steps + 8
-                   + (4 * SCENARIO_STEPS if args.e2e_steps > 0 else 0))
+                   + (4 * SCENARIO_STEPS if args.e2e_steps > 0 else 0)
+                   + int(args.warm_ms / 0.02) + 128)     # time-based warm-up steps
     st = RingStepper(subgrids, device=dev, rank=rank, world=world, max_steps=total_steps,
                      group=None)
     n_local = st.n
-    for _ in range(args.warmup):
-        st.step()
-    # Headline: steps back to back, no L2 flush. Each step reads the previous
-    # step's 128 MiB output (> the 126 MB L2) from the start while its tail is
-    # the most recently written, so nothing is re-read from L2: ncu
-    # --cache-control none on back-to-back launches measures 135 MB DRAM
-    # reads per launch (the whole input; profiles/r01_k2_back_to_back.txt). At N = 1 one launch per step, so the
-    # outer events also time K2; at N > 1 K2 is bracketed per step.
+    # Warm-up: W steps, then more back-to-back steps until >= WARM_MS of
+    # device time has run (a GPU that sat idle through process start-up and
+    # the parity check needs ~0.1 s of load before its clocks and memory
+    # settle; profiles/r02/k2_trace.json), ending right before the timed
+    # region with no idle gap. Declared in the line as "warmup_policy".
+    sampler = ClockSampler(local)
+    sampler.start()
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    warm_steps = 0
+    while warm_steps < args.warmup or time.perf_counter() - w0 < args.warm_ms * 1e-3:
+        k = max(1, min(args.warmup - warm_steps, 64)) if warm_steps < args.warmup else 32
+        for _ in range(k):
+            st.step()
+        warm_steps += k
+        if warm_steps >= args.warmup:
+            torch.cuda.synchronize()
+    warm_ms = (time.perf_counter() - w0) * 1e3
+    # Headline: K steps back to back, no L2 flush. Each step reads the
+    # previous step's 128 MiB output (> the 126 MB L2) from the start while
+    # its tail is the most recently written, so nothing is re-read from L2
+    # (ncu --cache-control none: profiles/r01_k2_back_to_back.txt). N = 1:
+    # one launch per step, so the outer events time K2; N > 1: K2 is
+    # bracketed per step.
     per_step_k2 = world > 1
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps if per_step_k2 else 0)]
     e_start, e_stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    sampler = ClockSampler(local)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    sampler.start()
+    sampler.edges["before"] = sampler.sample()
     t_wall = time.perf_counter()
     e_start.record()
     for i in range(args.steps):
         st.step(kernel_events=ev[i] if per_step_k2 else None)
+    timed_launches = (1 if world == 1 else 2) * args.steps
     e_stop.record()
+    while not e_stop.query():        # the launches are asynchronous: sample under load
+        sampler.sample(sampler.during)
     torch.cuda.synchronize()
-    wall = time.perf_counter() - t_wall
+    t_end = time.perf_counter()
+    wall = t_end - t_wall
+    sampler.window = (t_wall, t_end)
+    sampler.edges["after"] = sampler.sample()
     if world > 1:
         dist.barrier()
     clocks = sampler.stop()
@@ -784,15 +842,15 @@ def main(argv=None):
             "parity": {"run_reference_512x15_equals_GOLDEN_DEFAULTS": parity},
             "roofline": {"bound": "hbm",
                          "kernel": {"auto": "k_step_bulk<3,5,1 stage>",
-                                    "bulk": "k_step_bulk<3,5>",
-                                    "reg": "k_step<3,5>", "regpf": "k_step<3,5,pf>",
-                                    "lean": "k_step<3,5,lean48>",
-                                    "pair": "k_step_pair<3,5>",
-                                    "bulk1": "k_step_bulk<3,5,1 stage>"}[
-                                        args.step_impl] + (
-                                            " (tb_step_deferred: K2, the previous step's "
-                                            "exact close in its extra CTA)"
-                                            if world == 1 else " (tb_step)"),
+                               "bulk": "k_step_bulk<3,5>",
+                               "reg": "k_step<3,5>", "regpf": "k_step<3,5,pf>",
+                               "lean": "k_step<3,5,lean48>",
+                               "pair": "k_step_pair<3,5>",
+                               "bulk1": "k_step_bulk<3,5,1 stage>"}[
+                                   args.step_impl] + (
+                                       " (tb_step_deferred: K2, the previous step's "
+                                       "exact close in its extra CTA)"
+                                       if world == 1 else " (tb_step)"),
                          "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm,
                          "traffic": traffic,
@@ -813,7 +871,12 @@ def main(argv=None):
             "e2e": e2e,
             "ablation": ablation,
             "north_star_kernels": kernels,
-            "gpu_launches": (1 if world == 1 else 2) * args.steps,
+            "gpu_launches": timed_launches,
+            "warmup_policy": {"steps": warm_steps, "min_ms": args.warm_ms,
+                              "ms": warm_ms,
+                              "rule": "--warmup steps, then back-to-back steps until "
+                                      "--warm-ms of device time, immediately before the "
+                                      "timed region (synchronize, no idle gap)"},
             "clocks": clocks,
             "wall_s_timed_region": wall,
         }

@@ -433,6 +433,26 @@ struct SumBuf {
   int cnt = 0;
 };
 
+// min over the warp's 16x32 values on the integer pipe: order-preserving
+// int64 keys (min_key), a per-lane 64-bit min, then two 32-bit warp
+// reductions (high word; low word among the lanes holding the minimal high
+// word). The FP64 pipe — K2's co-limit with HBM — keeps only the transforms
+// and the pairwise sum (20 fewer FP64 instructions per lane and sub-grid).
+// Same result as the fmin tree for every non-NaN input.
+__device__ __forceinline__ double warp_min_alu(const double (&v)[16]) {
+  long long k = min_key(v[0]);
+#pragma unroll
+  for (int i = 1; i < 16; ++i) {
+    const long long x = min_key(v[i]);
+    k = x < k ? x : k;
+  }
+  const int hi = (int)(k >> 32);
+  const unsigned lo = (unsigned)(k & 0xffffffffLL);
+  const int hmin = __reduce_min_sync(0xffffffffu, hi);
+  const unsigned lmin = __reduce_min_sync(0xffffffffu, hi == hmin ? lo : 0xffffffffu);
+  return key_to_double((long long)(((unsigned long long)(unsigned)hmin << 32) | lmin));
+}
+
 __device__ __forceinline__ long long shfl_sum_s64(long long v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -572,7 +592,7 @@ __device__ __forceinline__ void fold_previous(const StepArgs &a, int64_t g0, int
   }
 }
 
-template <int CHAINS, int KPC>
+template <int CHAINS, int KPC, bool ALUMIN = false>
 __device__ __forceinline__ void subgrid_body(const StepArgs &a, int64_t g, int lane,
                                              double (&v)[16], double face,
                                              unsigned long long *s_limbs, double &wmin,
@@ -591,15 +611,23 @@ __device__ __forceinline__ void subgrid_body(const StepArgs &a, int64_t g, int l
   // numpy pairwise: r_j = a[j] + a[j+8] + ... sequentially, then
   // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) per block and (B0+B1)+(B2+B3).
   double s = v[0], m = v[0];
+  if (ALUMIN) {
 #pragma unroll
-  for (int i = 1; i < 16; ++i) {
-    s = __dadd_rn(s, v[i]);
-    m = fmin(m, v[i]);
-  }
+    for (int i = 1; i < 16; ++i) s = __dadd_rn(s, v[i]);
 #pragma unroll
-  for (int x = 1; x < 32; x <<= 1) {
-    s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, x));
-    m = fmin(m, __shfl_xor_sync(0xffffffffu, m, x));
+    for (int x = 1; x < 32; x <<= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, x));
+    m = warp_min_alu(v);
+  } else {
+#pragma unroll
+    for (int i = 1; i < 16; ++i) {
+      s = __dadd_rn(s, v[i]);
+      m = fmin(m, v[i]);
+    }
+#pragma unroll
+    for (int x = 1; x < 32; x <<= 1) {
+      s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, x));
+      m = fmin(m, __shfl_xor_sync(0xffffffffu, m, x));
+    }
   }
   if (lane == 0) {
     if (a.sums) a.sums[g] = s;
@@ -847,7 +875,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       : "memory");
 }
 
-template <int CHAINS, int KPC, int STAGES>
+template <int CHAINS, int KPC, int STAGES, bool ALUMIN = false>
 // 4 CTAs per SM (64 registers)
 __global__ void __launch_bounds__(kStepThreads, 4) k_step_bulk(StepArgs a) {
   constexpr int kStages = STAGES;
@@ -909,7 +937,7 @@ __global__ void __launch_bounds__(kStepThreads, 4) k_step_bulk(StepArgs a) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       bulk_load_subgrid(slots + s * kSlot, a.old + gn * TB_CELLS, &bars[warp][s]);
     }
-    subgrid_body<CHAINS, KPC>(a, g, lane, v, face, s_limbs, wmin, s_sums[warp], sb);
+    subgrid_body<CHAINS, KPC, ALUMIN>(a, g, lane, v, face, s_limbs, wmin, s_sums[warp], sb);
   }
   step_epilogue(a, s_limbs, s_min, wmin, s_sums[warp], sb.cnt);
 }
@@ -963,13 +991,20 @@ int occupancy(K kernel, int smem) {
   return o;
 }
 
-template <int CHAINS, int KPC, int STAGES>
-void launch_bulk(cudaStream_t st, const StepArgs &a) {
+// the per-sub-grid min on the integer pipe (warp_min_alu); TB_STEP_ALUMIN=0
+// keeps the FP64 fmin tree (A/B)
+const bool g_step_alumin = [] {
+  const char *e = getenv("TB_STEP_ALUMIN");
+  return !(e && e[0] == '0');
+}();
+
+template <int CHAINS, int KPC, int STAGES, bool ALUMIN>
+void launch_bulk_impl(cudaStream_t st, const StepArgs &a) {
   static int occ = 0;
   if (!occ) {
-    cudaFuncSetAttribute(k_step_bulk<CHAINS, KPC, STAGES>,
+    cudaFuncSetAttribute(k_step_bulk<CHAINS, KPC, STAGES, ALUMIN>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, bulk_smem(STAGES));
-    occ = occupancy(k_step_bulk<CHAINS, KPC, STAGES>, bulk_smem(STAGES));
+    occ = occupancy(k_step_bulk<CHAINS, KPC, STAGES, ALUMIN>, bulk_smem(STAGES));
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)step_grid(a.n, occ, a.finalizer));
@@ -981,7 +1016,15 @@ void launch_bulk(cudaStream_t st, const StepArgs &a) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = g_step_pdl ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, k_step_bulk<CHAINS, KPC, STAGES>, a);
+  cudaLaunchKernelEx(&cfg, k_step_bulk<CHAINS, KPC, STAGES, ALUMIN>, a);
+}
+
+template <int CHAINS, int KPC, int STAGES>
+void launch_bulk(cudaStream_t st, const StepArgs &a) {
+  if (g_step_alumin)
+    launch_bulk_impl<CHAINS, KPC, STAGES, true>(st, a);
+  else
+    launch_bulk_impl<CHAINS, KPC, STAGES, false>(st, a);
 }
 
 int launch_step(cudaStream_t st, StepArgs a) {
