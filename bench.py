@@ -257,6 +257,114 @@ def machine_ablation(subgrids=512, steps=5, repeats=3):
     return out
 
 
+# BASELINE config 4 (max_level 5) on the native machine with the reference
+# task structure; run_reference(32768, 1) pins step 1
+C4_CHECKSUM = float.fromhex("0x1.fffc131fd56c6p+22")
+C4_DT = float.fromhex("0x1.a73380416f1a6p-22")
+# the sweep's best polling configuration (scripts/c4_machine_sweep.py,
+# profiles/r02/c4_sweep.jsonl): 8 workers, 16 executors, max 128 aggregated,
+# batch members read and written in place in the tasks' pinned buffers
+C4_MACHINE = dict(workers=8, executors=16, max_agg=128, zero_copy=2)
+
+
+def machine_ablation_c4(steps=3):
+    """The paper's ablation at BASELINE config 4: the native machine on 32768
+    sub-grids with the reference task structure (one task and 15 schedule()
+    calls per sub-grid per step, src/miniapp.py:116-171, driven as
+    src/cli.py:199-232), POLLING vs HOSTTASK vs FENCE at identical
+    (W, E, M); plus the staged op sequence (H2D ; kernel ; D2H per batch) at
+    the same (W, E, M) under POLLING. Mean step time over steps 2..N, mean
+    batch size, speed-ups = fence_ms / mode_ms (src/cli.py:297-306); parity:
+    every run's first step equals run_reference(32768, 1)."""
+    from paper_2303_08058_b200.bridge import IntegrationMode
+    from paper_2303_08058_b200.native_machine import run_native
+    out = {"config": "native machine, 32768 sub-grids (max_level 5), reference task structure "
+                     f"(491,520 schedule() calls per step), {C4_MACHINE['workers']} workers, "
+                     f"{C4_MACHINE['executors']} executors, max {C4_MACHINE['max_agg']} "
+                     "aggregated, gather batches (members in place in pinned task buffers), "
+                     f"{steps} steps (mean of steps 2..{steps})"}
+    checks, golden = set(), True
+    runs = [(m.value, m, C4_MACHINE) for m in IntegrationMode]
+    runs.append(("staged_polling", IntegrationMode.POLLING, dict(C4_MACHINE, zero_copy=0)))
+    for name, mode, kw in runs:
+        res, _ = run_native(32768, steps, mode=mode, **kw)
+        out[f"{name}_ms_per_step"] = statistics.fmean(res.step_ms[1:])
+        out[f"{name}_mean_batch"] = res.per_step[-1].mean_batch
+        out[f"{name}_launches_per_step"] = res.per_step[-1].launches
+        checks.add(res.checksum.hex())
+        golden &= (res.per_step[0].checksum_piece == C4_CHECKSUM and res.dts[0] == C4_DT)
+    out["speedup_polling_vs_fence"] = out["fence_ms_per_step"] / out["polling_ms_per_step"]
+    out["speedup_hosttask_vs_fence"] = out["fence_ms_per_step"] / out["hosttask_ms_per_step"]
+    out["cells_per_s_polling"] = 32768 * 512 / (out["polling_ms_per_step"] * 1e-3)
+    out["checksums_identical"] = len(checks) == 1
+    out["step1_equals_run_reference_32768x1"] = golden
+    return out
+
+
+PCIE_BIDIR_GBS = 99.86   # measured concurrent H2D + D2H (profiles/r01/pcie_probe.json)
+
+
+def plugin_call_bench(steps=3):
+    """e2e through the reference's own plugin/operator API at BASELINE config
+    4: build_scenario + Runtime + CudaDevice + Integration(POLLING) +
+    ExecutorPool + AggregationExecutor(register_kind(k, kernel_transform(k)))
+    + run_scenario, wired as src/cli.py:199-232 does, on 32768 sub-grids
+    whose cells live in host memory (the reference's Scenario.grids). The
+    call delegates to the native machine (miniapp._native_plan); every
+    kernel round moves each sub-grid's 4 KiB over PCIe and back, 15 rounds
+    per step — the bound stated below."""
+    from paper_2303_08058_b200 import (AggregationExecutor, BufferPool, CudaDevice,
+                                       ExecutorPool, Integration, IntegrationMode, Runtime,
+                                       ScenarioConfig, build_scenario, kernel_transform,
+                                       run_scenario)
+    S = 32768
+    W, E, M = C4_MACHINE["workers"], C4_MACHINE["executors"], C4_MACHINE["max_agg"]
+    out = {"api": "run_scenario(build_scenario(ScenarioConfig(subgrids=32768, steps="
+                  f"{steps})), Runtime({W}), CudaDevice(0), aggs=[AggregationExecutor(ex, {M}, "
+                  f"BufferPool) for ex in ExecutorPool(Integration(POLLING), {E})], "
+                  "round-robin aggs_by_grid) -> native machine (reference task structure)",
+           "unit": "cells/s"}
+    pcie_bytes = S * 15 * 512 * 8 * 2
+    for copies in ("gather", "staged"):
+        rt = Runtime(W)
+        dev = CudaDevice(0)
+        try:
+            integ = Integration(rt, dev, IntegrationMode.POLLING)
+            pool = ExecutorPool(integ, E)
+            bufs = BufferPool(dev)
+            aggs = [AggregationExecutor(ex, M, bufs) for ex in pool.executors]
+            for a in aggs:
+                for k in range(5):
+                    a.register_kind(k, kernel_transform(k))
+            sc = build_scenario(ScenarioConfig(subgrids=S, steps=steps))
+            t0 = time.perf_counter()
+            res = run_scenario(sc, rt, dev, aggs, [aggs[g % E] for g in range(S)],
+                               batch_copies=copies)
+            call_s = time.perf_counter() - t0
+        finally:
+            rt.shutdown()
+            dev.destroy()
+        step_ms = statistics.fmean(res.step_ms[1:])
+        out[copies] = {"ms_per_step": step_ms, "value": S * 512 / (step_ms * 1e-3),
+                       "call_s": call_s, "call_value": S * 512 * steps / call_s,
+                       "engine": res.engine,
+                       "step1_equals_run_reference_32768x1":
+                           res.per_step[0].checksum_piece == C4_CHECKSUM
+                           and res.dts[0] == C4_DT}
+    out["value"] = out["gather"]["value"]
+    out["h2d_bytes_per_step"] = pcie_bytes // 2
+    out["d2h_bytes_per_step"] = pcie_bytes // 2
+    out["bound"] = {"kind": "pcie", "bytes_per_step": pcie_bytes,
+                    "measured_bidirectional_gbs": PCIE_BIDIR_GBS,
+                    "floor_ms": pcie_bytes / (PCIE_BIDIR_GBS * 1e9) * 1e3,
+                    "frac": pcie_bytes / (PCIE_BIDIR_GBS * 1e9) * 1e3
+                    / out["gather"]["ms_per_step"],
+                    "why": "15 kernel rounds per sub-grid per step, each a host->device->host "
+                           "trip of its 4 KiB (the reference machine's structure, "
+                           "src/miniapp.py:127-131, src/executors.py:257-284)"}
+    return out
+
+
 HYDRO_BYTES_PER_SUBGRID = 5 * 12 ** 3 * 8 + 5 * 8 ** 3 * 8 + 8   # U in, dU/dt + amax out
 
 def hydro_fp64_per_subgrid():
@@ -581,9 +689,11 @@ def main(argv=None):
                     help="skip the polling/host-task/fence machine ablation")
     ap.add_argument("--no-kernels", action="store_true",
                     help="skip the hydro (K6) / FMM (K7) lines of configs 2 and 3")
-    ap.add_argument("--warm-ms", type=float, default=250.0,
+    ap.add_argument("--warm-ms", type=float, default=20.0,
                     help="minimum device time of back-to-back warm-up steps before the "
-                         "timed region (after the --warmup steps)")
+                         "timed region (after the --warmup steps): long enough to leave "
+                         "the idle power state, short of the ~100 ms of K2 load after "
+                         "which sw_power_cap lowers SM clocks (profiles/r02/warmup_sweep.txt)")
     ap.add_argument("--spw", type=int, default=0,
                     help="K2 sub-grids per warp per CTA (0 = one persistent wave)")
     args = ap.parse_args(argv)
@@ -628,11 +738,13 @@ def main(argv=None):
     st = RingStepper(subgrids, device=dev, rank=rank, world=world, max_steps=total_steps,
                      group=None)
     n_local = st.n
-    # Warm-up: W steps, then more back-to-back steps until >= WARM_MS of
-    # device time has run (a GPU that sat idle through process start-up and
-    # the parity check needs ~0.1 s of load before its clocks and memory
-    # settle; profiles/r02/k2_trace.json), ending right before the timed
-    # region with no idle gap. Declared in the line as "warmup_policy".
+    # Warm-up: W steps, then more back-to-back steps until >= --warm-ms of
+    # device time has run, ending right before the timed region with no idle
+    # gap. After an idle gap the first steps run slow (profiles/r02/
+    # k2_trace.json: 140, 72, then 53 us); after >= ~100 ms of back-to-back
+    # K2 the board reaches sw_power_cap and SM clocks fall to ~1780 MHz
+    # (profiles/r02/warmup_sweep.txt) — the default 20 ms sits between.
+    # Declared in the line as "warmup_policy".
     sampler = ClockSampler(local)
     sampler.start()
     torch.cuda.synchronize()
@@ -775,6 +887,9 @@ def main(argv=None):
             "api": "RingStepper.load_cells(pinned host) + run(15) + cells to pinned host "
                    "(run_scenario's call granularity; the headline e2e above copies every step)"}
 
+        if world == 1 and not args.no_ablation:
+            e2e["plugin_call"] = plugin_call_bench()
+
     star_dist = None
     if world > 1 and not args.no_kernels:
         # a failure here must not cost the headline line (local errors, e.g.
@@ -803,6 +918,7 @@ def main(argv=None):
         ablation = None
         if not args.no_ablation:
             ablation = machine_ablation()
+            ablation["c4"] = machine_ablation_c4()
             ablation["hydro_machine"] = hydro_machine_ablation()
         kernels = None
         if not args.no_kernels:
@@ -876,7 +992,9 @@ def main(argv=None):
                               "ms": warm_ms,
                               "rule": "--warmup steps, then back-to-back steps until "
                                       "--warm-ms of device time, immediately before the "
-                                      "timed region (synchronize, no idle gap)"},
+                                      "timed region (synchronize, no idle gap); longer "
+                                      "warm-ups reach sw_power_cap (profiles/r02/"
+                                      "warmup_sweep.txt)"},
             "clocks": clocks,
             "wall_s_timed_region": wall,
         }

@@ -63,6 +63,7 @@ extern "C" {
 #define TB_OP_NONE 0            /* launch an empty kernel (timing-only op) */
 #define TB_OP_KIND 1            /* x = x*C1[kind] + C2[kind], two roundings */
 #define TB_OP_AFFINE 2          /* x = x*c1 + c2, two roundings             */
+#define TB_OP_TRAP 3            /* fault injection: the kernel traps (tests) */
 
 /* tb_set_option keys/values. */
 #define TB_OPT_STEP_IMPL 1      /* which K2 variant tb_step launches        */
@@ -334,14 +335,26 @@ int tb_poll_destroy(tb_poll_t reg);
  * an id of the in-order queue the event was recorded on — entries of one chain
  * complete in registration order, so poll only queries each chain's head. */
 int tb_poll_add(tb_poll_t reg, tb_event_t ev, uint64_t chain, uint64_t token);
+/* tb_poll_add with the event's record order on its chain (seq > 0, increasing
+ * in record order, assigned under the queue's lock): the entry is placed in
+ * record order even when it is registered after a later-recorded event of the
+ * same queue (registration runs outside the queue lock, as in the reference's
+ * Integration.get_future, src/bridge.py:54-70). */
+int tb_poll_add_seq(tb_poll_t reg, tb_event_t ev, uint64_t chain, uint64_t seq,
+                    uint64_t token);
 /* PollRegistry.poll (polling.py:80-120): drain inbox, re-check pending,
  * write up to cap fired tokens (FIFO within a chain). TB_NOT_READY (and
  * *nfired = 0) when another thread holds the guard. Complete entries beyond
- * cap stay pending. Never blocks (cudaEventQuery only). */
-int tb_poll(tb_poll_t reg, uint64_t *fired, int cap, int *nfired);
+ * cap stay pending. Never blocks (cudaEventQuery only). status (optional,
+ * parallel to fired): 0, or -cudaError when the event's query reported a
+ * device fault — the caller faults that entry's future instead of running
+ * its callback (errors surface as Faulted futures, src/executors.py:50-55,
+ * src/runtime/polling.py:71-75). */
+int tb_poll(tb_poll_t reg, uint64_t *fired, int32_t *status, int cap, int *nfired);
 int tb_poll_pending(tb_poll_t reg, int64_t *n);
 /* abandon_all (polling.py:122-147): remove every entry; complete[i] says
- * whether token i's event had completed (run callback) or not (abandon). */
+ * whether token i's event had completed (1: run callback), not (0: abandon)
+ * or faulted (2: fault the future). */
 int tb_poll_drain(tb_poll_t reg, uint64_t *tokens, uint8_t *complete, int cap,
                   int *n);
 int tb_poll_entry_high_water(tb_poll_t reg, int *hw);
@@ -350,13 +363,14 @@ int tb_poll_entry_high_water(tb_poll_t reg, int *hw);
 /* VirtualDevice.register_host_task (src/device.py:311-321) and its
  * dispatcher threads (src/device.py:541-567): after `ev` completes on the
  * device, `token` becomes available to tb_htq_next. Implemented with
- * cudaStreamWaitEvent + cudaLaunchHostFunc on side streams owned by the
- * queue; the CUDA callback only enqueues (no CUDA calls, no Python). */
+ * cudaStreamWaitEvent + a stream callback on side streams owned by the queue;
+ * the CUDA callback only enqueues (no CUDA calls, no Python). */
 int tb_htq_create(int side_streams, tb_htq_t *q);
 int tb_host_task(tb_htq_t q, tb_event_t ev, uint64_t token);
 /* Block up to timeout_us for the next ready token: TB_OK / TB_NOT_READY
- * (timeout) / TB_E_CLOSED (closed and empty). */
-int tb_htq_next(tb_htq_t q, uint64_t *token, int64_t timeout_us);
+ * (timeout) / TB_E_CLOSED (closed and empty). *status (optional): 0, or
+ * -cudaError when the device faulted before the event (fault the future). */
+int tb_htq_next(tb_htq_t q, uint64_t *token, int *status, int64_t timeout_us);
 int tb_htq_close(tb_htq_t q);
 int tb_htq_destroy(tb_htq_t q);
 
@@ -387,7 +401,17 @@ typedef struct {
                                 D2H per batch). 1: the batch kernel runs in
                                 place on the pinned staging buffer (mapped
                                 host memory over PCIe): one launch + one event
-                                per batch, no copy ops (mini-app only).     */
+                                per batch, no copy ops (mini-app only).
+                                2: no staging at all — the tasks' work
+                                buffers live in one pinned arena and the
+                                batch kernel reads each member's rows and
+                                writes its output rows there directly
+                                (tb_launch_gather): no marshal/scatter
+                                memcpy, one launch + one event per batch.   */
+  int64_t fault_at_launch;   /* fault injection (tests): the k-th batch launch
+                                of the run (k >= 1) runs a trapping kernel;
+                                the device fault must surface as this call's
+                                error, in every mode. 0 = off.               */
 } tb_machine_config;
 
 typedef struct {             /* StepMetrics (src/miniapp.py:103-113)         */
@@ -399,6 +423,23 @@ typedef struct {             /* StepMetrics (src/miniapp.py:103-113)         */
  * steps_out[cfg->steps] (optional); cells_out[subgrids*512] (optional). */
 int tb_machine_run(const tb_machine_config *cfg, double *checksum,
                    tb_machine_step *steps_out, double *cells_out);
+/* tb_machine_run on the caller's cells (run_scenario on an existing
+ * Scenario, src/miniapp.py:185-229): cells [subgrids][512] hold the initial
+ * state on entry and the final state on return. exec_stats (optional):
+ * [steps][executors][max_agg + 3] int64 — per step and executor, batches by
+ * member count (index = count) then full- and idle-triggered launches (the
+ * AggregationExecutor's batch_sizes / reasons, src/executors.py:166-169). */
+int tb_machine_run_cells(const tb_machine_config *cfg, double *cells, double *checksum,
+                         tb_machine_step *steps_out, int64_t *exec_stats);
+/* One aggregated batch whose members stay where they are (zero_copy = 2):
+ * dst[i][0..n[i]) = transform(src[i][0..n[i])) for i < members, the pointers
+ * being device-accessible (device or mapped pinned host memory, 16-B
+ * aligned, n[i] even). op/kind/c1/c2 as tb_launch. Up to
+ * TB_GATHER_MAX members per launch. */
+#define TB_GATHER_MAX 64
+int tb_launch_gather(tb_stream_t s, int op, int kind, double c1, double c2,
+                     const double *const *src, double *const *dst, const int64_t *n,
+                     int members);
 
 /* One aggregated hydro batch (the Octo-Tiger use of src/executors.py:257-284,
  * PAPER.md:762-773): H2D(din <- hin: nsub ghosted sub-grids [5][12^3]) ;

@@ -56,6 +56,8 @@ TB_PROBE_DMUL_DADD = 3
 TB_OP_NONE = 0
 TB_OP_KIND = 1
 TB_OP_AFFINE = 2
+TB_OP_TRAP = 3          # fault injection: the kernel traps
+TB_GATHER_MAX = 64
 
 ABI_VERSION = 1
 
@@ -81,6 +83,7 @@ _szt = ctypes.c_size_t
 _pu64 = ctypes.POINTER(ctypes.c_uint64)
 _pi64 = ctypes.POINTER(ctypes.c_int64)
 _pint = ctypes.POINTER(ctypes.c_int)
+_pi32 = ctypes.POINTER(ctypes.c_int32)
 _pu8 = ctypes.POINTER(ctypes.c_uint8)
 _pvp = ctypes.POINTER(ctypes.c_void_p)
 
@@ -130,16 +133,19 @@ SIGNATURES = {
     "tb_poll_create": [_pu64],
     "tb_poll_destroy": [_u64],
     "tb_poll_add": [_u64, _u64, _u64, _u64],
-    "tb_poll": [_u64, _pu64, _int, _pint],
+    "tb_poll_add_seq": [_u64, _u64, _u64, _u64, _u64],
+    "tb_poll": [_u64, _pu64, _pi32, _int, _pint],
     "tb_poll_pending": [_u64, _pi64],
     "tb_poll_drain": [_u64, _pu64, _pu8, _int, _pint],
     "tb_poll_entry_high_water": [_u64, _pint],
     "tb_htq_create": [_int, _pu64],
     "tb_host_task": [_u64, _u64, _u64],
-    "tb_htq_next": [_u64, _pu64, _i64],
+    "tb_htq_next": [_u64, _pu64, _pint, _i64],
     "tb_htq_close": [_u64],
     "tb_htq_destroy": [_u64],
     "tb_machine_run": [_vp, _vp, _vp, _vp],
+    "tb_machine_run_cells": [_vp, _vp, _vp, _vp, _vp],
+    "tb_launch_gather": [_u64, _int, _int, _dbl, _dbl, _vp, _vp, _vp, _int],
     "tb_agg_launch_hydro": [_u64, _vp, _vp, _i64, _vp, _vp, _dbl, _dbl, _pu64],
     "tb_machine_run_hydro": [_vp, _vp, _vp, _dbl, _dbl, _vp],
     "tb_ipc_get_handle": [_vp, _vp, _pu64],
@@ -171,7 +177,8 @@ SIGNATURES = {
 BLOCKING = {"tb_init", "tb_device_sync", "tb_stream_sync", "tb_event_wait",
             "tb_htq_next", "tb_htq_destroy", "tb_malloc", "tb_free",
             "tb_host_alloc", "tb_host_free", "tb_stream_destroy",
-            "tb_memcpy_h2d", "tb_memcpy_d2h", "tb_poll_drain", "tb_machine_run", "tb_machine_run_hydro",
+            "tb_memcpy_h2d", "tb_memcpy_d2h", "tb_poll_drain", "tb_machine_run", "tb_machine_run_cells",
+            "tb_machine_run_hydro",
             "tb_fp64_probe"}
 
 _lock = threading.Lock()

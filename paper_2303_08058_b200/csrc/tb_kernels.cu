@@ -75,6 +75,31 @@ __global__ void __launch_bounds__(256) k_launch(double *__restrict__ d, int64_t 
 }
 
 __global__ void k_empty() {}
+__global__ void k_trap() { __trap(); }
+
+// K1g: one aggregated batch whose members are read and written where they
+// live (mapped pinned host rows of the machine's task arena): member =
+// blockIdx.y, 16-byte vector accesses, the same two roundings as K1.
+struct GatherArgs {
+  const double *src[TB_GATHER_MAX];
+  double *dst[TB_GATHER_MAX];
+  int64_t n[TB_GATHER_MAX];
+  double c1, c2;
+};
+
+__global__ void __launch_bounds__(256) k_launch_gather(const __grid_constant__ GatherArgs a) {
+  const int m = blockIdx.y;
+  const double2 *s = reinterpret_cast<const double2 *>(a.src[m]);
+  double2 *d = reinterpret_cast<double2 *>(a.dst[m]);
+  const int64_t n2 = a.n[m] / 2;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double2 x = s[i];
+    x.x = xform(x.x, a.c1, a.c2);
+    x.y = xform(x.y, a.c1, a.c2);
+    d[i] = x;
+  }
+}
 
 __global__ void k_spin(int64_t ns) {
   uint64_t t0, t;
@@ -1183,6 +1208,10 @@ int tb_launch(tb_stream_t s, int op, int kind, double c1, double c2, double *d,
     c2 = h2[kind];
     op = TB_OP_AFFINE;
   }
+  if (op == TB_OP_TRAP) {   // fault injection: a device-side trap
+    k_trap<<<1, 32, 0, st>>>();
+    return tb::last_error();
+  }
   if (op == TB_OP_NONE || n == 0) {
     k_empty<<<1, 32, 0, st>>>();
     return tb::last_error();
@@ -1190,6 +1219,46 @@ int tb_launch(tb_stream_t s, int op, int kind, double c1, double c2, double *d,
   if (op != TB_OP_AFFINE) return TB_E_INVALID;
   const int blocks = grid_for((n + 1) / 2, 256, tb::sm_count() * 8);
   k_launch<TB_OP_AFFINE><<<blocks, 256, 0, st>>>(d, n, c1, c2);
+  return tb::last_error();
+}
+
+int tb_launch_gather(tb_stream_t s, int op, int kind, double c1, double c2,
+                     const double *const *src, double *const *dst, const int64_t *n,
+                     int members) {
+  if (members < 1 || members > TB_GATHER_MAX || !src || !dst || !n) return TB_E_INVALID;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
+  if (op == TB_OP_TRAP) {
+    k_trap<<<1, 32, 0, st>>>();
+    return tb::last_error();
+  }
+  if (op == TB_OP_KIND) {
+    if (kind < 0 || kind >= TB_KINDS) return TB_E_INVALID;
+    static const double h1[TB_KINDS] = {1.0000003, 0.9999998, 1.0000001, 0.9999997,
+                                        1.0000002};
+    static const double h2[TB_KINDS] = {1e-07, -1e-07, 2e-07, 5e-08, -2e-07};
+    c1 = h1[kind];
+    c2 = h2[kind];
+  } else if (op == TB_OP_NONE) {
+    k_empty<<<1, 32, 0, st>>>();
+    return tb::last_error();
+  } else if (op != TB_OP_AFFINE) {
+    return TB_E_INVALID;
+  }
+  GatherArgs a;
+  int64_t nmax = 0;
+  for (int i = 0; i < members; ++i) {
+    if (!src[i] || !dst[i] || n[i] < 0 || (n[i] & 1) ||
+        ((reinterpret_cast<uintptr_t>(src[i]) | reinterpret_cast<uintptr_t>(dst[i])) & 15))
+      return TB_E_INVALID;
+    a.src[i] = src[i];
+    a.dst[i] = dst[i];
+    a.n[i] = n[i];
+    nmax = n[i] > nmax ? n[i] : nmax;
+  }
+  a.c1 = c1;
+  a.c2 = c2;
+  const int bx = grid_for(nmax / 2 > 0 ? nmax / 2 : 1, 256, 64);
+  k_launch_gather<<<dim3((unsigned)bx, (unsigned)members), 256, 0, st>>>(a);
   return tb::last_error();
 }
 

@@ -184,7 +184,9 @@ class Pool {
 // continuations as pool tasks.
 class Poller {
  public:
-  explicit Poller(Pool *pool) : pool_(pool) {}
+  // fault: where a device error seen by the poll body is recorded (first
+  // error wins); the continuation still runs and sees the machine failed
+  Poller(Pool *pool, std::atomic<int> *fault) : pool_(pool), fault_(fault) {}
 
   void add(cudaEvent_t ev, uint64_t chain, Task cont) {
     std::lock_guard<std::mutex> g(inbox_mu_);
@@ -206,7 +208,13 @@ class Poller {
     int fired = 0;
     for (auto it = chains_.begin(); it != chains_.end();) {
       auto &dq = it->second;
-      while (!dq.empty() && cudaEventQuery(dq.front().ev) != cudaErrorNotReady) {
+      while (!dq.empty()) {
+        const cudaError_t q = cudaEventQuery(dq.front().ev);
+        if (q == cudaErrorNotReady) break;
+        if (q != cudaSuccess) {
+          int expect = 0;
+          fault_->compare_exchange_strong(expect, -(int)q);
+        }
         Entry e = dq.front();
         dq.pop_front();
         tb_event_release(reinterpret_cast<tb_event_t>(e.ev));
@@ -226,6 +234,7 @@ class Poller {
     Task cont;
   };
   Pool *pool_;
+  std::atomic<int> *fault_;
   std::mutex inbox_mu_;
   std::vector<Entry> inbox_;
   std::mutex body_;
@@ -236,7 +245,8 @@ class Poller {
 // ------------------------------------------------------ host-task threads --
 class HostTasks {
  public:
-  HostTasks(Pool *pool, int threads, int device, int side_streams) : pool_(pool) {
+  HostTasks(Pool *pool, int threads, int device, int side_streams, std::atomic<int> *fault)
+      : pool_(pool), fault_(fault) {
     cudaSetDevice(device);
     for (int i = 0; i < side_streams; ++i) {
       cudaStream_t s;
@@ -256,10 +266,16 @@ class HostTasks {
     for (auto s : side_) cudaStreamDestroy(s);
   }
   void add(cudaEvent_t ev, Task cont) {
-    auto *item = new Item{this, ev, cont};
+    auto *item = new Item{this, ev, cont, cudaSuccess};
     cudaStream_t side = side_[rr_.fetch_add(1) % side_.size()];
     cudaStreamWaitEvent(side, ev, 0);
-    cudaLaunchHostFunc(side, &HostTasks::trampoline, item);
+    // a stream callback is called with the stream's status even after a
+    // device fault (cudaLaunchHostFunc is not), so the fault reaches the
+    // machine instead of leaving its step waiting forever
+    if (cudaStreamAddCallback(side, &HostTasks::trampoline, item, 0) != cudaSuccess) {
+      item->status = cudaErrorLaunchFailure;
+      trampoline(side, cudaErrorLaunchFailure, item);
+    }
   }
   int64_t dispatched() const { return dispatched_.load(); }
 
@@ -268,9 +284,12 @@ class HostTasks {
     HostTasks *self;
     cudaEvent_t ev;
     Task cont;
+    cudaError_t status;
   };
-  static void CUDART_CB trampoline(void *p) {   // CUDA driver thread: enqueue only
+  static void CUDART_CB trampoline(cudaStream_t, cudaError_t status, void *p) {
+    // CUDA driver thread: enqueue only
     Item *it = static_cast<Item *>(p);
+    it->status = status;
     HostTasks *self = it->self;   // `it` may be consumed as soon as it is queued
     {
       std::lock_guard<std::mutex> g(self->mu_);
@@ -288,6 +307,10 @@ class HostTasks {
         it = ready_.front();
         ready_.pop_front();
       }
+      if (it->status != cudaSuccess) {
+        int expect = 0;
+        fault_->compare_exchange_strong(expect, -(int)it->status);
+      }
       tb_event_release(reinterpret_cast<tb_event_t>(it->ev));
       pool_->push(it->cont);   // foreign thread -> pool injector
       dispatched_.fetch_add(1);
@@ -295,6 +318,7 @@ class HostTasks {
     }
   }
   Pool *pool_;
+  std::atomic<int> *fault_;
   std::vector<cudaStream_t> side_;
   std::atomic<unsigned> rr_{0};
   std::mutex mu_;
@@ -352,6 +376,14 @@ struct Executor {
   int id;
   cudaStream_t stream;
   std::mutex mu;
+  // POLLING: an event is recorded and registered with the poller under this
+  // lock, so each stream's poll chain is in record order (the poll body
+  // queries only the chain head)
+  std::mutex rec_mu;
+  // per-executor batch statistics of the running step: [0, max_agg] = batches
+  // by member count, then full- and idle-triggered launches (the
+  // AggregationExecutor's batch_sizes / reasons, src/executors.py:166-169)
+  std::unique_ptr<std::atomic<int64_t>[]> stats;
   Batch *open[TB_KINDS] = {nullptr, nullptr, nullptr, nullptr, nullptr};
 };
 
@@ -360,7 +392,8 @@ struct SubTask {
   Executor *ex;
   int64_t lo, n;          // sub-grids [lo, lo+n)
   int round;
-  std::vector<double> a, b;
+  std::vector<double> a, b;   // work buffers (zero_copy = 2: abuf/bbuf live in the arena)
+  double *abuf, *bbuf;
   double *work, *out;
 };
 
@@ -384,7 +417,16 @@ struct Machine {
   // metrics
   std::atomic<int64_t> launches{0}, transfers{0}, event_waits{0}, full{0}, idle{0},
       members{0}, kernels{0};
-  int error = TB_OK;
+  // first device fault / API error (0 = none); once set, tasks stop
+  // scheduling and finish, the step loop stops, and the run returns it
+  std::atomic<int> fault{0};
+  std::atomic<int64_t> launch_seq{0};   // fault_at_launch counter
+  double *arena = nullptr;              // zero_copy = 2: pinned task buffers
+  void fail(int rc) {
+    int expect = 0;
+    if (rc != TB_OK) fault.compare_exchange_strong(expect, rc);
+  }
+  bool failed() const { return fault.load(std::memory_order_relaxed) != 0; }
   // hydro workload (tb_machine_run_hydro)
   bool hydro = false;
   int64_t nb = 0;                  // sub-grids per lattice edge
@@ -423,7 +465,10 @@ void staging_release(Machine *m, Staging *s) {
 }
 
 // Bridge a recorded event into the runtime: the continuation `cont` becomes
-// a pool task once the event completes (src/bridge.py:54-101).
+// a pool task once the event completes (src/bridge.py:54-101). A device
+// fault does not fail the continuation's scheduling — the continuation runs
+// and finds the machine failed (errors surface as the run's result, never as
+// a hang; src/executors.py:50-55, src/runtime/polling.py:71-75).
 void bridge(Machine *m, Executor *ex, cudaEvent_t ev, Task cont) {
   switch (m->cfg.mode) {
     case TB_MODE_POLLING:
@@ -432,13 +477,43 @@ void bridge(Machine *m, Executor *ex, cudaEvent_t ev, Task cont) {
     case TB_MODE_HOSTTASK:
       m->hosttasks->add(ev, cont);
       break;
-    default:  // FENCE: block this worker, then the future is ready
+    default: {  // FENCE: block this worker, then the future is ready
       m->event_waits.fetch_add(1, std::memory_order_relaxed);
-      cudaEventSynchronize(ev);
+      const cudaError_t e = cudaEventSynchronize(ev);
+      if (e != cudaSuccess) m->fail(-(int)e);
       tb_event_release(reinterpret_cast<tb_event_t>(ev));
       m->pool->push(cont);
       break;
+    }
   }
+}
+
+// Enqueue work on the executor's stream (`enqueue` records the completion
+// event into *ev) and bridge that event. POLLING keeps record + register
+// under the executor's record lock (poll chains in record order); a failed
+// enqueue still bridges (ev may be 0: the query reports an error) so the
+// continuation runs and sees the failure.
+template <typename F>
+void enqueue_and_bridge(Machine *m, Executor *ex, Task cont, F enqueue) {
+  tb_event_t ev = 0;
+  if (m->cfg.mode == TB_MODE_POLLING) {
+    std::lock_guard<std::mutex> g(ex->rec_mu);
+    const int rc = enqueue(&ev);
+    if (rc != TB_OK) m->fail(rc);
+    if (!ev) {
+      m->pool->push(cont);
+      return;
+    }
+    bridge(m, ex, reinterpret_cast<cudaEvent_t>(ev), cont);
+    return;
+  }
+  const int rc = enqueue(&ev);
+  if (rc != TB_OK) m->fail(rc);
+  if (!ev) {
+    m->pool->push(cont);
+    return;
+  }
+  bridge(m, ex, reinterpret_cast<cudaEvent_t>(ev), cont);
 }
 
 void resume_task(void *p);
@@ -447,7 +522,9 @@ void hydro_resume(void *p);
 void batch_done(void *p) {   // AggregationExecutor finish (src/executors.py:286-301)
   Batch *b = static_cast<Batch *>(p);
   Machine *m = b->ex->m;
-  if (m->hydro) {   // scatter each member's dU/dt rows and amax entries
+  if (m->failed()) {
+    // the batch's outputs are garbage: skip the scatter, let members finish
+  } else if (m->hydro) {   // scatter each member's dU/dt rows and amax entries
     int64_t total = 0;
     for (const Req &r : b->members) total += r.n;
     const int64_t nsub = total / kGhosted;
@@ -459,17 +536,23 @@ void batch_done(void *p) {   // AggregationExecutor finish (src/executors.py:286
       std::memcpy(r.dst + k * kInterior, am + o, sizeof(double) * k);
       o += k;
     }
-  } else {
+  } else if (b->staging) {
     int64_t off = 0;
     for (const Req &r : b->members) {
       std::memcpy(r.dst, b->staging->host + off, sizeof(double) * r.n);
       off += r.n;
     }
   }
-  staging_release(m, b->staging);
+  if (b->staging) staging_release(m, b->staging);
   m->launches.fetch_add(1, std::memory_order_relaxed);
   m->members.fetch_add((int64_t)b->members.size(), std::memory_order_relaxed);
   (b->idle ? m->idle : m->full).fetch_add(1, std::memory_order_relaxed);
+  if (b->ex->stats) {
+    const int64_t M = m->cfg.max_agg;
+    const int64_t k = std::min<int64_t>((int64_t)b->members.size(), M);
+    b->ex->stats[k].fetch_add(1, std::memory_order_relaxed);
+    b->ex->stats[M + 1 + (b->idle ? 1 : 0)].fetch_add(1, std::memory_order_relaxed);
+  }
   for (const Req &r : b->members)
     m->pool->push(Task{m->hydro ? hydro_resume : resume_task, r.task});
   batch_release(b);
@@ -479,6 +562,41 @@ void launch(Batch *b, bool idle) {   // src/executors.py:257-284 as one launch
   Executor *ex = b->ex;
   Machine *m = ex->m;
   b->idle = idle;
+  if (m->failed()) {   // the device is gone: no launch, members finish
+    for (const Req &r : b->members)
+      m->pool->push(Task{m->hydro ? hydro_resume : resume_task, r.task});
+    batch_release(b);
+    return;
+  }
+  const int64_t fat = m->cfg.fault_at_launch;
+  const bool trap = fat > 0 && m->launch_seq.fetch_add(1) + 1 == fat;
+  const int op = trap ? TB_OP_TRAP : TB_OP_KIND;
+  const int do_barrier = m->cfg.inject_barriers && !m->cfg.barrier_elision;
+  const tb_stream_t st = reinterpret_cast<tb_stream_t>(ex->stream);
+  m->kernels.fetch_add(1, std::memory_order_relaxed);
+  if (m->cfg.zero_copy == 2 && !m->hydro) {
+    // members read and written where they live (the pinned task arena)
+    enqueue_and_bridge(m, ex, Task{batch_done, b}, [&](tb_event_t *ev) {
+      const double *src[TB_GATHER_MAX];
+      double *dst[TB_GATHER_MAX];
+      int64_t n[TB_GATHER_MAX];
+      int rc = TB_OK;
+      for (size_t i0 = 0; i0 < b->members.size() && rc == TB_OK; i0 += TB_GATHER_MAX) {
+        const int k = (int)std::min<size_t>(TB_GATHER_MAX, b->members.size() - i0);
+        for (int i = 0; i < k; ++i) {
+          const Req &r = b->members[i0 + i];
+          src[i] = r.src;
+          dst[i] = r.dst;
+          n[i] = r.n;
+        }
+        rc = tb_launch_gather(st, op, b->kind, 0.0, 0.0, src, dst, n, k);
+      }
+      if (rc == TB_OK && do_barrier) rc = tb_barrier(st);
+      if (rc == TB_OK) rc = tb_event_record(st, ev);
+      return rc;
+    });
+    return;
+  }
   int64_t total = 0;
   for (const Req &r : b->members) total += r.n;
   // hydro: staging = [ghosted inputs | dU/dt + amax outputs], one size class
@@ -491,32 +609,30 @@ void launch(Batch *b, bool idle) {   // src/executors.py:257-284 as one launch
     std::memcpy(b->staging->host + off, r.src, sizeof(double) * r.n);
     off += r.n;
   }
-  tb_event_t ev = 0;
-  const int do_barrier = m->cfg.inject_barriers && !m->cfg.barrier_elision;
   if (m->cfg.zero_copy && !m->hydro) {
     // the batch kernel in place on the pinned staging buffer (mapped host
     // memory, read and written over PCIe): one launch + one event, no copies
-    const tb_stream_t st = reinterpret_cast<tb_stream_t>(ex->stream);
-    int rc = tb_launch(st, TB_OP_KIND, b->kind, 0.0, 0.0, b->staging->host, total);
-    if (rc == TB_OK && do_barrier) rc = tb_barrier(st);
-    if (rc == TB_OK) rc = tb_event_record(st, &ev);
-    if (rc != TB_OK) m->error = rc;
-    m->kernels.fetch_add(1, std::memory_order_relaxed);
-    bridge(m, ex, reinterpret_cast<cudaEvent_t>(ev), Task{batch_done, b});
+    enqueue_and_bridge(m, ex, Task{batch_done, b}, [&](tb_event_t *ev) {
+      int rc = tb_launch(st, op, b->kind, 0.0, 0.0, b->staging->host, total);
+      if (rc == TB_OK && do_barrier) rc = tb_barrier(st);
+      if (rc == TB_OK) rc = tb_event_record(st, ev);
+      return rc;
+    });
     return;
   }
-  const int rc =
-      m->hydro ? tb_agg_launch_hydro(reinterpret_cast<tb_stream_t>(ex->stream), b->staging->dev,
-                                     b->staging->host, total / kGhosted,
-                                     b->staging->dev + total, b->staging->host + total, m->dx,
-                                     m->gamma, &ev)
-               : tb_agg_launch(reinterpret_cast<tb_stream_t>(ex->stream), TB_OP_KIND, b->kind,
-                               0.0, 0.0, b->staging->dev, b->staging->host, bytes, do_barrier,
-                               &ev);
-  if (rc != TB_OK) m->error = rc;
   m->transfers.fetch_add(2, std::memory_order_relaxed);
-  m->kernels.fetch_add(1, std::memory_order_relaxed);
-  bridge(m, ex, reinterpret_cast<cudaEvent_t>(ev), Task{batch_done, b});
+  enqueue_and_bridge(m, ex, Task{batch_done, b}, [&](tb_event_t *ev) {
+    if (m->hydro && trap) {
+      const int rc = tb_launch(st, TB_OP_TRAP, 0, 0.0, 0.0, nullptr, 0);
+      return rc == TB_OK ? tb_event_record(st, ev) : rc;
+    }
+    if (m->hydro)
+      return tb_agg_launch_hydro(st, b->staging->dev, b->staging->host, total / kGhosted,
+                                        b->staging->dev + total, b->staging->host + total,
+                                        m->dx, m->gamma, ev);
+    return tb_agg_launch(st, op, b->kind, 0.0, 0.0, b->staging->dev, b->staging->host, bytes,
+                         do_barrier, ev);
+  });
 }
 
 void idle_fire(void *p) {   // the idleness probe completed (src/executors.py:209-218)
@@ -561,11 +677,18 @@ void schedule(Executor *ex, int kind, const double *src, double *dst, int64_t n,
   }
   if (opened && opened != full) {
     // One idleness probe per batch: a queue marker event (src/bridge.py:92-101).
-    tb_event_t ev = 0;
-    tb_event_record(reinterpret_cast<tb_stream_t>(ex->stream), &ev);
-    bridge(m, ex, reinterpret_cast<cudaEvent_t>(ev), Task{idle_fire, opened});
+    enqueue_and_bridge(m, ex, Task{idle_fire, opened}, [&](tb_event_t *ev) {
+      return tb_event_record(reinterpret_cast<tb_stream_t>(ex->stream), ev);
+    });
   }
   if (full) launch(full, false);
+}
+
+void task_finished(Machine *m) {
+  if (m->remaining.fetch_sub(1) == 1) {
+    std::lock_guard<std::mutex> g(m->done_mu);
+    m->done_cv.notify_all();
+  }
 }
 
 // numpy's pairwise sum of 512 contiguous doubles (see oracle/tb_oracle.c)
@@ -585,9 +708,13 @@ double pairwise512(const double *a) {
 void start_task(void *p) {   // ghost fold + first round (src/miniapp.py:116-130)
   SubTask *t = static_cast<SubTask *>(p);
   Machine *m = t->m;
+  if (m->failed()) {
+    task_finished(m);
+    return;
+  }
   const int64_t S = m->cfg.subgrids;
-  t->work = t->a.data();
-  t->out = t->b.data();
+  t->work = t->abuf;
+  t->out = t->bbuf;
   for (int64_t k = 0; k < t->n; ++k) {
     const int64_t g = t->lo + k;
     double *w = t->work + k * kCells;
@@ -605,6 +732,10 @@ void start_task(void *p) {   // ghost fold + first round (src/miniapp.py:116-130
 void resume_task(void *p) {   // next round, or write-back + post-process
   SubTask *t = static_cast<SubTask *>(p);
   Machine *m = t->m;
+  if (m->failed()) {
+    task_finished(m);
+    return;
+  }
   std::swap(t->work, t->out);
   const int kpc = (int)m->cfg.kernels_per_chain;
   const int rounds = (int)(m->cfg.chains * kpc);
@@ -621,10 +752,7 @@ void resume_task(void *p) {   // next round, or write-back + post-process
     m->mins[g] = mn;
     m->sums[g] = pairwise512(w);
   }
-  if (m->remaining.fetch_sub(1) == 1) {
-    std::lock_guard<std::mutex> g(m->done_mu);
-    m->done_cv.notify_all();
-  }
+  task_finished(m);
 }
 
 // ------------------------------------------------------- hydro workload --
@@ -655,12 +783,7 @@ void ghost_fill(const Machine *m, int64_t g, double *out) {
     }
 }
 
-void hydro_done(Machine *m) {
-  if (m->remaining.fetch_sub(1) == 1) {
-    std::lock_guard<std::mutex> g(m->done_mu);
-    m->done_cv.notify_all();
-  }
-}
+void hydro_done(Machine *m) { task_finished(m); }
 
 void hydro_resume(void *p) {   // outputs landed in t->b: keep dU/dt and amax
   SubTask *t = static_cast<SubTask *>(p);
@@ -673,6 +796,10 @@ void hydro_resume(void *p) {   // outputs landed in t->b: keep dU/dt and amax
 
 void hydro_start(void *p) {    // ghost exchange + one K6 request
   SubTask *t = static_cast<SubTask *>(p);
+  if (t->m->failed()) {
+    hydro_done(t->m);
+    return;
+  }
   for (int64_t k = 0; k < t->n; ++k) ghost_fill(t->m, t->lo + k, t->a.data() + k * kGhosted);
   schedule(t->ex, 0, t->a.data(), t->b.data(), t->n * kGhosted, t);
 }
@@ -755,13 +882,16 @@ double exact_sum(const double *x, int64_t n) {
 
 using namespace tbm;
 
-extern "C" int tb_machine_run(const tb_machine_config *cfg_in, double *checksum,
-                              tb_machine_step *steps_out, double *cells_out) {
+namespace tbm {
+
+int run_machine(const tb_machine_config *cfg_in, const double *cells_in, double *checksum,
+                tb_machine_step *steps_out, double *cells_out, int64_t *exec_stats) {
   if (!cfg_in || !checksum) return TB_E_INVALID;
   const tb_machine_config &c = *cfg_in;
   if (c.subgrids < 1 || c.steps < 0 || c.workers < 1 || c.executors < 1 || c.max_agg < 1 ||
       c.chains < 0 || c.kernels_per_chain < 1 || c.kernels_per_chain > TB_KINDS ||
-      c.task_subgrids < 1 || c.mode < TB_MODE_POLLING || c.mode > TB_MODE_FENCE)
+      c.task_subgrids < 1 || c.mode < TB_MODE_POLLING || c.mode > TB_MODE_FENCE ||
+      c.zero_copy < 0 || c.zero_copy > 2 || c.fault_at_launch < 0)
     return TB_E_INVALID;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -769,40 +899,60 @@ extern "C" int tb_machine_run(const tb_machine_config *cfg_in, double *checksum,
   m.cfg = c;
   const int64_t S = c.subgrids;
   m.cells.resize(S * kCells);
-  const double scale = (double)(S * 1000 + kCells);
-  for (int64_t g = 0; g < S; ++g)   // src/miniapp.py:72-77
-    for (int i = 0; i < kCells; ++i)
-      m.cells[g * kCells + i] = ((double)g * 1000.0 + (double)i) / scale;
+  if (cells_in) {
+    std::memcpy(m.cells.data(), cells_in, sizeof(double) * S * kCells);
+  } else {
+    const double scale = (double)(S * 1000 + kCells);
+    for (int64_t g = 0; g < S; ++g)   // src/miniapp.py:72-77
+      for (int i = 0; i < kCells; ++i)
+        m.cells[g * kCells + i] = ((double)g * 1000.0 + (double)i) / scale;
+  }
   m.faces.resize(S * 2 * kFace);
   m.mins.resize(S);
   m.sums.resize(S);
+  if (c.zero_copy == 2) {
+    // every task's two work buffers in one pinned, device-mapped arena
+    if (cudaHostAlloc(reinterpret_cast<void **>(&m.arena), sizeof(double) * 2 * S * kCells,
+                      cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess)
+      return tb::rc(cudaGetLastError());
+  }
   m.pool.reset(new Pool((int)c.workers, dev, 1234));
-  m.poller.reset(new Poller(m.pool.get()));
+  m.poller.reset(new Poller(m.pool.get(), &m.fault));
   if (c.mode == TB_MODE_POLLING) m.pool->set_idle_hook(&Poller::hook, m.poller.get());
   m.hosttasks.reset(new HostTasks(m.pool.get(), (int)std::max<int64_t>(1, c.hosttask_threads),
-                                  dev, 4));
+                                  dev, 4, &m.fault));
   for (int64_t e = 0; e < c.executors; ++e) {
     auto ex = std::make_unique<Executor>();
     ex->m = &m;
     ex->id = (int)e;
     cudaStreamCreateWithFlags(&ex->stream, cudaStreamNonBlocking);
+    if (exec_stats) {
+      ex->stats.reset(new std::atomic<int64_t>[c.max_agg + 3]);
+      for (int64_t i = 0; i < c.max_agg + 3; ++i) ex->stats[i].store(0);
+    }
     m.execs.push_back(std::move(ex));
   }
   // tasks: contiguous blocks of task_subgrids, round-robin over executors
   // (src/cli.py:224 aggs_by_grid)
-  int64_t k = 0;
-  for (int64_t lo = 0; lo < S; lo += c.task_subgrids, ++k) {
+  for (int64_t lo = 0; lo < S; lo += c.task_subgrids) {
     auto t = std::make_unique<SubTask>();
     t->m = &m;
     t->lo = lo;
     t->n = std::min<int64_t>(c.task_subgrids, S - lo);
     t->ex = m.execs[(size_t)(lo % c.executors)].get();
-    t->a.resize(t->n * kCells);
-    t->b.resize(t->n * kCells);
+    if (m.arena) {
+      t->abuf = m.arena + 2 * lo * kCells;
+      t->bbuf = t->abuf + t->n * kCells;
+    } else {
+      t->a.resize(t->n * kCells);
+      t->b.resize(t->n * kCells);
+      t->abuf = t->a.data();
+      t->bbuf = t->b.data();
+    }
     m.tasks.push_back(std::move(t));
   }
   double cs = 0.0;
-  for (int64_t step = 0; step < c.steps; ++step) {
+  for (int64_t step = 0; step < c.steps && !m.failed(); ++step) {
     const int64_t k0 = m.kernels, t0n = m.transfers, w0 = m.event_waits, f0 = m.full,
                   i0 = m.idle, mb0 = m.members;
     const auto t0 = Clock::now();
@@ -817,6 +967,7 @@ extern "C" int tb_machine_run(const tb_machine_config *cfg_in, double *checksum,
       std::unique_lock<std::mutex> lk(m.done_mu);
       m.done_cv.wait(lk, [&] { return m.remaining.load() == 0; });
     }
+    if (m.failed()) break;
     double dt = m.mins[0];
     for (int64_t g = 1; g < S; ++g) dt = m.mins[g] < dt ? m.mins[g] : dt;
     const double piece = exact_sum(m.sums.data(), S);
@@ -834,9 +985,16 @@ extern "C" int tb_machine_run(const tb_machine_config *cfg_in, double *checksum,
       o.idle = m.idle - i0;
       o.members = m.members - mb0;
     }
+    if (exec_stats) {   // [steps][executors][max_agg + 3], then reset
+      const int64_t W = c.max_agg + 3;
+      for (int64_t e = 0; e < c.executors; ++e)
+        for (int64_t i = 0; i < W; ++i)
+          exec_stats[(step * c.executors + e) * W + i] = m.execs[e]->stats[i].exchange(0);
+    }
   }
   *checksum = cs;
-  if (cells_out) std::memcpy(cells_out, m.cells.data(), sizeof(double) * S * kCells);
+  if (cells_out && !m.failed())
+    std::memcpy(cells_out, m.cells.data(), sizeof(double) * S * kCells);
   m.pool->stop();
   m.hosttasks.reset();
   for (auto &ex : m.execs) {
@@ -848,8 +1006,23 @@ extern "C" int tb_machine_run(const tb_machine_config *cfg_in, double *checksum,
     cudaFree(s->dev);
     delete s;
   }
+  if (m.arena) cudaFreeHost(m.arena);
   const int err = tb::rc(cudaGetLastError());
-  return m.error != TB_OK ? m.error : err;
+  return m.failed() ? m.fault.load() : err;
+}
+
+}  // namespace tbm
+
+extern "C" int tb_machine_run(const tb_machine_config *cfg_in, double *checksum,
+                              tb_machine_step *steps_out, double *cells_out) {
+  return run_machine(cfg_in, nullptr, checksum, steps_out, cells_out, nullptr);
+}
+
+extern "C" int tb_machine_run_cells(const tb_machine_config *cfg_in, double *cells,
+                                    double *checksum, tb_machine_step *steps_out,
+                                    int64_t *exec_stats) {
+  if (!cells) return TB_E_INVALID;
+  return run_machine(cfg_in, cells, checksum, steps_out, cells, exec_stats);
 }
 
 extern "C" int tb_machine_run_hydro(const tb_machine_config *cfg_in, const double *U_in,
@@ -876,10 +1049,10 @@ extern "C" int tb_machine_run_hydro(const tb_machine_config *cfg_in, const doubl
   m.dudt.resize(S * kInterior);
   m.amax.resize(S);
   m.pool.reset(new Pool((int)c.workers, dev, 1234));
-  m.poller.reset(new Poller(m.pool.get()));
+  m.poller.reset(new Poller(m.pool.get(), &m.fault));
   if (c.mode == TB_MODE_POLLING) m.pool->set_idle_hook(&Poller::hook, m.poller.get());
   m.hosttasks.reset(new HostTasks(m.pool.get(), (int)std::max<int64_t>(1, c.hosttask_threads),
-                                  dev, 4));
+                                  dev, 4, &m.fault));
   for (int64_t e = 0; e < c.executors; ++e) {
     auto ex = std::make_unique<Executor>();
     ex->m = &m;
@@ -895,6 +1068,8 @@ extern "C" int tb_machine_run_hydro(const tb_machine_config *cfg_in, const doubl
     t->ex = m.execs[(size_t)((lo / c.task_subgrids) % c.executors)].get();
     t->a.resize(t->n * kGhosted);
     t->b.resize(t->n * kHydroOut);
+    t->abuf = t->a.data();
+    t->bbuf = t->b.data();
     m.tasks.push_back(std::move(t));
   }
   {  // pre-allocate the pinned/device staging pool (two full batches per stream)
@@ -903,11 +1078,11 @@ extern "C" int tb_machine_run_hydro(const tb_machine_config *cfg_in, const doubl
     for (Staging *st : warm) staging_release(&m, st);
   }
   std::vector<double> rho(S * 512);
-  for (int64_t step = 0; step < c.steps; ++step) {
+  for (int64_t step = 0; step < c.steps && !m.failed(); ++step) {
     const int64_t k0 = m.kernels, t0n = m.transfers, w0 = m.event_waits, f0 = m.full,
                   i0 = m.idle, mb0 = m.members;
     const auto t0 = Clock::now();
-    for (int phase = 0; phase < 2; ++phase) {   // fluxes, then the update
+    for (int phase = 0; phase < 2 && !m.failed(); ++phase) {   // fluxes, then the update
       m.remaining.store((int64_t)m.tasks.size());
       for (auto &t : m.tasks) m.pool->push(Task{phase ? hydro_update : hydro_start, t.get()});
       std::unique_lock<std::mutex> lk(m.done_mu);
@@ -934,7 +1109,7 @@ extern "C" int tb_machine_run_hydro(const tb_machine_config *cfg_in, const doubl
       o.members = m.members - mb0;
     }
   }
-  if (U_out) std::memcpy(U_out, m.U.data(), sizeof(double) * S * kInterior);
+  if (U_out && !m.failed()) std::memcpy(U_out, m.U.data(), sizeof(double) * S * kInterior);
   m.pool->stop();
   m.hosttasks.reset();
   for (auto &ex : m.execs) {
@@ -947,5 +1122,5 @@ extern "C" int tb_machine_run_hydro(const tb_machine_config *cfg_in, const doubl
     delete st;
   }
   const int err = tb::rc(cudaGetLastError());
-  return m.error != TB_OK ? m.error : err;
+  return m.failed() ? m.fault.load() : err;
 }

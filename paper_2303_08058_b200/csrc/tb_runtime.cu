@@ -98,6 +98,7 @@ struct PollNode {
   cudaEvent_t ev;
   uint64_t chain;
   uint64_t token;
+  uint64_t seq;     // record order on the chain (0: append in registration order)
   PollNode *next;
 };
 
@@ -123,10 +124,18 @@ struct Registry {
     }
     while (fifo) {
       PollNode *nx = fifo->next;
-      if (fifo->chain)
-        chains[fifo->chain].push_back(fifo);
-      else
+      if (fifo->chain) {
+        // keep each chain in record order: a producer may register after a
+        // later-recorded event of the same stream (registration happens
+        // outside the queue lock), and the poll body queries only the head
+        std::deque<PollNode *> &dq = chains[fifo->chain];
+        auto pos = dq.end();
+        if (fifo->seq)
+          while (pos != dq.begin() && (*(pos - 1))->seq > fifo->seq) --pos;
+        dq.insert(pos, fifo);
+      } else {
         unchained.push_back(fifo);
+      }
       fifo = nx;
     }
   }
@@ -143,17 +152,20 @@ struct Htq {
   std::atomic<unsigned> rr{0};
   std::mutex mu;
   std::condition_variable cv;
-  std::deque<uint64_t> ready;
+  std::deque<std::pair<uint64_t, int>> ready;   // (token, 0 or -cudaError)
   bool closed = false;
 };
 
-void CUDART_CB ht_trampoline(void *p) {
+// A stream callback (not cudaLaunchHostFunc, which is never called once the
+// context has faulted): it receives the stream's status, so a device fault
+// reaches the waiting future as an error instead of leaving it pending.
+void CUDART_CB ht_trampoline(cudaStream_t, cudaError_t status, void *p) {
   // Runs on a CUDA driver thread: no CUDA calls, no Python — only enqueue.
   HtItem *it = static_cast<HtItem *>(p);
   Htq *q = it->q;
   {
     std::lock_guard<std::mutex> g(q->mu);
-    q->ready.push_back(it->token);
+    q->ready.emplace_back(it->token, status == cudaSuccess ? 0 : -(int)status);
   }
   q->cv.notify_one();
   delete it;
@@ -471,9 +483,14 @@ int tb_poll_destroy(tb_poll_t reg) {
 }
 
 int tb_poll_add(tb_poll_t reg, tb_event_t ev, uint64_t chain, uint64_t token) {
+  return tb_poll_add_seq(reg, ev, chain, 0, token);
+}
+
+int tb_poll_add_seq(tb_poll_t reg, tb_event_t ev, uint64_t chain, uint64_t seq,
+                    uint64_t token) {
   Registry *r = reinterpret_cast<Registry *>(reg);
   if (!r || !ev) return TB_E_INVALID;
-  PollNode *n = new (std::nothrow) PollNode{E(ev), chain, token, nullptr};
+  PollNode *n = new (std::nothrow) PollNode{E(ev), chain, token, seq, nullptr};
   if (!n) return TB_E_NOMEM;
   PollNode *head = r->inbox.load(std::memory_order_relaxed);
   do {
@@ -484,7 +501,7 @@ int tb_poll_add(tb_poll_t reg, tb_event_t ev, uint64_t chain, uint64_t token) {
   return TB_OK;
 }
 
-int tb_poll(tb_poll_t reg, uint64_t *fired, int cap, int *nfired) {
+int tb_poll(tb_poll_t reg, uint64_t *fired, int32_t *status, int cap, int *nfired) {
   Registry *r = reinterpret_cast<Registry *>(reg);
   if (!r || !nfired || cap < 0 || (cap > 0 && !fired)) return TB_E_INVALID;
   *nfired = 0;
@@ -501,9 +518,11 @@ int tb_poll(tb_poll_t reg, uint64_t *fired, int cap, int *nfired) {
     size_t keep = 0;
     for (size_t i = 0; i < u.size(); ++i) {
       PollNode *p = u[i];
-      // Errors are surfaced as completion: the waiting future must not hang;
-      // the CUDA error stays sticky for the next synchronous call to report.
-      if (n < cap && cudaEventQuery(p->ev) != cudaErrorNotReady) {
+      // A device fault fires the entry with its error code (status), so
+      // the waiting future faults instead of hanging or reading garbage.
+      const cudaError_t q = n < cap ? cudaEventQuery(p->ev) : cudaErrorNotReady;
+      if (q != cudaErrorNotReady) {
+        if (status) status[n] = q == cudaSuccess ? 0 : -(int)q;
         fired[n++] = p->token;
         delete p;
       } else {
@@ -515,7 +534,10 @@ int tb_poll(tb_poll_t reg, uint64_t *fired, int cap, int *nfired) {
   // Chains: pop completed heads; the first incomplete head blocks the chain.
   for (auto it = r->chains.begin(); it != r->chains.end();) {
     std::deque<PollNode *> &dq = it->second;
-    while (!dq.empty() && n < cap && cudaEventQuery(dq.front()->ev) != cudaErrorNotReady) {
+    while (!dq.empty() && n < cap) {
+      const cudaError_t q = cudaEventQuery(dq.front()->ev);
+      if (q == cudaErrorNotReady) break;
+      if (status) status[n] = q == cudaSuccess ? 0 : -(int)q;
       fired[n++] = dq.front()->token;
       delete dq.front();
       dq.pop_front();
@@ -552,7 +574,8 @@ int tb_poll_drain(tb_poll_t reg, uint64_t *tokens, uint8_t *complete, int cap,
   auto take = [&](PollNode *p) -> bool {
     if (k >= cap) return false;
     tokens[k] = p->token;
-    complete[k] = cudaEventQuery(p->ev) != cudaErrorNotReady ? 1 : 0;
+    const cudaError_t q = cudaEventQuery(p->ev);
+    complete[k] = q == cudaSuccess ? 1 : (q == cudaErrorNotReady ? 0 : 2);
     ++k;
     delete p;
     return true;
@@ -618,12 +641,12 @@ int tb_host_task(tb_htq_t q, tb_event_t ev, uint64_t token) {
   if (r != TB_OK) return r;
   HtItem *it = new (std::nothrow) HtItem{h, token};
   if (!it) return TB_E_NOMEM;
-  r = rc(cudaLaunchHostFunc(side, ht_trampoline, it));
+  r = rc(cudaStreamAddCallback(side, ht_trampoline, it, 0));
   if (r != TB_OK) delete it;
   return r;
 }
 
-int tb_htq_next(tb_htq_t q, uint64_t *token, int64_t timeout_us) {
+int tb_htq_next(tb_htq_t q, uint64_t *token, int *status, int64_t timeout_us) {
   Htq *h = reinterpret_cast<Htq *>(q);
   if (!h || !token) return TB_E_INVALID;
   std::unique_lock<std::mutex> lk(h->mu);
@@ -631,7 +654,8 @@ int tb_htq_next(tb_htq_t q, uint64_t *token, int64_t timeout_us) {
     h->cv.wait_for(lk, std::chrono::microseconds(timeout_us),
                    [&] { return !h->ready.empty() || h->closed; });
   if (!h->ready.empty()) {
-    *token = h->ready.front();
+    *token = h->ready.front().first;
+    if (status) *status = h->ready.front().second;
     h->ready.pop_front();
     return TB_OK;
   }

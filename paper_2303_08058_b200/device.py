@@ -135,14 +135,16 @@ class DeviceEvent:
     first observed (the device does not timestamp it).
     """
 
-    __slots__ = ("id", "native_handle", "chain", "completion_time", "_done", "__weakref__")
+    __slots__ = ("id", "native_handle", "chain", "seq", "completion_time", "_done",
+                 "__weakref__")
 
     _ids = itertools.count()
 
-    def __init__(self, handle: int, chain: int = 0):
+    def __init__(self, handle: int, chain: int = 0, seq: int = 0):
         self.id = next(DeviceEvent._ids)
         self.native_handle = handle
         self.chain = chain          # the in-order stream it was recorded on
+        self.seq = seq              # record order on that stream (1, 2, ...)
         self.completion_time: Optional[float] = None
         self._done = False
 
@@ -239,7 +241,7 @@ def _host_ptr(host, buf: Optional[DeviceBuffer]) -> int:
 class DeviceQueue:
     """In-order queue = one non-blocking CUDA stream (src/device.py:157-180)."""
 
-    __slots__ = ("device", "id", "stream", "_submit_count", "_lock")
+    __slots__ = ("device", "id", "stream", "_submit_count", "_record_count", "_lock")
 
     def __init__(self, device: "CudaDevice", queue_id: int):
         self.device = device
@@ -248,6 +250,7 @@ class DeviceQueue:
         N.call("tb_stream_create", ctypes.byref(h))
         self.stream = h.value
         self._submit_count = 0
+        self._record_count = 0      # events recorded, under _lock (poll-chain order)
         self._lock = threading.Lock()
 
     @property
@@ -412,7 +415,7 @@ class CudaDevice:
             real = issue()
             # hand the recorded CUDA event to the placeholder callers hold
             ev.native_handle, real.native_handle = real.native_handle, 0
-            ev.chain = real.chain
+            ev.chain, ev.seq = real.chain, real.seq
             if op is not None:
                 op.event = ev
 
@@ -469,11 +472,15 @@ class CudaDevice:
 
     # ------------------------------------------------------------ engine --
     def _record(self, queue: DeviceQueue) -> DeviceEvent:
+        """Record an event on ``queue`` (caller holds ``queue._lock``): its
+        sequence number orders it in the poll registry's chain for the
+        stream, whatever order producers register in."""
         h = ctypes.c_uint64(0)
         rc = N.fast().tb_event_record(queue.stream, ctypes.byref(h))
         if rc < 0:
             raise N.CudaError(rc, "tb_event_record")
-        return DeviceEvent(h.value, queue.stream)
+        queue._record_count += 1
+        return DeviceEvent(h.value, queue.stream, queue._record_count)
 
     def _park(self, queue: DeviceQueue, op, issue) -> DeviceEvent:
         ev = DeviceEvent(0)
@@ -557,9 +564,12 @@ class CudaDevice:
                                             staging.hptr, nbytes,
                                             1 if do_barrier else 0, ctypes.byref(h))
             queue._submit_count += 4 if barrier else 3
+            if rc >= 0:
+                queue._record_count += 1
+                seq = queue._record_count
         if rc < 0:
             raise N.CudaError(rc, "tb_agg_launch")
-        ev = DeviceEvent(h.value, queue.stream)
+        ev = DeviceEvent(h.value, queue.stream, seq)
         with self._lock:
             c = self.counters
             c.h2d += 1
@@ -575,9 +585,10 @@ class CudaDevice:
     # -------------------------------------------------------- host tasks --
     def _hosttask_loop(self) -> None:
         tok = ctypes.c_uint64(0)
+        status = ctypes.c_int(0)
         lib = N.blocking()
         while True:
-            rc = lib.tb_htq_next(self._htq, ctypes.byref(tok), 50_000)
+            rc = lib.tb_htq_next(self._htq, ctypes.byref(tok), ctypes.byref(status), 50_000)
             if rc == N.TB_E_CLOSED:
                 return
             if rc != N.TB_OK:
@@ -591,7 +602,13 @@ class CudaDevice:
             if entry is None:
                 continue
             try:
-                entry[0]()
+                if status.value < 0:
+                    # the device faulted before the event: fault the future
+                    # (src/executors.py:50-55), never run the completion
+                    if entry[1] is not None:
+                        entry[1](N.CudaError(status.value, "device fault before host task"))
+                else:
+                    entry[0]()
             except BaseException:  # noqa: BLE001 - callback faults land in futures
                 pass
             finally:

@@ -26,7 +26,7 @@ class MachineConfig(ctypes.Structure):
     _fields_ = [(name, ctypes.c_int64) for name in (
         "subgrids", "steps", "chains", "kernels_per_chain", "workers", "executors",
         "max_agg", "mode", "inject_barriers", "barrier_elision", "task_subgrids",
-        "hosttask_threads", "zero_copy")]
+        "hosttask_threads", "zero_copy", "fault_at_launch")]
 
 
 class MachineStep(ctypes.Structure):
@@ -36,26 +36,49 @@ class MachineStep(ctypes.Structure):
             "launches", "transfers", "event_waits", "full", "idle", "members")]
 
 
+ZERO_COPY_GATHER = 2
+
+
 def run_native(subgrids: int, steps: int, workers: int = 8, executors: int = 32,
                max_agg: int = 8, mode: IntegrationMode = IntegrationMode.POLLING,
                inject_barriers: bool = True, barrier_elision: bool = False,
                task_subgrids: int = 1, hosttask_threads: int = 2, device: int = 0,
                chains: int = 3, kernels_per_chain: int = 5,
-               return_cells: bool = False, zero_copy: bool = False):
+               return_cells: bool = False, zero_copy=False, fault_at_launch: int = 0,
+               cells: Optional[np.ndarray] = None, exec_stats: Optional[np.ndarray] = None):
     """Run the machine natively; returns (ScenarioResult, cells or None).
-    ``zero_copy``: each batch's kernel works in place on its pinned staging
-    buffer (one launch + one event per batch instead of H2D ; kernel ; D2H)."""
+
+    ``zero_copy``: False/0 = the reference op sequence per batch (H2D ;
+    kernel ; D2H); True/1 = the batch kernel works in place on its pinned
+    staging buffer; 2 (ZERO_COPY_GATHER) = no staging: the tasks' buffers
+    live in pinned memory and the batch kernel reads and writes each member
+    where it lives. ``cells`` ([subgrids, 512] float64, C-contiguous):
+    start from (and write the final state back into) these cells instead of
+    the closed-form initial state. ``fault_at_launch`` (tests): the k-th
+    batch launch traps; the device fault surfaces as a raised CudaError.
+    ``exec_stats`` (with ``cells``): int64 [steps, executors, max_agg + 3]
+    receiving per-executor batch-size histograms and full/idle counts."""
     N.init(device)
     cfg = MachineConfig(subgrids, steps, chains, kernels_per_chain, workers, executors,
                         max_agg, _MODES[mode], int(inject_barriers), int(barrier_elision),
-                        task_subgrids, hosttask_threads, int(zero_copy))
+                        task_subgrids, hosttask_threads, int(zero_copy), int(fault_at_launch))
     out = (MachineStep * max(steps, 1))()
     cs = ctypes.c_double(0.0)
-    cells: Optional[np.ndarray] = None
-    if return_cells:
-        cells = np.empty((subgrids, 512))
-    N.call("tb_machine_run", ctypes.addressof(cfg), ctypes.addressof(cs),
-           ctypes.addressof(out), None if cells is None else cells.ctypes.data)
+    if cells is not None:
+        if (cells.dtype != np.float64 or cells.shape != (subgrids, 512)
+                or not cells.flags.c_contiguous or not cells.flags.writeable):
+            raise ValueError("cells must be a writable C-contiguous float64 [subgrids, 512]")
+        if exec_stats is not None and (exec_stats.dtype != np.int64 or exec_stats.shape != (
+                steps, executors, max_agg + 3) or not exec_stats.flags.c_contiguous):
+            raise ValueError("exec_stats must be C-contiguous int64 [steps, executors, max_agg+3]")
+        N.call("tb_machine_run_cells", ctypes.addressof(cfg), cells.ctypes.data,
+               ctypes.addressof(cs), ctypes.addressof(out),
+               None if exec_stats is None else exec_stats.ctypes.data)
+    else:
+        if return_cells:
+            cells = np.empty((subgrids, 512))
+        N.call("tb_machine_run", ctypes.addressof(cfg), ctypes.addressof(cs),
+               ctypes.addressof(out), None if cells is None else cells.ctypes.data)
     per_step = []
     for k in range(steps):
         o = out[k]
@@ -65,13 +88,13 @@ def run_native(subgrids: int, steps: int, workers: int = 8, executors: int = 32,
             reasons_idle=o.idle, event_waits=o.event_waits))
         per_step[-1].mean_batch = o.members / max(o.full + o.idle, 1)
     return ScenarioResult(per_step=per_step, checksum=cs.value,
-                          dts=[o.dt for o in out[:steps]]), cells
+                          dts=[o.dt for o in out[:steps]], engine="native"), cells
 
 
 def run_native_hydro(state: np.ndarray, steps: int, workers: int = 8, executors: int = 32,
                      max_agg: int = 8, mode: IntegrationMode = IntegrationMode.POLLING,
                      task_subgrids: int = 1, hosttask_threads: int = 2, device: int = 0,
-                     cfl: float = 0.4, gamma: float = 5.0 / 3.0):
+                     cfl: float = 0.4, gamma: float = 5.0 / 3.0, fault_at_launch: int = 0):
     """The machine on the north_star's hydro kernel (tb_machine_run_hydro):
     per step one task per ``task_subgrids`` sub-grids does the periodic ghost
     exchange on the host and schedules an aggregated K6 request; completion
@@ -81,7 +104,7 @@ def run_native_hydro(state: np.ndarray, steps: int, workers: int = 8, executors:
     st = np.ascontiguousarray(state, dtype=np.float64)
     S = st.shape[0]
     cfg = MachineConfig(S, steps, 0, 1, workers, executors, max_agg, _MODES[mode], 0, 0,
-                        task_subgrids, hosttask_threads)
+                        task_subgrids, hosttask_threads, 0, int(fault_at_launch))
     out = (MachineStep * max(steps, 1))()
     final = np.empty_like(st)
     N.call("tb_machine_run_hydro", ctypes.addressof(cfg), st.ctypes.data, final.ctypes.data,

@@ -60,6 +60,7 @@ class PollRegistry:
         self._tokens: Dict[int, EventCallback] = {}
         self._next_token = itertools.count(1)
         self._fired_buf = None
+        self._status_buf = None
 
     # ------------------------------------------------------------- config --
     def set_activity_hooks(self, enter, exit) -> None:
@@ -76,6 +77,7 @@ class PollRegistry:
                     h = ctypes.c_uint64(0)
                     N.call("tb_poll_create", ctypes.byref(h))
                     self._fired_buf = (ctypes.c_uint64 * _FIRE_CAP)()
+                    self._status_buf = (ctypes.c_int32 * _FIRE_CAP)()
                     self._native = h.value
         return self._native
 
@@ -85,7 +87,8 @@ class PollRegistry:
             reg = self._native_reg()
             token = next(self._next_token)
             self._tokens[token] = ec
-            rc = N.fast().tb_poll_add(reg, handle, getattr(ec.event, "chain", 0), token)
+            rc = N.fast().tb_poll_add_seq(reg, handle, getattr(ec.event, "chain", 0),
+                                          getattr(ec.event, "seq", 0), token)
             if rc != 0:
                 del self._tokens[token]
                 raise N.CudaError(rc, "tb_poll_add")
@@ -138,26 +141,50 @@ class PollRegistry:
             self._guard.release()
         return fired
 
+    def _fault(self, ec: EventCallback, error: BaseException) -> None:
+        """A device fault behind ``ec``'s event: its future faults (the
+        callback, which would read the op's garbage outputs, never runs)."""
+        if ec.on_abandon is not None:
+            try:
+                ec.on_abandon(error)
+            except BaseException:  # noqa: BLE001
+                pass
+
     def _poll_native(self) -> int:
         n = ctypes.c_int(0)
-        buf = self._fired_buf
+        buf, status = self._fired_buf, self._status_buf
         # GIL held: the native body never blocks, and releasing the GIL here
         # would let a busy worker keep it for a whole switch interval.
-        rc = N.fast().tb_poll(self._native, buf, _FIRE_CAP, ctypes.byref(n))
+        rc = N.fast().tb_poll(self._native, buf, status, _FIRE_CAP, ctypes.byref(n))
         if rc < 0:
             raise N.CudaError(rc, "tb_poll")
         k = n.value
         pop = self._tokens.pop
         for i in range(k):
-            self._run(pop(buf[i]))
+            ec = pop(buf[i])
+            if status[i] < 0:
+                self._fault(ec, N.CudaError(status[i], "device fault before event"))
+            else:
+                self._run(ec)
         return k
+
+    def _complete(self, ec: EventCallback):
+        """True/False = event complete or not; None = the query faulted (the
+        entry is then faulted and dropped)."""
+        try:
+            return ec.event.is_complete()
+        except BaseException as e:  # noqa: BLE001 - device fault
+            self._fault(ec, e)
+            return None
 
     def _poll_python(self) -> int:
         fired = 0
         still = []
         for ec in self._pending:                 # older registrations first
-            if ec.event.is_complete():
+            done = self._complete(ec)
+            if done:
                 self._run(ec)
+            if done is not False:
                 fired += 1
             else:
                 still.append(ec)
@@ -166,8 +193,10 @@ class PollRegistry:
                 ec = self._inbox.popleft()
             except IndexError:
                 break
-            if ec.event.is_complete():
+            done = self._complete(ec)
+            if done:
                 self._run(ec)
+            if done is not False:
                 fired += 1
             else:
                 still.append(ec)
@@ -178,11 +207,11 @@ class PollRegistry:
     def abandon_all(self, error: BaseException) -> int:
         abandoned = 0
         with self._guard:
-            entries = [(ec, ec.event.is_complete()) for ec in self._pending]
+            entries = [(ec, self._complete(ec)) for ec in self._pending]
             self._pending = []
             while self._inbox:
                 ec = self._inbox.popleft()
-                entries.append((ec, ec.event.is_complete()))
+                entries.append((ec, self._complete(ec)))
             if self._native is not None:
                 cap = max(1, len(self._tokens))
                 toks = (ctypes.c_uint64 * cap)()
@@ -190,8 +219,15 @@ class PollRegistry:
                 n = ctypes.c_int(0)
                 N.call("tb_poll_drain", self._native, toks, done, cap, ctypes.byref(n))
                 for i in range(n.value):
-                    entries.append((self._tokens.pop(toks[i]), bool(done[i])))
+                    ec = self._tokens.pop(toks[i])
+                    if done[i] == 2:        # the device faulted before it
+                        self._fault(ec, N.CudaError(-1, "device fault before event"))
+                        entries.append((ec, None))
+                    else:
+                        entries.append((ec, bool(done[i])))
             for ec, complete in entries:
+                if complete is None:            # faulted above
+                    continue
                 if complete:
                     self._run(ec)
                     continue

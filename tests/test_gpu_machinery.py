@@ -70,7 +70,8 @@ def stacks():
 def run(stack, subgrids, steps):
     sc = build_scenario(ScenarioConfig(subgrids=subgrids, steps=steps))
     by_grid = [stack.aggs[i % len(stack.aggs)] for i in range(subgrids)]
-    return sc, run_scenario(sc, stack.runtime, stack.device, stack.aggs, by_grid)
+    return sc, run_scenario(sc, stack.runtime, stack.device, stack.aggs, by_grid,
+                            engine="python")
 
 
 @pytest.mark.parametrize("mode", MODES)
@@ -416,7 +417,7 @@ def test_lazy_device_machine_golden(golden, mode):
             for k in range(5):
                 a.register_kind(k, kernel_transform(k))
         sc = build_scenario(ScenarioConfig(subgrids=8, steps=2))
-        res = run_scenario(sc, rt, d, aggs, [aggs[i % 2] for i in range(8)])
+        res = run_scenario(sc, rt, d, aggs, [aggs[i % 2] for i in range(8)], engine="python")
         assert res.checksum == fx(golden["reference_test_literals"]["GOLDEN_8X2"])
     finally:
         rt.shutdown()

@@ -96,3 +96,47 @@ def test_native_machine_zero_copy_goldens(golden, mode):
     for m in res.per_step:
         assert m.launches == 8 * 15 and m.transfers == 0
     assert res.checksum == fx(lit["GOLDEN_8X2"])
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_native_machine_gather_mode_goldens(golden, mode):
+    # zero_copy = 2: members read and written in the tasks' pinned arena
+    res, cells = run_native(16, 3, workers=4, executors=3, max_agg=4, mode=mode,
+                            return_cells=True, zero_copy=2)
+    assert res.checksum.hex() == golden["machine"]["16x3"]["checksum"]
+    want = np.load(__import__("conftest").TESTS + "/golden/cells.npz")["cells_16x3"]
+    np.testing.assert_array_equal(cells, want)
+    for m in res.per_step:
+        assert m.transfers == 0 and m.launches > 0
+
+
+@pytest.mark.parametrize("zc", [0, 2])
+def test_native_machine_runs_on_caller_cells(zc):
+    rng = np.random.default_rng(7)
+    start = rng.random((40, 512))
+    cells = start.copy()
+    res, _ = run_native(40, 2, workers=4, executors=4, max_agg=8, cells=cells, zero_copy=zc)
+    want = start
+    pieces = []
+    for _ in range(2):
+        want, mins, sums = mo.step_cells(want)
+        pieces.append(__import__("math").fsum(sums.tolist()))
+    np.testing.assert_array_equal(cells, want)
+    assert [m.checksum_piece for m in res.per_step] == pieces
+
+
+# BASELINE config 4 (max_level 5 = 32768 sub-grids) with the reference task
+# structure (one task and 15 schedule() calls per sub-grid per step):
+# every completion mode reproduces run_reference(32768, 1).
+C4_KW = dict(workers=8, executors=32, max_agg=64)
+
+
+@pytest.mark.parametrize("zc", [0, 2])
+@pytest.mark.parametrize("mode", MODES)
+def test_native_machine_c4_golden_every_mode(golden, mode, zc):
+    g = golden["run_reference"]["32768x1"]
+    res, _ = run_native(32768, 1, mode=mode, zero_copy=zc, **C4_KW)
+    assert res.checksum.hex() == g["checksum"]
+    assert [d.hex() for d in res.dts] == g["dts"]
+    m = res.per_step[0]
+    assert round(m.mean_batch * (m.reasons_full + m.reasons_idle)) == 32768 * 15

@@ -68,7 +68,7 @@ def test_poll_registry_lifecycle_without_gpu(lib):
     assert f.tb_poll_pending(h.value, ctypes.byref(n)) == 0 and n.value == 0
     fired = (ctypes.c_uint64 * 4)()
     k = ctypes.c_int(-1)
-    assert f.tb_poll(h.value, fired, 4, ctypes.byref(k)) == 0 and k.value == 0
+    assert f.tb_poll(h.value, fired, None, 4, ctypes.byref(k)) == 0 and k.value == 0
     hw = ctypes.c_int(0)
     assert f.tb_poll_entry_high_water(h.value, ctypes.byref(hw)) == 0 and hw.value == 1
     assert f.tb_poll_destroy(h.value) == 0
