@@ -17,7 +17,7 @@ def test_defaults_match_reference():
 
 
 @pytest.mark.parametrize("argv", [["--workers", "0"], ["--executors", "x"],
-                                  ["--integration", "magic"], ["--clock", "virtual"],
+                                  ["--integration", "magic"], ["--clock", "sundial"],
                                   ["--watchdog", "-1"], ["--nope"]])
 def test_usage_errors_exit_1(argv):
     with pytest.raises(SystemExit) as e:
@@ -42,7 +42,7 @@ def _fake_cell(cfg, ms, checksum=1.5):
 
 
 def test_matrix_adds_fence_twin_and_formats(monkeypatch, tmp_path):
-    def fake_run_cell(cfg):
+    def fake_run_cell(cfg, devices=None):
         return _fake_cell(cfg, 10.0 if cfg.integration is IntegrationMode.FENCE else 5.0)
 
     monkeypatch.setattr(cli, "run_cell", fake_run_cell)
@@ -64,24 +64,30 @@ def test_matrix_adds_fence_twin_and_formats(monkeypatch, tmp_path):
 
 
 def test_exit_codes(monkeypatch, tmp_path):
-    monkeypatch.setattr(cli, "run_cell", lambda cfg: _fake_cell(cfg, 1.0))
+    monkeypatch.setattr(cli, "run_cell", lambda cfg, devices=None: _fake_cell(cfg, 1.0))
     assert cli.main(["--out", str(tmp_path / "a.csv")]) == cli.EXIT_OK
 
-    def boom(cfg):
+    def boom(cfg, devices=None):
         raise RuntimeError("cell died")
 
     monkeypatch.setattr(cli, "run_cell", boom)
     assert cli.main(["--out", str(tmp_path / "b.csv")]) == cli.EXIT_RUN_FAILED
 
-    monkeypatch.setattr(cli, "run_cell", lambda cfg: _fake_cell(cfg, 1.0, float(cfg.workers)))
+    monkeypatch.setattr(cli, "run_cell", lambda cfg, devices=None: _fake_cell(cfg, 1.0, float(cfg.workers)))
     assert cli.main(["--sweep", "workers", "--out", str(tmp_path / "c.csv")]) == \
         cli.EXIT_CHECKSUM
 
-    def interrupt(cfg):
+    def interrupt(cfg, devices=None):
         raise KeyboardInterrupt
 
     monkeypatch.setattr(cli, "run_cell", interrupt)
     assert cli.main(["--out", str(tmp_path / "d.csv")]) == cli.EXIT_INTERRUPTED
-    monkeypatch.setattr(cli, "run_cell", lambda cfg: _fake_cell(cfg, 1.0))
+    monkeypatch.setattr(cli, "run_cell", lambda cfg, devices=None: _fake_cell(cfg, 1.0))
     assert cli.main(["--out", str(tmp_path / "no" / "such" / "dir.csv")]) == \
         cli.EXIT_RUN_FAILED
+
+
+def test_virtual_clock_without_simulator_is_a_usage_error(tmp_path):
+    # the CUDA device runs on the real clock; --clock virtual needs the
+    # simulator double injected (tests/test_virtual_clock.py)
+    assert cli.main(["--clock", "virtual", "--out", str(tmp_path / "v.csv")]) == cli.EXIT_USAGE
