@@ -115,6 +115,12 @@ int tb_event_query(tb_event_t ev);
  * (the FENCE baseline). */
 int tb_event_wait(tb_event_t ev);
 int tb_event_release(tb_event_t ev);
+/* VirtualDevice(record_timeline=True) (src/device.py:223-224,512-514): a
+ * timing-enabled event (not pooled) recorded on s; tb_tevent_elapsed gives
+ * the ms from a to b once both completed (TB_NOT_READY before). */
+int tb_tevent_record(tb_stream_t s, tb_event_t *ev);
+int tb_tevent_elapsed(tb_event_t a, tb_event_t b, double *ms);
+int tb_tevent_release(tb_event_t ev);
 int tb_stream_wait_event(tb_stream_t s, tb_event_t ev);
 /* VirtualDevice(event_pool=...) (src/device.py:221,410-411): 1 = recycle
  * events through the pool, 0 = create/destroy per record (ablation). */

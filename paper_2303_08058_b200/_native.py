@@ -104,6 +104,9 @@ SIGNATURES = {
     "tb_event_query": [_u64],
     "tb_event_wait": [_u64],
     "tb_event_release": [_u64],
+    "tb_tevent_record": [_u64, _pu64],
+    "tb_tevent_elapsed": [_u64, _u64, ctypes.POINTER(ctypes.c_double)],
+    "tb_tevent_release": [_u64],
     "tb_stream_wait_event": [_u64, _u64],
     "tb_event_pool_set": [_int],
     "tb_event_pool_stats": [_pi64, _pi64, _pi64],

@@ -33,6 +33,8 @@
 #include <unordered_map>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/tb.h"
 #include "tb_internal.h"
 
@@ -200,6 +202,10 @@ class Poller {
     if (waiting_.load(std::memory_order_relaxed) == 0) return 0;
     std::unique_lock<std::mutex> guard(body_, std::try_to_lock);
     if (!guard.owns_lock()) return 0;
+    struct Range {   // NVTX range over the poll body (profilers only)
+      Range() { nvtxRangePushA("machine poll body"); }
+      ~Range() { nvtxRangePop(); }
+    } range;
     {
       std::lock_guard<std::mutex> g(inbox_mu_);
       for (const Entry &e : inbox_) chains_[e.chain].push_back(e);
@@ -559,6 +565,10 @@ void batch_done(void *p) {   // AggregationExecutor finish (src/executors.py:286
 }
 
 void launch(Batch *b, bool idle) {   // src/executors.py:257-284 as one launch
+  struct Range {   // NVTX range over the batch launch (profilers only)
+    Range() { nvtxRangePushA("machine batch launch"); }
+    ~Range() { nvtxRangePop(); }
+  } range;
   Executor *ex = b->ex;
   Machine *m = ex->m;
   b->idle = idle;

@@ -26,6 +26,8 @@
 #include <unordered_map>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/tb.h"
 #include "tb_internal.h"
 
@@ -312,6 +314,38 @@ int tb_event_record(tb_stream_t s, tb_event_t *ev) {
   return TB_OK;
 }
 
+// Timing events for CudaDevice(record_timeline=True): created per record
+// (not pooled — a diagnostic mode), destroyed on release.
+int tb_tevent_record(tb_stream_t s, tb_event_t *ev) {
+  if (!ev) return TB_E_INVALID;
+  ensure_device();
+  cudaEvent_t e;
+  int r = rc(cudaEventCreate(&e));
+  if (r != TB_OK) return r;
+  r = rc(cudaEventRecord(e, S(s)));
+  if (r != TB_OK) {
+    cudaEventDestroy(e);
+    return r;
+  }
+  *ev = reinterpret_cast<tb_event_t>(e);
+  return TB_OK;
+}
+
+int tb_tevent_elapsed(tb_event_t a, tb_event_t b, double *ms) {
+  if (!a || !b || !ms) return TB_E_INVALID;
+  const cudaError_t qa = cudaEventQuery(E(a)), qb = cudaEventQuery(E(b));
+  if (qa == cudaErrorNotReady || qb == cudaErrorNotReady) return TB_NOT_READY;
+  float f = 0.f;
+  const int r = rc(cudaEventElapsedTime(&f, E(a), E(b)));
+  if (r == TB_OK) *ms = (double)f;
+  return r;
+}
+
+int tb_tevent_release(tb_event_t ev) {
+  if (!ev) return TB_E_INVALID;
+  return rc(cudaEventDestroy(E(ev)));
+}
+
 int tb_event_query(tb_event_t ev) {
   const cudaError_t e = cudaEventQuery(E(ev));
   if (e == cudaErrorNotReady) return TB_NOT_READY;
@@ -441,11 +475,13 @@ int tb_agg_launch(tb_stream_t s, int op, int kind, double c1, double c2,
                   tb_event_t *done) {
   if (!dbuf || !hbuf || !done || (nbytes % sizeof(double)) != 0) return TB_E_INVALID;
   ensure_device();
+  nvtxRangePushA("tb_agg_launch");
   int r = tb_memcpy_h2d(s, dbuf, hbuf, nbytes);
   if (r == TB_OK) r = tb_launch(s, op, kind, c1, c2, dbuf, (int64_t)(nbytes / 8));
   if (r == TB_OK && barrier) r = tb_barrier(s);
   if (r == TB_OK) r = tb_memcpy_d2h(s, hbuf, dbuf, nbytes);
   if (r == TB_OK) r = tb_event_record(s, done);
+  nvtxRangePop();
   return r;
 }
 
@@ -506,6 +542,7 @@ int tb_poll(tb_poll_t reg, uint64_t *fired, int32_t *status, int cap, int *nfire
   if (!r || !nfired || cap < 0 || (cap > 0 && !fired)) return TB_E_INVALID;
   *nfired = 0;
   if (r->guard.exchange(true, std::memory_order_acquire)) return TB_NOT_READY;
+  nvtxRangePushA("tb_poll");
   const int e = r->entries.fetch_add(1) + 1;
   int hw = r->high_water.load();
   while (e > hw && !r->high_water.compare_exchange_weak(hw, e)) {
@@ -551,6 +588,7 @@ int tb_poll(tb_poll_t reg, uint64_t *fired, int32_t *status, int cap, int *nfire
   *nfired = n;
   r->entries.fetch_sub(1);
   r->guard.store(false, std::memory_order_release);
+  nvtxRangePop();
   return TB_OK;
 }
 

@@ -287,7 +287,12 @@ class CudaDevice:
     on the queue tail, src/device.py:419-432); ``event_pool`` toggles libtb's
     event pool (src/device.py:221,410-411). Host tasks are dispatched by
     ``hosttask_threads`` Python threads named ``tb-hosttask-i`` fed by libtb's
-    host-task queue (cudaLaunchHostFunc on side streams).
+    host-task queue (stream callbacks on side streams). ``record_timeline``
+    brackets every op with CUDA timing events and exposes the reference's
+    (queue, index, kind, start, completion) rows as ``timeline``.
+    ``latency`` and ``hosttask_dispatch_cost`` belong to the reference's
+    simulator (the hardware has its own) and are ignored; the virtual clock
+    lives in the CPU test double (tests/virtual_device.py).
     """
 
     def __init__(self, device_index: int = 0, compute_slots: int = 16,
@@ -314,13 +319,26 @@ class CudaDevice:
         self._held: list = []            # (queue, op, placeholder event, issue fn)
         self.event_pool = event_pool
         self.record_timeline = record_timeline
-        self.timeline: list = []
+        self._timeline_rows: list = []      # resolved (queue, index, kind, start, completion)
+        self._timeline_pending: list = []   # (queue id, index, kind, start ev, end ev)
+        self._epoch = 0
         self.counters = _Counters()
         self._lock = threading.Lock()
         self._alive = True
         self._queues: list = []
         self._buffer_ids = itertools.count()
         self._buffers: list = []
+        if record_timeline:
+            # the timeline's t = 0: a timing event on a private stream; op
+            # times are elapsed times from it (seconds, like the reference's
+            # virtual clock, src/device.py:223-224,512-514)
+            h = ctypes.c_uint64(0)
+            N.call("tb_stream_create", ctypes.byref(h))
+            self._epoch_stream = h.value
+            e = ctypes.c_uint64(0)
+            N.call("tb_tevent_record", self._epoch_stream, ctypes.byref(e))
+            N.call("tb_stream_sync", self._epoch_stream)
+            self._epoch = e.value
         # host tasks
         h = ctypes.c_uint64(0)
         N.call("tb_htq_create", hosttask_side_streams, ctypes.byref(h))
@@ -463,12 +481,56 @@ class CudaDevice:
         N.call("tb_htq_destroy", self._htq)
         try:
             N.call("tb_device_sync")
+            if self.record_timeline:
+                for *_, a, b in self._timeline_pending:
+                    N.fast().tb_tevent_release(a)
+                    N.fast().tb_tevent_release(b)
+                self._timeline_pending = []
+                N.fast().tb_tevent_release(self._epoch)
+                N.call("tb_stream_destroy", self._epoch_stream)
         finally:
             for q in self._queues:
                 N.call("tb_stream_destroy", q.stream)
             for b in self._buffers:
                 b.free()
             self._buffers.clear()
+
+    # ---------------------------------------------------------- timeline --
+    @property
+    def timeline(self) -> list:
+        """(queue, index, kind, start, completion) per completed op, seconds
+        from the device's creation, in completion order — the reference's
+        record_timeline rows (src/device.py:512-514), from CUDA timing events
+        recorded around every op."""
+        if not self.record_timeline:
+            return []
+        with self._lock:
+            pending, self._timeline_pending = self._timeline_pending, []
+            keep = []
+            ms0, ms1 = ctypes.c_double(0.0), ctypes.c_double(0.0)
+            for row in pending:
+                qid, idx, kind, a, b = row
+                r0 = N.fast().tb_tevent_elapsed(self._epoch, a, ctypes.byref(ms0))
+                r1 = N.fast().tb_tevent_elapsed(self._epoch, b, ctypes.byref(ms1))
+                if r0 == N.TB_NOT_READY or r1 == N.TB_NOT_READY:
+                    keep.append(row)
+                    continue
+                if r0 < 0 or r1 < 0:
+                    raise N.CudaError(min(r0, r1), "tb_tevent_elapsed")
+                self._timeline_rows.append((qid, idx, kind, ms0.value * 1e-3, ms1.value * 1e-3))
+                N.fast().tb_tevent_release(a)
+                N.fast().tb_tevent_release(b)
+            self._timeline_pending = keep + self._timeline_pending
+            self._timeline_rows.sort(key=lambda r: (r[4], r[0], r[1]))
+            return list(self._timeline_rows)
+
+    def _mark(self, queue: DeviceQueue) -> int:
+        """A timing event on ``queue`` now (record_timeline only)."""
+        e = ctypes.c_uint64(0)
+        rc = N.fast().tb_tevent_record(queue.stream, ctypes.byref(e))
+        if rc < 0:
+            raise N.CudaError(rc, "tb_tevent_record")
+        return e.value
 
     # ------------------------------------------------------------ engine --
     def _record(self, queue: DeviceQueue) -> DeviceEvent:
@@ -508,6 +570,7 @@ class CudaDevice:
             op.index = queue._submit_count
             queue._submit_count += 1
             k = op.kind
+            t0 = self._mark(queue) if self.record_timeline else 0
             if k is OpKind.KERNEL:
                 if op.spin_ns:
                     N.call("tb_spin", s, op.spin_ns)
@@ -540,6 +603,12 @@ class CudaDevice:
             else:
                 with self._lock:
                     c.dummies += 1
+            if self.record_timeline and not (k is OpKind.BARRIER and self.barrier_elision):
+                t1 = self._mark(queue)
+                with self._lock:
+                    self._timeline_pending.append((queue.id, op.index, k.value, t0, t1))
+            elif t0:
+                N.fast().tb_tevent_release(t0)
             op.event = self._record(queue)
         return op.event
 
@@ -554,10 +623,50 @@ class CudaDevice:
                 queue, kernel, staging, nbytes, barrier))
         return self._issue_batch(queue, kernel, staging, nbytes, barrier)
 
+    def _issue_batch_timed(self, queue: DeviceQueue, kernel: DeviceKernel,
+                           staging: DeviceBuffer, nbytes: int, barrier: bool,
+                           do_barrier: bool) -> int:
+        """The batch's ops one call each, timing events around each op
+        (record_timeline): one timeline row per op as in the reference
+        (H2D, KERNEL, [BARRIER], D2H: src/executors.py:277-284)."""
+        s = queue.stream
+        ops = [("h2d", lambda: N.call("tb_memcpy_h2d", s, staging.dptr, staging.hptr, nbytes)),
+               ("kernel", lambda: N.call("tb_launch", s, kernel.op, kernel.kind, kernel.c1,
+                                         kernel.c2, staging.dptr, nbytes // 8))]
+        if barrier and do_barrier:
+            ops.append(("barrier", lambda: N.call("tb_barrier", s)))
+        ops.append(("d2h", lambda: N.call("tb_memcpy_d2h", s, staging.hptr, staging.dptr,
+                                          nbytes)))
+        rows = []
+        index = queue._submit_count
+        for kind, issue in ops:
+            if kind == "d2h" and barrier and not do_barrier:
+                index += 1                      # the elided barrier's index
+            start = self._mark(queue)           # each row owns its two events
+            issue()
+            rows.append((queue.id, index, kind, start, self._mark(queue)))
+            index += 1
+        with self._lock:
+            self._timeline_pending.extend(rows)
+        h = ctypes.c_uint64(0)
+        rc = N.fast().tb_event_record(s, ctypes.byref(h))
+        if rc < 0:
+            raise N.CudaError(rc, "tb_event_record")
+        return h.value
+
     def _issue_batch(self, queue: DeviceQueue, kernel: DeviceKernel,
                      staging: DeviceBuffer, nbytes: int, barrier: bool) -> DeviceEvent:
         do_barrier = barrier and not self.barrier_elision
         h = ctypes.c_uint64(0)
+        if self.record_timeline:
+            with queue._lock:
+                h.value = self._issue_batch_timed(queue, kernel, staging, nbytes, barrier,
+                                                  do_barrier)
+                queue._submit_count += 4 if barrier else 3
+                queue._record_count += 1
+                seq = queue._record_count
+            return self._count_batch(DeviceEvent(h.value, queue.stream, seq), barrier,
+                                     do_barrier)
         with queue._lock:
             rc = N.fast().tb_agg_launch(queue.stream, kernel.op, kernel.kind,
                                             kernel.c1, kernel.c2, staging.dptr,
@@ -569,7 +678,9 @@ class CudaDevice:
                 seq = queue._record_count
         if rc < 0:
             raise N.CudaError(rc, "tb_agg_launch")
-        ev = DeviceEvent(h.value, queue.stream, seq)
+        return self._count_batch(DeviceEvent(h.value, queue.stream, seq), barrier, do_barrier)
+
+    def _count_batch(self, ev: DeviceEvent, barrier: bool, do_barrier: bool) -> DeviceEvent:
         with self._lock:
             c = self.counters
             c.h2d += 1

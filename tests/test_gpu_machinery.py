@@ -28,9 +28,11 @@ MODES = [IntegrationMode.POLLING, IntegrationMode.HOSTTASK, IntegrationMode.FENC
 
 class Stack:
     def __init__(self, workers=2, mode=IntegrationMode.POLLING, executors=1, max_agg=4,
-                 inject_barriers=True, barrier_elision=False, register=True):
+                 inject_barriers=True, barrier_elision=False, register=True,
+                 record_timeline=False):
         self.runtime = Runtime(workers, seed=7)
-        self.device = CudaDevice(barrier_elision=barrier_elision)
+        self.device = CudaDevice(barrier_elision=barrier_elision,
+                                 record_timeline=record_timeline)
         self.integration = Integration(self.runtime, self.device, mode)
         self.executors = ExecutorPool(self.integration, executors)
         self.buffers = BufferPool(self.device)
@@ -422,3 +424,46 @@ def test_lazy_device_machine_golden(golden, mode):
     finally:
         rt.shutdown()
         d.destroy()
+
+
+def test_record_timeline_rows_per_op():
+    # VirtualDevice(record_timeline=True) rows (src/device.py:223-224,512-514)
+    # from CUDA timing events around every op
+    from paper_2303_08058_b200.device import make_barrier, make_dummy, make_spin
+    d = CudaDevice(0, record_timeline=True)
+    try:
+        q0, q1 = d.queue(), d.queue()
+        script = [(q0, make_spin(300)), (q1, make_spin(100)), (q0, make_barrier()),
+                  (q1, make_dummy()), (q0, make_spin(50)), (q1, make_spin(200))]
+        for q, op in script:
+            q.submit(op)
+        d.synchronize()
+        rows = d.timeline
+        assert len(rows) == len(script)
+        by_q = {}
+        for qid, idx, kind, start, end in rows:
+            assert 0.0 <= start <= end
+            by_q.setdefault(qid, []).append((idx, kind, start, end))
+        for qid, ops in by_q.items():
+            ops.sort()
+            assert [o[0] for o in ops] == list(range(len(ops)))
+            for a, b in zip(ops, ops[1:]):           # in-order queues
+                assert b[2] >= a[3] - 1e-6
+        spins = [r for r in rows if r[0] == q0.id and r[2] == "kernel"]
+        assert spins[0][4] - spins[0][3] >= 290e-6    # the 300 us spin
+        assert [r[2] for r in sorted(rows) if r[0] == q0.id] == ["kernel", "barrier", "kernel"]
+    finally:
+        d.destroy()
+
+
+def test_record_timeline_through_aggregation(stacks):
+    s = stacks(executors=1, max_agg=4, record_timeline=True)
+    src = np.linspace(0.0, 1.0, 512)
+    futs = [s.aggs[0].schedule(0, src, np.empty(512)) for _ in range(3)]
+    for f in futs:
+        f.result(timeout=30)
+    s.device.synchronize()
+    kinds = [r[2] for r in sorted(s.device.timeline)]
+    # the batch's ops, one row each, plus the idleness probe's marker
+    assert kinds.count("h2d") == kinds.count("d2h") == kinds.count("barrier") >= 1
+    assert kinds.count("dummy") >= 1
