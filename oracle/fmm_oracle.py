@@ -175,16 +175,16 @@ def centres(level: int, idx: np.ndarray) -> np.ndarray:
 
 # ------------------------------------------------------------ upward pass --
 def leaf_moments(rho: np.ndarray) -> np.ndarray:
-    """[N,N,N] density -> [20, N, N, N] leaf multipoles (monopoles)."""
+    """[N,N,N] density -> [1, N, N, N] leaf multipoles: monopoles only (every
+    higher leaf moment is zero about the cell centre, so only the monopole
+    component is stored — max_level 5 would otherwise need 2.7 GB)."""
     N = rho.shape[0]
     h = 1.0 / N
-    M = np.zeros((NC,) + rho.shape)
-    M[0] = rho * (h * h * h)
-    return M
+    return (rho * (h * h * h))[None]
 
 
 def m2m(Mc: np.ndarray) -> np.ndarray:
-    """Children moments [20, 2N, 2N, 2N] -> parent moments [20, N, N, N]."""
+    """Children moments [20 or 1, 2N, 2N, 2N] -> parent moments [20, N, N, N]."""
     n2 = Mc.shape[1]
     hc = 1.0 / n2
     Mp = np.zeros((NC, n2 // 2, n2 // 2, n2 // 2))
@@ -194,7 +194,8 @@ def m2m(Mc: np.ndarray) -> np.ndarray:
         mono = monomials(d.reshape(3, 1))[:, 0]
         sub = Mc[:, cz::2, cy::2, cx::2]
         for t, s, b, c in M2M_TERMS:
-            Mp[t] += (c * mono[b]) * sub[s]
+            if s < sub.shape[0]:           # a monopole-only child level
+                Mp[t] += (c * mono[b]) * sub[s]
     return Mp
 
 
@@ -317,7 +318,9 @@ def solve(rho: np.ndarray, max_level: int, targets: np.ndarray | None = None):
     Lacc = None
     for lev in range(0, max_level):
         anc = targets >> (max_level - lev)
-        Ll = m2l(Ms[lev], lev, anc)
+        # each distinct ancestor once (many targets share one), then scatter
+        uniq, inv = np.unique(anc, axis=1, return_inverse=True)
+        Ll = m2l(Ms[lev], lev, uniq)[:, inv.reshape(-1)]
         if Lacc is not None:
             # child centre - parent centre, per target's ancestor at lev
             hc = 1.0 / lattice(lev)

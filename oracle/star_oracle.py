@@ -68,3 +68,56 @@ def step(U: np.ndarray, max_level: int, gamma: float = 5.0 / 3.0, cfl: float = 0
     U1 = U + dt * L1
     L2, _ = rhs(U1, max_level, gamma)
     return 0.5 * (U + (U1 + dt * L2)), dt
+
+
+# ----------------------------------------------- sampled (full-size) checks --
+# At max_level 3-5 the full oracle step is too slow for a test, but one stage
+# of the step at a few sub-grids needs only those sub-grids' ghosted blocks
+# (hydro) and gravity at their cells (the FMM oracle expands only the
+# targets' ancestors). tests/test_gpu_star.py feeds these the GPU's own state
+# before each stage, so every stage of every step is checked on the samples.
+def ghosted_blocks(U: np.ndarray, subs: np.ndarray) -> np.ndarray:
+    """[k, 5, 12, 12, 12] ghosted blocks (periodic) of sub-grids ``subs`` of
+    the lattice U [5, N, N, N] (sub-grid s = (bz*n + by)*n + bx)."""
+    N = U.shape[1]
+    n = N // NI
+    out = np.empty((len(subs), NF, NI + 4, NI + 4, NI + 4))
+    for k, s in enumerate(subs):
+        bz, by, bx = s // (n * n), (s // n) % n, s % n
+        iz = (np.arange(-2, NI + 2) + NI * bz) % N
+        iy = (np.arange(-2, NI + 2) + NI * by) % N
+        ix = (np.arange(-2, NI + 2) + NI * bx) % N
+        out[k] = U[:, iz][:, :, iy][:, :, :, ix]
+    return out
+
+
+def blocks(U: np.ndarray, subs: np.ndarray) -> np.ndarray:
+    """[k, 5, 8, 8, 8] interiors of sub-grids ``subs``."""
+    return ghosted_blocks(U, subs)[:, :, 2:-2, 2:-2, 2:-2]
+
+
+def sub_targets(N: int, subs: np.ndarray) -> np.ndarray:
+    """Leaf indices (x, y, z) [3, k*512] of the cells of ``subs``, in
+    [k][z][y][x] order."""
+    n = N // NI
+    z, y, x = np.meshgrid(np.arange(NI), np.arange(NI), np.arange(NI), indexing="ij")
+    t = []
+    for s in subs:
+        bz, by, bx = s // (n * n), (s // n) % n, s % n
+        t.append(np.stack([x + NI * bx, y + NI * by, z + NI * bz]).reshape(3, -1))
+    return np.concatenate(t, axis=1)
+
+
+def sampled_rhs(U: np.ndarray, max_level: int, subs: np.ndarray, gamma: float = 5.0 / 3.0):
+    """L(U) at the cells of sub-grids ``subs`` -> ([k, 5, 8, 8, 8], amax [k],
+    g [3, k, 8, 8, 8]) — rhs() restricted to the samples."""
+    N = U.shape[1]
+    du, amax = ho.hydro_flux(ghosted_blocks(U, subs), 1.0 / N, gamma)
+    g = fo.solve(U[0], max_level, sub_targets(N, subs))[1:]
+    g = g.reshape(3, len(subs), NI, NI, NI)
+    u = blocks(U, subs)
+    L = du.copy()
+    for c in range(3):
+        L[:, 1 + c] = du[:, 1 + c] + u[:, 0] * g[c]
+    L[:, 4] = du[:, 4] + ((u[:, 1] * g[0] + u[:, 2] * g[1]) + u[:, 3] * g[2])
+    return L, amax, g

@@ -35,7 +35,8 @@ class RotatingStarStep:
 
     def __init__(self, max_level: int, gamma: float = 5.0 / 3.0, cfl: float = 0.4,
                  omega: float = 0.3, device: Optional[torch.device] = None,
-                 state: Optional[torch.Tensor] = None, concurrent: bool = True):
+                 state: Optional[torch.Tensor] = None, concurrent: bool = True,
+                 record_stages: bool = False):
         self.device = torch.device(device) if device is not None else torch.device("cuda")
         if self.device.type != "cuda":
             raise RuntimeError("RotatingStarStep needs a CUDA device (no CPU fallback)")
@@ -62,6 +63,13 @@ class RotatingStarStep:
         self._graph = None
         self._concurrent = concurrent
         self._side = torch.cuda.Stream(self.device) if concurrent else None
+        # verification mode (tests): keep the stage-1 per-sub-grid amax and
+        # both stages' g (the step itself overwrites them); costs 3 copies
+        self.record_stages = record_stages
+        if record_stages:
+            self.amax1 = torch.empty_like(self.amax)
+            self.g1 = torch.empty((3, self.n, self.n, self.n), **f64)
+            self.g2 = torch.empty_like(self.g1)
 
     def _s(self) -> int:
         return torch.cuda.current_stream(self.device).cuda_stream
@@ -86,14 +94,22 @@ class RotatingStarStep:
     def _g(self) -> int:
         return self.gravity.out.data_ptr() + self.n ** 3 * 8     # rows 1..3 of [4][N^3]
 
+    def _gview(self) -> torch.Tensor:
+        return self.gravity.out[1:4].reshape(3, self.n, self.n, self.n)
+
     def _enqueue_step(self) -> None:
         s = self._s()
         self._rhs(self.U)
+        if self.record_stages:
+            self.amax1.copy_(self.amax)
+            self.g1.copy_(self._gview())
         N.call("tb_star_cfl", s, self.amax.data_ptr(), self.nsub, self.dx, self.cfl,
                self.dt.data_ptr())
         N.call("tb_star_stage", s, 1, None, self.U.data_ptr(), self.dudt.data_ptr(), self._g(),
                self.dt.data_ptr(), self.n, self.n, self.U1.data_ptr())
         self._rhs(self.U1)
+        if self.record_stages:
+            self.g2.copy_(self._gview())
         N.call("tb_star_stage", s, 2, self.U.data_ptr(), self.U1.data_ptr(),
                self.dudt.data_ptr(), self._g(), self.dt.data_ptr(), self.n, self.n,
                self.U.data_ptr())

@@ -31,3 +31,17 @@ def test_product_layout_helper_matches_the_oracle():
     I, _ = ho.rotating_star(8)
     assert np.array_equal(subgrids_to_lattice(torch.from_numpy(I)).numpy(),
                           so.subgrids_to_lattice(I))
+
+
+def test_sampled_rhs_equals_full_oracle():
+    # the full-size GPU checks (tests/test_gpu_star.py) rest on this: L(U)
+    # restricted to sampled sub-grids == the full oracle's rows, bit for bit
+    import numpy as np
+    from oracle import star_oracle as so
+    for L, subs in ((1, [0, 3, 5, 7]), (2, [0, 9, 36, 63])):
+        U, _ = so.initial_state(L)
+        U = U * (1.0 + 1e-3 * np.sin(np.arange(U.size)).reshape(U.shape))
+        full, am = so.rhs(U, L, 5 / 3)
+        Ls, ams, _ = so.sampled_rhs(U, L, np.array(subs))
+        assert np.array_equal(Ls, so.lattice_to_subgrids(full)[subs])
+        assert np.array_equal(ams, am[subs])
