@@ -230,10 +230,20 @@ int tb_ipc_close(void *dptr);
  * with system-scope atomics, bumps each rank's TB_ACC_COUNT_WORD, resets
  * local_acc, waits until my_acc has nranks arrivals, then finalises my_acc
  * exactly as tb_acc_finalize(..., reset=1). Accumulators must alternate
- * between two parities step to step. */
+ * between two parities step to step. The arrival wait traps after
+ * TB_P2P_TIMEOUT_S seconds (environment; default 30, 0 = never). */
 int tb_acc_allreduce_p2p(tb_stream_t s, int64_t *local_acc, int64_t *const *peer_accs,
                          int nranks, int64_t *my_acc, double *piece, double *dt,
                          double *checksum);
+/* The same with an explicit watchdog: timeout_ns (0 = wait forever) and a
+ * diagnostic record — diag: 4 int64 in mapped pinned host memory
+ * (tb_host_alloc), written before the trap as {0x7470325774696d65, rank,
+ * step, arrivals seen} so the host can say which rank waited for whom even
+ * after the context is lost. */
+int tb_acc_allreduce_p2p_ex(tb_stream_t s, int64_t *local_acc, int64_t *const *peer_accs,
+                            int nranks, int64_t *my_acc, double *piece, double *dt,
+                            double *checksum, int64_t timeout_ns, int64_t rank, int64_t step,
+                            int64_t *diag);
 
 /* K6 (north_star "hydro reconstruct+flux only", BASELINE config 2; PARITY
  * UNPINNED — no hydro exists in the reference, SPEC.md:17,490 — the spec is

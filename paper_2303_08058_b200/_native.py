@@ -155,6 +155,8 @@ SIGNATURES = {
     "tb_ipc_open_handle": [_vp, _pvp],
     "tb_ipc_close": [_vp],
     "tb_acc_allreduce_p2p": [_u64, _vp, _vp, _int, _vp, _vp, _vp, _vp],
+    "tb_acc_allreduce_p2p_ex": [_u64, _vp, _vp, _int, _vp, _vp, _vp, _vp, _i64, _i64, _i64,
+                                _vp],
     "tb_hydro_flux": [_u64, _vp, _vp, _vp, _i64, _dbl, _dbl],
     "tb_fp64_probe": [_int, _i64, _vp, _vp],
     "tb_divsqrt_fast": [_u64, _vp, _vp, _i64, _vp, _vp, _vp],

@@ -1131,9 +1131,15 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned 
   return v;
 }
 
+struct P2pWatch {          // the arrival wait's watchdog (tb_acc_allreduce_p2p_ex)
+  int64_t timeout_ns;      // 0: wait forever
+  int64_t rank, step;
+  volatile int64_t *diag;  // mapped pinned host words, readable after a trap
+};
+
 __global__ void k_acc_allreduce_p2p(int64_t *local_acc, int64_t *const *peer_accs,
                                     int nranks, int64_t *my_acc, double *piece, double *dt,
-                                    double *checksum) {
+                                    double *checksum, P2pWatch w) {
   const int lane = threadIdx.x & 31;
   if (threadIdx.x >= 32) return;
   // 1. publish this rank's contribution to every rank (including itself)
@@ -1161,14 +1167,27 @@ __global__ void k_acc_allreduce_p2p(int64_t *local_acc, int64_t *const *peer_acc
     const unsigned long long *cnt =
         reinterpret_cast<const unsigned long long *>(my_acc) + TB_ACC_COUNT_WORD;
     // a rank that never arrives (died, or launched a different step count)
-    // must not hang the job: after 30 s the kernel traps and the host sees
-    // a launch failure instead
-    unsigned long long t0, t;
+    // must not hang the job: after the watchdog's timeout the kernel leaves
+    // (rank, step, arrivals seen) in host memory and traps, and the host
+    // reports which rank waited for whom (timeout 0 = wait forever, e.g.
+    // under a debugger or a profiler's kernel replay on another rank)
+    unsigned long long t0, t, seen;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    while (ld_acquire_sys_u64(cnt) < (unsigned long long)nranks) {
+    while ((seen = ld_acquire_sys_u64(cnt)) < (unsigned long long)nranks) {
       __nanosleep(200);
+      if (w.timeout_ns <= 0) continue;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      if (t - t0 > 30000000000ULL) __trap();
+      if ((int64_t)(t - t0) > w.timeout_ns) {
+        if (w.diag) {
+          w.diag[1] = w.rank;
+          w.diag[2] = w.step;
+          w.diag[3] = (int64_t)seen;
+          __threadfence_system();
+          w.diag[0] = 0x7470325774696d65LL;   // "tp2Wtime": the words are valid
+          __threadfence_system();
+        }
+        __trap();
+      }
     }
   }
   __syncwarp();
@@ -1399,13 +1418,28 @@ int tb_acc_finalize(tb_stream_t s, int64_t *acc, double *piece, double *dt,
   return tb::last_error();
 }
 
+int tb_acc_allreduce_p2p_ex(tb_stream_t s, int64_t *local_acc, int64_t *const *peer_accs,
+                            int nranks, int64_t *my_acc, double *piece, double *dt,
+                            double *checksum, int64_t timeout_ns, int64_t rank, int64_t step,
+                            int64_t *diag) {
+  if (!local_acc || !peer_accs || !my_acc || nranks < 1 || timeout_ns < 0) return TB_E_INVALID;
+  P2pWatch w{timeout_ns, rank, step, diag};
+  k_acc_allreduce_p2p<<<1, 32, 0, reinterpret_cast<cudaStream_t>(s)>>>(
+      local_acc, peer_accs, nranks, my_acc, piece, dt, checksum, w);
+  return tb::last_error();
+}
+
 int tb_acc_allreduce_p2p(tb_stream_t s, int64_t *local_acc, int64_t *const *peer_accs,
                          int nranks, int64_t *my_acc, double *piece, double *dt,
                          double *checksum) {
-  if (!local_acc || !peer_accs || !my_acc || nranks < 1) return TB_E_INVALID;
-  k_acc_allreduce_p2p<<<1, 32, 0, reinterpret_cast<cudaStream_t>(s)>>>(
-      local_acc, peer_accs, nranks, my_acc, piece, dt, checksum);
-  return tb::last_error();
+  // default watchdog: TB_P2P_TIMEOUT_S seconds (default 30; 0 disables)
+  static const int64_t timeout_ns = [] {
+    const char *e = getenv("TB_P2P_TIMEOUT_S");
+    const double sec = e ? atof(e) : 30.0;
+    return (int64_t)(sec > 0 ? sec * 1e9 : 0);
+  }();
+  return tb_acc_allreduce_p2p_ex(s, local_acc, peer_accs, nranks, my_acc, piece, dt, checksum,
+                                 timeout_ns, -1, -1, nullptr);
 }
 
 }  // extern "C"

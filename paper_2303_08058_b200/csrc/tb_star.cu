@@ -77,20 +77,26 @@ __global__ void __launch_bounds__(256) k_star_pad(const double *__restrict__ U,
   }
 }
 
+// max that propagates NaN (numpy's np.maximum / amax.max(), which the spec's
+// dt follows): a sub-grid that blew up makes dt NaN instead of being skipped
+__device__ __forceinline__ double max_nan(double a, double b) {
+  return (a != a || a > b) ? a : b;
+}
+
 __global__ void __launch_bounds__(1024) k_star_cfl(const double *__restrict__ amax, int64_t nsub,
                                                    double dx, double cfl,
                                                    double *__restrict__ dt) {
   __shared__ double part[32];
   double m = -CUDART_INF;
-  for (int64_t i = threadIdx.x; i < nsub; i += blockDim.x) m = fmax(m, amax[i]);
+  for (int64_t i = threadIdx.x; i < nsub; i += blockDim.x) m = max_nan(m, amax[i]);
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  for (int o = 16; o > 0; o >>= 1) m = max_nan(m, __shfl_xor_sync(0xffffffffu, m, o));
   if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = m;
   __syncthreads();
   if (threadIdx.x < 32) {
     m = threadIdx.x < (blockDim.x >> 5) ? part[threadIdx.x] : -CUDART_INF;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    for (int o = 16; o > 0; o >>= 1) m = max_nan(m, __shfl_xor_sync(0xffffffffu, m, o));
     if (threadIdx.x == 0) *dt = __ddiv_rn(__dmul_rn(cfl, dx), m);
   }
 }

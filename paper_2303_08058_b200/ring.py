@@ -30,6 +30,8 @@ each other and the compute.
 
 from __future__ import annotations
 
+import ctypes
+import os
 from dataclasses import dataclass
 from typing import List, Optional, Tuple
 
@@ -230,10 +232,13 @@ class RingStepper:
         opened = {}
 
         def open_handle(handle, offset):
+            # cudaIpcOpenMemHandle reference-counts repeated opens of one
+            # allocation (small rings put several tensors in one caching-
+            # allocator segment): count them, close() closes each open
             base = ctypes.c_void_p()
             buf = (ctypes.c_uint8 * N.TB_IPC_HANDLE_BYTES).from_buffer_copy(handle)
             N.call("tb_ipc_open_handle", buf, ctypes.byref(base))
-            opened.setdefault(base.value, 0)
+            opened[base.value] = opened.get(base.value, 0) + 1
             return base.value, base.value + offset
 
         peers = None
@@ -253,24 +258,50 @@ class RingStepper:
                 for parity in range(2):
                     tab[parity][p] = base_ptr + parity * row
             self.peer_tab = torch.tensor(tab, dtype=torch.int64, device=self.device)
-            peers = {"left": state[left], "right": state[right], "bases": list(opened)}
+            peers = {"left": state[left], "right": state[right], "bases": dict(opened)}
         except Exception as e:          # noqa: BLE001 — reported after agreement
             err = e
         ok = [None] * self.world
         dist.all_gather_object(ok, peers is not None, group=self.group)
         if not all(ok):
-            for base in opened:
-                N.call("tb_ipc_close", base)
+            for base, count in opened.items():
+                for _ in range(count):
+                    N.call("tb_ipc_close", base)
             return None, err or "a peer could not map its neighbours' buffers"
+        # the arrival watchdog's diagnostic words (mapped pinned host memory:
+        # still readable after the trap has taken the context down)
+        p = ctypes.c_void_p()
+        N.call("tb_host_alloc", ctypes.byref(p), 32)
+        self._diag_ptr = p.value
+        self._diag = (ctypes.c_int64 * 4).from_address(p.value)
+        for i in range(4):
+            self._diag[i] = 0
         return peers, None
 
     def close(self) -> None:
-        """Unmap neighbours' buffers (p2p halo)."""
+        """Unmap neighbours' buffers (p2p halo): every open of each mapped
+        allocation is closed."""
         if self._peers is not None:
             torch.cuda.synchronize(self.device)
-            for base in self._peers["bases"]:
-                N.call("tb_ipc_close", base)
+            for base, count in self._peers["bases"].items():
+                for _ in range(count):
+                    N.call("tb_ipc_close", base)
             self._peers = None
+            N.call("tb_host_free", ctypes.c_void_p(self._diag_ptr))
+            self._diag = None
+
+    P2P_DIAG_MAGIC = 0x7470325774696d65
+    P2P_TIMEOUT_S = float(os.environ.get("TB_P2P_TIMEOUT_S", "30"))
+
+    def peer_timeout(self) -> Optional[str]:
+        """After a failed step: which rank's peer-memory arrival wait timed
+        out, at which step, with how many of the ranks arrived (None if the
+        watchdog did not fire)."""
+        d = getattr(self, "_diag", None)
+        if d is None or d[0] != self.P2P_DIAG_MAGIC:
+            return None
+        return (f"rank {d[1]} waited more than {self.P2P_TIMEOUT_S:g} s at step {d[2]} "
+                f"for the step's arrivals: {d[3]} of {self.world} ranks arrived")
 
     # -------------------------------------------------------------- state --
     @property
@@ -348,10 +379,11 @@ class RingStepper:
             self._step_partitioned(old, out, kernel_events)
             if self._peers is not None:
                 # exact cross-rank reduction + step barrier over peer memory
-                N.call("tb_acc_allreduce_p2p", self.ops.stream(), _ptr(self.acc),
+                N.call("tb_acc_allreduce_p2p_ex", self.ops.stream(), _ptr(self.acc),
                        self.peer_tab[k & 1].data_ptr(), self.world,
                        self.gacc[k & 1].data_ptr(), _ptr(self.pieces[k:k + 1]),
-                       _ptr(self.dts[k:k + 1]), _ptr(self.checksum))
+                       _ptr(self.dts[k:k + 1]), _ptr(self.checksum),
+                       int(self.P2P_TIMEOUT_S * 1e9), self.rank, k, self._diag_ptr)
             else:
                 self._close(k)
         else:

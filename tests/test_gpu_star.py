@@ -148,3 +148,19 @@ def test_pad_is_exact(n, nz, halo):
     else:
         want = np.pad(u, ((0, 0), (2, 2), (2, 2), (2, 2)), mode="wrap")
     np.testing.assert_array_equal(Up.cpu().numpy(), want)
+
+
+def test_cfl_propagates_nan():
+    # a sub-grid whose signal speed is NaN makes dt NaN (np.maximum / the
+    # spec's amax.max()), instead of a finite dt from the others
+    from paper_2303_08058_b200 import _native as N
+    dev = torch.device("cuda", 0)
+    amax = torch.linspace(0.5, 2.0, 3000, dtype=torch.float64, device=dev)
+    dt = torch.zeros(1, dtype=torch.float64, device=dev)
+    N.call("tb_star_cfl", 0, amax.data_ptr(), 3000, 0.01, 0.4, dt.data_ptr())
+    torch.cuda.synchronize()
+    assert dt.item() == (0.4 * 0.01) / 2.0
+    amax[1234] = float("nan")
+    N.call("tb_star_cfl", 0, amax.data_ptr(), 3000, 0.01, 0.4, dt.data_ptr())
+    torch.cuda.synchronize()
+    assert dt.isnan().item()
