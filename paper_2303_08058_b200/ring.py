@@ -191,6 +191,7 @@ class RingStepper:
                 err = "no process group to exchange IPC handles over"
             if self._peers is not None:
                 self.halo_mode = "p2p"
+                self._alloc_diag()
             elif halo == "p2p":
                 raise RuntimeError(f"peer-memory halo unavailable: {err}")
 
@@ -268,15 +269,17 @@ class RingStepper:
                 for _ in range(count):
                     N.call("tb_ipc_close", base)
             return None, err or "a peer could not map its neighbours' buffers"
-        # the arrival watchdog's diagnostic words (mapped pinned host memory:
-        # still readable after the trap has taken the context down)
+        return peers, None
+
+    def _alloc_diag(self) -> None:
+        """The arrival watchdog's diagnostic words: mapped pinned host memory,
+        still readable after a trap has taken the CUDA context down."""
         p = ctypes.c_void_p()
         N.call("tb_host_alloc", ctypes.byref(p), 32)
         self._diag_ptr = p.value
         self._diag = (ctypes.c_int64 * 4).from_address(p.value)
         for i in range(4):
             self._diag[i] = 0
-        return peers, None
 
     def close(self) -> None:
         """Unmap neighbours' buffers (p2p halo): every open of each mapped
