@@ -683,6 +683,11 @@ def main(argv=None):
     ap.add_argument("--dist-backend", default="nccl",
                     help="torch.distributed backend for N>1 (gloo only to exercise the "
                          "multi-rank code path with several ranks on one GPU)")
+    ap.add_argument("--halo", choices=["auto", "p2p", "nccl"], default="auto",
+                    help="N>1 ring halo + reduction: p2p = neighbour faces and the exact "
+                         "all-reduce over CUDA-IPC peer memory; nccl = NCCL send/recv of the "
+                         "faces + NCCL all-reduces; auto = p2p when every rank can map its "
+                         "neighbours, else nccl")
     ap.add_argument("--same-gpu", action="store_true",
                     help="all ranks on cuda:0 (with --dist-backend gloo: code-path test)")
     ap.add_argument("--no-ablation", action="store_true",
@@ -713,7 +718,12 @@ def main(argv=None):
     dev = torch.device("cuda", local)
     if world > 1:
         if args.dist_backend == "nccl":
+            # the communicator's init lines (ranks, devices, transport) on
+            # stderr, so the run shows NCCL formed the N-rank clique
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
+            dist.barrier()          # eager communicator creation
         else:   # code-path testing only (several ranks sharing one GPU)
             dist.init_process_group(args.dist_backend)
 
@@ -736,7 +746,7 @@ def main(argv=None):
                    + (4 * SCENARIO_STEPS if args.e2e_steps > 0 else 0)
                    + int(args.warm_ms / 0.02) + 128)     # time-based warm-up steps
     st = RingStepper(subgrids, device=dev, rank=rank, world=world, max_steps=total_steps,
-                     group=None)
+                     group=None, halo=args.halo)
     n_local = st.n
     # Warm-up: W steps, then more back-to-back steps until >= --warm-ms of
     # device time has run, ending right before the timed region with no idle

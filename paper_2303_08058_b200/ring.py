@@ -436,7 +436,14 @@ class RingStepper:
             if kernel_events is not None:
                 kernel_events[1].record()
             return
-        reqs = self._exchange_start(old[0, :FACE], old[n - 1, CELLS - FACE:])
+        import torch.distributed as dist
+        if old.is_cuda and dist.get_backend(self.group) != "nccl":
+            # gloo cannot post device memory: the host-staged blocking exchange
+            # (a code-path test configuration, e.g. several ranks on one GPU)
+            self._exchange(old[0, :FACE], old[n - 1, CELLS - FACE:])
+            reqs = []
+        else:
+            reqs = self._exchange_start(old[0, :FACE], old[n - 1, CELLS - FACE:])
         if kernel_events is not None:
             kernel_events[0].record()
         mins, sums = self.mins, self.sums

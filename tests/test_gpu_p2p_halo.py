@@ -18,7 +18,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, subgrids, steps, q):
+def _worker(rank, world, port, subgrids, steps, q, halo="p2p"):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
@@ -26,7 +26,7 @@ def _worker(rank, world, port, subgrids, steps, q):
     try:
         from paper_2303_08058_b200.ring import RingStepper
         st = RingStepper(subgrids, device=torch.device("cuda", 0), rank=rank, world=world,
-                         max_steps=steps, halo="p2p")
+                         max_steps=steps, halo=halo)
         mode = st.halo_mode
         res = st.run(steps)
         cells = st.cells.cpu().numpy()
@@ -37,8 +37,12 @@ def _worker(rank, world, port, subgrids, steps, q):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("halo", ["p2p", "nccl"])
 @pytest.mark.parametrize("world,subgrids,steps", [(2, 64, 3), (3, 1000, 2), (2, 3, 2)])
-def test_p2p_halo_ring_matches_reference(world, subgrids, steps):
+def test_p2p_halo_ring_matches_reference(world, subgrids, steps, halo):
+    """halo="nccl" here runs the message-passing path's orchestration on
+    device buffers (gloo stages the faces through the host: several ranks
+    cannot share one GPU under NCCL)."""
     import numpy as np
     import torch.multiprocessing as mp
 
@@ -46,7 +50,7 @@ def test_p2p_halo_ring_matches_reference(world, subgrids, steps):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, subgrids, steps, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, subgrids, steps, q, halo))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -60,6 +64,6 @@ def test_p2p_halo_ring_matches_reference(world, subgrids, steps):
     assert all(p.exitcode == 0 for p in procs)
     cs, dts, cells = mo.run_reference_cells(subgrids, steps)
     for rank, mode, got_cs, got_dts, lo, got in outs:
-        assert mode == "p2p"
+        assert mode == halo
         assert got_cs == cs and got_dts == dts
         np.testing.assert_array_equal(got, cells[lo:lo + got.shape[0]])
