@@ -386,6 +386,11 @@ def hydro_fp64_per_subgrid():
 
 
 HYDRO_FP64_PER_SUBGRID = hydro_fp64_per_subgrid()
+# the same spec counted as operations: each IEEE divide / square root is ONE
+# op instead of its 8-instruction sequence — 1,728 reciprocals (1/rho per
+# staged cell) + 3 x 576 faces x 2 states x (one divide + one square root)
+HYDRO_DIVSQRT_PER_SUBGRID = 12 ** 3 + 3 * 576 * 2 * 2
+HYDRO_FP64_OPS_PER_SUBGRID = HYDRO_FP64_PER_SUBGRID - 7 * HYDRO_DIVSQRT_PER_SUBGRID
 M2L_FMA, LEAF_FMA = 70, 4     # algorithmic FP64 FMAs per interaction (traceless M2L, K7)
 
 
@@ -485,6 +490,12 @@ def north_star_kernels(dev, reps=20):
                      "fp64_achieved": S * HYDRO_FP64_PER_SUBGRID / (ms * 1e-3),
                      "fp64_peak": f64, "fp64_peak_source": f64_src,
                      "fp64_frac": S * HYDRO_FP64_PER_SUBGRID / (ms * 1e-3) / f64,
+                     "fp64_ops_per_subgrid": HYDRO_FP64_OPS_PER_SUBGRID,
+                     "fp64_ops_frac": S * HYDRO_FP64_OPS_PER_SUBGRID / (ms * 1e-3) / f64,
+                     "fp64_frac_note": "fp64_frac: issued FP64 instructions (a divide or square "
+                                       "root = its 8-instruction sequence, the rate the FP64 "
+                                       "pipe sees); fp64_ops_frac: spec operations (a divide "
+                                       "or square root = 1 op), against the same peak",
                      "algorithmic_bytes_per_launch": S * HYDRO_BYTES_PER_SUBGRID},
         "parity": "unpinned (self-authored spec; bit-exact to oracle/hydro_oracle.py)"}
     # K7: FMM gravity, max_level 4 (config 3)
