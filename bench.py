@@ -261,10 +261,11 @@ def machine_ablation(subgrids=512, steps=5, repeats=3):
 # task structure; run_reference(32768, 1) pins step 1
 C4_CHECKSUM = float.fromhex("0x1.fffc131fd56c6p+22")
 C4_DT = float.fromhex("0x1.a73380416f1a6p-22")
-# the sweep's best polling configuration (scripts/c4_machine_sweep.py,
-# profiles/r02/c4_sweep.jsonl): 8 workers, 16 executors, max 128 aggregated,
-# batch members read and written in place in the tasks' pinned buffers
-C4_MACHINE = dict(workers=8, executors=16, max_agg=128, zero_copy=2)
+# the sweeps' best polling configuration (scripts/c4_machine_sweep.py and
+# scripts/c4_gather_sweep.py, profiles/r02/c4_*sweep.jsonl): 16 workers (the
+# box's host cores), 8 executors, max 256 aggregated, batch members read and
+# written in place in the tasks' pinned buffers
+C4_MACHINE = dict(workers=16, executors=8, max_agg=256, zero_copy=2)
 
 
 def machine_ablation_c4(steps=3):

@@ -123,7 +123,7 @@ def test_python_machine_when_not_delegable(rig, golden):
 @pytest.mark.parametrize("mode", MODES)
 def test_delegated_c4_golden(rig, golden, mode):
     g = golden["run_reference"]["32768x1"]
-    r = rig(workers=8, executors=16, max_agg=128, mode=mode)
+    r = rig(workers=16, executors=8, max_agg=256, mode=mode)
     _, res = r.run(32768, 1, batch_copies="gather")
     assert res.engine == "native"
     assert res.checksum.hex() == g["checksum"]
