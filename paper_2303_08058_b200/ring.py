@@ -437,7 +437,7 @@ class RingStepper:
                 kernel_events[1].record()
             return
         import torch.distributed as dist
-        if old.is_cuda and dist.get_backend(self.group) != "nccl":
+        if old.is_cuda and dist.is_initialized() and dist.get_backend(self.group) != "nccl":
             # gloo cannot post device memory: the host-staged blocking exchange
             # (a code-path test configuration, e.g. several ranks on one GPU)
             self._exchange(old[0, :FACE], old[n - 1, CELLS - FACE:])
