@@ -216,6 +216,28 @@ def cpu_reference_sample(subgrids: int, budget_s: float, threads: int = 0):
     return subgrids * 512 * steps / el, threads, steps, el
 
 
+def python_reference_sample(subgrids: int = 4096, budget_s: float = 3.0):
+    """The north_star's "Python CPU reference timed on the box's own host
+    cores": src/reference.py:23-50 restated with its execution shape (a
+    Python loop of 512-value numpy ops per sub-grid,
+    oracle/miniapp_oracle.run_reference_per_subgrid, equal to the pinned
+    oracle; the reference package itself cannot travel to the GPU box). One
+    core: numpy runs these ops single-threaded. Repeated one-step runs of
+    ``subgrids`` sub-grids until ``budget_s``."""
+    from oracle import miniapp_oracle as mo
+    runs, t0 = 0, time.perf_counter()
+    while True:
+        mo.run_reference_per_subgrid(subgrids, 1)
+        runs += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s:
+            break
+    return {"value": subgrids * 512 * runs / el, "unit": "cells/s", "cores": 1,
+            "kind": "port (src/reference.py:23-50 restated, per-sub-grid numpy loop)",
+            "sample": f"{runs} x run_reference({subgrids}, 1) in {el:.1f}s "
+                      "(initialisation included, as in the reference)"}
+
+
 def machine_ablation(subgrids=512, steps=5, repeats=3):
     """The paper's ablation in the same run: the mini-app machine (native C++
     runtime, tb_machine_run) at the paper's scenario size (512 sub-grids,
@@ -499,6 +521,35 @@ def north_star_kernels(dev, reps=20):
                                        "or square root = 1 op), against the same peak",
                      "algorithmic_bytes_per_launch": S * HYDRO_BYTES_PER_SUBGRID},
         "parity": "unpinned (self-authored spec; bit-exact to oracle/hydro_oracle.py)"}
+    # the same kernel at the star step's size (max_level 5, 32768 sub-grids):
+    # the per-launch fixed cost (launch, the first cold TMA loads of all CTAs,
+    # the last round's tail; ~10 us, profiles/r02/k6_experiments.md) is 7 % of
+    # a config-2 launch and <1 % here
+    del U, du, am
+    S5 = 8 ** 5
+    I5, dx5 = hydro.rotating_star(S5, device=dev)
+    U5 = hydro.with_ghosts(I5)
+    del I5
+    du5 = torch.empty((S5, 5, 8, 8, 8), dtype=torch.float64, device=dev)
+    am5 = torch.empty(S5, dtype=torch.float64, device=dev)
+    hydro.hydro_flux(U5, dx5, out=du5, amax=am5)
+    tot = 0.0
+    for _ in range(5):
+        flush.fill_(1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        hydro.hydro_flux(U5, dx5, out=du5, amax=am5)
+        b.record()
+        torch.cuda.synchronize()
+        tot += a.elapsed_time(b)
+    ms5 = tot / 5
+    out["hydro_k6"]["max_level_5"] = {
+        "subgrids": S5, "ms": ms5, "cells_per_s": S5 * 512 / (ms5 * 1e-3),
+        "fp64_frac": S5 * HYDRO_FP64_PER_SUBGRID / (ms5 * 1e-3) / f64,
+        "fp64_ops_frac": S5 * HYDRO_FP64_OPS_PER_SUBGRID / (ms5 * 1e-3) / f64,
+        "note": "same kernel and L2-flush method at 32768 sub-grids (the star step's "
+                "max_level-5 lattice size): the config-2 launch carries a ~10 us fixed cost"}
+    del U5, du5, am5
     # K7: FMM gravity, max_level 4 (config 3)
     L = 4
     rho = rotating_star_density(L, device=dev)
@@ -952,7 +1003,8 @@ def main(argv=None):
             v, cores, nsteps, el = cpu_reference_sample(per_gpu, args.cpu_budget)
             cpu = {"value": v, "unit": "cells/s", "cores": cores, "kind": "port",
                    "sample": f"{nsteps} full steps of {per_gpu} sub-grids in {el:.1f}s "
-                             "(oracle/tb_oracle.c, OpenMP)"}
+                             "(oracle/tb_oracle.c, OpenMP)",
+                   "python_reference": python_reference_sample()}
         line = {
             "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,

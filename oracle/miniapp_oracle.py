@@ -134,6 +134,34 @@ def run_reference_cells(subgrids: int, steps: int, chains: int = 3,
     return checksum, dts, cells
 
 
+def run_reference_per_subgrid(subgrids: int, steps: int, chains: int = 3,
+                               kernels_per_chain: int = 5) -> Tuple[float, List[float]]:
+    """``run_reference`` with the reference's execution shape — a Python loop
+    over sub-grids, each a separate 512-value numpy array (src/reference.py:
+    26-47) — for timing the Python reference on the GPU box's host, where
+    the reference package itself is absent (bench.py python_reference).
+    Same results as :func:`run_reference` (tests/test_oracle.py)."""
+    rows = list(initial_cells(subgrids))
+    checksum = 0.0
+    dts: List[float] = []
+    for _ in range(steps):
+        ghosts = [(r[:FACE].copy(), r[-FACE:].copy()) for r in rows]   # Jacobi snapshot
+        mins, sums = [], []
+        for g in range(subgrids):
+            w = rows[g].copy()
+            w[:FACE] = 0.5 * (w[:FACE] + ghosts[g - 1][1])
+            w[-FACE:] = 0.5 * (w[-FACE:] + ghosts[(g + 1) % subgrids][0])
+            for _chain in range(chains):
+                for kind in range(kernels_per_chain):
+                    transform(w, kind)
+            rows[g] = w
+            mins.append(float(w.min()))
+            sums.append(float(w.sum()))
+        dts.append(min(mins))
+        checksum += math.fsum(sums)
+    return checksum, dts
+
+
 def run_reference(subgrids: int, steps: int, chains: int = 3,
                   kernels_per_chain: int = 5) -> Tuple[float, List[float]]:
     """Same signature and result as src/reference.py:23."""
