@@ -423,7 +423,13 @@ typedef struct {
                                 batch kernel reads each member's rows and
                                 writes its output rows there directly
                                 (tb_launch_gather): no marshal/scatter
-                                memcpy, one launch + one event per batch.   */
+                                memcpy, one launch + one event per batch.
+                                3: gather, with each task's rounds resident
+                                in HBM — round 1 reads the host-folded rows
+                                from pinned memory, the last round writes
+                                them back there, the rounds between ping-pong
+                                in device memory (two PCIe crossings per
+                                sub-grid and step instead of 30).           */
   int64_t fault_at_launch;   /* fault injection (tests): the k-th batch launch
                                 of the run (k >= 1) runs a trapping kernel;
                                 the device fault must surface as this call's

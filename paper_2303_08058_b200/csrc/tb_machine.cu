@@ -401,6 +401,7 @@ struct SubTask {
   std::vector<double> a, b;   // work buffers (zero_copy = 2: abuf/bbuf live in the arena)
   double *abuf, *bbuf;
   double *work, *out;
+  double *d0 = nullptr, *d1 = nullptr;   // zero_copy = 3: device ping-pong buffers
 };
 
 struct Machine {
@@ -428,6 +429,8 @@ struct Machine {
   std::atomic<int> fault{0};
   std::atomic<int64_t> launch_seq{0};   // fault_at_launch counter
   double *arena = nullptr;              // zero_copy = 2: pinned task buffers
+                                        // zero_copy = 3: one pinned buffer per task
+  double *dev_arena = nullptr;          // zero_copy = 3: two device buffers per task
   void fail(int rc) {
     int expect = 0;
     if (rc != TB_OK) fault.compare_exchange_strong(expect, rc);
@@ -584,7 +587,7 @@ void launch(Batch *b, bool idle) {   // src/executors.py:257-284 as one launch
   const int do_barrier = m->cfg.inject_barriers && !m->cfg.barrier_elision;
   const tb_stream_t st = reinterpret_cast<tb_stream_t>(ex->stream);
   m->kernels.fetch_add(1, std::memory_order_relaxed);
-  if (m->cfg.zero_copy == 2 && !m->hydro) {
+  if (m->cfg.zero_copy >= 2 && !m->hydro) {
     // members read and written where they live (the pinned task arena)
     enqueue_and_bridge(m, ex, Task{batch_done, b}, [&](tb_event_t *ev) {
       const double *src[TB_GATHER_MAX];
@@ -736,6 +739,10 @@ void start_task(void *p) {   // ghost fold + first round (src/miniapp.py:116-130
       w[kCells - kFace + i] = 0.5 * (w[kCells - kFace + i] + right[i]);
   }
   t->round = 0;
+  // zero_copy = 3: round 0 reads the folded rows from pinned host memory and
+  // writes device memory; the rounds in between stay in HBM
+  if (m->dev_arena)
+    t->out = m->cfg.chains * m->cfg.kernels_per_chain <= 1 ? t->abuf : t->d0;
   schedule(t->ex, 0, t->work, t->out, t->n * kCells, t);
 }
 
@@ -746,12 +753,22 @@ void resume_task(void *p) {   // next round, or write-back + post-process
     task_finished(m);
     return;
   }
-  std::swap(t->work, t->out);
   const int kpc = (int)m->cfg.kernels_per_chain;
   const int rounds = (int)(m->cfg.chains * kpc);
-  if (++t->round < rounds) {
-    schedule(t->ex, t->round % kpc, t->work, t->out, t->n * kCells, t);
-    return;
+  if (m->dev_arena) {
+    // zero_copy = 3: device ping-pong; the last round writes the host rows
+    t->work = t->out;
+    if (++t->round < rounds) {
+      t->out = t->round == rounds - 1 ? t->abuf : (t->work == t->d0 ? t->d1 : t->d0);
+      schedule(t->ex, t->round % kpc, t->work, t->out, t->n * kCells, t);
+      return;
+    }
+  } else {
+    std::swap(t->work, t->out);
+    if (++t->round < rounds) {
+      schedule(t->ex, t->round % kpc, t->work, t->out, t->n * kCells, t);
+      return;
+    }
   }
   for (int64_t k = 0; k < t->n; ++k) {
     const int64_t g = t->lo + k;
@@ -901,7 +918,7 @@ int run_machine(const tb_machine_config *cfg_in, const double *cells_in, double 
   if (c.subgrids < 1 || c.steps < 0 || c.workers < 1 || c.executors < 1 || c.max_agg < 1 ||
       c.chains < 0 || c.kernels_per_chain < 1 || c.kernels_per_chain > TB_KINDS ||
       c.task_subgrids < 1 || c.mode < TB_MODE_POLLING || c.mode > TB_MODE_FENCE ||
-      c.zero_copy < 0 || c.zero_copy > 2 || c.fault_at_launch < 0)
+      c.zero_copy < 0 || c.zero_copy > 3 || c.fault_at_launch < 0)
     return TB_E_INVALID;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -925,6 +942,17 @@ int run_machine(const tb_machine_config *cfg_in, const double *cells_in, double 
     if (cudaHostAlloc(reinterpret_cast<void **>(&m.arena), sizeof(double) * 2 * S * kCells,
                       cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess)
       return tb::rc(cudaGetLastError());
+  } else if (c.zero_copy == 3) {
+    // one pinned, device-mapped row block per task (the host fold's input
+    // and the last round's output) + two device blocks per task
+    if (cudaHostAlloc(reinterpret_cast<void **>(&m.arena), sizeof(double) * S * kCells,
+                      cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess)
+      return tb::rc(cudaGetLastError());
+    if (cudaMalloc(reinterpret_cast<void **>(&m.dev_arena), sizeof(double) * 2 * S * kCells) !=
+        cudaSuccess) {
+      cudaFreeHost(m.arena);
+      return tb::rc(cudaGetLastError());
+    }
   }
   m.pool.reset(new Pool((int)c.workers, dev, 1234));
   m.poller.reset(new Poller(m.pool.get(), &m.fault));
@@ -950,7 +978,11 @@ int run_machine(const tb_machine_config *cfg_in, const double *cells_in, double 
     t->lo = lo;
     t->n = std::min<int64_t>(c.task_subgrids, S - lo);
     t->ex = m.execs[(size_t)(lo % c.executors)].get();
-    if (m.arena) {
+    if (m.dev_arena) {
+      t->abuf = t->bbuf = m.arena + lo * kCells;
+      t->d0 = m.dev_arena + 2 * lo * kCells;
+      t->d1 = t->d0 + t->n * kCells;
+    } else if (m.arena) {
       t->abuf = m.arena + 2 * lo * kCells;
       t->bbuf = t->abuf + t->n * kCells;
     } else {
@@ -1017,6 +1049,7 @@ int run_machine(const tb_machine_config *cfg_in, const double *cells_in, double 
     delete s;
   }
   if (m.arena) cudaFreeHost(m.arena);
+  if (m.dev_arena) cudaFree(m.dev_arena);
   const int err = tb::rc(cudaGetLastError());
   return m.failed() ? m.fault.load() : err;
 }

@@ -98,11 +98,13 @@ def test_native_machine_zero_copy_goldens(golden, mode):
     assert res.checksum == fx(lit["GOLDEN_8X2"])
 
 
+@pytest.mark.parametrize("zc", [2, 3])
 @pytest.mark.parametrize("mode", MODES)
-def test_native_machine_gather_mode_goldens(golden, mode):
-    # zero_copy = 2: members read and written in the tasks' pinned arena
+def test_native_machine_gather_mode_goldens(golden, mode, zc):
+    # zero_copy = 2: members read and written in the tasks' pinned arena;
+    # 3: the same with the rounds between the first and the last in HBM
     res, cells = run_native(16, 3, workers=4, executors=3, max_agg=4, mode=mode,
-                            return_cells=True, zero_copy=2)
+                            return_cells=True, zero_copy=zc)
     assert res.checksum.hex() == golden["machine"]["16x3"]["checksum"]
     want = np.load(__import__("conftest").TESTS + "/golden/cells.npz")["cells_16x3"]
     np.testing.assert_array_equal(cells, want)
@@ -110,7 +112,7 @@ def test_native_machine_gather_mode_goldens(golden, mode):
         assert m.transfers == 0 and m.launches > 0
 
 
-@pytest.mark.parametrize("zc", [0, 2])
+@pytest.mark.parametrize("zc", [0, 2, 3])
 def test_native_machine_runs_on_caller_cells(zc):
     rng = np.random.default_rng(7)
     start = rng.random((40, 512))
@@ -131,7 +133,7 @@ def test_native_machine_runs_on_caller_cells(zc):
 C4_KW = dict(workers=8, executors=32, max_agg=64)
 
 
-@pytest.mark.parametrize("zc", [0, 2])
+@pytest.mark.parametrize("zc", [0, 2, 3])
 @pytest.mark.parametrize("mode", MODES)
 def test_native_machine_c4_golden_every_mode(golden, mode, zc):
     g = golden["run_reference"]["32768x1"]
@@ -140,3 +142,18 @@ def test_native_machine_c4_golden_every_mode(golden, mode, zc):
     assert [d.hex() for d in res.dts] == g["dts"]
     m = res.per_step[0]
     assert round(m.mean_batch * (m.reasons_full + m.reasons_idle)) == 32768 * 15
+
+
+@pytest.mark.parametrize("chains,kpc", [(1, 1), (1, 2), (2, 5)])
+def test_native_machine_resident_round_counts(chains, kpc):
+    """zero_copy = 3 with one round (the only round reads and writes host
+    rows), two rounds (no device round between) and 10."""
+    rng = np.random.default_rng(11)
+    start = rng.random((24, 512))
+    cells = start.copy()
+    res, _ = run_native(24, 2, workers=3, executors=2, max_agg=4, cells=cells, zero_copy=3,
+                        chains=chains, kernels_per_chain=kpc)
+    want = start
+    for _ in range(2):
+        want, _, _ = mo.step_cells(want, chains=chains, kernels_per_chain=kpc)
+    np.testing.assert_array_equal(cells, want)

@@ -58,7 +58,7 @@ def rig():
         r.close()
 
 
-@pytest.mark.parametrize("copies", ["staged", "gather"])
+@pytest.mark.parametrize("copies", ["staged", "gather", "resident"])
 @pytest.mark.parametrize("mode", MODES)
 def test_delegated_goldens_every_mode(rig, golden, mode, copies):
     lit = golden["reference_test_literals"]
