@@ -458,7 +458,7 @@ int tb_machine_run_cells(const tb_machine_config *cfg, double *cells, double *ch
  * being device-accessible (device or mapped pinned host memory, 16-B
  * aligned, n[i] even). op/kind/c1/c2 as tb_launch. Up to
  * TB_GATHER_MAX members per launch. */
-#define TB_GATHER_MAX 64
+#define TB_GATHER_MAX 256
 int tb_launch_gather(tb_stream_t s, int op, int kind, double c1, double c2,
                      const double *const *src, double *const *dst, const int64_t *n,
                      int members);

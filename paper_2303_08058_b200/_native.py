@@ -57,7 +57,7 @@ TB_OP_NONE = 0
 TB_OP_KIND = 1
 TB_OP_AFFINE = 2
 TB_OP_TRAP = 3          # fault injection: the kernel traps
-TB_GATHER_MAX = 64
+TB_GATHER_MAX = 256
 
 ABI_VERSION = 1
 

@@ -675,6 +675,7 @@ void schedule(Executor *ex, int kind, const double *src, double *dst, int64_t n,
       b = new Batch();
       b->ex = ex;
       b->kind = kind;
+      b->members.reserve((size_t)std::min<int64_t>(m->cfg.max_agg, 1024));
       if (m->cfg.max_agg > 1) {
         ex->open[kind] = b;
         b->refs.store(2, std::memory_order_relaxed);   // launch + idleness probe

@@ -157,3 +157,13 @@ def test_native_machine_resident_round_counts(chains, kpc):
     for _ in range(2):
         want, _, _ = mo.step_cells(want, chains=chains, kernels_per_chain=kpc)
     np.testing.assert_array_equal(cells, want)
+
+
+@pytest.mark.parametrize("zc", [2, 3])
+def test_native_machine_full_gather_launches(golden, zc):
+    """Batches of up to TB_GATHER_MAX = 256 members in one gather launch
+    (6 KB of kernel parameters) reproduce run_reference(4096, 1)."""
+    g = golden["run_reference"]["4096x1"]
+    res, _ = run_native(4096, 1, workers=4, executors=2, max_agg=256, zero_copy=zc)
+    assert res.checksum.hex() == g["checksum"]
+    assert [d.hex() for d in res.dts] == g["dts"]
