@@ -447,7 +447,10 @@ int tb_machine_run(const tb_machine_config *cfg, double *checksum,
                    tb_machine_step *steps_out, double *cells_out);
 /* tb_machine_run on the caller's cells (run_scenario on an existing
  * Scenario, src/miniapp.py:185-229): cells [subgrids][512] hold the initial
- * state on entry and the final state on return. exec_stats (optional):
+ * state on entry and are advanced in place (each task writes its sub-grids
+ * back, src/miniapp.py:132), so they hold the final state on success and the
+ * state the tasks reached on a device fault. The task arenas of zero_copy
+ * 2/3 are cached in the library between runs. exec_stats (optional):
  * [steps][executors][max_agg + 3] int64 — per step and executor, batches by
  * member count (index = count) then full- and idle-triggered launches (the
  * AggregationExecutor's batch_sizes / reasons, src/executors.py:166-169). */

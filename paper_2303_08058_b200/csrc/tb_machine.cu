@@ -69,7 +69,6 @@ class Pool {
   }
 
   void push(Task t) {
-    active_.fetch_add(1, std::memory_order_relaxed);
     if (t_pool == this && t_worker >= 0) {
       std::lock_guard<std::mutex> g(qs_[t_worker]->mu);
       qs_[t_worker]->dq.push_back(t);
@@ -79,12 +78,32 @@ class Pool {
     }
   }
 
+  // Many ready tasks at once (a finished batch's members, a step's tasks):
+  // dealt in contiguous runs across every worker's deque from a rotating
+  // start — one lock per worker instead of every other worker stealing them
+  // one at a time from the pushing worker's deque.
+  void push_spread(const Task *t, size_t n) {
+    const size_t W = qs_.size();
+    if (n == 0) return;
+    if (W == 1 || n == 1) {
+      for (size_t i = 0; i < n; ++i) push(t[i]);
+      return;
+    }
+    const size_t start = spread_rr_.fetch_add(1, std::memory_order_relaxed) % W;
+    const size_t per = (n + W - 1) / W;
+    for (size_t k = 0, i = 0; i < n; ++k) {
+      const size_t m = std::min(per, n - i);
+      Queue &q = *qs_[(start + k) % W];
+      std::lock_guard<std::mutex> g(q.mu);
+      q.dq.insert(q.dq.end(), t + i, t + i + m);
+      i += m;
+    }
+  }
+
   void stop() {
     if (!alive_.exchange(false)) return;
     for (auto &t : threads_) t.join();
   }
-
-  int64_t busy_ns() const { return busy_ns_.load(); }
 
  private:
   struct Queue {
@@ -140,12 +159,7 @@ class Pool {
       Task t;
       if (take(w, rng, &t)) {
         spins = 0;
-        const auto t0 = Clock::now();
         t.fn(t.arg);
-        busy_ns_.fetch_add(
-            std::chrono::duration_cast<std::chrono::nanoseconds>(Clock::now() - t0).count(),
-            std::memory_order_relaxed);
-        active_.fetch_sub(1, std::memory_order_relaxed);
         nap_us = 5;
         if (hook_) hook_(hook_arg_);
         continue;
@@ -174,8 +188,7 @@ class Pool {
   std::deque<Task> inj_;
   std::vector<std::thread> threads_;
   std::atomic<bool> alive_{true};
-  std::atomic<int64_t> active_{0};
-  std::atomic<int64_t> busy_ns_{0};
+  std::atomic<size_t> spread_rr_{0};
   int (*hook_)(void *) = nullptr;
   void *hook_arg_ = nullptr;
 };
@@ -200,8 +213,16 @@ class Poller {
 
   int poll() {
     if (waiting_.load(std::memory_order_relaxed) == 0) return 0;
+    // Every worker calls this after every task; with many workers the
+    // try-lock itself becomes the contended line. A body started less than
+    // kPollGapNs ago (~1/10 of the shortest batch round trip) makes the
+    // call a read of one clock and one atomic.
+    const int64_t now = std::chrono::duration_cast<std::chrono::nanoseconds>(
+                            Clock::now().time_since_epoch()).count();
+    if (now - last_ns_.load(std::memory_order_relaxed) < kPollGapNs) return 0;
     std::unique_lock<std::mutex> guard(body_, std::try_to_lock);
     if (!guard.owns_lock()) return 0;
+    last_ns_.store(now, std::memory_order_relaxed);
     struct Range {   // NVTX range over the poll body (profilers only)
       Range() { nvtxRangePushA("machine poll body"); }
       ~Range() { nvtxRangePop(); }
@@ -246,6 +267,8 @@ class Poller {
   std::mutex body_;
   std::unordered_map<uint64_t, std::deque<Entry>> chains_;
   std::atomic<int64_t> waiting_{0};
+  static constexpr int64_t kPollGapNs = 2000;
+  std::atomic<int64_t> last_ns_{0};
 };
 
 // ------------------------------------------------------ host-task threads --
@@ -406,7 +429,8 @@ struct SubTask {
 
 struct Machine {
   tb_machine_config cfg;
-  std::vector<double> cells;       // [S][512]
+  double *cells = nullptr;         // [S][512]: the caller's (run_cells) or own_cells
+  std::vector<double> own_cells;
   std::vector<double> faces;       // [S][2][8] previous generation
   std::vector<double> mins, sums;  // per sub-grid, this step
   std::unique_ptr<Pool> pool;
@@ -444,6 +468,80 @@ struct Machine {
   std::vector<double> dudt;        // [S][5][512]
   std::vector<double> amax;        // [S]
 };
+
+// Task arenas outlive a run: the pinned (device-mapped) and the device arena
+// are taken from this cache when large enough and handed back at the end of
+// the run, so repeated run_scenario calls do not re-pin 128 MiB each time. A
+// run that finds the cache empty (another run holds it) allocates its own.
+struct ArenaCache {
+  std::mutex mu;
+  double *host = nullptr;
+  size_t host_bytes = 0;
+  double *dev = nullptr;
+  size_t dev_bytes = 0;
+  int dev_id = -1;
+};
+ArenaCache g_arena;
+
+double *arena_take_host(size_t bytes) {
+  {
+    std::lock_guard<std::mutex> g(g_arena.mu);
+    if (g_arena.host && g_arena.host_bytes >= bytes) {
+      double *p = g_arena.host;
+      g_arena.host = nullptr;
+      return p;
+    }
+  }
+  double *p = nullptr;
+  if (cudaHostAlloc(reinterpret_cast<void **>(&p), bytes,
+                    cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess)
+    return nullptr;
+  return p;
+}
+
+double *arena_take_dev(size_t bytes, int dev) {
+  {
+    std::lock_guard<std::mutex> g(g_arena.mu);
+    if (g_arena.dev && g_arena.dev_bytes >= bytes && g_arena.dev_id == dev) {
+      double *p = g_arena.dev;
+      g_arena.dev = nullptr;
+      return p;
+    }
+  }
+  double *p = nullptr;
+  if (cudaMalloc(reinterpret_cast<void **>(&p), bytes) != cudaSuccess) return nullptr;
+  return p;
+}
+
+// Hand arenas back (the cache keeps the larger of the cached and the
+// returned one of each kind and frees the other).
+void arena_give(double *host, size_t host_bytes, double *dev, size_t dev_bytes, int dev_id) {
+  double *free_host = nullptr, *free_dev = nullptr;
+  {
+    std::lock_guard<std::mutex> g(g_arena.mu);
+    if (host) {
+      if (!g_arena.host || g_arena.host_bytes < host_bytes) {
+        free_host = g_arena.host;
+        g_arena.host = host;
+        g_arena.host_bytes = host_bytes;
+      } else {
+        free_host = host;
+      }
+    }
+    if (dev) {
+      if (!g_arena.dev || g_arena.dev_bytes < dev_bytes || g_arena.dev_id != dev_id) {
+        free_dev = g_arena.dev;
+        g_arena.dev = dev;
+        g_arena.dev_bytes = dev_bytes;
+        g_arena.dev_id = dev_id;
+      } else {
+        free_dev = dev;
+      }
+    }
+  }
+  if (free_host) cudaFreeHost(free_host);
+  if (free_dev) cudaFree(free_dev);
+}
 
 Staging *staging_alloc(Machine *m, size_t bytes) {
   {
@@ -528,6 +626,16 @@ void enqueue_and_bridge(Machine *m, Executor *ex, Task cont, F enqueue) {
 void resume_task(void *p);
 void hydro_resume(void *p);
 
+// The members' continuations (src/executors.py:300-301: every member's
+// promise completes), spread over the workers.
+void resume_members(const Batch *b) {
+  Machine *m = b->ex->m;
+  std::vector<Task> ts;
+  ts.reserve(b->members.size());
+  for (const Req &r : b->members) ts.push_back(Task{m->hydro ? hydro_resume : resume_task, r.task});
+  m->pool->push_spread(ts.data(), ts.size());
+}
+
 void batch_done(void *p) {   // AggregationExecutor finish (src/executors.py:286-301)
   Batch *b = static_cast<Batch *>(p);
   Machine *m = b->ex->m;
@@ -562,8 +670,7 @@ void batch_done(void *p) {   // AggregationExecutor finish (src/executors.py:286
     b->ex->stats[k].fetch_add(1, std::memory_order_relaxed);
     b->ex->stats[M + 1 + (b->idle ? 1 : 0)].fetch_add(1, std::memory_order_relaxed);
   }
-  for (const Req &r : b->members)
-    m->pool->push(Task{m->hydro ? hydro_resume : resume_task, r.task});
+  resume_members(b);
   batch_release(b);
 }
 
@@ -576,8 +683,7 @@ void launch(Batch *b, bool idle) {   // src/executors.py:257-284 as one launch
   Machine *m = ex->m;
   b->idle = idle;
   if (m->failed()) {   // the device is gone: no launch, members finish
-    for (const Req &r : b->members)
-      m->pool->push(Task{m->hydro ? hydro_resume : resume_task, r.task});
+    resume_members(b);
     batch_release(b);
     return;
   }
@@ -732,7 +838,7 @@ void start_task(void *p) {   // ghost fold + first round (src/miniapp.py:116-130
   for (int64_t k = 0; k < t->n; ++k) {
     const int64_t g = t->lo + k;
     double *w = t->work + k * kCells;
-    std::memcpy(w, m->cells.data() + g * kCells, sizeof(double) * kCells);
+    std::memcpy(w, m->cells + g * kCells, sizeof(double) * kCells);
     const double *left = m->faces.data() + ((g - 1 + S) % S) * 2 * kFace + kFace;
     const double *right = m->faces.data() + ((g + 1) % S) * 2 * kFace;
     for (int i = 0; i < kFace; ++i) w[i] = 0.5 * (w[i] + left[i]);
@@ -774,7 +880,7 @@ void resume_task(void *p) {   // next round, or write-back + post-process
   for (int64_t k = 0; k < t->n; ++k) {
     const int64_t g = t->lo + k;
     const double *w = t->work + k * kCells;
-    std::memcpy(m->cells.data() + g * kCells, w, sizeof(double) * kCells);
+    std::memcpy(m->cells + g * kCells, w, sizeof(double) * kCells);
     double mn = w[0];
     for (int i = 1; i < kCells; ++i) mn = w[i] < mn ? w[i] : mn;
     m->mins[g] = mn;
@@ -912,7 +1018,10 @@ using namespace tbm;
 
 namespace tbm {
 
-int run_machine(const tb_machine_config *cfg_in, const double *cells_in, double *checksum,
+// cells_io: the caller's [S][512] cells, advanced in place (as the
+// reference's tasks write each grid back, src/miniapp.py:132); null = the
+// closed-form initial state in machine-owned memory, copied to cells_out.
+int run_machine(const tb_machine_config *cfg_in, double *cells_io, double *checksum,
                 tb_machine_step *steps_out, double *cells_out, int64_t *exec_stats) {
   if (!cfg_in || !checksum) return TB_E_INVALID;
   const tb_machine_config &c = *cfg_in;
@@ -926,10 +1035,11 @@ int run_machine(const tb_machine_config *cfg_in, const double *cells_in, double 
   Machine m;
   m.cfg = c;
   const int64_t S = c.subgrids;
-  m.cells.resize(S * kCells);
-  if (cells_in) {
-    std::memcpy(m.cells.data(), cells_in, sizeof(double) * S * kCells);
+  if (cells_io) {
+    m.cells = cells_io;
   } else {
+    m.own_cells.resize(S * kCells);
+    m.cells = m.own_cells.data();
     const double scale = (double)(S * 1000 + kCells);
     for (int64_t g = 0; g < S; ++g)   // src/miniapp.py:72-77
       for (int i = 0; i < kCells; ++i)
@@ -938,20 +1048,19 @@ int run_machine(const tb_machine_config *cfg_in, const double *cells_in, double 
   m.faces.resize(S * 2 * kFace);
   m.mins.resize(S);
   m.sums.resize(S);
+  size_t arena_bytes = 0, dev_arena_bytes = 0;
   if (c.zero_copy == 2) {
     // every task's two work buffers in one pinned, device-mapped arena
-    if (cudaHostAlloc(reinterpret_cast<void **>(&m.arena), sizeof(double) * 2 * S * kCells,
-                      cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess)
-      return tb::rc(cudaGetLastError());
+    arena_bytes = sizeof(double) * 2 * S * kCells;
+    if (!(m.arena = arena_take_host(arena_bytes))) return tb::rc(cudaGetLastError());
   } else if (c.zero_copy == 3) {
     // one pinned, device-mapped row block per task (the host fold's input
     // and the last round's output) + two device blocks per task
-    if (cudaHostAlloc(reinterpret_cast<void **>(&m.arena), sizeof(double) * S * kCells,
-                      cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess)
-      return tb::rc(cudaGetLastError());
-    if (cudaMalloc(reinterpret_cast<void **>(&m.dev_arena), sizeof(double) * 2 * S * kCells) !=
-        cudaSuccess) {
-      cudaFreeHost(m.arena);
+    arena_bytes = sizeof(double) * S * kCells;
+    dev_arena_bytes = 2 * arena_bytes;
+    if (!(m.arena = arena_take_host(arena_bytes))) return tb::rc(cudaGetLastError());
+    if (!(m.dev_arena = arena_take_dev(dev_arena_bytes, dev))) {
+      arena_give(m.arena, arena_bytes, nullptr, 0, dev);
       return tb::rc(cudaGetLastError());
     }
   }
@@ -1005,7 +1114,12 @@ int run_machine(const tb_machine_config *cfg_in, const double *cells_in, double 
                   sizeof(double) * kFace);
     }
     m.remaining.store((int64_t)m.tasks.size());
-    for (auto &t : m.tasks) m.pool->push(Task{start_task, t.get()});
+    {
+      std::vector<Task> ts;
+      ts.reserve(m.tasks.size());
+      for (auto &t : m.tasks) ts.push_back(Task{start_task, t.get()});
+      m.pool->push_spread(ts.data(), ts.size());
+    }
     {
       std::unique_lock<std::mutex> lk(m.done_mu);
       m.done_cv.wait(lk, [&] { return m.remaining.load() == 0; });
@@ -1036,8 +1150,8 @@ int run_machine(const tb_machine_config *cfg_in, const double *cells_in, double 
     }
   }
   *checksum = cs;
-  if (cells_out && !m.failed())
-    std::memcpy(cells_out, m.cells.data(), sizeof(double) * S * kCells);
+  if (cells_out && cells_out != m.cells && !m.failed())
+    std::memcpy(cells_out, m.cells, sizeof(double) * S * kCells);
   m.pool->stop();
   m.hosttasks.reset();
   for (auto &ex : m.execs) {
@@ -1049,9 +1163,13 @@ int run_machine(const tb_machine_config *cfg_in, const double *cells_in, double 
     cudaFree(s->dev);
     delete s;
   }
-  if (m.arena) cudaFreeHost(m.arena);
-  if (m.dev_arena) cudaFree(m.dev_arena);
   const int err = tb::rc(cudaGetLastError());
+  if (!m.failed()) {
+    arena_give(m.arena, arena_bytes, m.dev_arena, dev_arena_bytes, dev);
+  } else {   // a faulted context: do not keep its memory
+    if (m.arena) cudaFreeHost(m.arena);
+    if (m.dev_arena) cudaFree(m.dev_arena);
+  }
   return m.failed() ? m.fault.load() : err;
 }
 
@@ -1128,7 +1246,10 @@ extern "C" int tb_machine_run_hydro(const tb_machine_config *cfg_in, const doubl
     const auto t0 = Clock::now();
     for (int phase = 0; phase < 2 && !m.failed(); ++phase) {   // fluxes, then the update
       m.remaining.store((int64_t)m.tasks.size());
-      for (auto &t : m.tasks) m.pool->push(Task{phase ? hydro_update : hydro_start, t.get()});
+      std::vector<Task> ts;
+      ts.reserve(m.tasks.size());
+      for (auto &t : m.tasks) ts.push_back(Task{phase ? hydro_update : hydro_start, t.get()});
+      m.pool->push_spread(ts.data(), ts.size());
       std::unique_lock<std::mutex> lk(m.done_mu);
       m.done_cv.wait(lk, [&] { return m.remaining.load() == 0; });
       if (phase == 0) {
