@@ -238,41 +238,44 @@ def python_reference_sample(subgrids: int = 4096, budget_s: float = 3.0):
                       "(initialisation included, as in the reference)"}
 
 
-def machine_ablation(subgrids=512, steps=5, repeats=3):
+def machine_ablation(subgrids=512, steps=6, repeats=5, workers=(2, 4, 8)):
     """The paper's ablation in the same run: the mini-app machine (native C++
     runtime, tb_machine_run) at the paper's scenario size (512 sub-grids,
-    PAPER.md:775-782) with 32 executors x max 8 aggregated, 8 workers
-    (PAPER.md:931-933), completion by POLLING vs HOSTTASK vs FENCE. Median of
-    `repeats` runs of the mean step time over steps 2..N."""
+    PAPER.md:775-782) with the paper's best combination, 32 executors x max 8
+    aggregated, completion by POLLING vs HOSTTASK vs FENCE — at 8 workers
+    (the top-level keys) and, as the paper's third graph does (PAPER.md:
+    931-941), with fewer workers, where a fence-blocked worker weighs more.
+    Median of `repeats` runs of the mean step time over steps 2..N."""
     from paper_2303_08058_b200.bridge import IntegrationMode
     from paper_2303_08058_b200.native_machine import run_native
-    out = {"config": f"native machine, {subgrids} sub-grids x {steps} steps, "
-                     "8 workers, 32 executors, max 8 aggregated, median of "
+    out = {"config": f"native machine, {subgrids} sub-grids x {steps} steps, 32 executors, "
+                     f"max 8 aggregated, staged batches, workers {list(workers)}, median of "
                      f"{repeats}"}
     checks = set()
-    for mode in (IntegrationMode.POLLING, IntegrationMode.HOSTTASK, IntegrationMode.FENCE):
+
+    def cell(W, mode, zero_copy=0):
         ms = []
         for _ in range(repeats):
-            res, _ = run_native(subgrids, steps, workers=8, executors=32, max_agg=8,
-                                mode=mode)
+            res, _ = run_native(subgrids, steps, workers=W, executors=32, max_agg=8,
+                                mode=mode, zero_copy=zero_copy)
             ms.append(statistics.fmean(res.step_ms[1:]))
             checks.add(res.checksum.hex())
-        out[f"{mode.value}_ms_per_step"] = statistics.median(ms)
-    out["speedup_polling_vs_fence"] = out["fence_ms_per_step"] / out["polling_ms_per_step"]
-    out["speedup_hosttask_vs_fence"] = out["fence_ms_per_step"] / out["hosttask_ms_per_step"]
-    # the same machine with zero-copy batches: each batch kernel runs in place
-    # on its pinned staging buffer (one launch + one event per batch instead
-    # of H2D ; kernel ; D2H) — B200-side cost of a 4 KiB member is the PCIe
-    # round trip either way, the host saves two API calls per batch
-    zc = {}
-    for mode in (IntegrationMode.POLLING, IntegrationMode.FENCE):
-        ms = []
-        for _ in range(repeats):
-            res, _ = run_native(subgrids, steps, workers=8, executors=32, max_agg=8,
-                                mode=mode, zero_copy=True)
-            ms.append(statistics.fmean(res.step_ms[1:]))
-            checks.add(res.checksum.hex())
-        zc[f"{mode.value}_ms_per_step"] = statistics.median(ms)
+        return statistics.median(ms)
+
+    sweep = {}
+    for W in workers:
+        row = {f"{m.value}_ms_per_step": cell(W, m) for m in
+               (IntegrationMode.POLLING, IntegrationMode.HOSTTASK, IntegrationMode.FENCE)}
+        row["speedup_polling_vs_fence"] = row["fence_ms_per_step"] / row["polling_ms_per_step"]
+        row["speedup_hosttask_vs_fence"] = row["fence_ms_per_step"] / row["hosttask_ms_per_step"]
+        sweep[f"W{W}"] = row
+    out.update(sweep[f"W{max(workers)}"])
+    out["workers_sweep"] = sweep
+    # the same machine with zero-copy batches at 8 workers: each batch kernel
+    # in place on its pinned staging buffer (one launch + one event per batch
+    # instead of H2D ; kernel ; D2H)
+    zc = {f"{m.value}_ms_per_step": cell(max(workers), m, 1)
+          for m in (IntegrationMode.POLLING, IntegrationMode.FENCE)}
     zc["speedup_polling_vs_fence"] = zc["fence_ms_per_step"] / zc["polling_ms_per_step"]
     out["zero_copy"] = zc
     out["checksums_identical"] = len(checks) == 1

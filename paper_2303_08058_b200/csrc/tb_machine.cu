@@ -23,6 +23,7 @@
 #include <chrono>
 #include <condition_variable>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <deque>
@@ -78,14 +79,22 @@ class Pool {
     }
   }
 
-  // Many ready tasks at once (a finished batch's members, a step's tasks):
-  // dealt in contiguous runs across every worker's deque from a rotating
-  // start — one lock per worker instead of every other worker stealing them
-  // one at a time from the pushing worker's deque.
+  // Many ready tasks at once (a finished batch's members, a step's tasks).
+  // More than 2 per worker: dealt in contiguous runs across every worker's
+  // deque from a rotating start — one lock per worker instead of the others
+  // stealing them one at a time from the pusher's deque (with FENCE, whose
+  // worker then blocks in the next batch's probe, that trickle shrank C4's
+  // batches to ~1 member). Fewer: kept on the pusher's deque, where its
+  // members' next requests meet the same executor without contention.
   void push_spread(const Task *t, size_t n) {
     const size_t W = qs_.size();
     if (n == 0) return;
-    if (W == 1 || n == 1) {
+    static const size_t min_spread = [] {
+      const char *e = getenv("TB_PUSH_SPREAD_MIN");   // A/B: 0 = always, huge = never
+      return e ? (size_t)atoll(e) : (size_t)0;
+    }();
+    const size_t threshold = min_spread ? min_spread : 2 * W + 1;
+    if (W == 1 || n < threshold) {
       for (size_t i = 0; i < n; ++i) push(t[i]);
       return;
     }
@@ -215,11 +224,11 @@ class Poller {
     if (waiting_.load(std::memory_order_relaxed) == 0) return 0;
     // Every worker calls this after every task; with many workers the
     // try-lock itself becomes the contended line. A body started less than
-    // kPollGapNs ago (~1/10 of the shortest batch round trip) makes the
+    // gap_ns_ ago (~1/10 of the shortest batch round trip) makes the
     // call a read of one clock and one atomic.
     const int64_t now = std::chrono::duration_cast<std::chrono::nanoseconds>(
                             Clock::now().time_since_epoch()).count();
-    if (now - last_ns_.load(std::memory_order_relaxed) < kPollGapNs) return 0;
+    if (now - last_ns_.load(std::memory_order_relaxed) < gap_ns_) return 0;
     std::unique_lock<std::mutex> guard(body_, std::try_to_lock);
     if (!guard.owns_lock()) return 0;
     last_ns_.store(now, std::memory_order_relaxed);
@@ -267,7 +276,10 @@ class Poller {
   std::mutex body_;
   std::unordered_map<uint64_t, std::deque<Entry>> chains_;
   std::atomic<int64_t> waiting_{0};
-  static constexpr int64_t kPollGapNs = 2000;
+  const int64_t gap_ns_ = [] {
+    const char *e = getenv("TB_POLL_GAP_NS");
+    return e ? (int64_t)atoll(e) : (int64_t)2000;
+  }();
   std::atomic<int64_t> last_ns_{0};
 };
 
@@ -543,19 +555,31 @@ void arena_give(double *host, size_t host_bytes, double *dev, size_t dev_bytes, 
   if (free_dev) cudaFree(free_dev);
 }
 
+// Pooled pinned + device staging in power-of-two size classes (>= 4 KiB):
+// batches of every member count share a handful of classes, so a C4 step
+// reuses buffers instead of pinning new ones for each new batch size (the
+// reference BufferPool's exact-size buckets, src/executors.py:86-121, stay
+// the Python mirror's semantics). Null on an allocation failure.
 Staging *staging_alloc(Machine *m, size_t bytes) {
+  size_t cls = 4096;
+  while (cls < bytes) cls <<= 1;
   {
     std::lock_guard<std::mutex> g(m->staging_mu);
-    auto &v = m->staging_free[bytes];
+    auto &v = m->staging_free[cls];
     if (!v.empty()) {
       Staging *s = v.back();
       v.pop_back();
       return s;
     }
   }
-  Staging *s = new Staging{bytes, nullptr, nullptr};
-  cudaHostAlloc(reinterpret_cast<void **>(&s->host), bytes, cudaHostAllocPortable);
-  cudaMalloc(reinterpret_cast<void **>(&s->dev), bytes);
+  Staging *s = new Staging{cls, nullptr, nullptr};
+  if (cudaHostAlloc(reinterpret_cast<void **>(&s->host), cls, cudaHostAllocPortable) !=
+          cudaSuccess ||
+      cudaMalloc(reinterpret_cast<void **>(&s->dev), cls) != cudaSuccess) {
+    if (s->host) cudaFreeHost(s->host);
+    delete s;
+    return nullptr;
+  }
   std::lock_guard<std::mutex> g(m->staging_mu);
   m->staging_all.push_back(s);
   return s;
@@ -719,10 +743,16 @@ void launch(Batch *b, bool idle) {   // src/executors.py:257-284 as one launch
   int64_t total = 0;
   for (const Req &r : b->members) total += r.n;
   // hydro: staging = [ghosted inputs | dU/dt + amax outputs], one size class
-  // (a full batch) so buffers are always reused; the ring keeps the
-  // reference BufferPool's exact-size buckets (src/executors.py:86-121)
+  // (a full batch) so buffers are always reused
   const size_t bytes = m->hydro ? hydro_staging_bytes(m) : sizeof(double) * total;
   b->staging = staging_alloc(m, bytes);
+  if (!b->staging) {   // out of pinned/device memory: the run fails, members finish
+    const int rc = tb::rc(cudaGetLastError());
+    m->fail(rc != TB_OK ? rc : -(int)cudaErrorMemoryAllocation);
+    resume_members(b);
+    batch_release(b);
+    return;
+  }
   int64_t off = 0;
   for (const Req &r : b->members) {
     std::memcpy(b->staging->host + off, r.src, sizeof(double) * r.n);

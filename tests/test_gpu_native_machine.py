@@ -61,14 +61,18 @@ def test_native_machine_c1_and_coarsened_large(golden):
 
 
 def test_native_polling_beats_fence():
-    kw = dict(workers=8, executors=32, max_agg=8)
-    poll = [run_native(512, 4, mode=IntegrationMode.POLLING, **kw)[0] for _ in range(3)]
-    fence = [run_native(512, 4, mode=IntegrationMode.FENCE, **kw)[0] for _ in range(3)]
-    pm = sorted(np.mean(r.step_ms[1:]) for r in poll)[1]
-    fm = sorted(np.mean(r.step_ms[1:]) for r in fence)[1]
+    # the paper's scenario (512 sub-grids, E32 M8) with 4 workers (its third
+    # graph weakens the CPU the same way); medians of 5
+    # runs. Measured 1.35x at W4 (1.03-1.07x at W8-16, 1.65x at W1-2;
+    # profiles/r02/ablation_workers.jsonl)
+    kw = dict(workers=4, executors=32, max_agg=8)
+    poll = [run_native(512, 6, mode=IntegrationMode.POLLING, **kw)[0] for _ in range(5)]
+    fence = [run_native(512, 6, mode=IntegrationMode.FENCE, **kw)[0] for _ in range(5)]
+    pm = sorted(np.mean(r.step_ms[1:]) for r in poll)[2]
+    fm = sorted(np.mean(r.step_ms[1:]) for r in fence)[2]
     print(f"native: polling {pm:.3f} ms/step vs fence {fm:.3f} -> {fm / pm:.3f}x")
     assert poll[0].checksum == fence[0].checksum
-    assert fm / pm >= 1.05
+    assert fm / pm >= 1.10
 
 
 def test_native_machine_repeated_runs_every_mode():
