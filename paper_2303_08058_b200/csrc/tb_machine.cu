@@ -23,6 +23,7 @@
 #include <chrono>
 #include <condition_variable>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -42,6 +43,48 @@
 namespace tbm {
 
 using Clock = std::chrono::steady_clock;
+
+inline int64_t now_ns() {
+  return std::chrono::duration_cast<std::chrono::nanoseconds>(Clock::now().time_since_epoch())
+      .count();
+}
+
+// TB_MACHINE_DIAG=1: per-run counters of where the host threads spend the
+// step (poll bodies, event queries, enqueue calls, idle loops), printed to
+// stderr at the end of the run. Off: one predictable branch per site.
+struct Diag {
+  std::atomic<int64_t> bodies{0}, queries{0}, not_ready{0}, body_ns{0}, enqueues{0},
+      enqueue_ns{0}, fence_ns{0}, idle_loops{0}, sleeps{0}, tasks{0};
+};
+const bool g_diag = [] {
+  const char *e = getenv("TB_MACHINE_DIAG");
+  return e && *e && *e != '0';
+}();
+Diag g_d;
+inline void diag_add(std::atomic<int64_t> &c, int64_t v) {
+  if (g_diag) c.fetch_add(v, std::memory_order_relaxed);
+}
+
+void diag_reset() {
+  if (!g_diag) return;
+  for (auto *c : {&g_d.bodies, &g_d.queries, &g_d.not_ready, &g_d.body_ns, &g_d.enqueues,
+                  &g_d.enqueue_ns, &g_d.fence_ns, &g_d.idle_loops, &g_d.sleeps, &g_d.tasks})
+    c->store(0);
+}
+
+void diag_print(int mode, int64_t workers, int64_t executors, int64_t max_agg, int64_t steps) {
+  if (!g_diag) return;
+  fprintf(stderr,
+          "{\"diag\": \"machine\", \"mode\": %d, \"workers\": %lld, \"executors\": %lld, "
+          "\"max_agg\": %lld, \"steps\": %lld, \"tasks\": %lld, \"poll_bodies\": %lld, "
+          "\"queries\": %lld, \"not_ready\": %lld, \"body_ms\": %.3f, \"enqueues\": %lld, "
+          "\"enqueue_ms\": %.3f, \"fence_ms\": %.3f, \"idle_loops\": %lld, \"sleeps\": %lld}\n",
+          mode, (long long)workers, (long long)executors, (long long)max_agg, (long long)steps,
+          (long long)g_d.tasks.load(), (long long)g_d.bodies.load(), (long long)g_d.queries.load(),
+          (long long)g_d.not_ready.load(), g_d.body_ns.load() * 1e-6, (long long)g_d.enqueues.load(),
+          g_d.enqueue_ns.load() * 1e-6, g_d.fence_ns.load() * 1e-6,
+          (long long)g_d.idle_loops.load(), (long long)g_d.sleeps.load());
+}
 
 struct Task {
   void (*fn)(void *);
@@ -71,11 +114,14 @@ class Pool {
 
   void push(Task t) {
     if (t_pool == this && t_worker >= 0) {
-      std::lock_guard<std::mutex> g(qs_[t_worker]->mu);
-      qs_[t_worker]->dq.push_back(t);
+      Queue &q = *qs_[t_worker];
+      std::lock_guard<std::mutex> g(q.mu);
+      q.dq.push_back(t);
+      q.n.store((int64_t)q.dq.size(), std::memory_order_release);
     } else {
       std::lock_guard<std::mutex> g(inj_mu_);
       inj_.push_back(t);
+      inj_n_.store((int64_t)inj_.size(), std::memory_order_release);
     }
   }
 
@@ -105,8 +151,51 @@ class Pool {
       Queue &q = *qs_[(start + k) % W];
       std::lock_guard<std::mutex> g(q.mu);
       q.dq.insert(q.dq.end(), t + i, t + i + m);
+      q.n.store((int64_t)q.dq.size(), std::memory_order_release);
       i += m;
     }
+  }
+
+  // Executor-affine dealing: the ready tasks of executor group g (of G) go
+  // to the workers w with w % G == g (W >= G), or all to worker g % W, in
+  // contiguous runs. A task's next request then meets its executor's lock
+  // on one of ~W/G workers instead of on all W, and the members of one
+  // batch do not bounce the executor's lines across every core; stealing
+  // still balances the load. TB_AFFINITY=0 restores push_spread.
+  void push_group(const Task *t, size_t n, size_t g, size_t G) {
+    const size_t W = qs_.size();
+    if (n == 0) return;
+    if (!affinity() || W == 1 || G <= 1) {
+      push_spread(t, n);
+      return;
+    }
+    if (W < G) {
+      Queue &q = *qs_[g % W];
+      std::lock_guard<std::mutex> lk(q.mu);
+      q.dq.insert(q.dq.end(), t, t + n);
+      q.n.store((int64_t)q.dq.size(), std::memory_order_release);
+      return;
+    }
+    g %= G;
+    const size_t cnt = (W - g + G - 1) / G;   // workers g, g + G, g + 2G, ...
+    const size_t start = spread_rr_.fetch_add(1, std::memory_order_relaxed) % cnt;
+    const size_t per = (n + cnt - 1) / cnt;
+    for (size_t k = 0, i = 0; i < n; ++k) {
+      const size_t m = std::min(per, n - i);
+      Queue &q = *qs_[g + ((start + k) % cnt) * G];
+      std::lock_guard<std::mutex> lk(q.mu);
+      q.dq.insert(q.dq.end(), t + i, t + i + m);
+      q.n.store((int64_t)q.dq.size(), std::memory_order_release);
+      i += m;
+    }
+  }
+
+  static bool affinity() {
+    static const bool on = [] {
+      const char *e = getenv("TB_AFFINITY");
+      return !(e && *e == '0');
+    }();
+    return on;
   }
 
   void stop() {
@@ -115,26 +204,39 @@ class Pool {
   }
 
  private:
+  // n mirrors dq.size() (written under mu): idle workers read it before
+  // taking a lock, so 16 spinning workers do not turn every queue's and the
+  // injector's mutex into a contended line for the workers that have tasks.
+  // A stale 0 only delays a take to the next loop iteration.
   struct Queue {
     std::mutex mu;
     std::deque<Task> dq;
+    std::atomic<int64_t> n{0};
   };
 
-  bool take(int w, std::mt19937_64 &rng, Task *out) {
-    {
-      Queue &q = *qs_[w];
-      std::lock_guard<std::mutex> g(q.mu);
-      if (!q.dq.empty()) {
-        *out = q.dq.front();
-        q.dq.pop_front();
-        return true;
-      }
+  static bool pop(Queue &q, bool front, Task *out) {
+    if (q.n.load(std::memory_order_acquire) == 0) return false;
+    std::lock_guard<std::mutex> g(q.mu);
+    if (q.dq.empty()) return false;
+    if (front) {
+      *out = q.dq.front();
+      q.dq.pop_front();
+    } else {
+      *out = q.dq.back();
+      q.dq.pop_back();
     }
-    {
+    q.n.store((int64_t)q.dq.size(), std::memory_order_release);
+    return true;
+  }
+
+  bool take(int w, std::mt19937_64 &rng, Task *out) {
+    if (pop(*qs_[w], true, out)) return true;
+    if (inj_n_.load(std::memory_order_acquire) > 0) {
       std::lock_guard<std::mutex> g(inj_mu_);
       if (!inj_.empty()) {
         *out = inj_.front();
         inj_.pop_front();
+        inj_n_.store((int64_t)inj_.size(), std::memory_order_release);
         return true;
       }
     }
@@ -145,14 +247,7 @@ class Pool {
     const int start = n > 1 ? (int)(rng() % n) : 0;
     for (int k = 0; k < n; ++k) {
       const int v = (start + k) % n;
-      if (v == w) continue;
-      Queue &q = *qs_[v];
-      std::lock_guard<std::mutex> g(q.mu);
-      if (!q.dq.empty()) {
-        *out = q.dq.back();
-        q.dq.pop_back();
-        return true;
-      }
+      if (v != w && pop(*qs_[v], false, out)) return true;
     }
     return false;
   }
@@ -168,6 +263,7 @@ class Pool {
       Task t;
       if (take(w, rng, &t)) {
         spins = 0;
+        diag_add(g_d.tasks, 1);
         t.fn(t.arg);
         nap_us = 5;
         if (hook_) hook_(hook_arg_);
@@ -180,10 +276,12 @@ class Pool {
       }
       // Idle: yield-spin first (a Linux sleep is >= ~50 us of timer slack,
       // far longer than a B200 batch), then the reference's 5..100 us backoff.
+      diag_add(g_d.idle_loops, 1);
       if (++spins < kIdleSpins) {
         std::this_thread::yield();
         continue;
       }
+      diag_add(g_d.sleeps, 1);
       std::this_thread::sleep_for(std::chrono::microseconds(nap_us));
       nap_us = std::min(nap_us * 2, 100);
     }
@@ -195,6 +293,7 @@ class Pool {
   std::vector<std::unique_ptr<Queue>> qs_;
   std::mutex inj_mu_;
   std::deque<Task> inj_;
+  std::atomic<int64_t> inj_n_{0};
   std::vector<std::thread> threads_;
   std::atomic<bool> alive_{true};
   std::atomic<size_t> spread_rr_{0};
@@ -226,9 +325,9 @@ class Poller {
     // try-lock itself becomes the contended line. A body started less than
     // gap_ns_ ago (~1/10 of the shortest batch round trip) makes the
     // call a read of one clock and one atomic.
-    const int64_t now = std::chrono::duration_cast<std::chrono::nanoseconds>(
-                            Clock::now().time_since_epoch()).count();
-    if (now - last_ns_.load(std::memory_order_relaxed) < gap_ns_) return 0;
+    const int64_t now = now_ns();
+    if (now - last_ns_.load(std::memory_order_relaxed) < gap_.load(std::memory_order_relaxed))
+      return 0;
     std::unique_lock<std::mutex> guard(body_, std::try_to_lock);
     if (!guard.owns_lock()) return 0;
     last_ns_.store(now, std::memory_order_relaxed);
@@ -242,11 +341,16 @@ class Poller {
       inbox_.clear();
     }
     int fired = 0;
+    int64_t queries = 0, not_ready = 0;
     for (auto it = chains_.begin(); it != chains_.end();) {
       auto &dq = it->second;
       while (!dq.empty()) {
         const cudaError_t q = cudaEventQuery(dq.front().ev);
-        if (q == cudaErrorNotReady) break;
+        ++queries;
+        if (q == cudaErrorNotReady) {
+          ++not_ready;
+          break;
+        }
         if (q != cudaSuccess) {
           int expect = 0;
           fault_->compare_exchange_strong(expect, -(int)q);
@@ -260,6 +364,20 @@ class Poller {
       it = dq.empty() ? chains_.erase(it) : std::next(it);
     }
     waiting_.fetch_sub(fired, std::memory_order_relaxed);
+    // TB_POLL_GAP_MAX_NS > gap: a body that found nothing complete doubles
+    // the gap to the next one (up to the max), one that fired resets it.
+    // Off by default: at C4 it cut 96 %-not-ready queries without changing
+    // the step time, and it slowed 2-worker polling (profiles/r02/
+    // machine_env_ab.txt)
+    gap_.store(fired ? gap_ns_ : std::min<int64_t>(2 * gap_.load(std::memory_order_relaxed),
+                                                    gap_max_ns_),
+               std::memory_order_relaxed);
+    if (g_diag) {
+      diag_add(g_d.bodies, 1);
+      diag_add(g_d.queries, queries);
+      diag_add(g_d.not_ready, not_ready);
+      diag_add(g_d.body_ns, now_ns() - now);
+    }
     return fired;
   }
 
@@ -280,6 +398,11 @@ class Poller {
     const char *e = getenv("TB_POLL_GAP_NS");
     return e ? (int64_t)atoll(e) : (int64_t)2000;
   }();
+  const int64_t gap_max_ns_ = [this] {
+    const char *e = getenv("TB_POLL_GAP_MAX_NS");
+    return std::max<int64_t>(gap_ns_, e ? (int64_t)atoll(e) : (int64_t)0);
+  }();
+  std::atomic<int64_t> gap_{gap_ns_};
   std::atomic<int64_t> last_ns_{0};
 };
 
@@ -610,7 +733,9 @@ void bridge(Machine *m, Executor *ex, cudaEvent_t ev, Task cont) {
       break;
     default: {  // FENCE: block this worker, then the future is ready
       m->event_waits.fetch_add(1, std::memory_order_relaxed);
+      const int64_t t0 = g_diag ? now_ns() : 0;
       const cudaError_t e = cudaEventSynchronize(ev);
+      if (g_diag) diag_add(g_d.fence_ns, now_ns() - t0);
       if (e != cudaSuccess) m->fail(-(int)e);
       tb_event_release(reinterpret_cast<tb_event_t>(ev));
       m->pool->push(cont);
@@ -625,7 +750,15 @@ void bridge(Machine *m, Executor *ex, cudaEvent_t ev, Task cont) {
 // enqueue still bridges (ev may be 0: the query reports an error) so the
 // continuation runs and sees the failure.
 template <typename F>
-void enqueue_and_bridge(Machine *m, Executor *ex, Task cont, F enqueue) {
+void enqueue_and_bridge(Machine *m, Executor *ex, Task cont, F enqueue_) {
+  auto enqueue = [&](tb_event_t *ev) {
+    if (!g_diag) return enqueue_(ev);
+    const int64_t t0 = now_ns();
+    const int rc = enqueue_(ev);
+    diag_add(g_d.enqueues, 1);
+    diag_add(g_d.enqueue_ns, now_ns() - t0);
+    return rc;
+  };
   tb_event_t ev = 0;
   if (m->cfg.mode == TB_MODE_POLLING) {
     std::lock_guard<std::mutex> g(ex->rec_mu);
@@ -657,7 +790,7 @@ void resume_members(const Batch *b) {
   std::vector<Task> ts;
   ts.reserve(b->members.size());
   for (const Req &r : b->members) ts.push_back(Task{m->hydro ? hydro_resume : resume_task, r.task});
-  m->pool->push_spread(ts.data(), ts.size());
+  m->pool->push_group(ts.data(), ts.size(), (size_t)b->ex->id, m->execs.size());
 }
 
 void batch_done(void *p) {   // AggregationExecutor finish (src/executors.py:286-301)
@@ -1094,6 +1227,7 @@ int run_machine(const tb_machine_config *cfg_in, double *cells_io, double *check
       return tb::rc(cudaGetLastError());
     }
   }
+  diag_reset();
   m.pool.reset(new Pool((int)c.workers, dev, 1234));
   m.poller.reset(new Poller(m.pool.get(), &m.fault));
   if (c.mode == TB_MODE_POLLING) m.pool->set_idle_hook(&Poller::hook, m.poller.get());
@@ -1145,10 +1279,11 @@ int run_machine(const tb_machine_config *cfg_in, double *cells_io, double *check
     }
     m.remaining.store((int64_t)m.tasks.size());
     {
-      std::vector<Task> ts;
-      ts.reserve(m.tasks.size());
-      for (auto &t : m.tasks) ts.push_back(Task{start_task, t.get()});
-      m.pool->push_spread(ts.data(), ts.size());
+      // each executor's tasks to its worker group (Pool::push_group)
+      const size_t E = m.execs.size();
+      std::vector<std::vector<Task>> by(E);
+      for (auto &t : m.tasks) by[(size_t)t->ex->id].push_back(Task{start_task, t.get()});
+      for (size_t e = 0; e < E; ++e) m.pool->push_group(by[e].data(), by[e].size(), e, E);
     }
     {
       std::unique_lock<std::mutex> lk(m.done_mu);
@@ -1180,6 +1315,7 @@ int run_machine(const tb_machine_config *cfg_in, double *cells_io, double *check
     }
   }
   *checksum = cs;
+  diag_print((int)c.mode, c.workers, c.executors, c.max_agg, c.steps);
   if (cells_out && cells_out != m.cells && !m.failed())
     std::memcpy(cells_out, m.cells, sizeof(double) * S * kCells);
   m.pool->stop();
@@ -1240,6 +1376,7 @@ extern "C" int tb_machine_run_hydro(const tb_machine_config *cfg_in, const doubl
   m.U.assign(U_in, U_in + S * kInterior);
   m.dudt.resize(S * kInterior);
   m.amax.resize(S);
+  diag_reset();
   m.pool.reset(new Pool((int)c.workers, dev, 1234));
   m.poller.reset(new Poller(m.pool.get(), &m.fault));
   if (c.mode == TB_MODE_POLLING) m.pool->set_idle_hook(&Poller::hook, m.poller.get());
@@ -1279,7 +1416,7 @@ extern "C" int tb_machine_run_hydro(const tb_machine_config *cfg_in, const doubl
       std::vector<Task> ts;
       ts.reserve(m.tasks.size());
       for (auto &t : m.tasks) ts.push_back(Task{phase ? hydro_update : hydro_start, t.get()});
-      m.pool->push_spread(ts.data(), ts.size());
+      m.pool->push_spread(ts.data(), ts.size());   // hydro_update is host work: any worker
       std::unique_lock<std::mutex> lk(m.done_mu);
       m.done_cv.wait(lk, [&] { return m.remaining.load() == 0; });
       if (phase == 0) {
