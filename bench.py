@@ -286,44 +286,79 @@ def machine_ablation(subgrids=512, steps=6, repeats=5, workers=(2, 4, 8)):
 # task structure; run_reference(32768, 1) pins step 1
 C4_CHECKSUM = float.fromhex("0x1.fffc131fd56c6p+22")
 C4_DT = float.fromhex("0x1.a73380416f1a6p-22")
-# the sweeps' best polling configuration (scripts/c4_machine_sweep.py and
-# scripts/c4_gather_sweep.py, profiles/r02/c4_*sweep.jsonl): 16 workers (the
-# box's host cores), 8 executors, max 256 aggregated, batch members read and
-# written in place in the tasks' pinned buffers
-C4_MACHINE = dict(workers=16, executors=8, max_agg=256, zero_copy=2)
+# the sweeps' best polling configuration (scripts/c4_machine_sweep.py,
+# c4_gather_sweep.py, c4_resident_sweep.py; profiles/r02/c4_*sweep.jsonl):
+# 16 workers (the box's host cores), 8 executors, max 256 aggregated,
+# resident batches (each task's rounds between the first and the last stay in
+# HBM; gather batches move every round over PCIe: 4 GB per step, a 40 ms floor)
+C4_MACHINE = dict(workers=16, executors=8, max_agg=256, zero_copy=3)
+C4_SWEEP = [(8, 8), (8, 16), (16, 16)]   # (workers, executors) beside C4_MACHINE
 
 
-def machine_ablation_c4(steps=3):
+def machine_ablation_c4(steps=4, repeats=3):
     """The paper's ablation at BASELINE config 4: the native machine on 32768
     sub-grids with the reference task structure (one task and 15 schedule()
     calls per sub-grid per step, src/miniapp.py:116-171, driven as
     src/cli.py:199-232), POLLING vs HOSTTASK vs FENCE at identical
-    (W, E, M); plus the staged op sequence (H2D ; kernel ; D2H per batch) at
-    the same (W, E, M) under POLLING. Mean step time over steps 2..N, mean
-    batch size, speed-ups = fence_ms / mode_ms (src/cli.py:297-306); parity:
-    every run's first step equals run_reference(32768, 1)."""
+    (W, E, M); gather batches (every round over PCIe) under POLLING and FENCE
+    and the staged op sequence (H2D ; kernel ; D2H per batch) under POLLING at
+    the same (W, E, M); and a (workers, executors) sweep. A run's time is the
+    mean step time over steps 2..N; each cell is the median of `repeats`
+    runs, the runs of the modes compared interleaved (a host-side scheduler
+    on a shared box is noisy: one run to the next varies by up to 1.5x,
+    profiles/r02/c4_context_probe.txt). Speed-ups = fence_ms / mode_ms
+    (src/cli.py:297-306); parity: every run's first step equals
+    run_reference(32768, 1)."""
     from paper_2303_08058_b200.bridge import IntegrationMode
     from paper_2303_08058_b200.native_machine import run_native
+    P, H, F = IntegrationMode.POLLING, IntegrationMode.HOSTTASK, IntegrationMode.FENCE
     out = {"config": "native machine, 32768 sub-grids (max_level 5), reference task structure "
                      f"(491,520 schedule() calls per step), {C4_MACHINE['workers']} workers, "
                      f"{C4_MACHINE['executors']} executors, max {C4_MACHINE['max_agg']} "
-                     "aggregated, gather batches (members in place in pinned task buffers), "
-                     f"{steps} steps (mean of steps 2..{steps})"}
-    checks, golden = set(), True
-    runs = [(m.value, m, C4_MACHINE) for m in IntegrationMode]
-    runs.append(("staged_polling", IntegrationMode.POLLING, dict(C4_MACHINE, zero_copy=0)))
-    for name, mode, kw in runs:
-        res, _ = run_native(32768, steps, mode=mode, **kw)
-        out[f"{name}_ms_per_step"] = statistics.fmean(res.step_ms[1:])
+                     "aggregated, resident batches (rounds 2..14 of each task in HBM, rounds 1 "
+                     f"and 15 on its pinned rows), {steps} steps (mean of steps 2..{steps}), "
+                     f"median of {repeats} interleaved runs"}
+    checks, golden = set(), [True]
+
+    def compare(cells):
+        """cells: [(name, mode, machine kwargs)] -> {name: (median ms, last run)}"""
+        ms = {name: [] for name, _, _ in cells}
+        last = {}
+        for _ in range(repeats):
+            for name, mode, kw in cells:
+                res, _ = run_native(32768, steps, mode=mode, **kw)
+                ms[name].append(statistics.fmean(res.step_ms[1:]))
+                last[name] = res
+                checks.add(res.checksum.hex())
+                golden[0] &= (res.per_step[0].checksum_piece == C4_CHECKSUM
+                              and res.dts[0] == C4_DT)
+        return {name: (statistics.median(v), last[name]) for name, v in ms.items()}
+
+    main = compare([(m.value, m, C4_MACHINE) for m in (P, H, F)]
+                   + [("gather_polling", P, dict(C4_MACHINE, zero_copy=2)),
+                      ("gather_fence", F, dict(C4_MACHINE, zero_copy=2))])
+    main.update(compare([("staged_polling", P, dict(C4_MACHINE, zero_copy=0))]))
+    for name, (ms, res) in main.items():
+        out[f"{name}_ms_per_step"] = ms
         out[f"{name}_mean_batch"] = res.per_step[-1].mean_batch
         out[f"{name}_launches_per_step"] = res.per_step[-1].launches
-        checks.add(res.checksum.hex())
-        golden &= (res.per_step[0].checksum_piece == C4_CHECKSUM and res.dts[0] == C4_DT)
     out["speedup_polling_vs_fence"] = out["fence_ms_per_step"] / out["polling_ms_per_step"]
     out["speedup_hosttask_vs_fence"] = out["fence_ms_per_step"] / out["hosttask_ms_per_step"]
+    out["gather_speedup_polling_vs_fence"] = (out["gather_fence_ms_per_step"]
+                                              / out["gather_polling_ms_per_step"])
     out["cells_per_s_polling"] = 32768 * 512 / (out["polling_ms_per_step"] * 1e-3)
+    # the same at other (workers, executors): where a fence-blocked worker
+    # weighs more or less (polling and fence at identical settings)
+    sweep = {}
+    for W, E in C4_SWEEP:
+        kw = dict(C4_MACHINE, workers=W, executors=E)
+        r = compare([("polling", P, kw), ("fence", F, kw)])
+        row = {"polling_ms_per_step": r["polling"][0], "fence_ms_per_step": r["fence"][0]}
+        row["speedup_polling_vs_fence"] = row["fence_ms_per_step"] / row["polling_ms_per_step"]
+        sweep[f"W{W}_E{E}"] = row
+    out["sweep"] = sweep
     out["checksums_identical"] = len(checks) == 1
-    out["step1_equals_run_reference_32768x1"] = golden
+    out["step1_equals_run_reference_32768x1"] = golden[0]
     return out
 
 
@@ -642,14 +677,15 @@ def hydro_machine_ablation(subgrids=512, steps=8, repeats=3):
     out = {"config": f"native machine, hydro (K6) tasks, {subgrids} sub-grids x {steps} "
                      f"steps, 8 workers, 32 executors, max 8 aggregated, median of {repeats}"}
     finals = set()
-    for mode in IntegrationMode:
-        ms = []
-        for _ in range(repeats):
+    ms = {mode: [] for mode in IntegrationMode}
+    for _ in range(repeats):            # the modes' runs interleaved
+        for mode in IntegrationMode:
             per, U = run_native_hydro(I, steps, workers=8, executors=32, max_agg=8, mode=mode)
-            ms.append(statistics.fmean(m.wall_ms for m in per[2:]))
+            ms[mode].append(statistics.fmean(m.wall_ms for m in per[2:]))
             finals.add(hash(U.tobytes()))
-        out[f"{mode.value}_ms_per_step"] = statistics.median(ms)
-        out[f"{mode.value}_mean_batch"] = per[-1].mean_batch
+            out[f"{mode.value}_mean_batch"] = per[-1].mean_batch
+    for mode in IntegrationMode:
+        out[f"{mode.value}_ms_per_step"] = statistics.median(ms[mode])
     out["speedup_polling_vs_fence"] = out["fence_ms_per_step"] / out["polling_ms_per_step"]
     out["speedup_hosttask_vs_fence"] = out["fence_ms_per_step"] / out["hosttask_ms_per_step"]
     out["results_identical"] = len(finals) == 1

@@ -17,6 +17,8 @@
 // Results are bit-identical to the reference (the kernels are K1; the host
 // reductions follow numpy's pairwise order and math.fsum exactly).
 #include <cuda_runtime.h>
+#include <pthread.h>
+#include <sched.h>
 
 #include <algorithm>
 #include <atomic>
@@ -50,40 +52,52 @@ inline int64_t now_ns() {
 }
 
 // TB_MACHINE_DIAG=1: per-run counters of where the host threads spend the
-// step (poll bodies, event queries, enqueue calls, idle loops), printed to
+// step (tasks, poll bodies, event queries, enqueue calls, fences, idle
+// loops), kept per thread and summed when the workers exit, printed to
 // stderr at the end of the run. Off: one predictable branch per site.
-struct Diag {
-  std::atomic<int64_t> bodies{0}, queries{0}, not_ready{0}, body_ns{0}, enqueues{0},
-      enqueue_ns{0}, fence_ns{0}, idle_loops{0}, sleeps{0}, tasks{0};
+enum DiagField {
+  kTasks, kTaskNs, kHookNs, kSteals, kBodies, kQueries, kNotReady, kBodyNs, kEnqueues,
+  kEnqueueNs, kFenceNs, kIdleLoops, kSleeps, kDiagFields
 };
+const char *const kDiagNames[kDiagFields] = {
+    "tasks", "task_ms", "hook_ms", "steals", "poll_bodies", "queries", "not_ready", "body_ms",
+    "enqueues", "enqueue_ms", "fence_ms", "idle_loops", "sleeps"};
 const bool g_diag = [] {
   const char *e = getenv("TB_MACHINE_DIAG");
   return e && *e && *e != '0';
 }();
-Diag g_d;
-inline void diag_add(std::atomic<int64_t> &c, int64_t v) {
-  if (g_diag) c.fetch_add(v, std::memory_order_relaxed);
+std::atomic<int64_t> g_diag_sum[kDiagFields];
+thread_local int64_t t_diag[kDiagFields];
+inline void diag_add(DiagField f, int64_t v) {
+  if (g_diag) t_diag[f] += v;
+}
+// a worker's counters into the run's sums (at thread exit)
+inline void diag_flush() {
+  if (!g_diag) return;
+  for (int f = 0; f < kDiagFields; ++f) {
+    g_diag_sum[f].fetch_add(t_diag[f]);
+    t_diag[f] = 0;
+  }
 }
 
 void diag_reset() {
   if (!g_diag) return;
-  for (auto *c : {&g_d.bodies, &g_d.queries, &g_d.not_ready, &g_d.body_ns, &g_d.enqueues,
-                  &g_d.enqueue_ns, &g_d.fence_ns, &g_d.idle_loops, &g_d.sleeps, &g_d.tasks})
-    c->store(0);
+  for (auto &c : g_diag_sum) c.store(0);
 }
 
 void diag_print(int mode, int64_t workers, int64_t executors, int64_t max_agg, int64_t steps) {
   if (!g_diag) return;
-  fprintf(stderr,
-          "{\"diag\": \"machine\", \"mode\": %d, \"workers\": %lld, \"executors\": %lld, "
-          "\"max_agg\": %lld, \"steps\": %lld, \"tasks\": %lld, \"poll_bodies\": %lld, "
-          "\"queries\": %lld, \"not_ready\": %lld, \"body_ms\": %.3f, \"enqueues\": %lld, "
-          "\"enqueue_ms\": %.3f, \"fence_ms\": %.3f, \"idle_loops\": %lld, \"sleeps\": %lld}\n",
-          mode, (long long)workers, (long long)executors, (long long)max_agg, (long long)steps,
-          (long long)g_d.tasks.load(), (long long)g_d.bodies.load(), (long long)g_d.queries.load(),
-          (long long)g_d.not_ready.load(), g_d.body_ns.load() * 1e-6, (long long)g_d.enqueues.load(),
-          g_d.enqueue_ns.load() * 1e-6, g_d.fence_ns.load() * 1e-6,
-          (long long)g_d.idle_loops.load(), (long long)g_d.sleeps.load());
+  fprintf(stderr, "{\"diag\": \"machine\", \"mode\": %d, \"workers\": %lld, \"executors\": %lld, "
+          "\"max_agg\": %lld, \"steps\": %lld", mode, (long long)workers, (long long)executors,
+          (long long)max_agg, (long long)steps);
+  for (int f = 0; f < kDiagFields; ++f) {
+    const int64_t v = g_diag_sum[f].load();
+    if (strstr(kDiagNames[f], "_ms"))
+      fprintf(stderr, ", \"%s\": %.3f", kDiagNames[f], v * 1e-6);
+    else
+      fprintf(stderr, ", \"%s\": %lld", kDiagNames[f], (long long)v);
+  }
+  fprintf(stderr, "}\n");
 }
 
 struct Task {
@@ -247,13 +261,17 @@ class Pool {
     const int start = n > 1 ? (int)(rng() % n) : 0;
     for (int k = 0; k < n; ++k) {
       const int v = (start + k) % n;
-      if (v != w && pop(*qs_[v], false, out)) return true;
+      if (v != w && pop(*qs_[v], false, out)) {
+        diag_add(kSteals, 1);
+        return true;
+      }
     }
     return false;
   }
 
   void run(int w, uint64_t seed) {
     cudaSetDevice(device_);
+    pin(w);
     t_pool = this;
     t_worker = w;
     std::mt19937_64 rng(seed);
@@ -263,10 +281,19 @@ class Pool {
       Task t;
       if (take(w, rng, &t)) {
         spins = 0;
-        diag_add(g_d.tasks, 1);
-        t.fn(t.arg);
+        if (g_diag) {
+          const int64_t t0 = now_ns();
+          t.fn(t.arg);
+          const int64_t t1 = now_ns();
+          if (hook_) hook_(hook_arg_);
+          diag_add(kTasks, 1);
+          diag_add(kTaskNs, t1 - t0);
+          diag_add(kHookNs, now_ns() - t1);
+        } else {
+          t.fn(t.arg);
+          if (hook_) hook_(hook_arg_);
+        }
         nap_us = 5;
-        if (hook_) hook_(hook_arg_);
         continue;
       }
       if (hook_ && hook_(hook_arg_)) {
@@ -276,17 +303,38 @@ class Pool {
       }
       // Idle: yield-spin first (a Linux sleep is >= ~50 us of timer slack,
       // far longer than a B200 batch), then the reference's 5..100 us backoff.
-      diag_add(g_d.idle_loops, 1);
+      diag_add(kIdleLoops, 1);
       if (++spins < kIdleSpins) {
         std::this_thread::yield();
         continue;
       }
-      diag_add(g_d.sleeps, 1);
+      diag_add(kSleeps, 1);
       std::this_thread::sleep_for(std::chrono::microseconds(nap_us));
       nap_us = std::min(nap_us * 2, 100);
     }
+    diag_flush();
     t_pool = nullptr;
     t_worker = -1;
+  }
+
+  // TB_PIN_WORKERS=1: worker w runs on the w-th CPU of the process's
+  // affinity mask (modulo its size)
+  static void pin(int w) {
+    static const bool on = [] {
+      const char *e = getenv("TB_PIN_WORKERS");
+      return e && *e == '1';
+    }();
+    if (!on) return;
+    cpu_set_t mask;
+    if (sched_getaffinity(0, sizeof(mask), &mask) != 0) return;
+    std::vector<int> cpus;
+    for (int c = 0; c < CPU_SETSIZE; ++c)
+      if (CPU_ISSET(c, &mask)) cpus.push_back(c);
+    if (cpus.empty()) return;
+    cpu_set_t one;
+    CPU_ZERO(&one);
+    CPU_SET(cpus[(size_t)w % cpus.size()], &one);
+    pthread_setaffinity_np(pthread_self(), sizeof(one), &one);
   }
 
   int device_;
@@ -320,12 +368,19 @@ class Poller {
   static int hook(void *self) { return static_cast<Poller *>(self)->poll(); }
 
   int poll() {
+    // each thread looks at the shared lines (waiting_, last_ns_, the body
+    // lock) at most once per half gap: after every task the check is one
+    // clock read, not a cache miss on lines the body and add() write
+    thread_local int64_t next_try = 0;
+    const int64_t t = now_ns();
+    if (t < next_try) return 0;
+    next_try = t + gap_ns_ / 2;
     if (waiting_.load(std::memory_order_relaxed) == 0) return 0;
     // Every worker calls this after every task; with many workers the
     // try-lock itself becomes the contended line. A body started less than
     // gap_ns_ ago (~1/10 of the shortest batch round trip) makes the
     // call a read of one clock and one atomic.
-    const int64_t now = now_ns();
+    const int64_t now = t;
     if (now - last_ns_.load(std::memory_order_relaxed) < gap_.load(std::memory_order_relaxed))
       return 0;
     std::unique_lock<std::mutex> guard(body_, std::try_to_lock);
@@ -373,10 +428,10 @@ class Poller {
                                                     gap_max_ns_),
                std::memory_order_relaxed);
     if (g_diag) {
-      diag_add(g_d.bodies, 1);
-      diag_add(g_d.queries, queries);
-      diag_add(g_d.not_ready, not_ready);
-      diag_add(g_d.body_ns, now_ns() - now);
+      diag_add(kBodies, 1);
+      diag_add(kQueries, queries);
+      diag_add(kNotReady, not_ready);
+      diag_add(kBodyNs, now_ns() - now);
     }
     return fired;
   }
@@ -735,7 +790,7 @@ void bridge(Machine *m, Executor *ex, cudaEvent_t ev, Task cont) {
       m->event_waits.fetch_add(1, std::memory_order_relaxed);
       const int64_t t0 = g_diag ? now_ns() : 0;
       const cudaError_t e = cudaEventSynchronize(ev);
-      if (g_diag) diag_add(g_d.fence_ns, now_ns() - t0);
+      if (g_diag) diag_add(kFenceNs, now_ns() - t0);
       if (e != cudaSuccess) m->fail(-(int)e);
       tb_event_release(reinterpret_cast<tb_event_t>(ev));
       m->pool->push(cont);
@@ -755,8 +810,8 @@ void enqueue_and_bridge(Machine *m, Executor *ex, Task cont, F enqueue_) {
     if (!g_diag) return enqueue_(ev);
     const int64_t t0 = now_ns();
     const int rc = enqueue_(ev);
-    diag_add(g_d.enqueues, 1);
-    diag_add(g_d.enqueue_ns, now_ns() - t0);
+    diag_add(kEnqueues, 1);
+    diag_add(kEnqueueNs, now_ns() - t0);
     return rc;
   };
   tb_event_t ev = 0;
@@ -783,13 +838,53 @@ void enqueue_and_bridge(Machine *m, Executor *ex, Task cont, F enqueue_) {
 void resume_task(void *p);
 void hydro_resume(void *p);
 
+// A run of one batch's member continuations executed as one pool task: the
+// pool's per-task work (deque lock, pop, steal, poll hook) is paid once per
+// kResumeChunk members instead of once per member. Each member's
+// continuation still runs exactly once, on a worker, after the batch
+// completed (src/executors.py:300-301); the chunks are stealable.
+constexpr size_t kResumeChunk = 16;
+struct ResumeChunk {
+  void (*fn)(void *);
+  uint32_t n;
+  SubTask *t[kResumeChunk];
+};
+
+void resume_chunk(void *p) {
+  ResumeChunk *c = static_cast<ResumeChunk *>(p);
+  for (uint32_t i = 0; i < c->n; ++i) c->fn(c->t[i]);
+  delete c;
+}
+
+size_t resume_chunk_size() {
+  static const size_t k = [] {
+    const char *e = getenv("TB_RESUME_CHUNK");   // A/B: 1 = one pool task per member
+    const long v = e ? atol(e) : (long)kResumeChunk;
+    return (size_t)std::max<long>(1, std::min<long>(v, (long)kResumeChunk));
+  }();
+  return k;
+}
+
 // The members' continuations (src/executors.py:300-301: every member's
-// promise completes), spread over the workers.
+// promise completes), dealt to the executor's worker group in chunks.
 void resume_members(const Batch *b) {
   Machine *m = b->ex->m;
+  void (*fn)(void *) = m->hydro ? hydro_resume : resume_task;
+  const size_t n = b->members.size(), k = resume_chunk_size();
   std::vector<Task> ts;
-  ts.reserve(b->members.size());
-  for (const Req &r : b->members) ts.push_back(Task{m->hydro ? hydro_resume : resume_task, r.task});
+  if (k == 1) {
+    ts.reserve(n);
+    for (const Req &r : b->members) ts.push_back(Task{fn, r.task});
+  } else {
+    ts.reserve((n + k - 1) / k);
+    for (size_t i = 0; i < n; i += k) {
+      ResumeChunk *c = new ResumeChunk;
+      c->fn = fn;
+      c->n = (uint32_t)std::min(k, n - i);
+      for (uint32_t j = 0; j < c->n; ++j) c->t[j] = b->members[i + j].task;
+      ts.push_back(Task{resume_chunk, c});
+    }
+  }
   m->pool->push_group(ts.data(), ts.size(), (size_t)b->ex->id, m->execs.size());
 }
 
@@ -1315,10 +1410,10 @@ int run_machine(const tb_machine_config *cfg_in, double *cells_io, double *check
     }
   }
   *checksum = cs;
-  diag_print((int)c.mode, c.workers, c.executors, c.max_agg, c.steps);
   if (cells_out && cells_out != m.cells && !m.failed())
     std::memcpy(cells_out, m.cells, sizeof(double) * S * kCells);
   m.pool->stop();
+  diag_print((int)c.mode, c.workers, c.executors, c.max_agg, c.steps);
   m.hosttasks.reset();
   for (auto &ex : m.execs) {
     cudaStreamSynchronize(ex->stream);
