@@ -262,6 +262,10 @@ int tb_hydro_flux(tb_stream_t s, const double *U, double *dudt, double *amax,
  * of nz planes (Up [5][nz+4][n+4][n+4]) gives nb*nb*nz/8 sub-grids. */
 int tb_hydro_flux_lattice(tb_stream_t s, const double *Up, int64_t n, int64_t nz,
                           double *dudt, double *amax, double dx, double gamma);
+/* Profiling probe (not on the product path): the per-CTA %globaltimer
+ * stamps, ns, of the last K6 launch made with TB_HYDRO_VARIANT=1020 —
+ * out[n][4] = entry, first sub-grid staged, last faces done, exit; n <= 1024. */
+int tb_hydro_stamps(unsigned long long *out, int n);
 
 /* The coupled rotating-star step (PARITY UNPINNED; spec oracle/star_oracle.py):
  * U [5][n][n][n] lattice (rho, sx, sy, sz, E), periodic hydro, isolated FMM

@@ -17,6 +17,9 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <atomic>
+#include <type_traits>
+
 #include "../../include/tb.h"
 #include "tb_internal.h"
 
@@ -27,12 +30,32 @@ constexpr int NCELL = NT * NT * NT;            // 1728
 constexpr int NFACE = (NI + 1) * NI * NI;      // 576 faces per direction
 // threads per CTA: 256, or 320 with TB_HYDRO_VARIANT bit 4
 constexpr int threads_of(int v) { return (v & 16) ? 320 : 256; }
-constexpr int kDefaultVariant = 508;
+constexpr int kDefaultVariant = 1532;
 constexpr int kSmem = (NF * NCELL + 2 * NF * NFACE) * 8;   // 115,200 B (2 CTAs/SM)
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+
+// bit 9 (probe only): per-CTA %globaltimer stamps — entry, first sub-grid
+// staged, last sub-grid's faces done, exit — for the launch's head and tail
+// (tb_hydro_stamps; scripts/k6_stamps_probe.py)
+constexpr int kStampCtas = 1024;
+__device__ unsigned long long g_k6_stamps[kStampCtas][4];
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// bit 10's work counters: [slot][next sub-grid, finished CTAs], zero at
+// module load and reset by each launch's last CTA; a launch takes the next
+// slot of the ring, so launches on concurrent streams (the machine's
+// executors) do not share one
+constexpr unsigned kWorkSlots = 4096;
+__device__ unsigned int g_k6_work[kWorkSlots][2];
+std::atomic<unsigned> g_work_next{0};
 
 struct State {
   double u[NF], f[NF], a;
@@ -181,17 +204,27 @@ template <bool LATTICE, int V>
 __global__ void __launch_bounds__(threads_of(V), 2)
     k_hydro_flux(const double *__restrict__ U, const __grid_constant__ CUtensorMap map, int nb,
                  double *__restrict__ dudt, double *__restrict__ amax_out, int64_t nsub,
-                 double dx, double gamma) {
+                 double dx, double gamma, unsigned int slot) {
   extern __shared__ __align__(128) double sm[];
   double *W = sm;                        // [5][1728] primitives (staged U)
   double *Fb0 = sm + NF * NCELL;         // [2][5][576] face fluxes, by direction parity
   __shared__ __align__(8) uint64_t bar;
+  // bit 10: dynamic sub-grid assignment — after its first (blockIdx.x), a CTA
+  // takes the next sub-grid from work[0] when it starts one (work[1] counts
+  // finished CTAs; the last resets both for the slot's next launch). The
+  // static stride left CTAs finishing up to 43 us apart at config 2 (SM
+  // pairing, slow-path sub-grids; scripts/k6_stamps_probe.py).
+  constexpr bool kDynamic = (V & 1024) != 0;
+  __shared__ int64_t s_next[2];
+  unsigned int *const work = g_k6_work[slot % kWorkSlots];
   constexpr int kThreads = threads_of(V);
   constexpr int kCellsPerThread = (NI * NI * NI + kThreads - 1) / kThreads;   // 2
   __shared__ double s_amax[kThreads / 32];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const double gm1 = __dadd_rn(gamma, -1.0);
   const double igm1 = __ddiv_rn(1.0, gm1), idx = __ddiv_rn(1.0, dx);
+  constexpr bool kStamps = (V & 512) != 0;
+  if (kStamps && t == 0 && blockIdx.x < kStampCtas) g_k6_stamps[blockIdx.x][0] = gtimer();
   if (t == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -237,17 +270,33 @@ __global__ void __launch_bounds__(threads_of(V), 2)
                    : "memory");
     }
   };
-  if (t == 0 && blockIdx.x < nsub) issue(blockIdx.x);
-  uint32_t phase = 0;
-  for (int64_t s = blockIdx.x; s < nsub; s += gridDim.x, phase ^= 1) {
-    if ((V & 64) && t == 0 && s + gridDim.x < nsub) prefetch_l2(s + gridDim.x);
+  auto wait_bar = [&](uint64_t *b, uint32_t ph) {
     asm volatile(
         "{\n\t.reg .pred p;\nHW_%=:\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra HW_%=;\n}" ::"r"(smem_u32(&bar)),
-        "r"(phase)
+        "@!p bra HW_%=;\n}" ::"r"(smem_u32(b)),
+        "r"(ph)
         : "memory");
+  };
+  if (t == 0 && blockIdx.x < nsub) issue(blockIdx.x);
+  uint32_t phase = 0;
+  int it = 0;
+  for (int64_t s = blockIdx.x; s < nsub; phase ^= 1, ++it) {
+    // the sub-grid this CTA stages next (issued after the last face pass)
+    int64_t nxt = 0;
+    if constexpr (kDynamic) {
+      if (t == 0) {
+        nxt = (int64_t)gridDim.x + (int64_t)atomicAdd(work, 1u);
+        s_next[(it + 1) & 1] = nxt;
+      }
+    } else {
+      nxt = s + gridDim.x;
+    }
+    if ((V & 64) && t == 0 && nxt < nsub) prefetch_l2(nxt);
+    wait_bar(&bar, phase);
     if ((V & 256) && t == 0) amax_out[s] = 0.0;   // bit 8's atomic max starts at +0
+    if (kStamps && t == 0 && s == blockIdx.x && blockIdx.x < kStampCtas)
+      g_k6_stamps[blockIdx.x][1] = gtimer();
     // ---- conserved -> primitive, in place --------------------------------
     constexpr bool kFast = (V & 8) != 0;
     constexpr bool kSlowOut = (V & 32) != 0;
@@ -268,28 +317,32 @@ __global__ void __launch_bounds__(threads_of(V), 2)
       // group is redone with the intrinsic (bit 7: one group of 6 covers the
       // 5.4 cells per thread of a 320-thread CTA in a single pass)
       constexpr int kG = (V & 128) ? 6 : 4;
-#pragma unroll 1
-      for (int c0 = t; c0 < NCELL; c0 += kG * kThreads) {
-        double ir[kG];
+      // NU cells c0 + u * kThreads (u < NU): fast reciprocals interleaved, the
+      // group redone with the intrinsic if any flags, then converted
+      auto group = [&](int c0, auto nu) {
+        constexpr int NU = decltype(nu)::value;
+        double ir[NU];
         bool ok = true;
 #pragma unroll
-        for (int u = 0; u < kG; ++u) {
+        for (int u = 0; u < NU; ++u) {
           const int c = c0 + u * kThreads;
           ir[u] = tb::div_rn_fast(1.0, c < NCELL ? W[c] : 1.0, ok);
         }
         if (!ok) {
 #pragma unroll
-          for (int u = 0; u < kG; ++u) {
+          for (int u = 0; u < NU; ++u) {
             const int c = c0 + u * kThreads;
             ir[u] = __ddiv_rn(1.0, c < NCELL ? W[c] : 1.0);
           }
         }
 #pragma unroll
-        for (int u = 0; u < kG; ++u) {
+        for (int u = 0; u < NU; ++u) {
           const int c = c0 + u * kThreads;
           if (c < NCELL) to_primitive_ir(c, ir[u]);
         }
-      }
+      };
+#pragma unroll 1
+      for (int c0 = t; c0 < NCELL; c0 += kG * kThreads) group(c0, std::integral_constant<int, kG>());
     } else {
 #pragma unroll 4
       for (int c = t; c < NCELL; c += kThreads) to_primitive(c);
@@ -364,7 +417,9 @@ __global__ void __launch_bounds__(threads_of(V), 2)
       __syncthreads();
       // every face of this sub-grid is done with W: stream the next one in
       // under the last fold, the output and the signal-speed reduction
-      if (d == 2 && t == 0 && s + gridDim.x < nsub) issue(s + gridDim.x);
+      if (d == 2 && t == 0 && nxt < nsub) issue(nxt);
+      if (kStamps && d == 2 && t == 0 && nxt >= nsub && blockIdx.x < kStampCtas)
+        g_k6_stamps[blockIdx.x][2] = gtimer();
       // ---- fold this direction's flux differences into the cells ----------
 #pragma unroll
       for (int m = 0; m < kCellsPerThread; ++m) {
@@ -419,6 +474,27 @@ __global__ void __launch_bounds__(threads_of(V), 2)
         amax_out[s] = m;
       }
     }
+    // s_next[(it + 1) & 1] was written before this sub-grid's conversion
+    // barrier; thread 0 rewrites that slot only after the next sub-grid's
+    // barriers, which every thread must pass first
+    if constexpr (kDynamic)
+      s = s_next[(it + 1) & 1];
+    else
+      s = nxt;
+  }
+  if constexpr (kDynamic) {
+    if (t == 0) {
+      __threadfence();
+      if (atomicAdd(work + 1, 1u) == gridDim.x - 1) {   // last CTA out: reset the slot
+        work[0] = 0;
+        work[1] = 0;
+        __threadfence();
+      }
+    }
+  }
+  if (kStamps && blockIdx.x < kStampCtas) {
+    __syncthreads();
+    if (t == 0) g_k6_stamps[blockIdx.x][3] = gtimer();
   }
 }
 
@@ -436,8 +512,9 @@ int launch_v(tb_stream_t s, const double *U, const CUtensorMap &map, int nb, dou
   }
   int64_t blocks = (int64_t)tb::sm_count() * occ;
   if (blocks > nsub) blocks = nsub;
+  const unsigned slot = (V & 1024) ? g_work_next.fetch_add(1) % kWorkSlots : 0u;
   k_hydro_flux<LATTICE, V><<<(int)blocks, threads_of(V), kSmem, reinterpret_cast<cudaStream_t>(s)>>>(
-      U, map, nb, dudt, amax, nsub, dx, gamma);
+      U, map, nb, dudt, amax, nsub, dx, gamma, slot);
   return tb::last_error();
 }
 
@@ -448,15 +525,20 @@ int launch_v(tb_stream_t s, const double *U, const CUtensorMap &map, int nb, dou
 // paths' fallback out of line, bit 6 = the next sub-grid prefetched into L2
 // when this one starts, bit 7 = the conversion's reciprocals in one group of
 // 6 per thread, bit 8 = the sub-grid's max signal speed folded by per-warp
-// global atomics instead of a closing CTA barrier. Built: 0 (round 1's first
-// schedule), 1, 9, 13, 28, 60, 124, 252 and 508 (default); the other
-// measured variants were removed (round 2: 288 threads with two faces each
-// everywhere, 0.167 ms vs 0.148 — still 96 registers, fewer warps).
+// global atomics instead of a closing CTA barrier, bit 9 = per-CTA timer
+// stamps (probe only), bit 10 = dynamic sub-grid assignment from a work
+// counter. Built: 0 (round 1's first schedule), 1, 9, 13, 28, 60, 124, 252,
+// 508, 1532 (default: 508 + dynamic; config 2 0.149 -> 0.143 ms, 32768
+// sub-grids 1.073 -> 1.010 ms), 1020 / 2044 (508 / 1532 with stamps); the
+// other measured variants were removed (round 2: 288 threads with two faces
+// each everywhere, 0.167 ms vs 0.148 — still 96 registers, fewer warps; the
+// first sub-grid staged in two parts so its conversion starts on the first,
+// 0.1438 vs 0.1432 ms — no gain).
 int hydro_variant() {
   static int v = -1;
   if (v < 0) {
     const char *e = getenv("TB_HYDRO_VARIANT");
-    v = e ? (atoi(e) & 511) : kDefaultVariant;
+    v = e ? (atoi(e) & 2047) : kDefaultVariant;
   }
   return v;
 }
@@ -473,6 +555,9 @@ int launch(tb_stream_t s, const double *U, const CUtensorMap &map, int nb, doubl
     case 124: return launch_v<LATTICE, 124>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
     case 252: return launch_v<LATTICE, 252>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
     case 508: return launch_v<LATTICE, 508>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
+    case 1020: return launch_v<LATTICE, 1020>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
+    case 1532: return launch_v<LATTICE, 1532>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
+    case 2044: return launch_v<LATTICE, 2044>(s, U, map, nb, dudt, amax, nsub, dx, gamma);
 
     default: return launch_v<LATTICE, kDefaultVariant>(s, U, map, nb, dudt, amax, nsub, dx,
                                                        gamma);
@@ -480,6 +565,13 @@ int launch(tb_stream_t s, const double *U, const CUtensorMap &map, int nb, doubl
 }
 
 }  // namespace
+
+// Probe: the bit-9 variant's per-CTA stamps (ns) of the last launch,
+// [ctas][entry, first staged, last faces done, exit]; n <= 1024 CTAs.
+extern "C" int tb_hydro_stamps(unsigned long long *out, int n) {
+  if (!out || n < 0 || n > kStampCtas) return TB_E_INVALID;
+  return tb::rc(cudaMemcpyFromSymbol(out, g_k6_stamps, sizeof(unsigned long long) * 4 * n));
+}
 
 extern "C" int tb_hydro_flux(tb_stream_t s, const double *U, double *dudt, double *amax,
                              int64_t nsub, double dx, double gamma) {
