@@ -567,9 +567,10 @@ def north_star_kernels(dev, reps=20):
                      "algorithmic_bytes_per_launch": S * HYDRO_BYTES_PER_SUBGRID},
         "parity": "unpinned (self-authored spec; bit-exact to oracle/hydro_oracle.py)"}
     # the same kernel at the star step's size (max_level 5, 32768 sub-grids):
-    # the per-launch fixed cost (launch, the first cold TMA loads of all CTAs,
-    # the last round's tail; ~10 us, profiles/r02/k6_experiments.md) is 7 % of
-    # a config-2 launch and <1 % here
+    # the per-launch head (every CTA's first staging, 3-8 us) and the last
+    # wave's granularity (CTAs finish up to ~1.4 sub-grids apart even with
+    # dynamic assignment; profiles/r02/k6_experiments.md) are ~7 % of a
+    # config-2 launch and ~1 % here
     del U, du, am
     S5 = 8 ** 5
     I5, dx5 = hydro.rotating_star(S5, device=dev)
@@ -593,7 +594,8 @@ def north_star_kernels(dev, reps=20):
         "fp64_frac": S5 * HYDRO_FP64_PER_SUBGRID / (ms5 * 1e-3) / f64,
         "fp64_ops_frac": S5 * HYDRO_FP64_OPS_PER_SUBGRID / (ms5 * 1e-3) / f64,
         "note": "same kernel and L2-flush method at 32768 sub-grids (the star step's "
-                "max_level-5 lattice size): the config-2 launch carries a ~10 us fixed cost"}
+                "max_level-5 lattice size): the config-2 launch carries its head (first "
+                "staging of every CTA) and last-wave tail, ~10 us"}
     del U5, du5, am5
     # K7: FMM gravity, max_level 4 (config 3)
     L = 4
