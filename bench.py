@@ -289,10 +289,13 @@ C4_DT = float.fromhex("0x1.a73380416f1a6p-22")
 # the sweeps' best polling configuration (scripts/c4_machine_sweep.py,
 # c4_gather_sweep.py, c4_resident_sweep.py; profiles/r02/c4_*sweep.jsonl):
 # 16 workers (the box's host cores), 8 executors, max 256 aggregated,
-# resident batches (each task's rounds between the first and the last stay in
-# HBM; gather batches move every round over PCIe: 4 GB per step, a 40 ms floor)
-C4_MACHINE = dict(workers=16, executors=8, max_agg=256, zero_copy=3)
-C4_SWEEP = [(8, 8), (8, 16), (16, 16)]   # (workers, executors) beside C4_MACHINE
+# direct batches (each task's rounds between the first and the last stay in
+# HBM; the first round's kernel reads the pinned rows and folds the ghost
+# faces, the last writes them back with min and pairwise sum — no host copy
+# of the cells; gather batches move every round over PCIe: 4 GB per step, a
+# 40 ms floor; resident = direct with the fold / reductions on the host)
+C4_MACHINE = dict(workers=16, executors=8, max_agg=256, zero_copy=4)
+C4_SWEEP = [(4, 8), (8, 8), (16, 16)]   # (workers, executors) beside C4_MACHINE
 
 
 def machine_ablation_c4(steps=4, repeats=3):
@@ -315,8 +318,10 @@ def machine_ablation_c4(steps=4, repeats=3):
     out = {"config": "native machine, 32768 sub-grids (max_level 5), reference task structure "
                      f"(491,520 schedule() calls per step), {C4_MACHINE['workers']} workers, "
                      f"{C4_MACHINE['executors']} executors, max {C4_MACHINE['max_agg']} "
-                     "aggregated, resident batches (rounds 2..14 of each task in HBM, rounds 1 "
-                     f"and 15 on its pinned rows), {steps} steps (mean of steps 2..{steps}), "
+                     "aggregated, direct batches (rounds 2..14 of each task in HBM; round 1 reads "
+                     "the pinned rows and folds the ghost faces in its kernel, round 15 writes "
+                     "them back with min and pairwise sum), "
+                     f"{steps} steps (mean of steps 2..{steps}), "
                      f"median of {repeats} interleaved runs"}
     checks, golden = set(), [True]
 
@@ -335,7 +340,9 @@ def machine_ablation_c4(steps=4, repeats=3):
         return {name: (statistics.median(v), last[name]) for name, v in ms.items()}
 
     main = compare([(m.value, m, C4_MACHINE) for m in (P, H, F)]
-                   + [("gather_polling", P, dict(C4_MACHINE, zero_copy=2)),
+                   + [("resident_polling", P, dict(C4_MACHINE, zero_copy=3)),
+                      ("resident_fence", F, dict(C4_MACHINE, zero_copy=3)),
+                      ("gather_polling", P, dict(C4_MACHINE, zero_copy=2)),
                       ("gather_fence", F, dict(C4_MACHINE, zero_copy=2))])
     main.update(compare([("staged_polling", P, dict(C4_MACHINE, zero_copy=0))]))
     for name, (ms, res) in main.items():
@@ -344,6 +351,8 @@ def machine_ablation_c4(steps=4, repeats=3):
         out[f"{name}_launches_per_step"] = res.per_step[-1].launches
     out["speedup_polling_vs_fence"] = out["fence_ms_per_step"] / out["polling_ms_per_step"]
     out["speedup_hosttask_vs_fence"] = out["fence_ms_per_step"] / out["hosttask_ms_per_step"]
+    out["resident_speedup_polling_vs_fence"] = (out["resident_fence_ms_per_step"]
+                                                / out["resident_polling_ms_per_step"])
     out["gather_speedup_polling_vs_fence"] = (out["gather_fence_ms_per_step"]
                                               / out["gather_polling_ms_per_step"])
     out["cells_per_s_polling"] = 32768 * 512 / (out["polling_ms_per_step"] * 1e-3)
@@ -375,7 +384,11 @@ def plugin_call_bench(steps=3):
     and "gather": every kernel round moves each sub-grid's 4 KiB over PCIe
     and back, 15 rounds per step (the reference's op sequence) — the bound
     stated below; "resident": the task's rounds between the first and the
-    last stay in HBM (two PCIe crossings per sub-grid and step)."""
+    last stay in HBM (two PCIe crossings per sub-grid and step); "direct":
+    resident with the ghost fold and the per-sub-grid min / pairwise sum in
+    the first / last round's kernel, on the Scenario's pinned rows (no host
+    copy of the cells). The build_scenario call (which pins the rows) is
+    outside the timed call, as the reference's scenario construction is."""
     from paper_2303_08058_b200 import (AggregationExecutor, BufferPool, CudaDevice,
                                        ExecutorPool, Integration, IntegrationMode, Runtime,
                                        ScenarioConfig, build_scenario, kernel_transform,
@@ -388,7 +401,7 @@ def plugin_call_bench(steps=3):
                   "round-robin aggs_by_grid) -> native machine (reference task structure)",
            "unit": "cells/s"}
     pcie_bytes = S * 15 * 512 * 8 * 2
-    for copies in ("resident", "gather", "staged"):
+    for copies in ("direct", "resident", "gather", "staged"):
         rt = Runtime(W)
         dev = CudaDevice(0)
         try:
@@ -410,14 +423,15 @@ def plugin_call_bench(steps=3):
         step_ms = statistics.fmean(res.step_ms[1:])
         out[copies] = {"ms_per_step": step_ms, "value": S * 512 / (step_ms * 1e-3),
                        "call_s": call_s, "call_value": S * 512 * steps / call_s,
-                       "engine": res.engine,
+                       "engine": res.engine, "batch_copies": res.batch_copies,
                        "step1_equals_run_reference_32768x1":
                            res.per_step[0].checksum_piece == C4_CHECKSUM
                            and res.dts[0] == C4_DT}
-    out["value"] = out["resident"]["value"]
-    out["value_mode"] = "resident"
+    out["value"] = out["direct"]["value"]
+    out["value_mode"] = "direct"
     out["h2d_bytes_per_step"] = S * 512 * 8
     out["d2h_bytes_per_step"] = S * 512 * 8
+    out["direct"]["pcie_bytes_per_step"] = 2 * S * 512 * 8
     out["resident"]["pcie_bytes_per_step"] = 2 * S * 512 * 8
     out["gather"]["pcie_bytes_per_step"] = pcie_bytes
     out["staged"]["pcie_bytes_per_step"] = pcie_bytes

@@ -469,6 +469,19 @@ int tb_machine_run_cells(const tb_machine_config *cfg, double *cells, double *ch
 int tb_launch_gather(tb_stream_t s, int op, int kind, double c1, double c2,
                      const double *const *src, double *const *dst, const int64_t *n,
                      int members);
+/* A gather batch of kind `kind` whose members are whole sub-grids and may be
+ * a task's first and/or last round (the machine's direct mode, zero_copy =
+ * 4): member i = sub-grids [g0[i], g0[i] + nsub[i]) of the S-ring, read from
+ * src[i] and written to dst[i] ([nsub[i]][512], device-accessible, 16-B
+ * aligned). flags[i] bit 0: fold the first and last 8 cells of each input
+ * sub-grid with the neighbours' faces (faces [S][2][8] = (left, right) of the
+ * previous generation; src/miniapp.py:119-126) before the transform; bit 1:
+ * mins[g] / sums[g] = min and numpy-order pairwise sum of each output
+ * sub-grid (src/miniapp.py:133). Same two roundings as tb_launch. */
+int tb_launch_gather_edge(tb_stream_t s, int kind, const double *const *src,
+                          double *const *dst, const int64_t *g0, const int32_t *nsub,
+                          const uint8_t *flags, int members, const double *faces,
+                          double *mins, double *sums, int64_t S);
 
 /* One aggregated hydro batch (the Octo-Tiger use of src/executors.py:257-284,
  * PAPER.md:762-773): H2D(din <- hin: nsub ghosted sub-grids [5][12^3]) ;

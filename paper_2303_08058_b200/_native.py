@@ -149,6 +149,7 @@ SIGNATURES = {
     "tb_machine_run": [_vp, _vp, _vp, _vp],
     "tb_machine_run_cells": [_vp, _vp, _vp, _vp, _vp],
     "tb_launch_gather": [_u64, _int, _int, _dbl, _dbl, _vp, _vp, _vp, _int],
+    "tb_launch_gather_edge": [_u64, _int, _vp, _vp, _vp, _vp, _vp, _int, _vp, _vp, _vp, _i64],
     "tb_agg_launch_hydro": [_u64, _vp, _vp, _i64, _vp, _vp, _dbl, _dbl, _pu64],
     "tb_machine_run_hydro": [_vp, _vp, _vp, _dbl, _dbl, _vp],
     "tb_ipc_get_handle": [_vp, _vp, _pu64],
@@ -161,6 +162,7 @@ SIGNATURES = {
     "tb_fp64_probe": [_int, _i64, _vp, _vp],
     "tb_divsqrt_fast": [_u64, _vp, _vp, _i64, _vp, _vp, _vp],
     "tb_hydro_flux_lattice": [_u64, _vp, _i64, _i64, _vp, _vp, _dbl, _dbl],
+    "tb_hydro_stamps": [_vp, _int],
     "tb_star_pad": [_u64, _vp, _i64, _vp],
     "tb_star_pad_slab": [_u64, _vp, _i64, _i64, _vp, _vp, _vp],
     "tb_star_cfl": [_u64, _vp, _i64, _dbl, _dbl, _vp],

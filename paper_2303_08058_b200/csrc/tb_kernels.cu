@@ -101,6 +101,80 @@ __global__ void __launch_bounds__(256) k_launch_gather(const __grid_constant__ G
   }
 }
 
+// K1e: a gather batch whose members may be a task's FIRST round (flag bit 0:
+// the input rows are the sub-grids' cells, folded with the previous
+// generation's neighbour faces before the transform — src/miniapp.py:119-126)
+// and/or its LAST round (bit 1: per sub-grid, the min and numpy's pairwise sum
+// of the 512 transformed values — src/miniapp.py:133). One CTA of 256 threads
+// per (sub-grid, member); each thread owns cells 2t, 2t+1.
+struct GatherEdgeArgs {
+  const double *src[TB_GATHER_MAX];
+  double *dst[TB_GATHER_MAX];
+  int64_t g0[TB_GATHER_MAX];      // the member's first sub-grid (ring index)
+  int32_t nsub[TB_GATHER_MAX];    // sub-grids in the member
+  uint8_t flags[TB_GATHER_MAX];
+  const double *faces;            // [S][2][8]: (left face, right face) snapshot
+  double *mins, *sums;            // [S]
+  int64_t S;
+  double c1, c2;
+};
+
+__global__ void __launch_bounds__(256) k_launch_gather_edge(const __grid_constant__ GatherEdgeArgs a) {
+  const int m = blockIdx.y, k = blockIdx.x, t = threadIdx.x;
+  if (k >= a.nsub[m]) return;
+  const int flags = a.flags[m];
+  const int64_t g = a.g0[m] + k;
+  const double2 *src = reinterpret_cast<const double2 *>(a.src[m] + (int64_t)k * TB_CELLS);
+  double2 *dst = reinterpret_cast<double2 *>(a.dst[m] + (int64_t)k * TB_CELLS);
+  double2 x = src[t];
+  if ((flags & 1) && (t < TB_FACE / 2 || t >= (TB_CELLS - TB_FACE) / 2)) {
+    // ghost fold against the neighbours' previous-generation faces
+    const bool left = t < TB_FACE / 2;
+    const int64_t nb = left ? (g - 1 + a.S) % a.S : (g + 1) % a.S;
+    const double *f = a.faces + nb * 2 * TB_FACE + (left ? TB_FACE : 0);
+    const int i = left ? 2 * t : 2 * t - (TB_CELLS - TB_FACE);
+    x.x = __dmul_rn(0.5, __dadd_rn(x.x, f[i]));
+    x.y = __dmul_rn(0.5, __dadd_rn(x.y, f[i + 1]));
+  }
+  x.x = xform(x.x, a.c1, a.c2);
+  x.y = xform(x.y, a.c1, a.c2);
+  dst[t] = x;
+  if (!(flags & 2)) return;
+  // per-sub-grid min (exact) and pairwise sum in numpy's order: four blocks
+  // of 128, each summed by 8 strided accumulators r[j] = p[j] + p[j+8] + ...
+  // (in that order), combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then
+  // (b0+b1)+(b2+b3) — the host's pairwise512 (oracle/tb_oracle.c)
+  __shared__ double v[TB_CELLS];
+  __shared__ double wmin[8];
+  v[2 * t] = x.x;
+  v[2 * t + 1] = x.y;
+  double mn = fmin(x.x, x.y);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+  if ((t & 31) == 0) wmin[t >> 5] = mn;
+  __syncthreads();
+  if (t < 32) {
+    const int blk = t >> 3, j = t & 7;
+    const double *p = v + 128 * blk + j;
+    double r = p[0];
+#pragma unroll
+    for (int i = 8; i < 128; i += 8) r = __dadd_rn(r, p[i]);
+    // lanes 8*blk .. 8*blk+7 hold r[0..7] of block blk
+    const double r01 = __dadd_rn(r, __shfl_down_sync(0xffffffffu, r, 1));        // j even
+    const double r0123 = __dadd_rn(r01, __shfl_down_sync(0xffffffffu, r01, 2));  // j % 4 == 0
+    const double b = __dadd_rn(r0123, __shfl_down_sync(0xffffffffu, r0123, 4));  // j == 0
+    const double b01 = __dadd_rn(b, __shfl_down_sync(0xffffffffu, b, 8));        // blk even
+    const double tot = __dadd_rn(b01, __shfl_down_sync(0xffffffffu, b01, 16));   // lane 0
+    double wm = t < 8 ? wmin[t] : CUDART_INF;
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) wm = fmin(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+    if (t == 0) {
+      a.sums[g] = tot;
+      a.mins[g] = wm;
+    }
+  }
+}
+
 __global__ void k_spin(int64_t ns) {
   uint64_t t0, t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
@@ -1278,6 +1352,43 @@ int tb_launch_gather(tb_stream_t s, int op, int kind, double c1, double c2,
   a.c2 = c2;
   const int bx = grid_for(nmax / 2 > 0 ? nmax / 2 : 1, 256, 64);
   k_launch_gather<<<dim3((unsigned)bx, (unsigned)members), 256, 0, st>>>(a);
+  return tb::last_error();
+}
+
+int tb_launch_gather_edge(tb_stream_t s, int kind, const double *const *src,
+                          double *const *dst, const int64_t *g0, const int32_t *nsub,
+                          const uint8_t *flags, int members, const double *faces,
+                          double *mins, double *sums, int64_t S) {
+  if (members < 1 || members > TB_GATHER_MAX || !src || !dst || !g0 || !nsub || !flags ||
+      kind < 0 || kind >= TB_KINDS || S < 1)
+    return TB_E_INVALID;
+  static const double h1[TB_KINDS] = {1.0000003, 0.9999998, 1.0000001, 0.9999997, 1.0000002};
+  static const double h2[TB_KINDS] = {1e-07, -1e-07, 2e-07, 5e-08, -2e-07};
+  GatherEdgeArgs a;
+  int nmax = 1;
+  bool fold = false, reduce = false;
+  for (int i = 0; i < members; ++i) {
+    if (!src[i] || !dst[i] || nsub[i] < 1 || g0[i] < 0 || g0[i] + nsub[i] > S ||
+        ((reinterpret_cast<uintptr_t>(src[i]) | reinterpret_cast<uintptr_t>(dst[i])) & 15))
+      return TB_E_INVALID;
+    a.src[i] = src[i];
+    a.dst[i] = dst[i];
+    a.g0[i] = g0[i];
+    a.nsub[i] = nsub[i];
+    a.flags[i] = flags[i];
+    fold |= (flags[i] & 1) != 0;
+    reduce |= (flags[i] & 2) != 0;
+    nmax = nsub[i] > nmax ? nsub[i] : nmax;
+  }
+  if ((fold && !faces) || (reduce && (!mins || !sums))) return TB_E_INVALID;
+  a.faces = faces;
+  a.mins = mins;
+  a.sums = sums;
+  a.S = S;
+  a.c1 = h1[kind];
+  a.c2 = h2[kind];
+  k_launch_gather_edge<<<dim3((unsigned)nmax, (unsigned)members), TB_CELLS / 2, 0,
+                         reinterpret_cast<cudaStream_t>(s)>>>(a);
   return tb::last_error();
 }
 

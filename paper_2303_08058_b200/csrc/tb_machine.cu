@@ -57,11 +57,13 @@ inline int64_t now_ns() {
 // stderr at the end of the run. Off: one predictable branch per site.
 enum DiagField {
   kTasks, kTaskNs, kHookNs, kSteals, kBodies, kQueries, kNotReady, kBodyNs, kEnqueues,
-  kEnqueueNs, kFenceNs, kIdleLoops, kSleeps, kDiagFields
+  kEnqueueNs, kFenceNs, kIdleLoops, kSleeps, kStartNs, kFinishNs, kLaunchNs, kBatchDoneNs,
+  kScheduleNs, kDiagFields
 };
 const char *const kDiagNames[kDiagFields] = {
     "tasks", "task_ms", "hook_ms", "steals", "poll_bodies", "queries", "not_ready", "body_ms",
-    "enqueues", "enqueue_ms", "fence_ms", "idle_loops", "sleeps"};
+    "enqueues", "enqueue_ms", "fence_ms", "idle_loops", "sleeps", "start_ms", "finish_ms",
+    "launch_ms", "batch_done_ms", "schedule_ms"};
 const bool g_diag = [] {
   const char *e = getenv("TB_MACHINE_DIAG");
   return e && *e && *e != '0';
@@ -71,6 +73,16 @@ thread_local int64_t t_diag[kDiagFields];
 inline void diag_add(DiagField f, int64_t v) {
   if (g_diag) t_diag[f] += v;
 }
+// time of a scope into field f (diag on)
+struct DiagScope {
+  DiagField f;
+  int64_t t0;
+  explicit DiagScope(DiagField f_) : f(f_), t0(g_diag ? now_ns() : 0) {}
+  ~DiagScope() {
+    if (g_diag) t_diag[f] += now_ns() - t0;
+  }
+};
+
 // a worker's counters into the run's sums (at thread exit)
 inline void diag_flush() {
   if (!g_diag) return;
@@ -569,6 +581,7 @@ struct Req {
   double *dst;
   int64_t n;
   SubTask *task;
+  uint8_t flags = 0;   // direct mode: bit 0 first round (fold), bit 1 last (reduce)
 };
 
 struct Executor;
@@ -621,8 +634,11 @@ struct Machine {
   tb_machine_config cfg;
   double *cells = nullptr;         // [S][512]: the caller's (run_cells) or own_cells
   std::vector<double> own_cells;
-  std::vector<double> faces;       // [S][2][8] previous generation
-  std::vector<double> mins, sums;  // per sub-grid, this step
+  std::vector<double> faces_v, mins_v, sums_v;
+  double *faces = nullptr;         // [S][2][8] previous generation
+  double *mins = nullptr, *sums = nullptr;   // per sub-grid, this step
+  double *pinned_small = nullptr;  // zero_copy = 4: faces | mins | sums, mapped
+  bool own_cells_pinned = false;   // zero_copy = 4 without caller cells
   std::unique_ptr<Pool> pool;
   std::unique_ptr<Poller> poller;
   std::unique_ptr<HostTasks> hosttasks;
@@ -850,9 +866,14 @@ struct ResumeChunk {
   SubTask *t[kResumeChunk];
 };
 
+void resume_task_chunk(SubTask *const *ts, uint32_t n);
+
 void resume_chunk(void *p) {
   ResumeChunk *c = static_cast<ResumeChunk *>(p);
-  for (uint32_t i = 0; i < c->n; ++i) c->fn(c->t[i]);
+  if (c->fn == resume_task)
+    resume_task_chunk(c->t, c->n);
+  else
+    for (uint32_t i = 0; i < c->n; ++i) c->fn(c->t[i]);
   delete c;
 }
 
@@ -889,6 +910,7 @@ void resume_members(const Batch *b) {
 }
 
 void batch_done(void *p) {   // AggregationExecutor finish (src/executors.py:286-301)
+  DiagScope ds(kBatchDoneNs);
   Batch *b = static_cast<Batch *>(p);
   Machine *m = b->ex->m;
   if (m->failed()) {
@@ -927,6 +949,7 @@ void batch_done(void *p) {   // AggregationExecutor finish (src/executors.py:286
 }
 
 void launch(Batch *b, bool idle) {   // src/executors.py:257-284 as one launch
+  DiagScope ds(kLaunchNs);
   struct Range {   // NVTX range over the batch launch (profilers only)
     Range() { nvtxRangePushA("machine batch launch"); }
     ~Range() { nvtxRangePop(); }
@@ -945,6 +968,35 @@ void launch(Batch *b, bool idle) {   // src/executors.py:257-284 as one launch
   const int do_barrier = m->cfg.inject_barriers && !m->cfg.barrier_elision;
   const tb_stream_t st = reinterpret_cast<tb_stream_t>(ex->stream);
   m->kernels.fetch_add(1, std::memory_order_relaxed);
+  if (m->cfg.zero_copy == 4 && !m->hydro && !trap) {
+    // direct: members' rows where they live; first / last rounds fold and
+    // reduce in the kernel (tb_launch_gather_edge)
+    enqueue_and_bridge(m, ex, Task{batch_done, b}, [&](tb_event_t *ev) {
+      const double *src[TB_GATHER_MAX];
+      double *dst[TB_GATHER_MAX];
+      int64_t g0[TB_GATHER_MAX];
+      int32_t nsub[TB_GATHER_MAX];
+      uint8_t flags[TB_GATHER_MAX];
+      int rc = TB_OK;
+      for (size_t i0 = 0; i0 < b->members.size() && rc == TB_OK; i0 += TB_GATHER_MAX) {
+        const int k = (int)std::min<size_t>(TB_GATHER_MAX, b->members.size() - i0);
+        for (int i = 0; i < k; ++i) {
+          const Req &r = b->members[i0 + i];
+          src[i] = r.src;
+          dst[i] = r.dst;
+          g0[i] = r.task->lo;
+          nsub[i] = (int32_t)r.task->n;
+          flags[i] = r.flags;
+        }
+        rc = tb_launch_gather_edge(st, b->kind, src, dst, g0, nsub, flags, k, m->faces, m->mins,
+                                   m->sums, m->cfg.subgrids);
+      }
+      if (rc == TB_OK && do_barrier) rc = tb_barrier(st);
+      if (rc == TB_OK) rc = tb_event_record(st, ev);
+      return rc;
+    });
+    return;
+  }
   if (m->cfg.zero_copy >= 2 && !m->hydro) {
     // members read and written where they live (the pinned task arena)
     enqueue_and_bridge(m, ex, Task{batch_done, b}, [&](tb_event_t *ev) {
@@ -1028,38 +1080,62 @@ void idle_fire(void *p) {   // the idleness probe completed (src/executors.py:20
   batch_release(b);                     // the probe's reference
 }
 
-void schedule(Executor *ex, int kind, const double *src, double *dst, int64_t n,
-              SubTask *t) {   // src/executors.py:174-221
+// n requests of one kind on one executor under ONE acquisition of its lock
+// (a resumed chunk's members all come from one batch, so their next
+// requests share executor and kind): each joins the open batch or opens one
+// (with its idleness probe), and a batch that reaches max_agg launches —
+// src/executors.py:174-221 applied to each request in order.
+void schedule_many(Executor *ex, int kind, const Req *reqs, int n) {
+  DiagScope ds(kScheduleNs);
   Machine *m = ex->m;
-  Batch *opened = nullptr, *full = nullptr;
+  Batch *opened[kResumeChunk + 1], *full[kResumeChunk + 1];
+  bool filled_here[kResumeChunk + 1];   // opened[i] also filled by this call
+  int nopened = 0, nfull = 0;
   {
     std::lock_guard<std::mutex> g(ex->mu);
-    Batch *b = ex->open[kind];
-    if (!b) {
-      b = new Batch();
-      b->ex = ex;
-      b->kind = kind;
-      b->members.reserve((size_t)std::min<int64_t>(m->cfg.max_agg, 1024));
-      if (m->cfg.max_agg > 1) {
-        ex->open[kind] = b;
-        b->refs.store(2, std::memory_order_relaxed);   // launch + idleness probe
+    for (int i = 0; i < n; ++i) {
+      Batch *b = ex->open[kind];
+      if (!b) {
+        b = new Batch();
+        b->ex = ex;
+        b->kind = kind;
+        b->members.reserve((size_t)std::min<int64_t>(m->cfg.max_agg, 1024));
+        if (m->cfg.max_agg > 1) {
+          ex->open[kind] = b;
+          b->refs.store(2, std::memory_order_relaxed);   // launch + idleness probe
+        }
+        filled_here[nopened] = false;
+        opened[nopened++] = b;
       }
-      opened = b;
-    }
-    b->members.push_back(Req{src, dst, n, t});
-    if ((int64_t)b->members.size() >= m->cfg.max_agg) {
-      if (ex->open[kind] == b) ex->open[kind] = nullptr;
-      b->launched = true;
-      full = b;
+      b->members.push_back(reqs[i]);
+      if ((int64_t)b->members.size() >= m->cfg.max_agg) {
+        if (ex->open[kind] == b) ex->open[kind] = nullptr;
+        b->launched = true;
+        full[nfull++] = b;
+        for (int j = 0; j < nopened; ++j)
+          if (opened[j] == b) filled_here[j] = true;
+      }
     }
   }
-  if (opened && opened != full) {
+  for (int i = 0; i < nopened; ++i) {
+    Batch *b = opened[i];
+    if (m->cfg.max_agg <= 1) continue;   // M = 1: launched at once, no probe
+    if (filled_here[i]) {                // opened and filled by this call: no probe
+      b->refs.fetch_sub(1, std::memory_order_relaxed);
+      continue;
+    }
     // One idleness probe per batch: a queue marker event (src/bridge.py:92-101).
-    enqueue_and_bridge(m, ex, Task{idle_fire, opened}, [&](tb_event_t *ev) {
+    enqueue_and_bridge(m, ex, Task{idle_fire, b}, [&](tb_event_t *ev) {
       return tb_event_record(reinterpret_cast<tb_stream_t>(ex->stream), ev);
     });
   }
-  if (full) launch(full, false);
+  for (int i = 0; i < nfull; ++i) launch(full[i], false);
+}
+
+void schedule(Executor *ex, int kind, const double *src, double *dst, int64_t n,
+              SubTask *t) {   // src/executors.py:174-221
+  const Req r{src, dst, n, t};
+  schedule_many(ex, kind, &r, 1);
 }
 
 void task_finished(Machine *m) {
@@ -1084,6 +1160,7 @@ double pairwise512(const double *a) {
 }
 
 void start_task(void *p) {   // ghost fold + first round (src/miniapp.py:116-130)
+  DiagScope ds(kStartNs);
   SubTask *t = static_cast<SubTask *>(p);
   Machine *m = t->m;
   if (m->failed()) {
@@ -1093,17 +1170,27 @@ void start_task(void *p) {   // ghost fold + first round (src/miniapp.py:116-130
   const int64_t S = m->cfg.subgrids;
   t->work = t->abuf;
   t->out = t->bbuf;
+  t->round = 0;
+  if (m->cfg.zero_copy == 4) {
+    // direct: round 0's batch kernel reads the task's rows of the caller's
+    // (pinned) cells and folds the neighbour faces itself; the last round
+    // writes the rows back with their min and pairwise sum
+    const bool one = m->cfg.chains * m->cfg.kernels_per_chain <= 1;
+    t->out = one ? t->abuf : t->d0;
+    Req r{t->work, t->out, t->n * kCells, t, (uint8_t)(one ? 3 : 1)};
+    schedule_many(t->ex, 0, &r, 1);
+    return;
+  }
   for (int64_t k = 0; k < t->n; ++k) {
     const int64_t g = t->lo + k;
     double *w = t->work + k * kCells;
     std::memcpy(w, m->cells + g * kCells, sizeof(double) * kCells);
-    const double *left = m->faces.data() + ((g - 1 + S) % S) * 2 * kFace + kFace;
-    const double *right = m->faces.data() + ((g + 1) % S) * 2 * kFace;
+    const double *left = m->faces + ((g - 1 + S) % S) * 2 * kFace + kFace;
+    const double *right = m->faces + ((g + 1) % S) * 2 * kFace;
     for (int i = 0; i < kFace; ++i) w[i] = 0.5 * (w[i] + left[i]);
     for (int i = 0; i < kFace; ++i)
       w[kCells - kFace + i] = 0.5 * (w[kCells - kFace + i] + right[i]);
   }
-  t->round = 0;
   // zero_copy = 3: round 0 reads the folded rows from pinned host memory and
   // writes device memory; the rounds in between stay in HBM
   if (m->dev_arena)
@@ -1111,12 +1198,14 @@ void start_task(void *p) {   // ghost fold + first round (src/miniapp.py:116-130
   schedule(t->ex, 0, t->work, t->out, t->n * kCells, t);
 }
 
-void resume_task(void *p) {   // next round, or write-back + post-process
-  SubTask *t = static_cast<SubTask *>(p);
+// A task's continuation after its batch: the next round's request into *r
+// (returns its kind), or -1 after the write-back + post-process of the last
+// round (src/miniapp.py:127-133).
+int advance_task(SubTask *t, Req *r) {
   Machine *m = t->m;
   if (m->failed()) {
     task_finished(m);
-    return;
+    return -1;
   }
   const int kpc = (int)m->cfg.kernels_per_chain;
   const int rounds = (int)(m->cfg.chains * kpc);
@@ -1124,17 +1213,24 @@ void resume_task(void *p) {   // next round, or write-back + post-process
     // zero_copy = 3: device ping-pong; the last round writes the host rows
     t->work = t->out;
     if (++t->round < rounds) {
-      t->out = t->round == rounds - 1 ? t->abuf : (t->work == t->d0 ? t->d1 : t->d0);
-      schedule(t->ex, t->round % kpc, t->work, t->out, t->n * kCells, t);
-      return;
+      const bool last = t->round == rounds - 1;
+      t->out = last ? t->abuf : (t->work == t->d0 ? t->d1 : t->d0);
+      *r = Req{t->work, t->out, t->n * kCells, t,
+               (uint8_t)(last && m->cfg.zero_copy == 4 ? 2 : 0)};
+      return t->round % kpc;
+    }
+    if (m->cfg.zero_copy == 4) {   // direct: rows, min and sum written by the kernel
+      task_finished(m);
+      return -1;
     }
   } else {
     std::swap(t->work, t->out);
     if (++t->round < rounds) {
-      schedule(t->ex, t->round % kpc, t->work, t->out, t->n * kCells, t);
-      return;
+      *r = Req{t->work, t->out, t->n * kCells, t};
+      return t->round % kpc;
     }
   }
+  DiagScope ds(kFinishNs);
   for (int64_t k = 0; k < t->n; ++k) {
     const int64_t g = t->lo + k;
     const double *w = t->work + k * kCells;
@@ -1145,6 +1241,35 @@ void resume_task(void *p) {   // next round, or write-back + post-process
     m->sums[g] = pairwise512(w);
   }
   task_finished(m);
+  return -1;
+}
+
+void resume_task(void *p) {   // next round, or write-back + post-process
+  SubTask *t = static_cast<SubTask *>(p);
+  Req r;
+  const int kind = advance_task(t, &r);
+  if (kind >= 0) schedule_many(t->ex, kind, &r, 1);
+}
+
+// A chunk of one batch's members (all on one executor; their next requests
+// share one kind): advanced in turn, the continuing ones scheduled together.
+void resume_task_chunk(SubTask *const *ts, uint32_t n) {
+  Req reqs[kResumeChunk];
+  int nreq = 0, kind = -1;
+  Executor *ex = nullptr;
+  for (uint32_t i = 0; i < n; ++i) {
+    Req r;
+    const int k = advance_task(ts[i], &r);
+    if (k < 0) continue;
+    if (nreq && (k != kind || ts[i]->ex != ex)) {   // not expected; keep order anyway
+      schedule_many(ex, kind, reqs, nreq);
+      nreq = 0;
+    }
+    kind = k;
+    ex = ts[i]->ex;
+    reqs[nreq++] = r;
+  }
+  if (nreq) schedule_many(ex, kind, reqs, nreq);
 }
 
 // ------------------------------------------------------- hydro workload --
@@ -1286,27 +1411,67 @@ int run_machine(const tb_machine_config *cfg_in, double *cells_io, double *check
   if (c.subgrids < 1 || c.steps < 0 || c.workers < 1 || c.executors < 1 || c.max_agg < 1 ||
       c.chains < 0 || c.kernels_per_chain < 1 || c.kernels_per_chain > TB_KINDS ||
       c.task_subgrids < 1 || c.mode < TB_MODE_POLLING || c.mode > TB_MODE_FENCE ||
-      c.zero_copy < 0 || c.zero_copy > 3 || c.fault_at_launch < 0)
+      c.zero_copy < 0 || c.zero_copy > 4 || c.fault_at_launch < 0)
     return TB_E_INVALID;
   int dev = 0;
   cudaGetDevice(&dev);
   Machine m;
   m.cfg = c;
   const int64_t S = c.subgrids;
+  const bool direct = c.zero_copy == 4;
+  if (direct && cells_io) {
+    // the batch kernels read and write the caller's rows: they must be
+    // pinned host memory mapped at the same address (UVA)
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, cells_io) != cudaSuccess ||
+        pa.type != cudaMemoryTypeHost || pa.devicePointer != cells_io) {
+      cudaGetLastError();
+      return TB_E_INVALID;
+    }
+  }
+  size_t own_bytes = 0;
   if (cells_io) {
     m.cells = cells_io;
   } else {
-    m.own_cells.resize(S * kCells);
-    m.cells = m.own_cells.data();
+    if (direct) {   // machine-owned rows, pinned (the cached host arena)
+      own_bytes = sizeof(double) * S * kCells;
+      if (!(m.cells = arena_take_host(own_bytes))) return tb::rc(cudaGetLastError());
+      m.own_cells_pinned = true;
+    } else {
+      m.own_cells.resize(S * kCells);
+      m.cells = m.own_cells.data();
+    }
     const double scale = (double)(S * 1000 + kCells);
     for (int64_t g = 0; g < S; ++g)   // src/miniapp.py:72-77
       for (int i = 0; i < kCells; ++i)
         m.cells[g * kCells + i] = ((double)g * 1000.0 + (double)i) / scale;
   }
-  m.faces.resize(S * 2 * kFace);
-  m.mins.resize(S);
-  m.sums.resize(S);
   size_t arena_bytes = 0, dev_arena_bytes = 0;
+  if (direct) {
+    // faces | mins | sums where the batch kernels read and write them
+    if (cudaHostAlloc(reinterpret_cast<void **>(&m.pinned_small),
+                      sizeof(double) * S * (2 * kFace + 2),
+                      cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess) {
+      if (m.own_cells_pinned) arena_give(m.cells, own_bytes, nullptr, 0, dev);
+      return tb::rc(cudaGetLastError());
+    }
+    m.faces = m.pinned_small;
+    m.mins = m.faces + S * 2 * kFace;
+    m.sums = m.mins + S;
+    dev_arena_bytes = sizeof(double) * 2 * S * kCells;
+    if (!(m.dev_arena = arena_take_dev(dev_arena_bytes, dev))) {
+      cudaFreeHost(m.pinned_small);
+      if (m.own_cells_pinned) arena_give(m.cells, own_bytes, nullptr, 0, dev);
+      return tb::rc(cudaGetLastError());
+    }
+  } else {
+    m.faces_v.resize(S * 2 * kFace);
+    m.mins_v.resize(S);
+    m.sums_v.resize(S);
+    m.faces = m.faces_v.data();
+    m.mins = m.mins_v.data();
+    m.sums = m.sums_v.data();
+  }
   if (c.zero_copy == 2) {
     // every task's two work buffers in one pinned, device-mapped arena
     arena_bytes = sizeof(double) * 2 * S * kCells;
@@ -1347,7 +1512,11 @@ int run_machine(const tb_machine_config *cfg_in, double *cells_io, double *check
     t->lo = lo;
     t->n = std::min<int64_t>(c.task_subgrids, S - lo);
     t->ex = m.execs[(size_t)(lo % c.executors)].get();
-    if (m.dev_arena) {
+    if (direct) {   // the caller's rows in, the caller's rows out
+      t->abuf = t->bbuf = m.cells + lo * kCells;
+      t->d0 = m.dev_arena + 2 * lo * kCells;
+      t->d1 = t->d0 + t->n * kCells;
+    } else if (m.dev_arena) {
       t->abuf = t->bbuf = m.arena + lo * kCells;
       t->d0 = m.dev_arena + 2 * lo * kCells;
       t->d1 = t->d0 + t->n * kCells;
@@ -1368,8 +1537,8 @@ int run_machine(const tb_machine_config *cfg_in, double *cells_io, double *check
                   i0 = m.idle, mb0 = m.members;
     const auto t0 = Clock::now();
     for (int64_t g = 0; g < S; ++g) {   // face snapshot (src/miniapp.py:89-93)
-      std::memcpy(&m.faces[g * 2 * kFace], &m.cells[g * kCells], sizeof(double) * kFace);
-      std::memcpy(&m.faces[g * 2 * kFace + kFace], &m.cells[g * kCells + kCells - kFace],
+      std::memcpy(m.faces + g * 2 * kFace, &m.cells[g * kCells], sizeof(double) * kFace);
+      std::memcpy(m.faces + g * 2 * kFace + kFace, &m.cells[g * kCells + kCells - kFace],
                   sizeof(double) * kFace);
     }
     m.remaining.store((int64_t)m.tasks.size());
@@ -1387,7 +1556,7 @@ int run_machine(const tb_machine_config *cfg_in, double *cells_io, double *check
     if (m.failed()) break;
     double dt = m.mins[0];
     for (int64_t g = 1; g < S; ++g) dt = m.mins[g] < dt ? m.mins[g] : dt;
-    const double piece = exact_sum(m.sums.data(), S);
+    const double piece = exact_sum(m.sums, S);
     const auto t1 = Clock::now();
     cs += piece;
     if (steps_out) {
@@ -1425,12 +1594,16 @@ int run_machine(const tb_machine_config *cfg_in, double *cells_io, double *check
     delete s;
   }
   const int err = tb::rc(cudaGetLastError());
+  // direct mode: the machine-owned pinned rows go back as the host arena
+  double *host_arena = m.own_cells_pinned ? m.cells : m.arena;
+  const size_t host_bytes = m.own_cells_pinned ? own_bytes : arena_bytes;
   if (!m.failed()) {
-    arena_give(m.arena, arena_bytes, m.dev_arena, dev_arena_bytes, dev);
+    arena_give(host_arena, host_bytes, m.dev_arena, dev_arena_bytes, dev);
   } else {   // a faulted context: do not keep its memory
-    if (m.arena) cudaFreeHost(m.arena);
+    if (host_arena) cudaFreeHost(host_arena);
     if (m.dev_arena) cudaFree(m.dev_arena);
   }
+  if (m.pinned_small) cudaFreeHost(m.pinned_small);
   return m.failed() ? m.fault.load() : err;
 }
 

@@ -52,7 +52,12 @@ def run_native(subgrids: int, steps: int, workers: int = 8, executors: int = 32,
     kernel ; D2H); True/1 = the batch kernel works in place on its pinned
     staging buffer; 2 (ZERO_COPY_GATHER) = no staging: the tasks' buffers
     live in pinned memory and the batch kernel reads and writes each member
-    where it lives. ``cells`` ([subgrids, 512] float64, C-contiguous):
+    where it lives; 3 = gather with each task's rounds between the first and
+    the last in device memory; 4 = direct: 3 without any host copy of the
+    cells — the first round's kernel reads the rows and folds the neighbour
+    faces, the last writes them back with their min and pairwise sum (the
+    rows must be pinned, mapped host memory: ``cells`` from a pinned
+    allocation, or the machine's own). ``cells`` ([subgrids, 512] float64, C-contiguous):
     start from (and write the final state back into) these cells instead of
     the closed-form initial state. ``fault_at_launch`` (tests): the k-th
     batch launch traps; the device fault surfaces as a raised CudaError.

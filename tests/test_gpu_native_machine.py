@@ -137,7 +137,7 @@ def test_native_machine_runs_on_caller_cells(zc):
 C4_KW = dict(workers=8, executors=32, max_agg=64)
 
 
-@pytest.mark.parametrize("zc", [0, 2, 3])
+@pytest.mark.parametrize("zc", [0, 2, 3, 4])
 @pytest.mark.parametrize("mode", MODES)
 def test_native_machine_c4_golden_every_mode(golden, mode, zc):
     g = golden["run_reference"]["32768x1"]
@@ -148,22 +148,61 @@ def test_native_machine_c4_golden_every_mode(golden, mode, zc):
     assert round(m.mean_batch * (m.reasons_full + m.reasons_idle)) == 32768 * 15
 
 
+def _pinned(shape):
+    import torch
+    return torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
+
+
+@pytest.mark.parametrize("zc", [3, 4])
 @pytest.mark.parametrize("chains,kpc", [(1, 1), (1, 2), (2, 5)])
-def test_native_machine_resident_round_counts(chains, kpc):
-    """zero_copy = 3 with one round (the only round reads and writes host
-    rows), two rounds (no device round between) and 10."""
+def test_native_machine_resident_round_counts(chains, kpc, zc):
+    """zero_copy = 3 / 4 (direct: fold and reductions in the first / last
+    round's kernel, on pinned rows) with one round (the only round reads and
+    writes host rows, folding and reducing), two rounds (no device round
+    between) and 10; per-cell against the oracle, dts and pieces too."""
     rng = np.random.default_rng(11)
     start = rng.random((24, 512))
-    cells = start.copy()
-    res, _ = run_native(24, 2, workers=3, executors=2, max_agg=4, cells=cells, zero_copy=3,
+    cells = _pinned((24, 512)) if zc == 4 else np.empty((24, 512))
+    cells[:] = start
+    res, _ = run_native(24, 2, workers=3, executors=2, max_agg=4, cells=cells, zero_copy=zc,
                         chains=chains, kernels_per_chain=kpc)
     want = start
-    for _ in range(2):
-        want, _, _ = mo.step_cells(want, chains=chains, kernels_per_chain=kpc)
+    for k in range(2):
+        want, mins, sums = mo.step_cells(want, chains=chains, kernels_per_chain=kpc)
+        assert res.dts[k] == float(mins.min())
+        assert res.per_step[k].checksum_piece == __import__("math").fsum(sums.tolist())
     np.testing.assert_array_equal(cells, want)
 
 
-@pytest.mark.parametrize("zc", [2, 3])
+def test_native_machine_direct_needs_pinned_rows():
+    # pageable caller rows cannot be read by the batch kernels: refused
+    with pytest.raises(Exception):
+        run_native(8, 1, workers=2, executors=2, max_agg=4, cells=np.zeros((8, 512)),
+                   zero_copy=4)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_native_machine_direct_goldens(golden, mode):
+    """Direct batches on the machine's own (pinned) rows and on caller rows
+    with coarsened tasks (a member spans several sub-grids: the fold and the
+    reductions per sub-grid inside one member)."""
+    lit = golden["reference_test_literals"]
+    res, _ = run_native(4, 2, workers=2, executors=2, max_agg=8, mode=mode, zero_copy=4)
+    assert res.checksum == fx(lit["GOLDEN_4X2"])
+    assert res.dts == [fx(h) for h in lit["GOLDEN_4X2_DTS"]]
+    res, cells = run_native(16, 3, workers=4, executors=3, max_agg=4, mode=mode,
+                            return_cells=True, zero_copy=4)
+    assert res.checksum.hex() == golden["machine"]["16x3"]["checksum"]
+    want = np.load(__import__("conftest").TESTS + "/golden/cells.npz")["cells_16x3"]
+    np.testing.assert_array_equal(cells, want)
+    g = golden["run_reference"]["4096x1"]
+    res, _ = run_native(4096, 1, workers=4, executors=3, max_agg=16, mode=mode,
+                        task_subgrids=5, zero_copy=4)
+    assert res.checksum.hex() == g["checksum"]
+    assert [d.hex() for d in res.dts] == g["dts"]
+
+
+@pytest.mark.parametrize("zc", [2, 3, 4])
 def test_native_machine_full_gather_launches(golden, zc):
     """Batches of up to TB_GATHER_MAX = 256 members in one gather launch
     (6 KB of kernel parameters) reproduce run_reference(4096, 1)."""

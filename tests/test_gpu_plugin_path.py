@@ -58,13 +58,13 @@ def rig():
         r.close()
 
 
-@pytest.mark.parametrize("copies", ["staged", "gather", "resident"])
+@pytest.mark.parametrize("copies", ["staged", "gather", "resident", "direct"])
 @pytest.mark.parametrize("mode", MODES)
 def test_delegated_goldens_every_mode(rig, golden, mode, copies):
     lit = golden["reference_test_literals"]
     r = rig(workers=2, executors=2, max_agg=8, mode=mode)
-    _, res = r.run(4, 2, batch_copies=copies)
-    assert res.engine == "native"
+    sc, res = r.run(4, 2, batch_copies=copies)
+    assert res.engine == "native" and res.batch_copies == copies and sc.pinned
     assert res.checksum == fx(lit["GOLDEN_4X2"])
     assert res.dts == [fx(h) for h in lit["GOLDEN_4X2_DTS"]]
     r2 = rig(workers=4, executors=3, max_agg=4, mode=mode)
