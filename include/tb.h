@@ -438,7 +438,22 @@ typedef struct {
                                 of the run (k >= 1) runs a trapping kernel;
                                 the device fault must surface as this call's
                                 error, in every mode. 0 = off.               */
+  int64_t completion;        /* how batch completion reaches the scheduler:
+                                TB_COMPLETION_EVENTS (0): a CUDA event per
+                                batch and idleness probe, queried by the poll
+                                body / synchronized by FENCE / stream
+                                callbacks for HOSTTASK. TB_COMPLETION_WORDS
+                                (1, zero_copy >= 2, POLLING or FENCE): the
+                                batch kernel's last CTA stores the batch's
+                                sequence number in its executor's mapped
+                                word (tb_done); the poll body / FENCE read
+                                memory, a probe waits for the executor's
+                                last issued number — no event records, no
+                                driver queries.                              */
 } tb_machine_config;
+
+#define TB_COMPLETION_EVENTS 0
+#define TB_COMPLETION_WORDS 1
 
 typedef struct {             /* StepMetrics (src/miniapp.py:103-113)         */
   double wall_ms, dt, piece;
@@ -469,6 +484,23 @@ int tb_machine_run_cells(const tb_machine_config *cfg, double *cells, double *ch
 int tb_launch_gather(tb_stream_t s, int op, int kind, double c1, double c2,
                      const double *const *src, double *const *dst, const int64_t *n,
                      int members);
+/* A batch's completion word: the launch's last CTA stores seq into *word
+ * (mapped pinned host memory, 8-B aligned) after every CTA's writes are
+ * visible system-wide; ctas is a device counter that is 0 before the launch
+ * and reset to 0 by the last CTA (one per stream: launches on a stream are
+ * ordered). The host then sees completion by reading memory — no event
+ * record, no driver query (the machine's completion = words). */
+typedef struct {
+  uint64_t *word;
+  uint64_t seq;
+  unsigned *ctas;
+} tb_done;
+/* tb_launch_gather that also signals *done (NULL = none; op must be
+ * TB_OP_KIND / TB_OP_AFFINE, or TB_OP_TRAP for fault injection, which never
+ * signals). */
+int tb_launch_gather_done(tb_stream_t s, int op, int kind, double c1, double c2,
+                          const double *const *src, double *const *dst, const int64_t *n,
+                          int members, const tb_done *done);
 /* A gather batch of kind `kind` whose members are whole sub-grids and may be
  * a task's first and/or last round (the machine's direct mode, zero_copy =
  * 4): member i = sub-grids [g0[i], g0[i] + nsub[i]) of the S-ring, read from
@@ -477,11 +509,12 @@ int tb_launch_gather(tb_stream_t s, int op, int kind, double c1, double c2,
  * sub-grid with the neighbours' faces (faces [S][2][8] = (left, right) of the
  * previous generation; src/miniapp.py:119-126) before the transform; bit 1:
  * mins[g] / sums[g] = min and numpy-order pairwise sum of each output
- * sub-grid (src/miniapp.py:133). Same two roundings as tb_launch. */
+ * sub-grid (src/miniapp.py:133). Same two roundings as tb_launch. done:
+ * as tb_launch_gather_done (NULL = none). */
 int tb_launch_gather_edge(tb_stream_t s, int kind, const double *const *src,
                           double *const *dst, const int64_t *g0, const int32_t *nsub,
                           const uint8_t *flags, int members, const double *faces,
-                          double *mins, double *sums, int64_t S);
+                          double *mins, double *sums, int64_t S, const tb_done *done);
 
 /* One aggregated hydro batch (the Octo-Tiger use of src/executors.py:257-284,
  * PAPER.md:762-773): H2D(din <- hin: nsub ghosted sub-grids [5][12^3]) ;

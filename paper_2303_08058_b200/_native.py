@@ -48,6 +48,9 @@ TB_MODE_POLLING = 0
 TB_MODE_HOSTTASK = 1
 TB_MODE_FENCE = 2
 
+TB_COMPLETION_EVENTS = 0
+TB_COMPLETION_WORDS = 1
+
 TB_PROBE_DADD = 0
 TB_PROBE_DMUL = 1
 TB_PROBE_DFMA = 2
@@ -149,7 +152,9 @@ SIGNATURES = {
     "tb_machine_run": [_vp, _vp, _vp, _vp],
     "tb_machine_run_cells": [_vp, _vp, _vp, _vp, _vp],
     "tb_launch_gather": [_u64, _int, _int, _dbl, _dbl, _vp, _vp, _vp, _int],
-    "tb_launch_gather_edge": [_u64, _int, _vp, _vp, _vp, _vp, _vp, _int, _vp, _vp, _vp, _i64],
+    "tb_launch_gather_edge": [_u64, _int, _vp, _vp, _vp, _vp, _vp, _int, _vp, _vp, _vp, _i64,
+                              _vp],
+    "tb_launch_gather_done": [_u64, _int, _int, _dbl, _dbl, _vp, _vp, _vp, _int, _vp],
     "tb_agg_launch_hydro": [_u64, _vp, _vp, _i64, _vp, _vp, _dbl, _dbl, _pu64],
     "tb_machine_run_hydro": [_vp, _vp, _vp, _dbl, _dbl, _vp],
     "tb_ipc_get_handle": [_vp, _vp, _pu64],

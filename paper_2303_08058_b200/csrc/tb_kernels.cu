@@ -80,11 +80,46 @@ __global__ void k_trap() { __trap(); }
 // K1g: one aggregated batch whose members are read and written where they
 // live (mapped pinned host rows of the machine's task arena): member =
 // blockIdx.y, 16-byte vector accesses, the same two roundings as K1.
+// Completion word (tb_done): the launch's last CTA stores seq into a mapped
+// pinned host word once every CTA's writes are visible system-wide, so the
+// host sees the batch complete by reading memory — no event record, no
+// driver query. The CTA counter lives in device memory, is zero before the
+// launch and is reset by the last CTA (launches on one stream are ordered).
+struct DoneArgs {
+  unsigned long long *word;
+  unsigned long long seq;
+  unsigned *ctas;
+};
+
+static bool done_args(const tb_done *done, DoneArgs *d) {
+  *d = DoneArgs{nullptr, 0, nullptr};
+  if (!done) return true;
+  if (!done->word || !done->ctas || (reinterpret_cast<uintptr_t>(done->word) & 7)) return false;
+  *d = DoneArgs{reinterpret_cast<unsigned long long *>(done->word),
+                (unsigned long long)done->seq, done->ctas};
+  return true;
+}
+
+__device__ __forceinline__ void signal_done(const DoneArgs &d) {
+  if (!d.word) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const unsigned total = gridDim.x * gridDim.y;
+    if (atomicAdd(d.ctas, 1u) == total - 1) {
+      *d.ctas = 0;
+      __threadfence_system();
+      *reinterpret_cast<volatile unsigned long long *>(d.word) = d.seq;
+    }
+  }
+}
+
 struct GatherArgs {
   const double *src[TB_GATHER_MAX];
   double *dst[TB_GATHER_MAX];
   int64_t n[TB_GATHER_MAX];
   double c1, c2;
+  DoneArgs done;
 };
 
 __global__ void __launch_bounds__(256) k_launch_gather(const __grid_constant__ GatherArgs a) {
@@ -99,6 +134,7 @@ __global__ void __launch_bounds__(256) k_launch_gather(const __grid_constant__ G
     x.y = xform(x.y, a.c1, a.c2);
     d[i] = x;
   }
+  signal_done(a.done);
 }
 
 // K1e: a gather batch whose members may be a task's FIRST round (flag bit 0:
@@ -117,11 +153,15 @@ struct GatherEdgeArgs {
   double *mins, *sums;            // [S]
   int64_t S;
   double c1, c2;
+  DoneArgs done;
 };
 
 __global__ void __launch_bounds__(256) k_launch_gather_edge(const __grid_constant__ GatherEdgeArgs a) {
   const int m = blockIdx.y, k = blockIdx.x, t = threadIdx.x;
-  if (k >= a.nsub[m]) return;
+  if (k >= a.nsub[m]) {   // no sub-grid here (a shorter member): only count in
+    signal_done(a.done);
+    return;
+  }
   const int flags = a.flags[m];
   const int64_t g = a.g0[m] + k;
   const double2 *src = reinterpret_cast<const double2 *>(a.src[m] + (int64_t)k * TB_CELLS);
@@ -139,7 +179,10 @@ __global__ void __launch_bounds__(256) k_launch_gather_edge(const __grid_constan
   x.x = xform(x.x, a.c1, a.c2);
   x.y = xform(x.y, a.c1, a.c2);
   dst[t] = x;
-  if (!(flags & 2)) return;
+  if (!(flags & 2)) {
+    signal_done(a.done);
+    return;
+  }
   // per-sub-grid min (exact) and pairwise sum in numpy's order: four blocks
   // of 128, each summed by 8 strided accumulators r[j] = p[j] + p[j+8] + ...
   // (in that order), combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then
@@ -173,6 +216,7 @@ __global__ void __launch_bounds__(256) k_launch_gather_edge(const __grid_constan
       a.mins[g] = wm;
     }
   }
+  signal_done(a.done);
 }
 
 __global__ void k_spin(int64_t ns) {
@@ -1315,9 +1359,9 @@ int tb_launch(tb_stream_t s, int op, int kind, double c1, double c2, double *d,
   return tb::last_error();
 }
 
-int tb_launch_gather(tb_stream_t s, int op, int kind, double c1, double c2,
-                     const double *const *src, double *const *dst, const int64_t *n,
-                     int members) {
+int tb_launch_gather_done(tb_stream_t s, int op, int kind, double c1, double c2,
+                          const double *const *src, double *const *dst, const int64_t *n,
+                          int members, const tb_done *done) {
   if (members < 1 || members > TB_GATHER_MAX || !src || !dst || !n) return TB_E_INVALID;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(s);
   if (op == TB_OP_TRAP) {
@@ -1332,6 +1376,7 @@ int tb_launch_gather(tb_stream_t s, int op, int kind, double c1, double c2,
     c1 = h1[kind];
     c2 = h2[kind];
   } else if (op == TB_OP_NONE) {
+    if (done) return TB_E_INVALID;   // nothing would signal the word
     k_empty<<<1, 32, 0, st>>>();
     return tb::last_error();
   } else if (op != TB_OP_AFFINE) {
@@ -1350,15 +1395,22 @@ int tb_launch_gather(tb_stream_t s, int op, int kind, double c1, double c2,
   }
   a.c1 = c1;
   a.c2 = c2;
+  if (!done_args(done, &a.done)) return TB_E_INVALID;
   const int bx = grid_for(nmax / 2 > 0 ? nmax / 2 : 1, 256, 64);
   k_launch_gather<<<dim3((unsigned)bx, (unsigned)members), 256, 0, st>>>(a);
   return tb::last_error();
 }
 
+int tb_launch_gather(tb_stream_t s, int op, int kind, double c1, double c2,
+                     const double *const *src, double *const *dst, const int64_t *n,
+                     int members) {
+  return tb_launch_gather_done(s, op, kind, c1, c2, src, dst, n, members, nullptr);
+}
+
 int tb_launch_gather_edge(tb_stream_t s, int kind, const double *const *src,
                           double *const *dst, const int64_t *g0, const int32_t *nsub,
                           const uint8_t *flags, int members, const double *faces,
-                          double *mins, double *sums, int64_t S) {
+                          double *mins, double *sums, int64_t S, const tb_done *done) {
   if (members < 1 || members > TB_GATHER_MAX || !src || !dst || !g0 || !nsub || !flags ||
       kind < 0 || kind >= TB_KINDS || S < 1)
     return TB_E_INVALID;
@@ -1387,6 +1439,7 @@ int tb_launch_gather_edge(tb_stream_t s, int kind, const double *const *src,
   a.S = S;
   a.c1 = h1[kind];
   a.c2 = h2[kind];
+  if (!done_args(done, &a.done)) return TB_E_INVALID;
   k_launch_gather_edge<<<dim3((unsigned)nmax, (unsigned)members), TB_CELLS / 2, 0,
                          reinterpret_cast<cudaStream_t>(s)>>>(a);
   return tb::last_error();

@@ -373,7 +373,15 @@ class Poller {
 
   void add(cudaEvent_t ev, uint64_t chain, Task cont) {
     std::lock_guard<std::mutex> g(inbox_mu_);
-    inbox_.push_back(Entry{ev, chain, cont});
+    inbox_.push_back(Entry{ev, chain, cont, nullptr, 0});
+    waiting_.fetch_add(1, std::memory_order_relaxed);
+  }
+
+  // completion = words: fire cont once *word >= target (chain = the stream
+  // that will store it; targets arrive in nondecreasing order per chain)
+  void add_word(const uint64_t *word, uint64_t target, uint64_t chain, Task cont) {
+    std::lock_guard<std::mutex> g(inbox_mu_);
+    inbox_.push_back(Entry{nullptr, chain, cont, word, target});
     waiting_.fetch_add(1, std::memory_order_relaxed);
   }
 
@@ -412,7 +420,17 @@ class Poller {
     for (auto it = chains_.begin(); it != chains_.end();) {
       auto &dq = it->second;
       while (!dq.empty()) {
-        const cudaError_t q = cudaEventQuery(dq.front().ev);
+        cudaError_t q;
+        if (dq.front().word) {
+          // a memory read; the stream is asked (a driver call) only when a
+          // word has not moved for a millisecond: a faulted kernel never
+          // stores its word
+          q = __atomic_load_n(dq.front().word, __ATOMIC_ACQUIRE) >= dq.front().target
+                  ? cudaSuccess
+                  : stalled_stream_error(it->first, now);
+        } else {
+          q = cudaEventQuery(dq.front().ev);
+        }
         ++queries;
         if (q == cudaErrorNotReady) {
           ++not_ready;
@@ -424,7 +442,8 @@ class Poller {
         }
         Entry e = dq.front();
         dq.pop_front();
-        tb_event_release(reinterpret_cast<tb_event_t>(e.ev));
+        if (e.ev) tb_event_release(reinterpret_cast<tb_event_t>(e.ev));
+        stalled_since_.erase(it->first);
         pool_->push(e.cont);
         ++fired;
       }
@@ -453,7 +472,19 @@ class Poller {
     cudaEvent_t ev;
     uint64_t chain;
     Task cont;
+    const uint64_t *word;
+    uint64_t target;
   };
+  // a word head not reached: cudaErrorNotReady, unless the chain's stream
+  // (chain = its cudaStream_t) reports an error after >= 1 ms of waiting
+  cudaError_t stalled_stream_error(uint64_t chain, int64_t now) {
+    auto ins = stalled_since_.emplace(chain, now);
+    if (now - ins.first->second < 1000000) return cudaErrorNotReady;
+    ins.first->second = now;
+    const cudaError_t q = cudaStreamQuery(reinterpret_cast<cudaStream_t>(chain));
+    return (q == cudaSuccess || q == cudaErrorNotReady) ? cudaErrorNotReady : q;
+  }
+  std::unordered_map<uint64_t, int64_t> stalled_since_;
   Pool *pool_;
   std::atomic<int> *fault_;
   std::mutex inbox_mu_;
@@ -617,6 +648,12 @@ struct Executor {
   // AggregationExecutor's batch_sizes / reasons, src/executors.py:166-169)
   std::unique_ptr<std::atomic<int64_t>[]> stats;
   Batch *open[TB_KINDS] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  // completion = words: the mapped word this stream's batch kernels store
+  // their sequence numbers in, its CTA counter, the last number issued
+  // (under rec_mu)
+  uint64_t *word = nullptr;
+  unsigned *ctas = nullptr;
+  uint64_t issued = 0;
 };
 
 struct SubTask {
@@ -638,6 +675,9 @@ struct Machine {
   double *faces = nullptr;         // [S][2][8] previous generation
   double *mins = nullptr, *sums = nullptr;   // per sub-grid, this step
   double *pinned_small = nullptr;  // zero_copy = 4: faces | mins | sums, mapped
+  bool words = false;              // completion = TB_COMPLETION_WORDS
+  uint64_t *words_host = nullptr;  // executors' completion words (mapped)
+  unsigned *ctas_dev = nullptr;    // their CTA counters
   bool own_cells_pinned = false;   // zero_copy = 4 without caller cells
   std::unique_ptr<Pool> pool;
   std::unique_ptr<Poller> poller;
@@ -948,6 +988,73 @@ void batch_done(void *p) {   // AggregationExecutor finish (src/executors.py:286
   batch_release(b);
 }
 
+// A gather / direct batch's kernel launches (TB_GATHER_MAX members each);
+// done (completion = words) is signalled by the last one — the earlier ones
+// precede it on the stream.
+int launch_gather_kernels(Batch *b, tb_stream_t st, int op, const tb_done *done) {
+  Machine *m = b->ex->m;
+  const bool direct = m->cfg.zero_copy == 4 && op != TB_OP_TRAP;
+  const double *src[TB_GATHER_MAX];
+  double *dst[TB_GATHER_MAX];
+  int64_t n[TB_GATHER_MAX], g0[TB_GATHER_MAX];
+  int32_t nsub[TB_GATHER_MAX];
+  uint8_t flags[TB_GATHER_MAX];
+  int rc = TB_OK;
+  for (size_t i0 = 0; i0 < b->members.size() && rc == TB_OK; i0 += TB_GATHER_MAX) {
+    const int k = (int)std::min<size_t>(TB_GATHER_MAX, b->members.size() - i0);
+    const tb_done *d = i0 + (size_t)k >= b->members.size() ? done : nullptr;
+    for (int i = 0; i < k; ++i) {
+      const Req &r = b->members[i0 + i];
+      src[i] = r.src;
+      dst[i] = r.dst;
+      n[i] = r.n;
+      g0[i] = r.task->lo;
+      nsub[i] = (int32_t)r.task->n;
+      flags[i] = r.flags;
+    }
+    rc = direct ? tb_launch_gather_edge(st, b->kind, src, dst, g0, nsub, flags, k, m->faces,
+                                        m->mins, m->sums, m->cfg.subgrids, d)
+                : tb_launch_gather_done(st, op, b->kind, 0.0, 0.0, src, dst, n, k, d);
+  }
+  return rc;
+}
+
+// completion = words, FENCE: block this worker until the executor's word
+// reaches target (spin, then yield); a stream that reports an error after a
+// millisecond without progress fails the machine instead of hanging it
+void wait_word(Machine *m, Executor *ex, uint64_t target) {
+  m->event_waits.fetch_add(1, std::memory_order_relaxed);
+  const int64_t t0 = now_ns();
+  int64_t last_check = t0;
+  for (uint64_t spins = 0;; ++spins) {
+    if (__atomic_load_n(ex->word, __ATOMIC_ACQUIRE) >= target) break;
+    if ((spins & 255) == 255) {
+      const int64_t t = now_ns();
+      if (t - last_check > 1000000) {
+        last_check = t;
+        const cudaError_t q = cudaStreamQuery(ex->stream);
+        if (q != cudaSuccess && q != cudaErrorNotReady) {
+          m->fail(-(int)q);
+          break;
+        }
+      }
+      if (t - t0 > 50000) std::this_thread::yield();
+    }
+  }
+  if (g_diag) diag_add(kFenceNs, now_ns() - t0);
+}
+
+// completion = words: continuation cont runs once ex's word reaches target
+// (POLLING: registered with the poller under rec_mu, which the caller holds;
+// FENCE: the caller waits after releasing it)
+void bridge_word_locked(Machine *m, Executor *ex, uint64_t target, Task cont) {
+  if (__atomic_load_n(ex->word, __ATOMIC_ACQUIRE) >= target) {
+    m->pool->push(cont);
+    return;
+  }
+  m->poller->add_word(ex->word, target, reinterpret_cast<uint64_t>(ex->stream), cont);
+}
+
 void launch(Batch *b, bool idle) {   // src/executors.py:257-284 as one launch
   DiagScope ds(kLaunchNs);
   struct Range {   // NVTX range over the batch launch (profilers only)
@@ -968,6 +1075,33 @@ void launch(Batch *b, bool idle) {   // src/executors.py:257-284 as one launch
   const int do_barrier = m->cfg.inject_barriers && !m->cfg.barrier_elision;
   const tb_stream_t st = reinterpret_cast<tb_stream_t>(ex->stream);
   m->kernels.fetch_add(1, std::memory_order_relaxed);
+  if (m->words) {
+    // completion = words (zero_copy >= 2): the batch kernel itself stores
+    // the batch's number in the executor's word; no event
+    uint64_t seq = 0;
+    int rc;
+    {
+      std::lock_guard<std::mutex> g(ex->rec_mu);
+      const int64_t t0 = g_diag ? now_ns() : 0;
+      seq = ++ex->issued;
+      const tb_done d{ex->word, seq, ex->ctas};
+      rc = launch_gather_kernels(b, st, op, &d);
+      if (rc == TB_OK && do_barrier) rc = tb_barrier(st);
+      if (g_diag) {
+        diag_add(kEnqueues, 1);
+        diag_add(kEnqueueNs, now_ns() - t0);
+      }
+      if (rc != TB_OK) {
+        m->fail(rc);
+      } else if (m->cfg.mode == TB_MODE_POLLING) {
+        bridge_word_locked(m, ex, seq, Task{batch_done, b});
+        return;
+      }
+    }
+    if (rc == TB_OK) wait_word(m, ex, seq);
+    m->pool->push(Task{batch_done, b});
+    return;
+  }
   if (m->cfg.zero_copy == 4 && !m->hydro && !trap) {
     // direct: members' rows where they live; first / last rounds fold and
     // reduce in the kernel (tb_launch_gather_edge)
@@ -989,7 +1123,7 @@ void launch(Batch *b, bool idle) {   // src/executors.py:257-284 as one launch
           flags[i] = r.flags;
         }
         rc = tb_launch_gather_edge(st, b->kind, src, dst, g0, nsub, flags, k, m->faces, m->mins,
-                                   m->sums, m->cfg.subgrids);
+                                   m->sums, m->cfg.subgrids, nullptr);
       }
       if (rc == TB_OK && do_barrier) rc = tb_barrier(st);
       if (rc == TB_OK) rc = tb_event_record(st, ev);
@@ -1122,6 +1256,21 @@ void schedule_many(Executor *ex, int kind, const Req *reqs, int n) {
     if (m->cfg.max_agg <= 1) continue;   // M = 1: launched at once, no probe
     if (filled_here[i]) {                // opened and filled by this call: no probe
       b->refs.fetch_sub(1, std::memory_order_relaxed);
+      continue;
+    }
+    if (m->words) {
+      // the queue is idle once its word reaches the last number issued
+      uint64_t target;
+      {
+        std::lock_guard<std::mutex> g(ex->rec_mu);
+        target = ex->issued;
+        if (m->cfg.mode == TB_MODE_POLLING) {
+          bridge_word_locked(m, ex, target, Task{idle_fire, b});
+          continue;
+        }
+      }
+      wait_word(m, ex, target);
+      m->pool->push(Task{idle_fire, b});
       continue;
     }
     // One idleness probe per batch: a queue marker event (src/bridge.py:92-101).
@@ -1411,7 +1560,13 @@ int run_machine(const tb_machine_config *cfg_in, double *cells_io, double *check
   if (c.subgrids < 1 || c.steps < 0 || c.workers < 1 || c.executors < 1 || c.max_agg < 1 ||
       c.chains < 0 || c.kernels_per_chain < 1 || c.kernels_per_chain > TB_KINDS ||
       c.task_subgrids < 1 || c.mode < TB_MODE_POLLING || c.mode > TB_MODE_FENCE ||
-      c.zero_copy < 0 || c.zero_copy > 4 || c.fault_at_launch < 0)
+      c.zero_copy < 0 || c.zero_copy > 4 || c.fault_at_launch < 0 ||
+      (c.completion != TB_COMPLETION_EVENTS && c.completion != TB_COMPLETION_WORDS))
+    return TB_E_INVALID;
+  // completion words are stored by the gather kernels: kernel-only batches,
+  // and a worker (not a host-task thread) must observe them
+  if (c.completion == TB_COMPLETION_WORDS &&
+      (c.zero_copy < 2 || c.mode == TB_MODE_HOSTTASK))
     return TB_E_INVALID;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -1493,11 +1648,28 @@ int run_machine(const tb_machine_config *cfg_in, double *cells_io, double *check
   if (c.mode == TB_MODE_POLLING) m.pool->set_idle_hook(&Poller::hook, m.poller.get());
   m.hosttasks.reset(new HostTasks(m.pool.get(), (int)std::max<int64_t>(1, c.hosttask_threads),
                                   dev, 4, &m.fault));
+  if (c.completion == TB_COMPLETION_WORDS) {
+    // one 64-B line per executor for its word, one 128-B line for its counter
+    m.words = true;
+    if (cudaHostAlloc(reinterpret_cast<void **>(&m.words_host), 64 * c.executors,
+                      cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess ||
+        cudaMalloc(reinterpret_cast<void **>(&m.ctas_dev), 128 * c.executors) != cudaSuccess ||
+        cudaMemset(m.ctas_dev, 0, 128 * c.executors) != cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess) {
+      m.fail(tb::rc(cudaGetLastError()));
+    } else {
+      std::memset(m.words_host, 0, 64 * c.executors);
+    }
+  }
   for (int64_t e = 0; e < c.executors; ++e) {
     auto ex = std::make_unique<Executor>();
     ex->m = &m;
     ex->id = (int)e;
     cudaStreamCreateWithFlags(&ex->stream, cudaStreamNonBlocking);
+    if (m.words && m.words_host && m.ctas_dev) {
+      ex->word = m.words_host + 8 * e;
+      ex->ctas = m.ctas_dev + 32 * e;
+    }
     if (exec_stats) {
       ex->stats.reset(new std::atomic<int64_t>[c.max_agg + 3]);
       for (int64_t i = 0; i < c.max_agg + 3; ++i) ex->stats[i].store(0);
@@ -1604,6 +1776,8 @@ int run_machine(const tb_machine_config *cfg_in, double *cells_io, double *check
     if (m.dev_arena) cudaFree(m.dev_arena);
   }
   if (m.pinned_small) cudaFreeHost(m.pinned_small);
+  if (m.words_host) cudaFreeHost(m.words_host);
+  if (m.ctas_dev) cudaFree(m.ctas_dev);
   return m.failed() ? m.fault.load() : err;
 }
 
@@ -1630,7 +1804,7 @@ extern "C" int tb_machine_run_hydro(const tb_machine_config *cfg_in, const doubl
   while (nb * nb * nb < c.subgrids) ++nb;
   if (c.subgrids < 1 || nb * nb * nb != c.subgrids || c.steps < 0 || c.workers < 1 ||
       c.executors < 1 || c.max_agg < 1 || c.task_subgrids < 1 || c.mode < TB_MODE_POLLING ||
-      c.mode > TB_MODE_FENCE)
+      c.mode > TB_MODE_FENCE || c.completion != TB_COMPLETION_EVENTS)
     return TB_E_INVALID;
   int dev = 0;
   cudaGetDevice(&dev);

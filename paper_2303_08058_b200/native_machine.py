@@ -26,7 +26,10 @@ class MachineConfig(ctypes.Structure):
     _fields_ = [(name, ctypes.c_int64) for name in (
         "subgrids", "steps", "chains", "kernels_per_chain", "workers", "executors",
         "max_agg", "mode", "inject_barriers", "barrier_elision", "task_subgrids",
-        "hosttask_threads", "zero_copy", "fault_at_launch")]
+        "hosttask_threads", "zero_copy", "fault_at_launch", "completion")]
+
+
+_COMPLETION = {"events": N.TB_COMPLETION_EVENTS, "words": N.TB_COMPLETION_WORDS}
 
 
 class MachineStep(ctypes.Structure):
@@ -45,7 +48,8 @@ def run_native(subgrids: int, steps: int, workers: int = 8, executors: int = 32,
                task_subgrids: int = 1, hosttask_threads: int = 2, device: int = 0,
                chains: int = 3, kernels_per_chain: int = 5,
                return_cells: bool = False, zero_copy=False, fault_at_launch: int = 0,
-               cells: Optional[np.ndarray] = None, exec_stats: Optional[np.ndarray] = None):
+               cells: Optional[np.ndarray] = None, exec_stats: Optional[np.ndarray] = None,
+               completion: str = "events"):
     """Run the machine natively; returns (ScenarioResult, cells or None).
 
     ``zero_copy``: False/0 = the reference op sequence per batch (H2D ;
@@ -61,12 +65,17 @@ def run_native(subgrids: int, steps: int, workers: int = 8, executors: int = 32,
     start from (and write the final state back into) these cells instead of
     the closed-form initial state. ``fault_at_launch`` (tests): the k-th
     batch launch traps; the device fault surfaces as a raised CudaError.
+    ``completion``: "events" (a CUDA event per batch and probe, queried /
+    synchronized / called back) or "words" (zero_copy >= 2, POLLING or
+    FENCE: the batch kernel stores its sequence number in the executor's
+    mapped completion word; polling and fencing read memory).
     ``exec_stats`` (with ``cells``): int64 [steps, executors, max_agg + 3]
     receiving per-executor batch-size histograms and full/idle counts."""
     N.init(device)
     cfg = MachineConfig(subgrids, steps, chains, kernels_per_chain, workers, executors,
                         max_agg, _MODES[mode], int(inject_barriers), int(barrier_elision),
-                        task_subgrids, hosttask_threads, int(zero_copy), int(fault_at_launch))
+                        task_subgrids, hosttask_threads, int(zero_copy), int(fault_at_launch),
+                        _COMPLETION[completion])
     out = (MachineStep * max(steps, 1))()
     cs = ctypes.c_double(0.0)
     if cells is not None:

@@ -210,3 +210,41 @@ def test_native_machine_full_gather_launches(golden, zc):
     res, _ = run_native(4096, 1, workers=4, executors=2, max_agg=256, zero_copy=zc)
     assert res.checksum.hex() == g["checksum"]
     assert [d.hex() for d in res.dts] == g["dts"]
+
+
+WORD_MODES = [IntegrationMode.POLLING, IntegrationMode.FENCE]
+
+
+@pytest.mark.parametrize("zc", [2, 3, 4])
+@pytest.mark.parametrize("mode", WORD_MODES)
+def test_native_machine_completion_words_goldens(golden, mode, zc):
+    """completion = words: the batch kernels store their sequence numbers in
+    the executors' mapped words, polled / fenced from memory (no events)."""
+    lit = golden["reference_test_literals"]
+    res, _ = run_native(4, 2, workers=2, executors=2, max_agg=8, mode=mode, zero_copy=zc,
+                        completion="words")
+    assert res.checksum == fx(lit["GOLDEN_4X2"])
+    assert res.dts == [fx(h) for h in lit["GOLDEN_4X2_DTS"]]
+    res, cells = run_native(16, 3, workers=4, executors=3, max_agg=4, mode=mode,
+                            return_cells=True, zero_copy=zc, completion="words")
+    want = np.load(__import__("conftest").TESTS + "/golden/cells.npz")["cells_16x3"]
+    np.testing.assert_array_equal(cells, want)
+    g = golden["run_reference"]["4096x1"]
+    res, _ = run_native(4096, 1, workers=4, executors=2, max_agg=256, mode=mode, zero_copy=zc,
+                        completion="words")
+    assert res.checksum.hex() == g["checksum"] and [d.hex() for d in res.dts] == g["dts"]
+
+
+@pytest.mark.parametrize("mode", WORD_MODES)
+def test_native_machine_completion_words_c4(golden, mode):
+    g = golden["run_reference"]["32768x1"]
+    res, _ = run_native(32768, 1, mode=mode, zero_copy=4, completion="words", **C4_KW)
+    assert res.checksum.hex() == g["checksum"] and [d.hex() for d in res.dts] == g["dts"]
+
+
+def test_native_machine_completion_words_refused():
+    with pytest.raises(Exception):     # host-task threads do not read words
+        run_native(8, 1, workers=2, executors=2, max_agg=4, mode=IntegrationMode.HOSTTASK,
+                   zero_copy=2, completion="words")
+    with pytest.raises(Exception):     # staged batches end in a copy, not a kernel
+        run_native(8, 1, workers=2, executors=2, max_agg=4, zero_copy=0, completion="words")

@@ -75,6 +75,18 @@ def test_delegated_goldens_every_mode(rig, golden, mode, copies):
     np.testing.assert_array_equal(sc.cells(), cells)
 
 
+@pytest.mark.parametrize("mode", [IntegrationMode.POLLING, IntegrationMode.FENCE])
+def test_delegated_completion_words(rig, golden, mode):
+    r = rig(workers=4, executors=3, max_agg=4, mode=mode)
+    sc, res = r.run(16, 3, batch_copies="direct", completion="words")
+    assert res.engine == "native" and res.batch_copies == "direct"
+    assert res.checksum.hex() == golden["machine"]["16x3"]["checksum"]
+    cells = np.load(__import__("conftest").TESTS + "/golden/cells.npz")["cells_16x3"]
+    np.testing.assert_array_equal(sc.cells(), cells)
+    with pytest.raises(ValueError):     # staged batches end in a copy, not a kernel
+        r.run(16, 1, batch_copies="staged", completion="words")
+
+
 def test_delegated_unfused_counts_and_agg_counters(rig, golden):
     # pkg/tests/test_miniapp.py:65-75 on the delegated path
     r = rig(executors=1, max_agg=1)

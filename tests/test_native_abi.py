@@ -41,7 +41,8 @@ def test_abi_version_and_constants(lib):
                  "TB_ACC_MIN_WORD", "TB_ACC_COUNT_WORD", "TB_ACC_WORDS", "TB_OPT_STEP_IMPL",
                  "TB_STEP_AUTO", "TB_STEP_REG", "TB_STEP_BULK", "TB_STEP_REGPF", "TB_STEP_LEAN", "TB_STEP_PAIR", "TB_STEP_BULK1", "TB_OPT_STEP_SPW", "TB_OP_NONE", "TB_OP_KIND",
                  "TB_OP_AFFINE", "TB_OK", "TB_NOT_READY", "TB_MODE_POLLING", "TB_MODE_HOSTTASK",
-                 "TB_MODE_FENCE", "TB_IPC_HANDLE_BYTES"):
+                 "TB_MODE_FENCE", "TB_IPC_HANDLE_BYTES", "TB_COMPLETION_EVENTS",
+                 "TB_COMPLETION_WORDS"):
         m = re.search(rf"#define {name} \(?(-?\d+)\)?", text)
         assert m and int(m.group(1)) == getattr(N, name), name
 
