@@ -87,6 +87,27 @@ def test_delegated_completion_words(rig, golden, mode):
         r.run(16, 1, batch_copies="staged", completion="words")
 
 
+def test_fused_engine_goldens(rig, golden):
+    """engine='fused': one K2 launch of all sub-grids per step through
+    run_scenario — the reference's literals, cells and C4."""
+    lit = golden["reference_test_literals"]
+    r = rig(workers=2, executors=2, max_agg=8)
+    sc, res = r.run(4, 2, engine="fused")
+    assert res.engine == "fused"
+    assert res.checksum == fx(lit["GOLDEN_4X2"])
+    assert res.dts == [fx(h) for h in lit["GOLDEN_4X2_DTS"]]
+    r2 = rig(workers=4, executors=3, max_agg=4)
+    sc, res = r2.run(16, 3, engine="fused")
+    assert res.checksum.hex() == golden["machine"]["16x3"]["checksum"]
+    cells = np.load(__import__("conftest").TESTS + "/golden/cells.npz")["cells_16x3"]
+    np.testing.assert_array_equal(sc.cells(), cells)
+    r3 = rig(workers=4, executors=8, max_agg=64)
+    _, res = r3.run(32768, 1, engine="fused")
+    g = golden["run_reference"]["32768x1"]
+    assert res.checksum.hex() == g["checksum"] and [d.hex() for d in res.dts] == g["dts"]
+    assert res.per_step[0].launches == 1
+
+
 def test_delegated_unfused_counts_and_agg_counters(rig, golden):
     # pkg/tests/test_miniapp.py:65-75 on the delegated path
     r = rig(executors=1, max_agg=1)
