@@ -898,8 +898,10 @@ void hydro_resume(void *p);
 // pool's per-task work (deque lock, pop, steal, poll hook) is paid once per
 // kResumeChunk members instead of once per member. Each member's
 // continuation still runs exactly once, on a worker, after the batch
-// completed (src/executors.py:300-301); the chunks are stealable.
-constexpr size_t kResumeChunk = 16;
+// completed (src/executors.py:300-301); the chunks are stealable. 64: a full
+// C4 batch (256) is 4 chunks (C4 resident/direct 15.2 -> 14.0 ms/step against
+// 16 at 8 workers, profiles/r02/machine_chunk_ab.txt; 4 was worse).
+constexpr size_t kResumeChunk = 64;
 struct ResumeChunk {
   void (*fn)(void *);
   uint32_t n;
