@@ -248,3 +248,20 @@ def test_native_machine_completion_words_refused():
                    zero_copy=2, completion="words")
     with pytest.raises(Exception):     # staged batches end in a copy, not a kernel
         run_native(8, 1, workers=2, executors=2, max_agg=4, zero_copy=0, completion="words")
+
+
+@pytest.mark.parametrize("case", ["1x2", "3x3", "64x3", "512x15"])
+@pytest.mark.parametrize("completion,mode", [("events", IntegrationMode.POLLING),
+                                             ("words", IntegrationMode.POLLING),
+                                             ("words", IntegrationMode.FENCE)])
+def test_native_machine_direct_edge_rings(golden, case, completion, mode):
+    """Direct batches on the self ring (S = 1: a sub-grid's neighbours are
+    itself), odd rings and the reference's 15-step default, unaggregated
+    (M = 1) and aggregated, against run_reference's goldens."""
+    S, steps = (int(x) for x in case.split("x"))
+    g = golden["run_reference"][case]
+    for M in (1, 8):
+        res, _ = run_native(S, steps, workers=3, executors=2, max_agg=M, mode=mode,
+                            zero_copy=4, completion=completion)
+        assert res.checksum.hex() == g["checksum"], (case, M)
+        assert [d.hex() for d in res.dts] == g["dts"], (case, M)
