@@ -29,8 +29,11 @@ def test_paper_scenario_512_polling_vs_fence():
     # 512 sub-grids, 32 executors x max 8 aggregated
     from paper_2303_08058_b200.bridge import IntegrationMode
     from paper_2303_08058_b200.cli import RunConfig, run_matrix
-    rows, failures = run_matrix([RunConfig(subgrids=512, steps=3, repeats=1, executors=32,
-                                           max_agg=8, workers=8,
+    # 4 workers: the paper's best combination on a weakened CPU (its third
+    # graph); at 8 of the box's 16 cores the two modes are within a few %
+    # (1.03-1.09x, profiles/r02/bench_session4*.json), too close to assert
+    rows, failures = run_matrix([RunConfig(subgrids=512, steps=4, repeats=3, executors=32,
+                                           max_agg=8, workers=4,
                                            integration=IntegrationMode.POLLING)])
     assert not failures
     print(rows[0])
