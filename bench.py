@@ -305,13 +305,15 @@ C4_DT = float.fromhex("0x1.a73380416f1a6p-22")
 # saturates there (15.2 ms/step vs 14.8 at 16 workers), and, as in the
 # paper's best-combination test, the other half is what a fence-blocked
 # worker would otherwise leave the host (16 workers are in the sweep) —
-# 8 executors, max 256 aggregated,
+# 8 executors, max 512 aggregated (two gather launches of 256 per batch;
+# 12.4 ms/step against 14.8 at 256 and 11.9 at 1024, where polling and
+# fence draw level: profiles/r02/c4_m_probe.txt, c4_m_ablation_probe.txt),
 # direct batches (each task's rounds between the first and the last stay in
 # HBM; the first round's kernel reads the pinned rows and folds the ghost
 # faces, the last writes them back with min and pairwise sum — no host copy
 # of the cells; gather batches move every round over PCIe: 4 GB per step, a
 # 40 ms floor; resident = direct with the fold / reductions on the host)
-C4_MACHINE = dict(workers=8, executors=8, max_agg=256, zero_copy=4)
+C4_MACHINE = dict(workers=8, executors=8, max_agg=512, zero_copy=4)
 C4_SWEEP = [(4, 8), (16, 8), (16, 16)]   # (workers, executors) beside C4_MACHINE
 
 
