@@ -265,3 +265,17 @@ def test_native_machine_direct_edge_rings(golden, case, completion, mode):
                             zero_copy=4, completion=completion)
         assert res.checksum.hex() == g["checksum"], (case, M)
         assert [d.hex() for d in res.dts] == g["dts"], (case, M)
+
+
+@pytest.mark.parametrize("completion,mode", [("events", IntegrationMode.POLLING),
+                                             ("events", IntegrationMode.FENCE),
+                                             ("words", IntegrationMode.POLLING),
+                                             ("words", IntegrationMode.FENCE)])
+def test_native_machine_batches_wider_than_one_launch(golden, completion, mode):
+    """max_agg above TB_GATHER_MAX: a batch is several gather launches (the
+    completion word is stored by the last); direct and gather batches."""
+    g = golden["run_reference"]["4096x1"]
+    for zc in (2, 4):
+        res, _ = run_native(4096, 1, workers=4, executors=2, max_agg=700, mode=mode,
+                            zero_copy=zc, completion=completion)
+        assert res.checksum.hex() == g["checksum"] and [d.hex() for d in res.dts] == g["dts"]
