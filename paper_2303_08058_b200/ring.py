@@ -307,6 +307,16 @@ class RingStepper:
                 f"for the step's arrivals: {d[3]} of {self.world} ranks arrived")
 
     # -------------------------------------------------------------- state --
+    def reset(self) -> None:
+        """Begin a new run on this stepper's buffers: step count, checksum
+        and exact accumulator zeroed (the cells are left to load_cells)."""
+        self.flush()
+        self.steps_done = 0
+        self.checksum.zero_()
+        self.ops.acc_reset(self.acc)
+        self._pending = None
+        self._host_prev = None
+
     @property
     def cells(self) -> torch.Tensor:
         """This rank's current generation, [n_local, 512] (device)."""

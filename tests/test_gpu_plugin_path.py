@@ -92,10 +92,11 @@ def test_fused_engine_goldens(rig, golden):
     run_scenario — the reference's literals, cells and C4."""
     lit = golden["reference_test_literals"]
     r = rig(workers=2, executors=2, max_agg=8)
-    sc, res = r.run(4, 2, engine="fused")
-    assert res.engine == "fused"
-    assert res.checksum == fx(lit["GOLDEN_4X2"])
-    assert res.dts == [fx(h) for h in lit["GOLDEN_4X2_DTS"]]
+    for _ in range(2):           # the second call reuses the cached stepper
+        sc, res = r.run(4, 2, engine="fused")
+        assert res.engine == "fused"
+        assert res.checksum == fx(lit["GOLDEN_4X2"])
+        assert res.dts == [fx(h) for h in lit["GOLDEN_4X2_DTS"]]
     r2 = rig(workers=4, executors=3, max_agg=4)
     sc, res = r2.run(16, 3, engine="fused")
     assert res.checksum.hex() == golden["machine"]["16x3"]["checksum"]
@@ -106,6 +107,8 @@ def test_fused_engine_goldens(rig, golden):
     g = golden["run_reference"]["32768x1"]
     assert res.checksum.hex() == g["checksum"] and [d.hex() for d in res.dts] == g["dts"]
     assert res.per_step[0].launches == 1
+    from paper_2303_08058_b200.miniapp import release_fused
+    release_fused()
 
 
 def test_delegated_unfused_counts_and_agg_counters(rig, golden):
