@@ -594,6 +594,18 @@ def north_star_kernels(dev, reps=20):
     am = torch.empty(S, dtype=torch.float64, device=dev)
     for _ in range(3):
         hydro.hydro_flux(U, dx, out=du, amax=am)
+    # back to back, as the K2 headline: the 283 MB input exceeds the 126 MB
+    # L2 and every launch reads all of it from DRAM (ncu --cache-control
+    # none: 283.1 MB read per launch, profiles/r02/k6_b2b_probe.txt); the
+    # L2-flushed figure (a 256 MiB write before each launch) beside it
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        hydro.hydro_flux(U, dx, out=du, amax=am)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / reps
     tot = 0.0
     for _ in range(reps):
         flush.fill_(1)
@@ -603,12 +615,17 @@ def north_star_kernels(dev, reps=20):
         b.record()
         torch.cuda.synchronize()
         tot += a.elapsed_time(b)
-    ms = tot / reps
+    ms_flushed = tot / reps
     gbs = S * HYDRO_BYTES_PER_SUBGRID / (ms * 1e-3) / 1e9
     out["hydro_k6"] = {
         "config": "BASELINE config 2: hydro reconstruct+flux, 4096 synthetic 8^3 sub-grids "
                   "with 2-cell ghost layers (rotating star), 1 B200",
         "kernel": "k_hydro_flux", "ms": ms, "cells_per_s": S * 512 / (ms * 1e-3),
+        "l2": "launches back to back, input (283 MB) larger than L2: every launch reads it "
+              "all from DRAM (ncu --cache-control none: 283.1 MB per launch)",
+        "l2_flushed": {"ms": ms_flushed,
+                       "fp64_frac": S * HYDRO_FP64_PER_SUBGRID / (ms_flushed * 1e-3) / f64,
+                       "method": "256 MiB write before each launch, events per launch"},
         "roofline": {"bound": "fp64 (divide/sqrt-heavy; see profiles)", "hbm_achieved_gbs": gbs,
                      "hbm_frac": gbs / hbm,
                      "fp64_instr_per_subgrid": HYDRO_FP64_PER_SUBGRID,
@@ -636,23 +653,21 @@ def north_star_kernels(dev, reps=20):
     du5 = torch.empty((S5, 5, 8, 8, 8), dtype=torch.float64, device=dev)
     am5 = torch.empty(S5, dtype=torch.float64, device=dev)
     hydro.hydro_flux(U5, dx5, out=du5, amax=am5)
-    tot = 0.0
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
     for _ in range(5):
-        flush.fill_(1)
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
         hydro.hydro_flux(U5, dx5, out=du5, amax=am5)
-        b.record()
-        torch.cuda.synchronize()
-        tot += a.elapsed_time(b)
-    ms5 = tot / 5
+    b.record()
+    torch.cuda.synchronize()
+    ms5 = a.elapsed_time(b) / 5
     out["hydro_k6"]["max_level_5"] = {
         "subgrids": S5, "ms": ms5, "cells_per_s": S5 * 512 / (ms5 * 1e-3),
         "fp64_frac": S5 * HYDRO_FP64_PER_SUBGRID / (ms5 * 1e-3) / f64,
         "fp64_ops_frac": S5 * HYDRO_FP64_OPS_PER_SUBGRID / (ms5 * 1e-3) / f64,
-        "note": "same kernel and L2-flush method at 32768 sub-grids (the star step's "
-                "max_level-5 lattice size): the config-2 launch carries its head (first "
-                "staging of every CTA) and last-wave tail, ~10 us"}
+        "note": "same kernel, launches back to back (2.26 GB input) at 32768 sub-grids "
+                "(the star step's max_level-5 lattice size): the config-2 launch carries "
+                "its head (first staging of every CTA) and last-wave tail, ~7 us"}
     del U5, du5, am5
     # K7: FMM gravity, max_level 4 (config 3)
     L = 4
