@@ -1,7 +1,8 @@
 """Small invocations of every kernel family for compute-sanitizer
-(memcheck / racecheck / synccheck): K2 ring step, K1 via the machine, K6
-hydro (ghosted and lattice/TMA), K7 FMM (one device and slab geometry),
-star step and its slab decomposition, the hydro machine."""
+(memcheck / racecheck / synccheck): K2 ring step, K1 via the machine
+(staged, direct and gather batches, events and completion words), K6 hydro
+(ghosted and lattice/TMA, dynamic assignment), K7 FMM (one device and slab
+geometry), star step and its slab decomposition, the hydro machine."""
 import os
 import sys
 
@@ -33,6 +34,19 @@ def main():
     vc = VirtualCluster(2, 2, s1.U.clone())
     vc.step()
     run_native(16, 1, workers=2, executors=2, max_agg=4, mode=IntegrationMode.POLLING)
+    # round 2: direct batches (k_launch_gather_edge: fold + reductions) with
+    # events and with completion words (the last CTA's counter and word),
+    # gather batches with words, a batch wider than one launch, and K6 on
+    # enough sub-grids for its dynamic work counter to hand out more
+    for comp in ("events", "words"):
+        run_native(16, 2, workers=2, executors=2, max_agg=4, mode=IntegrationMode.POLLING,
+                   zero_copy=4, completion=comp)
+    run_native(16, 1, workers=2, executors=2, max_agg=4, mode=IntegrationMode.FENCE,
+               zero_copy=2, completion="words")
+    run_native(64, 1, workers=2, executors=1, max_agg=300, mode=IntegrationMode.POLLING,
+               zero_copy=4, completion="words")
+    I3, dx3 = rotating_star(512, device=dev)
+    hydro_flux(with_ghosts(I3), dx3)
     run_native_hydro(rotating_star(8)[0].numpy(), 1, workers=2, executors=2, max_agg=4)
     torch.cuda.synchronize()
     print("cases ok")
