@@ -656,15 +656,19 @@ struct Executor {
   uint64_t issued = 0;
 };
 
+// A task's state, 88 B, held contiguously in Machine::tasks (a chunk's
+// members are a fixed stride apart, so resuming them streams through memory
+// instead of chasing heap objects). Work buffers: the machine's task_bufs
+// (staged / in place), its pinned arena (gather / resident) or the caller's
+// rows (direct); d0 / d1 the device ping-pong rows (resident / direct).
 struct SubTask {
   Machine *m;
   Executor *ex;
   int64_t lo, n;          // sub-grids [lo, lo+n)
-  int round;
-  std::vector<double> a, b;   // work buffers (zero_copy = 2: abuf/bbuf live in the arena)
+  int32_t round;
   double *abuf, *bbuf;
   double *work, *out;
-  double *d0 = nullptr, *d1 = nullptr;   // zero_copy = 3: device ping-pong buffers
+  double *d0 = nullptr, *d1 = nullptr;
 };
 
 struct Machine {
@@ -683,7 +687,8 @@ struct Machine {
   std::unique_ptr<Poller> poller;
   std::unique_ptr<HostTasks> hosttasks;
   std::vector<std::unique_ptr<Executor>> execs;
-  std::vector<std::unique_ptr<SubTask>> tasks;
+  std::vector<SubTask> tasks;       // reserved up front: addresses stay put
+  std::vector<double> task_bufs;    // staged / in-place modes and hydro: per-task buffers
   std::mutex staging_mu;
   std::map<size_t, std::vector<Staging *>> staging_free;
   std::vector<Staging *> staging_all;
@@ -1456,9 +1461,9 @@ void hydro_done(Machine *m) { task_finished(m); }
 void hydro_resume(void *p) {   // outputs landed in t->b: keep dU/dt and amax
   SubTask *t = static_cast<SubTask *>(p);
   Machine *m = t->m;
-  std::memcpy(m->dudt.data() + t->lo * kInterior, t->b.data(),
+  std::memcpy(m->dudt.data() + t->lo * kInterior, t->bbuf,
               sizeof(double) * t->n * kInterior);
-  std::memcpy(m->amax.data() + t->lo, t->b.data() + t->n * kInterior, sizeof(double) * t->n);
+  std::memcpy(m->amax.data() + t->lo, t->bbuf + t->n * kInterior, sizeof(double) * t->n);
   hydro_done(m);
 }
 
@@ -1468,8 +1473,8 @@ void hydro_start(void *p) {    // ghost exchange + one K6 request
     hydro_done(t->m);
     return;
   }
-  for (int64_t k = 0; k < t->n; ++k) ghost_fill(t->m, t->lo + k, t->a.data() + k * kGhosted);
-  schedule(t->ex, 0, t->a.data(), t->b.data(), t->n * kGhosted, t);
+  for (int64_t k = 0; k < t->n; ++k) ghost_fill(t->m, t->lo + k, t->abuf + k * kGhosted);
+  schedule(t->ex, 0, t->abuf, t->bbuf, t->n * kGhosted, t);
 }
 
 void hydro_update(void *p) {   // U += dt * dU/dt (two roundings, as the oracle)
@@ -1680,8 +1685,11 @@ int run_machine(const tb_machine_config *cfg_in, double *cells_io, double *check
   }
   // tasks: contiguous blocks of task_subgrids, round-robin over executors
   // (src/cli.py:224 aggs_by_grid)
+  m.tasks.reserve((size_t)((S + c.task_subgrids - 1) / c.task_subgrids));
+  if (!direct && !m.dev_arena && !m.arena) m.task_bufs.resize((size_t)(2 * S * kCells));
   for (int64_t lo = 0; lo < S; lo += c.task_subgrids) {
-    auto t = std::make_unique<SubTask>();
+    m.tasks.emplace_back();
+    SubTask *t = &m.tasks.back();
     t->m = &m;
     t->lo = lo;
     t->n = std::min<int64_t>(c.task_subgrids, S - lo);
@@ -1698,12 +1706,9 @@ int run_machine(const tb_machine_config *cfg_in, double *cells_io, double *check
       t->abuf = m.arena + 2 * lo * kCells;
       t->bbuf = t->abuf + t->n * kCells;
     } else {
-      t->a.resize(t->n * kCells);
-      t->b.resize(t->n * kCells);
-      t->abuf = t->a.data();
-      t->bbuf = t->b.data();
+      t->abuf = m.task_bufs.data() + 2 * lo * kCells;
+      t->bbuf = t->abuf + t->n * kCells;
     }
-    m.tasks.push_back(std::move(t));
   }
   double cs = 0.0;
   for (int64_t step = 0; step < c.steps && !m.failed(); ++step) {
@@ -1720,7 +1725,7 @@ int run_machine(const tb_machine_config *cfg_in, double *cells_io, double *check
       // each executor's tasks to its worker group (Pool::push_group)
       const size_t E = m.execs.size();
       std::vector<std::vector<Task>> by(E);
-      for (auto &t : m.tasks) by[(size_t)t->ex->id].push_back(Task{start_task, t.get()});
+      for (auto &t : m.tasks) by[(size_t)t.ex->id].push_back(Task{start_task, &t});
       for (size_t e = 0; e < E; ++e) m.pool->push_group(by[e].data(), by[e].size(), e, E);
     }
     {
@@ -1833,17 +1838,17 @@ extern "C" int tb_machine_run_hydro(const tb_machine_config *cfg_in, const doubl
     cudaStreamCreateWithFlags(&ex->stream, cudaStreamNonBlocking);
     m.execs.push_back(std::move(ex));
   }
+  m.tasks.reserve((size_t)((S + c.task_subgrids - 1) / c.task_subgrids));
+  m.task_bufs.resize((size_t)(S * (kGhosted + kHydroOut)));
   for (int64_t lo = 0; lo < S; lo += c.task_subgrids) {
-    auto t = std::make_unique<SubTask>();
+    m.tasks.emplace_back();
+    SubTask *t = &m.tasks.back();
     t->m = &m;
     t->lo = lo;
     t->n = std::min<int64_t>(c.task_subgrids, S - lo);
     t->ex = m.execs[(size_t)((lo / c.task_subgrids) % c.executors)].get();
-    t->a.resize(t->n * kGhosted);
-    t->b.resize(t->n * kHydroOut);
-    t->abuf = t->a.data();
-    t->bbuf = t->b.data();
-    m.tasks.push_back(std::move(t));
+    t->abuf = m.task_bufs.data() + lo * (kGhosted + kHydroOut);   // ghosted inputs
+    t->bbuf = t->abuf + t->n * kGhosted;                           // dU/dt + amax
   }
   {  // pre-allocate the pinned/device staging pool (two full batches per stream)
     std::vector<Staging *> warm;
@@ -1859,7 +1864,7 @@ extern "C" int tb_machine_run_hydro(const tb_machine_config *cfg_in, const doubl
       m.remaining.store((int64_t)m.tasks.size());
       std::vector<Task> ts;
       ts.reserve(m.tasks.size());
-      for (auto &t : m.tasks) ts.push_back(Task{phase ? hydro_update : hydro_start, t.get()});
+      for (auto &t : m.tasks) ts.push_back(Task{phase ? hydro_update : hydro_start, &t});
       m.pool->push_spread(ts.data(), ts.size());   // hydro_update is host work: any worker
       std::unique_lock<std::mutex> lk(m.done_mu);
       m.done_cv.wait(lk, [&] { return m.remaining.load() == 0; });
