@@ -1685,9 +1685,18 @@ int run_machine(const tb_machine_config *cfg_in, double *cells_io, double *check
   }
   // tasks: contiguous blocks of task_subgrids, round-robin over executors
   // (src/cli.py:224 aggs_by_grid)
-  m.tasks.reserve((size_t)((S + c.task_subgrids - 1) / c.task_subgrids));
+  const int64_t ntasks = (S + c.task_subgrids - 1) / c.task_subgrids;
+  m.tasks.reserve((size_t)ntasks);
   if (!direct && !m.dev_arena && !m.arena) m.task_bufs.resize((size_t)(2 * S * kCells));
-  for (int64_t lo = 0; lo < S; lo += c.task_subgrids) {
+  // executor-major order: task i (executor i mod E) sits among its
+  // executor's tasks, so a batch's members — consecutive tasks of one
+  // executor — are neighbours in memory when their continuations run
+  for (int64_t k = 0; k < ntasks; ++k) {
+    const int64_t E = c.executors, q = ntasks / E, r = ntasks % E;
+    // k-th slot of the executor-major layout -> task index i
+    const int64_t e = k < r * (q + 1) ? k / (q + 1) : r + (k - r * (q + 1)) / q;
+    const int64_t j = k < r * (q + 1) ? k % (q + 1) : (k - r * (q + 1)) % q;
+    const int64_t lo = (j * E + e) * c.task_subgrids;
     m.tasks.emplace_back();
     SubTask *t = &m.tasks.back();
     t->m = &m;
